@@ -1,0 +1,263 @@
+/*
+ * ta.h — C ABI of the B200-native ThunderAgent KV-manager hot path (libta.so).
+ *
+ * The library implements, in hand-written sm_100a CUDA, the per-tick scheduler
+ * step of ThunderAgent's program-aware KV-cache manager (arXiv 2602.13692,
+ * PAPER.md §4.3) over all live agentic programs, and the paged-KV
+ * block movement its decisions trigger (HBM <-> pinned host, HBM -> peer HBM,
+ * HBM -> HBM compaction).  Policy semantics are defined step by step in
+ * DESIGN.md §2 (readings A1-A27).
+ *
+ * Conventions (apply to every entry point):
+ *  - Every call returns ta_status; TA_OK == 0.  No exceptions cross the ABI.
+ *    A failed call leaves the context unchanged, except TA_E_CUDA / TA_E_PEER,
+ *    which poison the context (every later call returns the same code).
+ *    ta_last_error() returns a human-readable reason for the last failure.
+ *  - Ownership: the CALLER allocates and owns every buffer (KV pools, host
+ *    tiers, workspaces) and the CUDA stream, and keeps them alive until
+ *    ta_destroy().  The library never frees caller memory.
+ *  - Calls on one context are serialized by the caller (single writer,
+ *    SPEC.md:82, 283).  All device work is stream-ordered on the context stream.
+ *  - Multi-replica: replica state (program table, block tables, bitmaps) is
+ *    replicated on every rank; each rank holds the KV pools of
+ *    `replicas_here` replicas starting at `first_replica`.  ta_sched_step is
+ *    then collective: every rank passes the same now_ms and events.
+ *  - Block-table entry encoding (u32): TA_LOC_NONE = no KV; bit 31 clear =
+ *    HBM block index on the program's home replica; bit 31 set = slot index in
+ *    the home replica's pinned host tier.
+ */
+#ifndef TA_H_
+#define TA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TA_ABI_VERSION 1
+#define TA_MAX_REPLICAS 32
+#define TA_LOC_NONE 0xFFFFFFFFu
+#define TA_LOC_HOST 0x80000000u
+
+typedef struct ta_ctx ta_ctx;
+
+typedef enum {
+  TA_OK = 0,
+  TA_E_INVAL = 1,              /* bad argument / config / time */
+  TA_E_NOMEM = 2,              /* workspace too small */
+  TA_E_DUP_ID = 3,             /* ARRIVE on a used pid */
+  TA_E_UNKNOWN_PROGRAM = 4,    /* pid never arrived */
+  TA_E_ILLEGAL_TRANSITION = 5, /* event/verb not legal in the program's status */
+  TA_E_CAPACITY = 6,           /* restore/migrate would exceed lambda_max*C or cannot be fetched */
+  TA_E_TRUNCATED = 7,          /* more decisions than out_cap; *n_out holds the needed count */
+  TA_E_CUDA = 8,               /* CUDA error (context poisoned) */
+  TA_E_PEER = 9,               /* peer / IPC error (context poisoned) */
+  TA_E_STATE = 10              /* call not valid in this mode (e.g. events in trace mode) */
+} ta_status;
+
+/* Program status s (PAPER.md:670-676 ProgramStatus, plus UNARRIVED for unused slots). */
+enum { TA_UNARRIVED = 0, TA_PAUSED = 1, TA_REASONING = 2, TA_ACTING = 3, TA_STOPPED = 4 };
+/* Execution phase tau. */
+enum { TA_PHASE_R = 0, TA_PHASE_A = 1 };
+/* Decision kinds, emitted in canonical order PAUSE, RESTORE, EVICT, FETCH/STALL, COMPACT. */
+enum { TA_D_PAUSE = 1, TA_D_RESTORE = 2, TA_D_EVICT = 3, TA_D_FETCH = 4, TA_D_STALL = 5,
+       TA_D_MIGRATE = 6, TA_D_COMPACT = 7 };
+/* API-mode events (the three-change protocol). */
+enum { TA_EV_ARRIVE = 1, TA_EV_DECODE = 2, TA_EV_TOOL_CALL = 3, TA_EV_TOOL_RESULT = 4,
+       TA_EV_RELEASE = 5 };
+/* ta_pause modes: LAZY is the paper's Pause (KV becomes evictable). */
+enum { TA_PAUSE_LAZY = 0, TA_PAUSE_OFFLOAD = 1, TA_PAUSE_DROP = 2 };
+/* ta_config.flags */
+enum {
+  TA_F_TRACE_MODE = 1u << 0,   /* program scripts come from ta_load_trace (closed-loop) */
+  TA_F_FILL = 1u << 1,         /* write KV content for new/recomputed tokens (engine stand-in) */
+  TA_F_NO_GRAPH = 1u << 2,     /* launch the tick kernel by kernel instead of a CUDA graph */
+  TA_F_TIMING = 1u << 3,       /* record per-phase CUDA events (implies no graph) */
+  TA_F_COPY_BULK = 1u << 4     /* HBM->HBM copies via cp.async.bulk (TMA) instead of LDG/STG.128 */
+};
+
+typedef struct {
+  /* KV shape of one token (BackendState.cache_config) */
+  int32_t n_layers, n_kv_heads, head_dim, elem_bytes; /* elem_bytes must be 2 */
+  int32_t block_tokens;        /* bt: tokens per KV block (16/32/64; 1 for pins) */
+  int32_t layout;              /* 0: layer-major pool[l][kv][NB][bt][H][D]; 1: block-major pool[NB][l][kv][bt][H][D] */
+  int32_t n_replicas;          /* R data-parallel replicas (<= TA_MAX_REPLICAS) */
+  int32_t replicas_here;       /* replicas whose pools this process holds */
+  int32_t first_replica;       /* index of the first of them */
+  int32_t max_programs;        /* N program slots */
+  int32_t max_blocks_per_program; /* MAXB = ceil(max_ctx / bt) */
+  int32_t max_trace_turns;     /* capacity of the trace script arrays */
+  int64_t hbm_blocks;          /* NB per replica */
+  int64_t host_blocks;         /* NH per replica (0 = no host tier) */
+  int64_t delta_t_ms;          /* Delta t of the periodic monitor (reading A1) */
+  int64_t decay_unit_ms;       /* time unit of t_q in f(t_q) (reading A2) */
+  uint32_t lambda_max_q16;     /* high watermark, 65536 == 1.0 */
+  uint32_t lambda_min_q16;     /* low watermark */
+  uint64_t decay_q32[64];      /* F[k] = floor(f(k) * 2^32), F[0] = 2^32 (eq. 7) */
+  int32_t decode_tok_per_s;    /* synthetic engine decode rate (trace mode) */
+  int32_t compact_every;       /* two-finger compaction every k ticks; 0 = off */
+  uint32_t flags;              /* TA_F_* */
+  int32_t reserved;
+} ta_config;
+
+typedef struct {
+  /* Device pointer of replica r's HBM KV pool (NB * block_bytes bytes) for every
+   * replica this process can address: local replicas, and peers mapped with
+   * ta_import_peer_pool().  NULL for replicas it cannot address. */
+  void* hbm_pool[TA_MAX_REPLICAS];
+  /* Page-locked host pointer of replica r's host tier (NH * block_bytes bytes),
+   * local replicas only; NULL otherwise. */
+  void* host_pool[TA_MAX_REPLICAS];
+  void* dev_workspace;         /* >= dev_bytes from ta_workspace_bytes, 256-B aligned */
+  void* host_workspace;        /* page-locked, >= host_bytes from ta_workspace_bytes */
+} ta_buffers;
+
+typedef struct {               /* API-mode event */
+  uint32_t kind;               /* TA_EV_* */
+  uint32_t pid;                /* program slot */
+  uint32_t uid;                /* ARRIVE: program identity used by the KV content */
+  uint32_t tokens;             /* ARRIVE: prompt tokens; DECODE: n; TOOL_RESULT: result tokens */
+  int64_t t_ms;                /* TOOL_CALL: time the tool call started (0 <= t_ms < 2^40) */
+} ta_event;
+
+typedef struct {               /* one scheduling decision (48 bytes) */
+  uint32_t kind;               /* TA_D_* */
+  uint32_t pid;                /* program slot; 0xFFFFFFFF for COMPACT */
+  int32_t src;                 /* PAUSE: replica left; RESTORE/FETCH/STALL: KV home before; EVICT/COMPACT: replica */
+  int32_t dst;                 /* RESTORE/MIGRATE/FETCH/STALL: target replica; -1 otherwise */
+  uint32_t blocks;             /* EVICT: blocks evicted; FETCH/STALL: blocks needed; COMPACT: blocks moved */
+  uint32_t to_host, dropped;   /* EVICT: blocks offloaded to the host tier / dropped */
+  uint32_t hit_tok, peer_tok, host_tok, miss_tok; /* FETCH of a resumed program: history by location */
+  uint32_t new_tok;            /* FETCH: tokens [c_kv, c) written now */
+} ta_decision;
+
+typedef struct {               /* cumulative counters (order fixed) */
+  uint64_t ticks, arrivals, stops, pauses, restores, oversized_skips, shortfalls;
+  uint64_t evict_blocks, evict_to_host, evict_dropped, fetch_blocks, p2p_blocks, h2d_blocks;
+  uint64_t recompute_blocks, new_blocks, compact_blocks, stalls;
+  uint64_t hit_tok, peer_tok, host_tok, miss_tok, new_tok, fill_tok;
+  uint64_t imbalance_max_blocks, imbalance_last_blocks;   /* max_r used - min_r used */
+  uint64_t L[TA_MAX_REPLICAS];          /* effective load after the last restore pass (eq. 7) */
+  uint64_t hbm_used[TA_MAX_REPLICAS];   /* HBM blocks in use */
+  uint64_t host_used[TA_MAX_REPLICAS];  /* host-tier slots in use */
+  uint64_t block_bytes;                 /* bytes per KV block (bytes moved = blocks * block_bytes) */
+} ta_stats_t;
+
+typedef struct {               /* trace-mode program scripts (tracegen layout; host pointers) */
+  int32_t n_slots;             /* <= max_programs */
+  int32_t n_initial;           /* slots [0, n_initial) arrive at tick 0; then closed loop */
+  const uint32_t* uid;         /* [n_slots] */
+  const uint32_t* p0;          /* [n_slots] prompt tokens */
+  const uint32_t* turn_off;    /* [n_slots + 1] CSR offsets into g / d_ms / o */
+  const uint32_t* g;           /* tokens generated per turn */
+  const uint32_t* d_ms;        /* tool latency after the turn */
+  const uint32_t* o;           /* tool-result tokens after the turn */
+} ta_trace_view;
+
+typedef struct {               /* host mirror of the device state (parity tests); NULL = skip */
+  uint32_t *uid, *c, *c_kv, *paused_since, *step_count, *turn, *gen_done;   /* [N] */
+  uint8_t *status, *phase, *satisfied;                                      /* [N] */
+  int8_t *placement, *home;                                                 /* [N] */
+  int64_t *acting_since, *tool_return;                                      /* [N] */
+  uint32_t *loc;              /* [N * MAXB] */
+  uint32_t *hbm_free;         /* [R * ceil(NB/32)] bit set = free */
+  uint32_t *host_free;        /* [R * ceil(NH/32)] */
+  uint32_t *owner_hbm;        /* [R * NB]  pid * MAXB + j of the block's owner (valid if used) */
+  uint32_t *owner_host;       /* [R * NH] */
+  uint64_t *L;                /* [R] */
+  uint32_t *nb, *n_hbm, *n_host, *prefix_hbm, *contrib;   /* [N] step-1/2 values of the last tick (download only) */
+  int64_t *scalars;           /* [4]: tick, next_arrival, last_T, reserved */
+} ta_state_view;
+
+/* Bytes of device / page-locked host workspace a context needs for cfg. */
+ta_status ta_workspace_bytes(const ta_config* cfg, size_t* dev_bytes, size_t* host_bytes);
+
+/* Bytes of one KV block for cfg (2 * L * bt * H * D * elem_bytes). */
+ta_status ta_block_bytes(const ta_config* cfg, size_t* block_bytes);
+
+/* Create a context over caller-owned buffers on the caller's CUDA stream
+ * (cudaStream_t passed as void*).  Initialises the program table (all slots
+ * UNARRIVED), empty block tables and all-free bitmaps.  nccl_comm is reserved
+ * (must be NULL in ABI v1).  Errors: TA_E_INVAL (config), TA_E_NOMEM, TA_E_CUDA. */
+ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_stream,
+                       void* nccl_comm, ta_ctx** out);
+
+/* Trace mode: copy program scripts to the device.  Must be
+ * called before the first tick.  Errors: TA_E_INVAL (sizes), TA_E_STATE (not trace mode). */
+ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* trace);
+
+/* One scheduler tick (the periodic monitor, every Delta t):
+ *   step 0  ingest (trace script or the API events ev[0..n_ev), validated in
+ *           order, all-or-nothing); releases free their blocks;
+ *   step 1  per-program footprint and prefix residency from the block table;
+ *   step 2  decayed effective load per replica (eq. 7);
+ *   step 3  pause pass, shortest-first acting-first;
+ *   step 4  restore pass from the global queue;
+ *   step 5  materialize: stall cut, program-aware eviction (host tier first),
+ *           lowest-free-first allocation, hit accounting;
+ *   step 6  block movement: D2H evictions, then P2P/H2D fetches and fills;
+ *   step 7  deferred frees, optional compaction, statistics.
+ * now_ms: trace mode: -1 (or exactly tick*Delta t); API mode: the tick's time.
+ * Decisions are written to out[0..*n_out) in canonical order when out != NULL
+ * (the call then returns after they land); with out == NULL the tick is only
+ * enqueued on the stream.  Errors: TA_E_INVAL, TA_E_STATE, event errors
+ * (TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM, TA_E_ILLEGAL_TRANSITION: nothing applied,
+ * the tick does not run), TA_E_TRUNCATED (tick ran; *n_out = needed count). */
+ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t n_ev,
+                        ta_decision* out, int32_t out_cap, int32_t* n_out);
+
+/* Pause one active program now.  mode: TA_PAUSE_LAZY (blocks
+ * become evictable, no bytes move), TA_PAUSE_OFFLOAD (evict its HBM blocks to the
+ * host tier now, dropping when full), TA_PAUSE_DROP (free them).
+ * Errors: TA_E_UNKNOWN_PROGRAM, TA_E_ILLEGAL_TRANSITION (not REASONING/ACTING). */
+ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, int32_t out_cap,
+                   int32_t* n_out);
+
+/* Restore one paused program now on `replica` (-1: the
+ * restore pass's least-loaded choice).  Phase R programs fetch their KV now
+ * (eviction allowed).  Errors: TA_E_ILLEGAL_TRANSITION (not PAUSED),
+ * TA_E_CAPACITY (L + contrib > lambda_max*C, or the fetch cannot be satisfied;
+ * nothing changes). */
+ta_status ta_resume(ta_ctx* ctx, uint32_t pid, int32_t replica, ta_decision* out, int32_t out_cap,
+                    int32_t* n_out);
+
+/* Move an active program to replica dst (dynamic migration):
+ * a REASONING program's HBM blocks move to dst now (P2P over NVLink or D2D for
+ * co-located replicas); an ACTING program's blocks move when its tool returns.
+ * Errors: TA_E_ILLEGAL_TRANSITION, TA_E_INVAL (dst), TA_E_CAPACITY. */
+ta_status ta_migrate(ta_ctx* ctx, uint32_t pid, int32_t dst_replica, ta_decision* out,
+                     int32_t out_cap, int32_t* n_out);
+
+/* Cumulative counters and per-replica occupancy (synchronizes the stream). */
+ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out);
+
+/* Per-phase device times of the last tick in microseconds (TA_F_TIMING only):
+ * [0] ingest+footprint [1] pause+restore [2] plan [3] D2H evict copies
+ * [4] fetch copies (P2P/H2D) [5] fills [6] finalize+compaction plan
+ * [7] compaction copies [8] decision assembly.  n <= 9. */
+ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
+
+/* Count KV words that differ from the content closed form
+ * over every valid token slot of every owned HBM and host block of the local
+ * replicas (test aid; needs TA_F_FILL runs).  Synchronizes. */
+ta_status ta_verify_content(ta_ctx* ctx, uint64_t* mismatched_words, uint64_t* checked_words);
+
+/* Parity tests: dir 0 = download device state into v, 1 = upload v (all
+ * fields required except the download-only ones).  Synchronizes. */
+ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v);
+
+/* Multi-GPU: export this process's local HBM pool as a 64-byte CUDA IPC handle,
+ * and map a peer replica's pool from its handle (sets hbm_pool[replica]). */
+ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle64);
+ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle64);
+
+ta_status ta_destroy(ta_ctx* ctx);
+const char* ta_last_error(const ta_ctx* ctx);
+int32_t ta_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TA_H_ */

@@ -1,0 +1,370 @@
+"""ctypes binding over libta.so (include/ta.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libta.so; PyTorch is used
+for device memory, pinned host memory and the CUDA stream.  There is no CPU
+fallback: if libta.so or a CUDA device is missing, constructing a Pool raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libta.so")
+MAXR = 32
+
+TA_OK, TA_E_INVAL, TA_E_NOMEM, TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM = 0, 1, 2, 3, 4
+TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA_E_STATE = 5, 6, 7, 8, 9, 10
+F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK = 1, 2, 4, 8, 16
+STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
+                5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",
+                9: "E_PEER", 10: "E_STATE"}
+
+
+class TAError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("elem_bytes", C.c_int32), ("block_tokens", C.c_int32), ("layout", C.c_int32),
+                ("n_replicas", C.c_int32), ("replicas_here", C.c_int32), ("first_replica", C.c_int32),
+                ("max_programs", C.c_int32), ("max_blocks_per_program", C.c_int32),
+                ("max_trace_turns", C.c_int32), ("hbm_blocks", C.c_int64), ("host_blocks", C.c_int64),
+                ("delta_t_ms", C.c_int64), ("decay_unit_ms", C.c_int64),
+                ("lambda_max_q16", C.c_uint32), ("lambda_min_q16", C.c_uint32),
+                ("decay_q32", C.c_uint64 * 64), ("decode_tok_per_s", C.c_int32),
+                ("compact_every", C.c_int32), ("flags", C.c_uint32), ("reserved", C.c_int32)]
+
+
+class Buffers(C.Structure):
+    _fields_ = [("hbm_pool", C.c_void_p * MAXR), ("host_pool", C.c_void_p * MAXR),
+                ("dev_workspace", C.c_void_p), ("host_workspace", C.c_void_p)]
+
+
+class Event(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("pid", C.c_uint32), ("uid", C.c_uint32),
+                ("tokens", C.c_uint32), ("t_ms", C.c_int64)]
+
+
+DECISION_DTYPE = np.dtype([("kind", "<u4"), ("pid", "<u4"), ("src", "<i4"), ("dst", "<i4"),
+                           ("blocks", "<u4"), ("to_host", "<u4"), ("dropped", "<u4"),
+                           ("hit_tok", "<u4"), ("peer_tok", "<u4"), ("host_tok", "<u4"),
+                           ("miss_tok", "<u4"), ("new_tok", "<u4")])
+assert DECISION_DTYPE.itemsize == 48
+
+STAT_KEYS = ("ticks", "arrivals", "stops", "pauses", "restores", "oversized_skips", "shortfalls",
+             "evict_blocks", "evict_to_host", "evict_dropped", "fetch_blocks", "p2p_blocks",
+             "h2d_blocks", "recompute_blocks", "new_blocks", "compact_blocks", "stalls",
+             "hit_tok", "peer_tok", "host_tok", "miss_tok", "new_tok", "fill_tok",
+             "imbalance_max_blocks", "imbalance_last_blocks")
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in STAT_KEYS] + [
+        ("L", C.c_uint64 * MAXR), ("hbm_used", C.c_uint64 * MAXR), ("host_used", C.c_uint64 * MAXR),
+        ("block_bytes", C.c_uint64)]
+
+
+class TraceView(C.Structure):
+    _fields_ = [("n_slots", C.c_int32), ("n_initial", C.c_int32)] + [
+        (k, C.POINTER(C.c_uint32)) for k in ("uid", "p0", "turn_off", "g", "d_ms", "o")]
+
+
+_VIEW_FIELDS = [
+    ("uid", C.c_uint32), ("c", C.c_uint32), ("c_kv", C.c_uint32), ("paused_since", C.c_uint32),
+    ("step_count", C.c_uint32), ("turn", C.c_uint32), ("gen_done", C.c_uint32),
+    ("status", C.c_uint8), ("phase", C.c_uint8), ("satisfied", C.c_uint8),
+    ("placement", C.c_int8), ("home", C.c_int8),
+    ("acting_since", C.c_int64), ("tool_return", C.c_int64),
+    ("loc", C.c_uint32), ("hbm_free", C.c_uint32), ("host_free", C.c_uint32),
+    ("owner_hbm", C.c_uint32), ("owner_host", C.c_uint32), ("L", C.c_uint64),
+    ("nb", C.c_uint32), ("n_hbm", C.c_uint32), ("n_host", C.c_uint32), ("prefix_hbm", C.c_uint32),
+    ("contrib", C.c_uint32), ("scalars", C.c_int64)]
+
+
+class StateView(C.Structure):
+    _fields_ = [(n, C.POINTER(t)) for n, t in _VIEW_FIELDS]
+
+
+_lib = None
+
+
+def lib():
+    """Load libta.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2602_13692_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
+        sig = {
+            "ta_workspace_bytes": [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)],
+            "ta_block_bytes": [vp, C.POINTER(C.c_size_t)],
+            "ta_init_pool": [vp, vp, vp, vp, C.POINTER(vp)],
+            "ta_load_trace": [vp, vp],
+            "ta_sched_step": [vp, i64, vp, i32, vp, i32, C.POINTER(i32)],
+            "ta_pause": [vp, u32, u32, vp, i32, C.POINTER(i32)],
+            "ta_resume": [vp, u32, i32, vp, i32, C.POINTER(i32)],
+            "ta_migrate": [vp, u32, i32, vp, i32, C.POINTER(i32)],
+            "ta_stats": [vp, vp],
+            "ta_phase_times": [vp, C.POINTER(C.c_float), i32],
+            "ta_verify_content": [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
+            "ta_debug_state": [vp, i32, vp],
+            "ta_export_pool_handle": [vp, vp],
+            "ta_import_peer_pool": [vp, i32, vp],
+            "ta_destroy": [vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.ta_last_error.argtypes = [vp]
+        L.ta_last_error.restype = C.c_char_p
+        L.ta_abi_version.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
+            "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
+            "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
+            "ta_last_error", "ta_abi_version")
+
+
+def decay_q32(x: int) -> list:
+    """F[k] = floor(2^32 * x^-k) (eq. 7 time decay; f(t) = x^-t,
+    PAPER.md:458), by repeated floor division (floor(floor(a/x)/x) = floor(a/x^2))."""
+    F = [1 << 32]
+    for _ in range(63):
+        F.append(F[-1] // x)
+    return F
+
+
+def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = True, fill: bool = True,
+                flags: int = 0, replicas_here: int | None = None, first_replica: int = 0) -> Config:
+    from tracegen import KV_SHAPES   # parameters only
+    kv = KV_SHAPES[cfg.get("kv", "toy")] if isinstance(cfg.get("kv", "toy"), str) else cfg["kv"]
+    c = Config()
+    c.n_layers, c.n_kv_heads, c.head_dim, c.elem_bytes = (kv["n_layers"], kv["n_kv_heads"],
+                                                          kv["head_dim"], kv.get("elem_bytes", 2))
+    c.block_tokens = cfg["block_tokens"]
+    c.layout = cfg.get("layout", 0)
+    c.n_replicas = cfg["n_replicas"]
+    c.replicas_here = cfg["n_replicas"] if replicas_here is None else replicas_here
+    c.first_replica = first_replica
+    c.max_programs = n_programs
+    c.max_blocks_per_program = -(-cfg["max_ctx"] // cfg["block_tokens"])
+    c.max_trace_turns = max(1, max_turns)
+    c.hbm_blocks = cfg["hbm_blocks"]
+    c.host_blocks = cfg["host_blocks"]
+    c.delta_t_ms = cfg["delta_t_ms"]
+    c.decay_unit_ms = cfg["decay_unit_ms"]
+    c.lambda_max_q16 = cfg["lambda_max_q16"]
+    c.lambda_min_q16 = cfg["lambda_min_q16"]
+    for k, v in enumerate(decay_q32(cfg["decay_x"])):
+        c.decay_q32[k] = v
+    c.decode_tok_per_s = cfg["decode_tok_per_s"]
+    c.compact_every = cfg.get("compact_every", 0)
+    c.flags = flags | (F_TRACE_MODE if trace_mode else 0) | (F_FILL if fill else 0)
+    return c
+
+
+def _u32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+class Pool:
+    """One libta context plus the torch-owned buffers it runs on."""
+
+    def __init__(self, cfg: dict, n_programs: int, max_turns: int = 1, trace_mode: bool = True,
+                 fill: bool = True, flags: int = 0, device: int = 0, host_blocks: int | None = None,
+                 replicas_here: int | None = None, first_replica: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libta needs a CUDA device (no CPU fallback)")
+        L = lib()
+        self.torch = torch
+        self.cfg = dict(cfg)
+        if host_blocks is not None:
+            self.cfg["host_blocks"] = host_blocks
+        self.device = torch.device("cuda", device)
+        self.c = make_config(self.cfg, n_programs, max_turns, trace_mode, fill, flags,
+                             replicas_here, first_replica)
+        dev_b, host_b, blk = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._chk(L.ta_workspace_bytes(C.byref(self.c), C.byref(dev_b), C.byref(host_b)), "workspace")
+        L.ta_block_bytes(C.byref(self.c), C.byref(blk))
+        self.block_bytes = blk.value
+        self.N = n_programs
+        self.R = self.c.n_replicas
+        self.MAXB = self.c.max_blocks_per_program
+        self.NB, self.NH = self.c.hbm_blocks, self.c.host_blocks
+        self.first, self.here = self.c.first_replica, self.c.replicas_here
+        self.dev_ws = torch.empty(dev_b.value, dtype=torch.uint8, device=self.device)
+        self.host_ws = torch.empty(host_b.value, dtype=torch.uint8, pin_memory=True)
+        self.hbm = {}
+        self.host = {}
+        b = Buffers()
+        for r in range(self.first, self.first + self.here):
+            self.hbm[r] = torch.empty(self.NB * self.block_bytes, dtype=torch.uint8, device=self.device)
+            b.hbm_pool[r] = self.hbm[r].data_ptr()
+            if self.NH > 0:
+                self.host[r] = torch.empty(self.NH * self.block_bytes, dtype=torch.uint8, pin_memory=True)
+                b.host_pool[r] = self.host[r].data_ptr()
+        b.dev_workspace = self.dev_ws.data_ptr()
+        b.host_workspace = self.host_ws.data_ptr()
+        self.buffers = b
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.ctx = C.c_void_p()
+        with torch.cuda.device(self.device):
+            st = L.ta_init_pool(C.byref(self.c), C.byref(b), C.c_void_p(self.stream.cuda_stream), None,
+                                C.byref(self.ctx))
+        if st != TA_OK:
+            raise TAError(st, "ta_init_pool failed")
+        self.dec_buf = np.zeros(4 * n_programs + self.R + 64, dtype=DECISION_DTYPE)
+
+    # ------------------------------------------------------------------ helpers
+    def _chk(self, st, what):
+        if st != TA_OK:
+            msg = lib().ta_last_error(self.ctx).decode() if getattr(self, "ctx", None) else ""
+            raise TAError(st, f"{what}: {msg}")
+
+    def close(self):
+        if getattr(self, "ctx", None) and self.ctx.value:
+            lib().ta_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ ABI calls
+    def load_trace(self, tr):
+        self._trace_arrays = [np.ascontiguousarray(a, dtype=np.uint32)
+                              for a in (tr.uid, tr.p0, tr.turn_off, tr.g, tr.d_ms, tr.o)]
+        v = TraceView()
+        v.n_slots = tr.n_slots
+        v.n_initial = tr.n_initial
+        for name, a in zip(("uid", "p0", "turn_off", "g", "d_ms", "o"), self._trace_arrays):
+            setattr(v, name, _u32p(a))
+        self._chk(lib().ta_load_trace(self.ctx, C.byref(v)), "ta_load_trace")
+
+    def step(self, now_ms: int = -1, events=None, decisions: bool = True, raise_on_error=True):
+        """One ta_sched_step.  Returns (status, decisions ndarray or None)."""
+        n_ev = 0
+        evp = None
+        if events:
+            arr = (Event * len(events))()
+            for i, e in enumerate(events):
+                arr[i].kind, arr[i].pid, arr[i].uid, arr[i].tokens, arr[i].t_ms = e
+            evp, n_ev = arr, len(events)
+        n_out = C.c_int32(0)
+        if decisions:
+            st = lib().ta_sched_step(self.ctx, now_ms, evp, n_ev, self.dec_buf.ctypes.data,
+                                     len(self.dec_buf), C.byref(n_out))
+        else:
+            st = lib().ta_sched_step(self.ctx, now_ms, evp, n_ev, None, 0, None)
+        if st not in (TA_OK,) and raise_on_error and st in (TA_E_CUDA, TA_E_PEER, TA_E_INVAL, TA_E_STATE):
+            self._chk(st, "ta_sched_step")
+        if not decisions or st != TA_OK:
+            return st, None
+        return st, self.dec_buf[:n_out.value].copy()
+
+    def _verb(self, fn, *args):
+        n_out = C.c_int32(0)
+        st = fn(self.ctx, *args, self.dec_buf.ctypes.data, len(self.dec_buf), C.byref(n_out))
+        if st in (TA_E_CUDA, TA_E_PEER):
+            self._chk(st, fn.__name__)
+        return st, (self.dec_buf[:n_out.value].copy() if st == TA_OK else None)
+
+    def pause(self, pid, mode=0):
+        return self._verb(lib().ta_pause, pid, mode)
+
+    def resume(self, pid, replica=-1):
+        return self._verb(lib().ta_resume, pid, replica)
+
+    def migrate(self, pid, dst):
+        return self._verb(lib().ta_migrate, pid, dst)
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._chk(lib().ta_stats(self.ctx, C.byref(s)), "ta_stats")
+        out = {k: getattr(s, k) for k in STAT_KEYS}
+        out["L"] = list(s.L[:self.R])
+        out["hbm_used"] = list(s.hbm_used[:self.R])
+        out["host_used"] = list(s.host_used[:self.R])
+        out["block_bytes"] = s.block_bytes
+        return out
+
+    def phase_times(self):
+        a = (C.c_float * 9)()
+        self._chk(lib().ta_phase_times(self.ctx, a, 9), "ta_phase_times")
+        return list(a)
+
+    def verify_content(self):
+        bad, seen = C.c_uint64(), C.c_uint64()
+        self._chk(lib().ta_verify_content(self.ctx, C.byref(bad), C.byref(seen)), "ta_verify_content")
+        return bad.value, seen.value
+
+    def _view_arrays(self):
+        N, R, NB, NH, MAXB = self.N, self.R, self.NB, self.NH, self.MAXB
+        NBW, NHW = -(-NB // 32), -(-NH // 32)
+        shapes = dict(uid=N, c=N, c_kv=N, paused_since=N, step_count=N, turn=N, gen_done=N, status=N,
+                      phase=N, satisfied=N, placement=N, home=N, acting_since=N, tool_return=N,
+                      loc=N * MAXB, hbm_free=R * NBW, host_free=max(1, R * NHW), owner_hbm=R * NB,
+                      owner_host=max(1, R * NH), L=R, nb=N, n_hbm=N, n_host=N, prefix_hbm=N, contrib=N,
+                      scalars=4)
+        npt = {C.c_uint32: np.uint32, C.c_uint8: np.uint8, C.c_int8: np.int8, C.c_int64: np.int64,
+               C.c_uint64: np.uint64}
+        return {n: np.zeros(shapes[n], dtype=npt[t]) for n, t in _VIEW_FIELDS}
+
+    def debug_download(self) -> dict:
+        arrs = self._view_arrays()
+        v = StateView()
+        for n, t in _VIEW_FIELDS:
+            setattr(v, n, arrs[n].ctypes.data_as(C.POINTER(t)))
+        self._chk(lib().ta_debug_state(self.ctx, 0, C.byref(v)), "ta_debug_state")
+        arrs["loc"] = arrs["loc"].reshape(self.N, self.MAXB)
+        return arrs
+
+    def debug_upload(self, arrs: dict):
+        v = StateView()
+        keep = {}
+        for n, t in _VIEW_FIELDS:
+            if n in ("nb", "n_hbm", "n_host", "prefix_hbm", "contrib") or n not in arrs:
+                continue
+            a = np.ascontiguousarray(arrs[n]).ravel()
+            keep[n] = a
+            setattr(v, n, a.ctypes.data_as(C.POINTER(t)))
+        self._chk(lib().ta_debug_state(self.ctx, 1, C.byref(v)), "ta_debug_state upload")
+
+    def export_handle(self) -> bytes:
+        h = (C.c_char * 64)()
+        self._chk(lib().ta_export_pool_handle(self.ctx, h), "ta_export_pool_handle")
+        return bytes(h)
+
+    def import_peer(self, replica: int, handle: bytes):
+        h = (C.c_char * 64).from_buffer_copy(handle)
+        self._chk(lib().ta_import_peer_pool(self.ctx, replica, h), "ta_import_peer_pool")
+
+    def read_block(self, r: int, tier: str, idx: int) -> np.ndarray:
+        """Bytes of one KV block as uint64 words, shaped [2L, bt, H, D/4] (test aid)."""
+        import torch
+        c = self.c
+        nseg = 2 * c.n_layers
+        seg = self.block_bytes // nseg
+        nblk = self.NB if tier == "hbm" else self.NH
+        buf = self.hbm[r] if tier == "hbm" else self.host[r]
+        self.torch.cuda.synchronize(self.device)
+        if c.layout == 0:
+            v = buf.view(nseg, nblk, seg)[:, idx, :]
+        else:
+            v = buf.view(nblk, nseg, seg)[idx]
+        a = v.contiguous().cpu().numpy().view(np.uint64)
+        return a.reshape(nseg, c.block_tokens, c.n_kv_heads, c.head_dim // 4)

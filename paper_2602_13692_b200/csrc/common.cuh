@@ -1,0 +1,346 @@
+// common.cuh — device state layout and CTA-level primitives for libta (sm_100a).
+//
+// Control plane is replicated: every process holds the program table, block
+// tables, bitmaps and owner maps of ALL replicas and computes every decision;
+// only the copy kernels are restricted to the replicas whose pools it holds.
+// Everything is integer arithmetic with total orders ending in the slot index,
+// so results are bit-identical to the CPU oracle.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ta.h"
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef int32_t i32;
+typedef uint8_t u8;
+typedef int8_t i8;
+typedef unsigned long long ull;
+
+#define LOC_NONE 0xFFFFFFFFu
+#define LOC_HOST 0x80000000u
+#define FULL_MASK 0xFFFFFFFFu
+#define CTA 1024          // threads of the single-CTA planner kernels
+#define NWARP (CTA / 32)
+
+enum StatIdx {
+  ST_TICKS = 0, ST_ARRIVALS, ST_STOPS, ST_PAUSES, ST_RESTORES, ST_OVERSIZED, ST_SHORTFALLS,
+  ST_EVICT_BLOCKS, ST_EVICT_TO_HOST, ST_EVICT_DROPPED, ST_FETCH_BLOCKS, ST_P2P, ST_H2D,
+  ST_RECOMPUTE, ST_NEW_BLOCKS, ST_COMPACT, ST_STALLS, ST_HIT, ST_PEER, ST_HOST, ST_MISS,
+  ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST, ST_N
+};
+
+enum MoveKind { MV_P2P = 2, MV_H2D = 3 };
+
+struct Ctr {                 // device-resident scalars of the context
+  i64 tick;                  // k
+  i64 next_arrival;          // lowest UNARRIVED slot (arrivals are a suffix)
+  i64 T;                     // time of the current tick (ms)
+  i64 now_ms;                // API mode: time passed by the host
+  u32 stops;                 // releases this tick
+  u32 restore_cnt;           // RESTORE decisions this tick
+  u32 n_dec;                 // decisions assembled this tick
+  u32 n_arr;                 // arrivals this tick
+  i32 err;                   // API-mode event validation status
+  i32 n_events;              // API-mode events this tick
+  u32 verb_pid;              // single-program materialize (verbs)
+  i32 verb_replica;
+  i32 verb_ok;
+  u32 pad[5];
+};
+
+struct EvDesc { u32 src; u32 dst; };                     // HBM block -> host slot (replica r)
+struct FeDesc { u32 kind; u32 src_r; u32 src; u32 dst; };  // P2P / H2D into HBM block dst
+struct FillDesc { u32 idx; u32 uid; u32 t0; u32 t1; u32 j; u32 pad; };
+struct CpDesc { u32 src; u32 dst; };
+
+struct Dev {
+  // ---- configuration ----
+  int N, MAXB, MAXBP, R, bt, nL, Hkv, D, layout;
+  i64 NB, NH;
+  int NBW, NHW;
+  i64 dt, unit;
+  int rate;
+  u32 flags;
+  int compact_every;
+  i64 seg_bytes, block_bytes;
+  int first_local, n_local;
+  int api_mode;
+  i64 cap_max[TA_MAX_REPLICAS], cap_min[TA_MAX_REPLICAS];
+  ull F[64];
+  char* hbm[TA_MAX_REPLICAS];      // device-addressable HBM pool per replica (NULL if not here)
+  char* host[TA_MAX_REPLICAS];     // device alias of the pinned host tier (local replicas)
+  // ---- program table (SoA, N slots) ----
+  u32 *uid, *c, *c_kv, *paused_since, *step_count, *turn, *gen_done;
+  u8 *status, *phase, *satisfied;
+  i8 *placement, *home;
+  i64 *acting_since, *tool_return;
+  u32* loc;                        // [N][MAXBP]
+  // ---- per-tick derived values ----
+  u32 *nb, *n_hbm, *n_host, *prefix_hbm, *contrib;
+  u8* released;                    // released during this tick's ingest
+  u8* sat_new;                     // 1 + replica that satisfied the program this tick
+  u8* evs;                         // [3N] API-mode validation scratch (kept zero)
+  // ---- trace scripts ----
+  int n_slots, n_initial;
+  u32 *t_uid, *t_p0, *t_off, *t_g, *t_d, *t_o;
+  // ---- replica state (all replicas) ----
+  u32 *hbm_free, *host_free;       // [R][NBW], [R][NHW]; bit set = free
+  u32 *owner_hbm, *owner_host;     // [R][NB], [R][NH]: pid * MAXB + j
+  ull* L;                          // [R]
+  Ctr* ctr;
+  ull* stats;                      // [ST_N]
+  // ---- scratch ----
+  u64 *ska, *skb;                  // sort keys  [R+1][N]
+  u32 *sva, *svb;                  // sort values[R+1][N]
+  u32* pause_list;                 // [R][N]
+  u32* pause_cnt;                  // [R]
+  u32 *restore_pid, *restore_dst;  // [N]
+  u32 *f_pid, *f_cum;              // [R][N]  REASONING list per replica, inclusive need prefix
+  u32 *f_cnt, *s_cnt;              // [R]
+  ta_decision* dec_fs;             // [R][N]  FETCH/STALL record per F entry (kind 0 = none)
+  ta_decision* dec_ev;             // [R][N]  EVICT records (victim order)
+  u32* ev_cnt;                     // [R]     victims
+  u32* e_pid;                      // [R][N]  eviction order (sorted candidates)
+  u32* e_cum;                      // [R][N]  inclusive n_hbm prefix in eviction order
+  EvDesc* evd; u32* evd_cnt;       // [R][NB]
+  FeDesc* fed; u32* fed_cnt;       // [R][NB]
+  FillDesc* fld; u32* fld_cnt;     // [R][NB]
+  u32* dfh; u32* dfh_cnt;          // deferred HBM frees  [R][NB]: (replica << 27) | idx
+  u32* dfs; u32* dfs_cnt;          // deferred host frees [R][NB]
+  CpDesc* cpd; u32* cpd_cnt;       // [R][NB/2+1]
+  ta_decision* dec_out;            // host-mapped decision buffer (canonical order)
+  u32* dec_out_cnt;                // host-mapped count
+  u32 dec_cap;
+  ull* verify;                     // [2] mismatches, checked
+  ta_event* events;                // [kMaxEvents] API-mode event batch
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ u32 ceil_div_u32(u32 a, u32 b) { return (a + b - 1) / b; }
+__device__ __forceinline__ bool is_hbm(u32 e) { return e != LOC_NONE && !(e & LOC_HOST); }
+__device__ __forceinline__ bool is_host(u32 e) { return e != LOC_NONE && (e & LOC_HOST); }
+__device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Eq. 7 contribution in blocks: nb for tau=R, floor(nb * F[k] / 2^32) for tau=A (readings A4, A5).
+__device__ __forceinline__ u32 contrib_of(const Dev& d, u32 nbv, u8 ph, i64 acting_since, i64 T) {
+  if (ph == TA_PHASE_R) return nbv;
+  i64 el = T - acting_since;
+  i64 k = el < 0 ? 0 : el / d.unit;
+  if (k > 63) k = 63;
+  return (u32)(((ull)nbv * d.F[k]) >> 32);
+}
+
+// Closed-loop arrivals of this tick (trace mode): n_initial at tick 0, then one per
+// release, taking the lowest UNARRIVED slots (reading A12).
+__device__ __forceinline__ i64 trace_arrivals(const Dev& d) {
+  i64 n = (d.ctr->tick == 0 ? (i64)d.n_initial : 0) + (i64)d.ctr->stops;
+  i64 room = (i64)d.n_slots - d.ctr->next_arrival;
+  return n < room ? n : room;
+}
+
+// S_restore order (reading A8): R first, nb up, paused_since up; ties by slot
+// via sort stability on slot-ordered input.
+__device__ __forceinline__ u64 restore_key(u8 ph, u32 nbv, u32 ps) {
+  return ((u64)(ph == TA_PHASE_A) << 63) | ((u64)nbv << 32) | (u64)ps;
+}
+// S_pause order (reading A7): A first, nb up, acting_since DOWN; ties by slot.
+#define AS_MAX ((1ull << 40) - 1)
+__device__ __forceinline__ u64 pause_key(u8 ph, u32 nbv, i64 as) {
+  if (ph == TA_PHASE_A) return ((u64)nbv << 40) | (AS_MAX - (u64)as);
+  return (1ull << 63) | ((u64)nbv << 40);
+}
+
+// ------------------------------------------------------------------ warp / CTA scans
+__device__ __forceinline__ u32 warp_incl_scan(u32 v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 t = __shfl_up_sync(FULL_MASK, v, o);
+    if (lane_id() >= (u32)o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ ull warp_sum_u64(ull v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+// Exclusive scan of one u32 per thread across the CTA (blockDim.x == CTA).
+// s_tmp: >= NWARP+1 u32 of shared memory.  Returns exclusive prefix; *total = sum.
+__device__ u32 cta_excl_scan(u32 v, u32* s_tmp, u32* total) {
+  u32 inc = warp_incl_scan(v);
+  int w = threadIdx.x >> 5;
+  if (lane_id() == 31) s_tmp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    u32 x = lane_id() < NWARP ? s_tmp[lane_id()] : 0;
+    u32 xi = warp_incl_scan(x);
+    if (lane_id() < NWARP) s_tmp[lane_id()] = xi - x;
+    if (lane_id() == NWARP - 1) s_tmp[NWARP] = xi;
+  }
+  __syncthreads();
+  u32 r = s_tmp[w] + inc - v;
+  *total = s_tmp[NWARP];
+  __syncthreads();
+  return r;
+}
+
+template <typename T, typename Op>
+__device__ T cta_reduce(T v, T* s_tmp, Op op, T ident) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(FULL_MASK, v, o));
+  int w = threadIdx.x >> 5;
+  if (lane_id() == 0) s_tmp[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    T x = lane_id() < NWARP ? s_tmp[lane_id()] : ident;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = op(x, __shfl_xor_sync(FULL_MASK, x, o));
+    if (lane_id() == 0) s_tmp[0] = x;
+  }
+  __syncthreads();
+  T r = s_tmp[0];
+  __syncthreads();
+  return r;
+}
+
+// Ordered stream compaction over [0, n): every thread owns a contiguous chunk, so
+// emitted items keep slot order.  pred(i) -> bool; emit(pos, i).  Returns count.
+template <typename Pred, typename Emit>
+__device__ u32 cta_ordered_gather(int n, u32* s_tmp, Pred pred, Emit emit) {
+  int chunk = (n + CTA - 1) / CTA;
+  int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+  u32 cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += pred(i) ? 1u : 0u;
+  u32 total;
+  u32 pos = cta_excl_scan(cnt, s_tmp, &total);
+  for (int i = lo; i < hi; ++i)
+    if (pred(i)) emit(pos++, i);
+  __syncthreads();
+  return total;
+}
+
+// In-place inclusive scan of a global u32 array a[0..n) by one CTA.
+__device__ void cta_incl_scan_array(u32* a, int n, u32* s_tmp) {
+  int chunk = (n + CTA - 1) / CTA;
+  int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+  u32 s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  u32 total;
+  u32 run = cta_excl_scan(s, s_tmp, &total);
+  for (int i = lo; i < hi; ++i) { run += a[i]; a[i] = run; }
+  __syncthreads();
+}
+
+// First index i in [0, n) with a[i] > x for a non-decreasing array (n if none).
+__device__ __forceinline__ int upper_bound_u32(const u32* a, int n, u32 x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------ stable CTA radix sort
+// Sorts (key, val) pairs [0, n) ascending by key, stable.  8-bit digits; only the
+// digits in which keys differ are processed (vary = OR ^ AND over all keys).
+// Buffers a -> b -> a ...; returns 0 if the result is in (ka, va), 1 if in (kb, vb).
+// s_hist: NWARP * 256 u32 of shared memory; s_tmp: >= NWARP + 1 u32.
+__device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp) {
+  if (n <= 1) return 0;
+  // which digits vary
+  u64 o = 0, a = ~0ull;
+  for (int i = threadIdx.x; i < n; i += CTA) { u64 k = ka[i]; o |= k; a &= k; }
+  __shared__ u64 s_red[NWARP];
+  o = cta_reduce<u64>(o, s_red, [](u64 x, u64 y) { return x | y; }, 0ull);
+  a = cta_reduce<u64>(a, s_red, [](u64 x, u64 y) { return x & y; }, ~0ull);
+  u64 vary = o ^ a;
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  const int tile = (n + NWARP - 1) / NWARP;
+  const int lo = w * tile, hi = min(n, lo + tile);
+  int cur = 0;
+  for (int shift = 0; shift < 64; shift += 8) {
+    if (((vary >> shift) & 0xFF) == 0) continue;
+    u64* kin = cur ? kb : ka;
+    u32* vin = cur ? vb : va;
+    u64* kout = cur ? ka : kb;
+    u32* vout = cur ? va : vb;
+    for (int i = threadIdx.x; i < NWARP * 256; i += CTA) s_hist[i] = 0;
+    __syncthreads();
+    for (int base = lo; base < hi; base += 32) {
+      int i = base + lane;
+      bool v = i < hi;
+      u32 dg = v ? (u32)((kin[i] >> shift) & 0xFF) : 256u + lane;
+      u32 peers = __match_any_sync(FULL_MASK, dg);
+      if (v && (__ffs(peers) - 1) == lane) s_hist[dg * NWARP + w] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive scan over (digit, warp) order: 8 consecutive entries per thread
+    {
+      u32 loc8[8];
+      u32 s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { loc8[q] = s_hist[threadIdx.x * 8 + q]; s += loc8[q]; }
+      u32 total;
+      u32 run = cta_excl_scan(s, s_tmp, &total);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { s_hist[threadIdx.x * 8 + q] = run; run += loc8[q]; }
+    }
+    __syncthreads();
+    for (int base = lo; base < hi; base += 32) {
+      int i = base + lane;
+      bool v = i < hi;
+      u64 k = v ? kin[i] : 0;
+      u32 dg = v ? (u32)((k >> shift) & 0xFF) : 256u + lane;
+      u32 peers = __match_any_sync(FULL_MASK, dg);
+      u32 rank = __popc(peers & lanemask_lt());
+      if (v) {
+        u32 pos = s_hist[dg * NWARP + w] + rank;
+        kout[pos] = k;
+        vout[pos] = vin[i];
+      }
+      __syncwarp();
+      if (v && (__ffs(peers) - 1) == lane) s_hist[dg * NWARP + w] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  return cur;
+}
+
+// ------------------------------------------------------------------ bitmap rank / select
+// s_pre[w] = number of set bits in words [0, w) for w in [0, nw]; built by one CTA.
+__device__ void cta_bitmap_prefix(const u32* words, int nw, u32* s_pre, u32* s_tmp) {
+  int chunk = (nw + CTA - 1) / CTA;
+  int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
+  u32 s = 0;
+  for (int i = lo; i < hi; ++i) s += __popc(words[i]);
+  u32 total;
+  u32 run = cta_excl_scan(s, s_tmp, &total);
+  for (int i = lo; i < hi; ++i) { s_pre[i] = run; run += __popc(words[i]); }
+  if (threadIdx.x == 0) s_pre[nw] = total;
+  __syncthreads();
+}
+// Index of the q-th (0-based) set bit, given prefix counts s_pre (q < s_pre[nw]).
+__device__ __forceinline__ u32 bitmap_select(const u32* words, const u32* s_pre, int nw, u32 q) {
+  int lo = 0, hi = nw;                    // last word w with s_pre[w] <= q
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (s_pre[mid] <= q) lo = mid; else hi = mid;
+  }
+  u32 w = words[lo];
+  u32 k = q - s_pre[lo];                  // k-th set bit inside w
+  u32 pos = __fns(w, 0, (int)k + 1);
+  return (u32)lo * 32u + pos;
+}

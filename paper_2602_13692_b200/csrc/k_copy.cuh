@@ -1,0 +1,173 @@
+// k_copy.cuh — step 6 (KV block movement) and the engine stand-in (content fill).
+//
+// A KV block is 2L segments of seg_bytes = bt*Hkv*D*2 bytes.  Layer-major pools
+// (layout 0, vLLM-like) place segment s = 2l+kv of block b at base + (s*NB + b)*seg;
+// block-major pools (layout 1) at base + (b*2L + s)*seg.  Every copy kernel is
+// driven by a device-resident descriptor list whose length is read on the device,
+// so the whole tick is one CUDA-graph replay with no host round trip.
+#pragma once
+#include "common.cuh"
+
+__device__ __forceinline__ char* seg_addr(char* base, int layout, i64 nblk, i64 seg, int nseg, u32 b, int s) {
+  return layout == 0 ? base + ((i64)s * nblk + b) * seg : base + ((i64)b * nseg + s) * seg;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// CTA-wide copy of n16 16-byte words: 8 independent 128-bit loads in flight per thread.
+__device__ __forceinline__ void cta_copy16(const uint4* __restrict__ src, uint4* __restrict__ dst, i64 n16) {
+  const int T = blockDim.x;
+  i64 i = threadIdx.x;
+  for (; i + 7 * (i64)T < n16; i += 8 * (i64)T) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ld_stream(src + i + k * T);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) st_stream(dst + i + k * T, v[k]);
+  }
+  for (; i < n16; i += T) st_stream(dst + i, ld_stream(src + i));
+}
+
+// Map a flat item index onto (local replica, entry, segment) given per-replica counts.
+__device__ __forceinline__ bool locate(const Dev& d, const u32* cnt, i64 item, int nseg, int* r, u32* e, int* s) {
+  for (int q = 0; q < d.n_local; ++q) {
+    int rr = d.first_local + q;
+    i64 n = (i64)cnt[rr] * nseg;
+    if (item < n) { *r = rr; *e = (u32)(item / nseg); *s = (int)(item % nseg); return true; }
+    item -= n;
+  }
+  return false;
+}
+__device__ __forceinline__ i64 local_items(const Dev& d, const u32* cnt, int nseg) {
+  i64 n = 0;
+  for (int q = 0; q < d.n_local; ++q) n += (i64)cnt[d.first_local + q] * nseg;
+  return n;
+}
+
+// D2H evictions: HBM block of replica r -> slot of r's pinned host tier (PCIe).
+__global__ void __launch_bounds__(256) k_copy_evict(Dev d) {
+  const int nseg = 2 * d.nL;
+  const i64 items = local_items(d, d.evd_cnt, nseg);
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int r, s; u32 e;
+    locate(d, d.evd_cnt, it, nseg, &r, &e, &s);
+    EvDesc x = d.evd[(size_t)r * d.NB + e];
+    const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
+    uint4* dst = (uint4*)seg_addr(d.host[r], d.layout, d.NH, d.seg_bytes, nseg, x.dst, s);
+    cta_copy16(src, dst, d.seg_bytes >> 4);
+  }
+}
+
+// Fetches into the local replicas' HBM: P2P from a peer (or co-located) replica's
+// HBM over NVLink, or H2D from a host tier.
+__global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
+  const int nseg = 2 * d.nL;
+  const i64 items = local_items(d, d.fed_cnt, nseg);
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int r, s; u32 e;
+    locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
+    FeDesc x = d.fed[(size_t)r * d.NB + e];
+    const char* sbase = x.kind == MV_P2P ? d.hbm[x.src_r] : d.host[x.src_r];
+    i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
+    if (sbase == nullptr) continue;      // executed by the source's owner (multi-process push)
+    const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
+    uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
+    cta_copy16(src, dst, d.seg_bytes >> 4);
+  }
+}
+
+// Two-finger compaction moves inside one replica's HBM pool (D2D).
+__global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
+  const int nseg = 2 * d.nL;
+  const i64 items = local_items(d, d.cpd_cnt, nseg);
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int r, s; u32 e;
+    locate(d, d.cpd_cnt, it, nseg, &r, &e, &s);
+    CpDesc x = d.cpd[(size_t)r * (d.NB / 2 + 1) + e];
+    const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
+    uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
+    cta_copy16(src, dst, d.seg_bytes >> 4);
+  }
+}
+
+// ---- KV content closed form: word(uid, t, l, kv, h, w) =
+// splitmix64((uid << 40) + (((t*L + l)*2 + kv)*Hkv + h)*(D/4) + w)
+__device__ __forceinline__ ull splitmix64(ull x) {
+  ull z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Engine stand-in: write the content of tokens [t0, t1) of block j into HBM block idx.
+__global__ void __launch_bounds__(256) k_fill(Dev d) {
+  const int nseg = 2 * d.nL;
+  const i64 items = local_items(d, d.fld_cnt, nseg);
+  const u32 wtok = (u32)(d.Hkv * d.D / 4);            // 8-byte words per (token, layer, kv)
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int r, s; u32 e;
+    locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
+    FillDesc x = d.fld[(size_t)r * d.NB + e];
+    ull* seg = (ull*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.idx, s);
+    const u32 l = (u32)s >> 1, kv = (u32)s & 1;
+    const u32 slot0 = x.t0 - x.j * (u32)d.bt;
+    const u32 nw = (x.t1 - x.t0) * wtok;
+    const ull ubase = (ull)x.uid << 40;
+    for (u32 q = threadIdx.x * 2; q < nw; q += blockDim.x * 2) {
+      u32 t = x.t0 + q / wtok, rem = q % wtok;        // wtok is even: q, q+1 share t
+      ull i = (((ull)t * d.nL + l) * 2 + kv) * wtok + rem;
+      ull a = splitmix64(ubase + i), b = splitmix64(ubase + i + 1);
+      uint4 v = make_uint4((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32));
+      *reinterpret_cast<uint4*>(seg + (size_t)slot0 * wtok + q) = v;
+    }
+  }
+}
+
+// Test aid: count words of every owned block (HBM and host tier of the local
+// replicas) that differ from the closed form, over valid token slots only.
+__global__ void __launch_bounds__(256) k_verify(Dev d, int tier) {
+  const int nseg = 2 * d.nL;
+  const u32 wtok = (u32)(d.Hkv * d.D / 4);
+  const i64 nblk = tier ? d.NH : d.NB;
+  const i64 items = (i64)d.n_local * nblk * nseg;
+  ull bad = 0, seen = 0;
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int q = (int)(it / (nblk * nseg));
+    i64 rem = it % (nblk * nseg);
+    u32 b = (u32)(rem / nseg);
+    int s = (int)(rem % nseg);
+    int r = d.first_local + q;
+    const u32* fw = tier ? d.host_free + (size_t)r * d.NHW : d.hbm_free + (size_t)r * d.NBW;
+    if (fw[b >> 5] & (1u << (b & 31))) continue;      // free
+    u32 o = tier ? d.owner_host[(size_t)r * d.NH + b] : d.owner_hbm[(size_t)r * d.NB + b];
+    u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
+    u32 t0 = j * (u32)d.bt, t1 = min(t0 + (u32)d.bt, d.c_kv[p]);
+    if (t1 <= t0) continue;
+    char* base = tier ? d.host[r] : d.hbm[r];
+    const ull* seg = (const ull*)seg_addr(base, d.layout, nblk, d.seg_bytes, nseg, b, s);
+    const u32 l = (u32)s >> 1, kv = (u32)s & 1;
+    const ull ubase = (ull)d.uid[p] << 40;
+    const u32 nw = (t1 - t0) * wtok;
+    for (u32 w = threadIdx.x; w < nw; w += blockDim.x) {
+      u32 t = t0 + w / wtok, rw = w % wtok;
+      ull i = (((ull)t * d.nL + l) * 2 + kv) * wtok + rw;
+      bad += seg[w] != splitmix64(ubase + i);
+      seen += 1;
+    }
+  }
+  bad = warp_sum_u64(bad);
+  seen = warp_sum_u64(seen);
+  if (lane_id() == 0) {
+    if (bad) atomicAdd(&d.verify[0], bad);
+    atomicAdd(&d.verify[1], seen);
+  }
+}

@@ -1,0 +1,182 @@
+// k_finalize.cuh — step 7: deferred frees, materialized-program updates, two-finger
+// compaction plan, statistics and canonical decision assembly.
+#pragma once
+#include "common.cuh"
+
+// Deferred frees (P2P sources and fetched host slots become free only after the
+// movement, reading A16) and the per-program results of step 5.7.
+__global__ void __launch_bounds__(256) k_finalize(Dev d, int verb) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  for (int r = 0; r < d.R; ++r) {
+    const u32 nh = d.dfh_cnt[r], ns = d.dfs_cnt[r];
+    const u32* fh = d.dfh + (size_t)r * d.NB;
+    const u32* fs = d.dfs + (size_t)r * d.NB;
+    for (u32 e = t; e < nh; e += stride) {
+      u32 x = fh[e], h = x >> 27, idx = x & ((1u << 27) - 1);
+      atomicOr(&d.hbm_free[(size_t)h * d.NBW + (idx >> 5)], 1u << (idx & 31));
+    }
+    for (u32 e = t; e < ns; e += stride) {
+      u32 x = fs[e], h = x >> 27, s = x & ((1u << 27) - 1);
+      atomicOr(&d.host_free[(size_t)h * d.NHW + (s >> 5)], 1u << (s & 31));
+    }
+  }
+  for (int p = t; p < d.N; p += stride) {
+    u8 s = d.sat_new[p];
+    if (s) {
+      d.satisfied[p] = 1;
+      d.home[p] = (i8)(s - 1);
+      d.c_kv[p] = d.c[p];
+      d.n_hbm[p] = d.nb[p];
+      d.sat_new[p] = 0;
+    } else if (!verb) {
+      d.satisfied[p] = 0;
+    }
+  }
+}
+
+// Two-finger compaction (reading A20), one CTA per replica: with U used blocks, the
+// m-th lowest free block below U receives the m-th highest used block (all moves
+// of the sequential two-finger loop, computed at once by rank/select).
+__global__ void __launch_bounds__(CTA, 1) k_compact_plan(Dev d) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  const int r = blockIdx.x;
+  if (d.compact_every <= 0 || (d.ctr->tick % d.compact_every) != 0) return;
+  u32* fw = d.hbm_free + (size_t)r * d.NBW;
+  const int nw = d.NBW;
+  u32* s_free = s_big;                  // [nw + 1]
+  u32* s_used = s_big + nw + 1;         // [nw + 1]
+  cta_bitmap_prefix(fw, nw, s_free, s_tmp);
+  const u32 U = (u32)d.NB - s_free[nw];
+  // used bitmap prefix (bits >= NB are neither free nor used)
+  {
+    int chunk = (nw + CTA - 1) / CTA;
+    int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
+    auto used_word = [&](int w) {
+      u32 valid = (w == nw - 1 && (d.NB & 31)) ? ((1u << (d.NB & 31)) - 1) : 0xFFFFFFFFu;
+      return ~fw[w] & valid;
+    };
+    u32 s = 0;
+    for (int w = lo; w < hi; ++w) s += __popc(used_word(w));
+    u32 total;
+    u32 run = cta_excl_scan(s, s_tmp, &total);
+    for (int w = lo; w < hi; ++w) { s_used[w] = run; run += __popc(used_word(w)); }
+    if (threadIdx.x == 0) s_used[nw] = total;
+    __syncthreads();
+  }
+  // K = free blocks below U
+  u32 K = 0;
+  if (U > 0) {
+    u32 wU = U >> 5, bU = U & 31;
+    K = s_free[wU] + (bU ? __popc(fw[wU] & ((1u << bU) - 1)) : 0);
+  }
+  CpDesc* cp = d.cpd + (size_t)r * (d.NB / 2 + 1);
+  for (u32 m = threadIdx.x; m < K; m += CTA) {
+    u32 dst = bitmap_select(fw, s_free, nw, m);
+    // (U-1-m)-th used block in ascending order = m-th highest used
+    u32 q = U - 1 - m;
+    int lo = 0, hi = nw;
+    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_used[mid] <= q) lo = mid; else hi = mid; }
+    u32 uw = ~fw[lo];
+    if (lo == nw - 1 && (d.NB & 31)) uw &= (1u << (d.NB & 31)) - 1;
+    u32 src = (u32)lo * 32u + __fns(uw, 0, (int)(q - s_used[lo]) + 1);
+    u32 o = d.owner_hbm[(size_t)r * d.NB + src];
+    u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
+    d.loc[(size_t)p * d.MAXBP + j] = dst;
+    d.owner_hbm[(size_t)r * d.NB + dst] = o;
+    cp[m] = CpDesc{src, dst};
+  }
+  __syncthreads();
+  for (u32 m = threadIdx.x; m < K; m += CTA) {
+    CpDesc c = cp[m];
+    atomicOr(&fw[c.src >> 5], 1u << (c.src & 31));
+    atomicAnd(&fw[c.dst >> 5], ~(1u << (c.dst & 31)));
+  }
+  if (threadIdx.x == 0) {
+    d.cpd_cnt[r] = K;
+    atomicAdd(&d.stats[ST_COMPACT], (ull)K);
+  }
+}
+
+// Canonical decision list (PAUSE by replica, RESTORE in queue order, EVICT by
+// replica, FETCH/STALL by replica in slot order, COMPACT by replica), written to
+// the host-mapped buffer; tick bookkeeping and occupancy statistics.
+__global__ void __launch_bounds__(CTA, 1) k_assemble(Dev d, int verb) {
+  __shared__ u32 s_tmp[NWARP + 1];
+  __shared__ ull s_red[NWARP];
+  const int N = d.N, R = d.R;
+  const u32 cap = d.dec_cap;
+  u32 pos = 0;                           // uniform across the CTA
+  auto put = [&](u32 at, const ta_decision& rec) { if (at < cap) d.dec_out[at] = rec; };
+  for (int r = 0; r < R; ++r) {          // PAUSE
+    u32 n = d.pause_cnt[r];
+    for (u32 i = threadIdx.x; i < n; i += CTA) {
+      ta_decision rec = {};
+      rec.kind = TA_D_PAUSE; rec.pid = d.pause_list[(size_t)r * N + i]; rec.src = r; rec.dst = -1;
+      put(pos + i, rec);
+    }
+    pos += n;
+  }
+  {                                      // RESTORE / MIGRATE
+    u32 n = d.ctr->restore_cnt;
+    for (u32 i = threadIdx.x; i < n; i += CTA) {
+      ta_decision rec = {};
+      u32 x = d.restore_dst[i];
+      rec.kind = (x >> 16) ? TA_D_MIGRATE : TA_D_RESTORE;
+      rec.pid = d.restore_pid[i];
+      rec.src = (int)((x >> 8) & 0xFF) - 1;
+      rec.dst = (int)(x & 0xFF);
+      put(pos + i, rec);
+    }
+    pos += n;
+  }
+  for (int r = 0; r < R; ++r) {          // EVICT
+    u32 n = d.ev_cnt[r];
+    for (u32 i = threadIdx.x; i < n; i += CTA) put(pos + i, d.dec_ev[(size_t)r * N + i]);
+    pos += n;
+  }
+  for (int r = 0; r < R; ++r) {          // FETCH / STALL (kind 0 = no decision)
+    const ta_decision* fs = d.dec_fs + (size_t)r * N;
+    u32 n = cta_ordered_gather((int)d.f_cnt[r], s_tmp,
+        [&](int i) { return fs[i].kind != 0; },
+        [&](u32 at, int i) { put(pos + at, fs[i]); });
+    pos += n;
+  }
+  for (int r = 0; r < R; ++r) {          // COMPACT
+    u32 n = d.cpd_cnt[r];
+    if (n) {
+      if (threadIdx.x == 0) {
+        ta_decision rec = {};
+        rec.kind = TA_D_COMPACT; rec.pid = 0xFFFFFFFFu; rec.src = r; rec.dst = r; rec.blocks = n;
+        put(pos, rec);
+      }
+      pos += 1;
+    }
+  }
+  // occupancy / imbalance (SPEC.md:151-157 at block granularity)
+  ull umax = 0, umin = ~0ull;
+  for (int r = 0; r < R; ++r) {
+    ull fr = 0;
+    for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(d.hbm_free[(size_t)r * d.NBW + w]);
+    fr = cta_reduce<ull>(fr, s_red, [](ull a, ull b) { return a + b; }, 0ull);
+    ull used = (ull)d.NB - fr;
+    umax = used > umax ? used : umax;
+    umin = used < umin ? used : umin;
+  }
+  if (threadIdx.x == 0) {
+    *d.dec_out_cnt = pos;
+    d.ctr->n_dec = pos;
+    if (!verb) {
+      ull imb = umax - umin;
+      d.stats[ST_IMB_LAST] = imb;
+      if (imb > d.stats[ST_IMB_MAX]) d.stats[ST_IMB_MAX] = imb;
+      i64 n_arr = d.api_mode ? (i64)d.ctr->n_arr : trace_arrivals(d);
+      d.stats[ST_ARRIVALS] += (ull)n_arr;
+      d.stats[ST_STOPS] += d.ctr->stops;
+      d.stats[ST_TICKS] += 1;
+      if (!d.api_mode) d.ctr->next_arrival += n_arr;
+      d.ctr->tick += 1;
+    }
+  }
+}

@@ -1,0 +1,289 @@
+// k_plan.cuh — step 5 (materialize): stall cut, program-aware eviction, lowest-free
+// allocation, sources, hit accounting, fill descriptors.  One CTA per replica.
+#pragma once
+#include "common.cuh"
+
+// need(p) on replica r = #{j < nb : loc[j] is not HBM on r}.  HBM entries of a
+// program always form the prefix [0, n_hbm) of its row (invariant I10: growth
+// appends, eviction is tail-first), so need = nb - n_hbm on the home replica.
+__device__ __forceinline__ u32 need_of(const Dev& d, u32 p, int r) {
+  return d.home[p] == r ? d.nb[p] - d.n_hbm[p] : d.nb[p];
+}
+
+// warp-aggregated add of a per-thread counter into a shared accumulator
+__device__ __forceinline__ void warp_add_shared(ull v, ull* s) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  if (lane_id() == 0 && v) atomicAdd(s, v);
+}
+
+enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_MISS, PC_NEWTOK,
+       PC_STALL, PC_N };
+
+__global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
+  __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
+  __shared__ u32 s_tmp[NWARP + 1];
+  __shared__ ull s_red[NWARP];
+  __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs
+  __shared__ ull s_pc[PC_N];
+  const int r = blockIdx.x;
+  const int N = d.N;
+  const u32 bt = (u32)d.bt;
+  const bool fill = (d.flags & TA_F_FILL) != 0;
+  if (verb && r != d.ctr->verb_replica) return;
+  if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
+  if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
+  u32* fp = d.f_pid + (size_t)r * N;
+  u32* fc = d.f_cum + (size_t)r * N;
+  // ---- 5.1 F_r: REASONING programs placed on r, slot order, with their need
+  u32 nF;
+  if (verb) {
+    if (threadIdx.x == 0) {
+      u32 p = d.ctr->verb_pid;
+      fp[0] = p;
+      fc[0] = need_of(d, p, r);
+    }
+    nF = 1;
+    __syncthreads();
+  } else {
+    nF = cta_ordered_gather(N, s_tmp,
+        [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r; },
+        [&](u32 pos, int i) { fp[pos] = (u32)i; fc[pos] = need_of(d, (u32)i, r); });
+    cta_incl_scan_array(fc, (int)nF, s_tmp);
+  }
+  // ---- free blocks on r and eviction supply
+  u32* hf = d.hbm_free + (size_t)r * d.NBW;
+  ull fr = 0, es = 0;
+  for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
+  for (int i = threadIdx.x; i < N; i += CTA) {
+    u8 s = d.status[i];
+    if (d.home[i] == r && (s == TA_PAUSED || s == TA_ACTING)) es += d.n_hbm[i];
+  }
+  auto add = [](ull a, ull b) { return a + b; };
+  fr = cta_reduce<ull>(fr, s_red, add, 0ull);
+  es = cta_reduce<ull>(es, s_red, add, 0ull);
+  const ull supply = fr + es;
+  // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
+  const u32 m = nF ? (u32)upper_bound_u32(fc, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
+  if (verb) {
+    if (m < nF) {                        // all-or-nothing: fail before any mutation
+      if (threadIdx.x == 0) d.ctr->verb_ok = 0;
+      return;
+    }
+    if (threadIdx.x == 0) d.ctr->verb_ok = 1;
+  }
+  const u32 tot = m ? fc[m - 1] : 0;
+  const u32 X = tot > fr ? (u32)(tot - fr) : 0;
+  // ---- 5.3 eviction: E_r ordered (group 0 PAUSED, reverse restore order; group 1
+  // ACTING placed elsewhere; group 2 ACTING placed on r; groups 1-2 by contrib),
+  // whole programs tail-first, last victim partially; host tier first, else drop.
+  if (X > 0) {
+    u64* ka = d.ska + (size_t)r * N;
+    u64* kb = d.skb + (size_t)r * N;
+    u32* va = d.sva + (size_t)r * N;
+    u32* vb = d.svb + (size_t)r * N;
+    u32 n0 = cta_ordered_gather(N, s_tmp,
+        [&](int ii) {
+          int i = N - 1 - ii;            // descending slot: ties in group 0 go slot-down
+          return d.home[i] == r && d.n_hbm[i] > 0 && d.status[i] == TA_PAUSED;
+        },
+        [&](u32 pos, int ii) {
+          int i = N - 1 - ii;
+          u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
+          ka[pos] = ((1ull << 56) - 1) - rk;
+          va[pos] = (u32)i;
+        });
+    u32 n12 = cta_ordered_gather(N, s_tmp,
+        [&](int i) { return d.home[i] == r && d.n_hbm[i] > 0 && d.status[i] == TA_ACTING; },
+        [&](u32 pos, int i) {
+          u64 g = d.placement[i] != r ? 1 : 2;
+          ka[n0 + pos] = (g << 62) | d.contrib[i];
+          va[n0 + pos] = (u32)i;
+        });
+    const u32 ne = n0 + n12;
+    int res = cta_radix_sort(ka, va, kb, vb, (int)ne, s_big, s_tmp);
+    const u32* sv = res ? vb : va;
+    u32* ep = d.e_pid + (size_t)r * N;
+    u32* ec = d.e_cum + (size_t)r * N;
+    for (u32 i = threadIdx.x; i < ne; i += CTA) { ep[i] = sv[i]; ec[i] = d.n_hbm[sv[i]]; }
+    __syncthreads();
+    cta_incl_scan_array(ec, (int)ne, s_tmp);
+    const u32 nv = (u32)upper_bound_u32(ec, (int)ne, X - 1) + 1;   // victims
+    const u32* sf = d.host_free + (size_t)r * d.NHW;
+    cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
+    const u32 hfree = s_big[d.NHW];
+    EvDesc* evd = d.evd + (size_t)r * d.NB;
+    u32* scr = (u32*)(res ? ka : kb);    // free sort buffer: evicted HBM index per e
+    for (u32 e = threadIdx.x; e < X; e += CTA) {
+      u32 v = (u32)upper_bound_u32(ec, (int)nv, e);
+      u32 excl = v ? ec[v - 1] : 0;
+      u32 p = ep[v];
+      u32 j = d.n_hbm[p] - 1 - (e - excl);
+      u32* row = d.loc + (size_t)p * d.MAXBP;
+      u32 idx = row[j];
+      scr[e] = idx;
+      if (e < hfree) {
+        u32 slot = bitmap_select(sf, s_big, d.NHW, e);
+        row[j] = LOC_HOST | slot;
+        d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
+        evd[e].src = idx;
+        evd[e].dst = slot;
+      } else {
+        row[j] = LOC_NONE;
+      }
+    }
+    __syncthreads();
+    u32* shf = d.host_free + (size_t)r * d.NHW;
+    for (u32 e = threadIdx.x; e < X; e += CTA) {
+      u32 idx = scr[e];
+      atomicOr(&hf[idx >> 5], 1u << (idx & 31));
+      if (e < hfree) {
+        u32 slot = evd[e].dst;
+        atomicAnd(&shf[slot >> 5], ~(1u << (slot & 31)));
+      }
+    }
+    for (u32 v = threadIdx.x; v < nv; v += CTA) {
+      u32 p = ep[v];
+      u32 excl = v ? ec[v - 1] : 0;
+      u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p];
+      u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
+      ta_decision rec;
+      rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
+      rec.to_host = toh; rec.dropped = take - toh;
+      rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
+      d.dec_ev[(size_t)r * N + v] = rec;
+      d.n_hbm[p] -= take;
+      d.n_host[p] += toh;
+    }
+    if (threadIdx.x == 0) {
+      u32 toh = min(X, hfree);
+      d.ev_cnt[r] = nv;
+      d.evd_cnt[r] = toh;
+      atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
+      atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)toh);
+      atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - toh));
+    }
+    __syncthreads();
+  }
+  // ---- 5.4 allocation prefix (after the evictions' frees)
+  cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
+  ull pc[PC_N];
+#pragma unroll
+  for (int i = 0; i < PC_N; ++i) pc[i] = 0;
+  FillDesc* fld = d.fld + (size_t)r * d.NB;
+  // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
+  for (u32 i = threadIdx.x; i < nF; i += CTA) {
+    u32 p = fp[i];
+    u32 need = fc[i] - (i ? fc[i - 1] : 0);
+    int h = d.home[p];
+    ta_decision rec;
+    rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
+    rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
+    if (i < m) {
+      const u32 ckv = d.c_kv[p], c = d.c[p];
+      const bool resumed = !(d.satisfied[p] && h == r);
+      if (resumed && ckv > 0) {
+        u32 hb = ceil_div_u32(ckv, bt);
+        u32 sh = bt - (ckv - (hb - 1) * bt);           // missing slots of the last block
+        u32 nh = d.n_hbm[p], ns = d.n_host[p], nn = hb - nh - ns;
+        ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
+        u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
+        if (is_hbm(el)) th -= sh; else if (is_host(el)) ts -= sh; else tn -= sh;
+        if (h == r) rec.hit_tok = (u32)th; else rec.peer_tok = (u32)th;
+        rec.host_tok = (u32)ts;
+        rec.miss_tok = (u32)tn;
+      }
+      rec.new_tok = c - ckv;
+      rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
+      pc[PC_HIT] += rec.hit_tok; pc[PC_PEER] += rec.peer_tok; pc[PC_HOST] += rec.host_tok;
+      pc[PC_MISS] += rec.miss_tok; pc[PC_NEWTOK] += rec.new_tok;
+      if (h == r && c > ckv && (ckv % bt) != 0) {      // partial last block already resident
+        u32 j = ckv / bt;
+        if (j < d.n_hbm[p]) {
+          u32 t1 = min((j + 1) * bt, c);
+          pc[PC_FILLTOK] += t1 - ckv;
+          if (fill) {
+            u32 pos = atomicAdd(&s_app[1], 1u);
+            fld[pos] = FillDesc{d.loc[(size_t)p * d.MAXBP + j], d.uid[p], ckv, t1, j, 0};
+          }
+        }
+      }
+      d.sat_new[p] = (u8)(r + 1);
+    } else {
+      rec.kind = TA_D_STALL;
+      pc[PC_STALL] += 1;
+    }
+    d.dec_fs[(size_t)r * N + i] = rec;
+  }
+  __syncthreads();
+  // ---- 5.4 / 5.5 requests: (p in S_r slot order, needed j ascending) -> q-th lowest free block
+  FeDesc* fed = d.fed + (size_t)r * d.NB;
+  u32* dfh = d.dfh + (size_t)r * d.NB;
+  u32* dfs = d.dfs + (size_t)r * d.NB;
+  for (u32 q = threadIdx.x; q < tot; q += CTA) {
+    u32 i = (u32)upper_bound_u32(fc, (int)m, q);
+    u32 excl = i ? fc[i - 1] : 0;
+    u32 p = fp[i];
+    int h = d.home[p];
+    u32 j = (h == r ? d.n_hbm[p] : 0) + (q - excl);
+    u32 dst = bitmap_select(hf, s_big, d.NBW, q);
+    u32* row = d.loc + (size_t)p * d.MAXBP;
+    u32 old = row[j];
+    const u32 ckv = d.c_kv[p], c = d.c[p];
+    const u32 hb = ceil_div_u32(ckv, bt);
+    const u32 jb = j * bt, je = min(jb + bt, c);
+    bool copied = false;
+    if (is_hbm(old)) {                                  // HBM on h != r: peer copy (P2P)
+      u32 pos = atomicAdd(&s_app[0], 1u);
+      fed[pos] = FeDesc{MV_P2P, (u32)h, old, dst};
+      dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
+      pc[PC_P2P] += 1;
+      copied = true;
+    } else if (is_host(old)) {                          // host tier of h: H2D
+      u32 pos = atomicAdd(&s_app[0], 1u);
+      fed[pos] = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst};
+      dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
+      pc[PC_H2D] += 1;
+      copied = true;
+    } else {                                            // recompute history / brand-new tokens
+      if (j < hb) pc[PC_REC] += 1; else pc[PC_NEW] += 1;
+      pc[PC_FILLTOK] += je - jb;
+      if (fill) fld[atomicAdd(&s_app[1], 1u)] = FillDesc{dst, d.uid[p], jb, je, j, 0};
+    }
+    if (copied && ckv < c && jb < c && jb + bt > ckv) { // copied block that also gets new tokens
+      u32 t0 = max(jb, ckv);
+      pc[PC_FILLTOK] += je - t0;
+      if (fill) fld[atomicAdd(&s_app[1], 1u)] = FillDesc{dst, d.uid[p], t0, je, j, 0};
+    }
+    row[j] = dst;
+    d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
+  }
+  __syncthreads();
+  for (u32 q = threadIdx.x; q < tot; q += CTA) {
+    u32 dst = bitmap_select(hf, s_big, d.NBW, q);
+    atomicAnd(&hf[dst >> 5], ~(1u << (dst & 31)));
+  }
+#pragma unroll
+  for (int i = 0; i < PC_N; ++i) warp_add_shared(pc[i], &s_pc[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d.f_cnt[r] = nF;
+    d.s_cnt[r] = m;
+    d.fed_cnt[r] = s_app[0];
+    d.fld_cnt[r] = s_app[1];
+    d.dfh_cnt[r] = s_app[2];
+    d.dfs_cnt[r] = s_app[3];
+    atomicAdd(&d.stats[ST_FETCH_BLOCKS], (ull)tot);
+    atomicAdd(&d.stats[ST_P2P], s_pc[PC_P2P]);
+    atomicAdd(&d.stats[ST_H2D], s_pc[PC_H2D]);
+    atomicAdd(&d.stats[ST_RECOMPUTE], s_pc[PC_REC]);
+    atomicAdd(&d.stats[ST_NEW_BLOCKS], s_pc[PC_NEW]);
+    atomicAdd(&d.stats[ST_FILL_TOK], s_pc[PC_FILLTOK]);
+    atomicAdd(&d.stats[ST_HIT], s_pc[PC_HIT]);
+    atomicAdd(&d.stats[ST_PEER], s_pc[PC_PEER]);
+    atomicAdd(&d.stats[ST_HOST], s_pc[PC_HOST]);
+    atomicAdd(&d.stats[ST_MISS], s_pc[PC_MISS]);
+    atomicAdd(&d.stats[ST_NEW_TOK], s_pc[PC_NEWTOK]);
+    atomicAdd(&d.stats[ST_STALLS], s_pc[PC_STALL]);
+  }
+}

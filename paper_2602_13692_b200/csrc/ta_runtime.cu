@@ -1,0 +1,577 @@
+// ta_runtime.cu — host side of libta: the C ABI of include/ta.h.
+//
+// Owns no memory: every buffer comes from the caller (ta_buffers).  The tick is a
+// fixed sequence of kernels on the caller's stream; in trace mode it is captured
+// once into a CUDA graph and replayed (all sizes are read on the device).
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "k_copy.cuh"
+#include "k_finalize.cuh"
+#include "k_ingest.cuh"
+#include "k_plan.cuh"
+#include "k_sched.cuh"
+
+namespace {
+
+const int kCopyGrid = 148 * 8;   // copy kernels: 8 resident 256-thread CTAs per SM
+const int kMaxEvents = 4096;
+
+struct Layout {                  // workspace carving (dry run when base == nullptr)
+  char* base;
+  size_t off = 0;
+  template <class T> T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct HostWs {
+  ta_decision* dec;              // [dec_cap]
+  u32* dec_cnt;
+  ta_event* ev;                  // [kMaxEvents]
+  i64* scal;                     // [8] small H2D/D2H staging
+};
+
+}  // namespace
+
+struct ta_ctx {
+  ta_config cfg;
+  ta_buffers bufs;
+  cudaStream_t stream;
+  Dev d;
+  HostWs h;
+  ta_event* ev_dev = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  bool trace_loaded = false;
+  int poisoned = TA_OK;
+  std::string err;
+  size_t block_bytes = 0;
+  cudaEvent_t ev[10] = {};
+  bool timing = false;
+};
+
+#define FAIL(ctx, code, ...)                                          \
+  do {                                                                \
+    char _b[512];                                                     \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);                            \
+    if (ctx) (ctx)->err = _b;                                         \
+    return (code);                                                    \
+  } while (0)
+
+#define CK(ctx, x)                                                                     \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess) {                                                           \
+      if (ctx) {                                                                       \
+        (ctx)->err = std::string(#x) + ": " + cudaGetErrorString(_e);                  \
+        (ctx)->poisoned = TA_E_CUDA;                                                   \
+      }                                                                                \
+      return TA_E_CUDA;                                                                \
+    }                                                                                  \
+  } while (0)
+
+static size_t blk_bytes(const ta_config* c) {
+  return (size_t)2 * c->n_layers * c->block_tokens * c->n_kv_heads * c->head_dim * c->elem_bytes;
+}
+
+static const char* validate(const ta_config* c) {
+  if (!c) return "null config";
+  if (c->elem_bytes != 2) return "elem_bytes must be 2";
+  if (c->n_layers <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 || c->block_tokens <= 0)
+    return "KV shape must be positive";
+  if ((c->n_kv_heads * c->head_dim) % 8) return "n_kv_heads*head_dim must be a multiple of 8";
+  if (c->layout != 0 && c->layout != 1) return "layout must be 0 or 1";
+  if (c->n_replicas < 1 || c->n_replicas > TA_MAX_REPLICAS) return "n_replicas out of range";
+  if (c->replicas_here < 1 || c->first_replica < 0 || c->first_replica + c->replicas_here > c->n_replicas)
+    return "replicas_here/first_replica out of range";
+  if (c->max_programs < 1 || c->max_blocks_per_program < 1) return "max_programs/max_blocks must be >= 1";
+  if (c->max_blocks_per_program >= (1 << 23)) return "max_blocks_per_program must be < 2^23";
+  if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (1ull << 32))
+    return "max_programs * max_blocks_per_program must be < 2^32";
+  if (c->hbm_blocks < 1 || c->hbm_blocks > 131040) return "hbm_blocks must be in [1, 131040]";
+  if (c->host_blocks < 0 || c->host_blocks > 262112) return "host_blocks must be in [0, 262112]";
+  if (c->delta_t_ms <= 0 || c->decay_unit_ms <= 0) return "delta_t_ms and decay_unit_ms must be > 0";
+  if (c->decode_tok_per_s < 0 || c->compact_every < 0 || c->max_trace_turns < 0) return "negative rate/compact/turns";
+  return nullptr;
+}
+
+static size_t carve(const ta_config* c, char* base, Dev* d) {
+  Layout L{base};
+  const size_t N = c->max_programs, R = c->n_replicas, NB = c->hbm_blocks;
+  const size_t NH = c->host_blocks > 0 ? c->host_blocks : 1;
+  const size_t MAXBP = (c->max_blocks_per_program + 3) & ~3;
+  const size_t NBW = (NB + 31) / 32, NHW = (NH + 31) / 32;
+  const size_t TT = c->max_trace_turns > 0 ? c->max_trace_turns : 1;
+  Dev x{};
+  x.ctr = L.take<Ctr>(1);
+  x.stats = L.take<ull>(ST_N);
+  x.verify = L.take<ull>(2);
+  x.uid = L.take<u32>(N); x.c = L.take<u32>(N); x.c_kv = L.take<u32>(N);
+  x.paused_since = L.take<u32>(N); x.step_count = L.take<u32>(N); x.turn = L.take<u32>(N);
+  x.gen_done = L.take<u32>(N);
+  x.status = L.take<u8>(N); x.phase = L.take<u8>(N); x.satisfied = L.take<u8>(N);
+  x.placement = L.take<i8>(N); x.home = L.take<i8>(N);
+  x.acting_since = L.take<i64>(N); x.tool_return = L.take<i64>(N);
+  x.loc = L.take<u32>(N * MAXBP);
+  x.nb = L.take<u32>(N); x.n_hbm = L.take<u32>(N); x.n_host = L.take<u32>(N);
+  x.prefix_hbm = L.take<u32>(N); x.contrib = L.take<u32>(N);
+  x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
+  x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
+  x.t_g = L.take<u32>(TT); x.t_d = L.take<u32>(TT); x.t_o = L.take<u32>(TT);
+  x.hbm_free = L.take<u32>(R * NBW); x.host_free = L.take<u32>(R * NHW);
+  x.owner_hbm = L.take<u32>(R * NB); x.owner_host = L.take<u32>(R * NH);
+  x.L = L.take<ull>(R);
+  x.ska = L.take<u64>((R + 1) * N); x.skb = L.take<u64>((R + 1) * N);
+  x.sva = L.take<u32>((R + 1) * N); x.svb = L.take<u32>((R + 1) * N);
+  x.pause_list = L.take<u32>(R * N); x.pause_cnt = L.take<u32>(R);
+  x.restore_pid = L.take<u32>(N); x.restore_dst = L.take<u32>(N);
+  x.f_pid = L.take<u32>(R * N); x.f_cum = L.take<u32>(R * N);
+  x.f_cnt = L.take<u32>(R); x.s_cnt = L.take<u32>(R);
+  x.dec_fs = L.take<ta_decision>(R * N); x.dec_ev = L.take<ta_decision>(R * N);
+  x.ev_cnt = L.take<u32>(R);
+  x.e_pid = L.take<u32>(R * N); x.e_cum = L.take<u32>(R * N);
+  x.evd = L.take<EvDesc>(R * NB); x.evd_cnt = L.take<u32>(R);
+  x.fed = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R);
+  x.fld = L.take<FillDesc>(R * NB); x.fld_cnt = L.take<u32>(R);
+  x.dfh = L.take<u32>(R * NB); x.dfh_cnt = L.take<u32>(R);
+  x.dfs = L.take<u32>(R * NB); x.dfs_cnt = L.take<u32>(R);
+  x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
+  x.events = L.take<ta_event>(kMaxEvents);
+  if (d) *d = x;
+  return L.off + 256;
+}
+
+static size_t host_carve(const ta_config* c, char* base, HostWs* h) {
+  Layout L{base};
+  HostWs x{};
+  const size_t cap = 4 * (size_t)c->max_programs + c->n_replicas + 64;
+  x.dec = L.take<ta_decision>(cap);
+  x.dec_cnt = L.take<u32>(1);
+  x.ev = L.take<ta_event>(kMaxEvents);
+  x.scal = L.take<i64>(8);
+  if (h) *h = x;
+  return L.off + 256;
+}
+
+__global__ void k_init(Dev d) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (int r = 0; r < d.R; ++r) {
+    for (int w = t; w < d.NBW; w += stride) {
+      i64 lo = (i64)w * 32, n = d.NB - lo;
+      d.hbm_free[(size_t)r * d.NBW + w] = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1);
+    }
+    for (int w = t; w < d.NHW; w += stride) {
+      i64 lo = (i64)w * 32, n = d.NH - lo;
+      d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
+    }
+  }
+  for (int p = t; p < d.N; p += stride) {
+    d.tool_return[p] = INT64_MAX;
+    d.placement[p] = -1;
+    d.home[p] = -1;
+  }
+}
+
+// ------------------------------------------------------------------ tick launch sequence
+static void rec(ta_ctx* x, int i) {
+  if (x->timing) cudaEventRecord(x->ev[i], x->stream);
+}
+
+static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
+  Dev& d = x->d;
+  cudaStream_t s = x->stream;
+  const int N = d.N, R = d.R;
+  rec(x, 0);
+  k_begin<<<1, 32, 0, s>>>(d);
+  if (d.api_mode) k_apply_events<<<1, 32, 0, s>>>(d, x->ev_dev, n_ev, 1);
+  else k_ingest_trace<<<(N + 255) / 256, 256, 0, s>>>(d);
+  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);
+  rec(x, 1);
+  k_pause<<<R, CTA, 0, s>>>(d);
+  k_restore<<<1, CTA, 0, s>>>(d);
+  rec(x, 2);
+  k_plan<<<R, CTA, 0, s>>>(d, 0);
+  rec(x, 3);
+  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  rec(x, 4);
+  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
+  rec(x, 5);
+  if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
+  rec(x, 6);
+  k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 0);
+  k_compact_plan<<<R, CTA, 0, s>>>(d);
+  rec(x, 7);
+  k_copy_compact<<<kCopyGrid, 256, 0, s>>>(d);
+  rec(x, 8);
+  k_assemble<<<1, CTA, 0, s>>>(d, 0);
+  rec(x, 9);
+  return cudaGetLastError();
+}
+
+static ta_status check_ctx(ta_ctx* ctx) {
+  if (!ctx) return TA_E_INVAL;
+  if (ctx->poisoned) return (ta_status)ctx->poisoned;
+  return TA_OK;
+}
+
+static ta_status copy_out(ta_ctx* ctx, ta_decision* out, int32_t out_cap, int32_t* n_out) {
+  u32 n = *ctx->h.dec_cnt;
+  if (n_out) *n_out = (int32_t)n;
+  if (!out) return TA_OK;
+  u32 m = n < (u32)out_cap ? n : (u32)out_cap;
+  memcpy(out, ctx->h.dec, (size_t)m * sizeof(ta_decision));
+  return n > (u32)out_cap ? TA_E_TRUNCATED : TA_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int32_t ta_abi_version(void) { return TA_ABI_VERSION; }
+
+ta_status ta_block_bytes(const ta_config* cfg, size_t* block_bytes) {
+  if (!cfg || !block_bytes) return TA_E_INVAL;
+  *block_bytes = blk_bytes(cfg);
+  return TA_OK;
+}
+
+ta_status ta_workspace_bytes(const ta_config* cfg, size_t* dev_bytes, size_t* host_bytes) {
+  if (validate(cfg)) return TA_E_INVAL;
+  if (dev_bytes) *dev_bytes = carve(cfg, nullptr, nullptr);
+  if (host_bytes) *host_bytes = host_carve(cfg, nullptr, nullptr);
+  return TA_OK;
+}
+
+ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_stream, void* nccl_comm,
+                       ta_ctx** out) {
+  if (!out || !bufs) return TA_E_INVAL;
+  *out = nullptr;
+  if (const char* why = validate(cfg)) {
+    fprintf(stderr, "ta_init_pool: %s\n", why);
+    return TA_E_INVAL;
+  }
+  if (nccl_comm) return TA_E_INVAL;
+  if (!bufs->dev_workspace || !bufs->host_workspace) return TA_E_NOMEM;
+  for (int q = 0; q < cfg->replicas_here; ++q) {
+    int r = cfg->first_replica + q;
+    if (!bufs->hbm_pool[r]) return TA_E_INVAL;
+    if (cfg->host_blocks > 0 && !bufs->host_pool[r]) return TA_E_INVAL;
+  }
+  ta_ctx* x = new ta_ctx();
+  x->cfg = *cfg;
+  x->bufs = *bufs;
+  x->stream = (cudaStream_t)cuda_stream;
+  x->block_bytes = blk_bytes(cfg);
+  Dev& d = x->d;
+  carve(cfg, (char*)bufs->dev_workspace, &d);
+  host_carve(cfg, (char*)bufs->host_workspace, &x->h);
+  x->ev_dev = d.events;
+  d.N = cfg->max_programs;
+  d.MAXB = cfg->max_blocks_per_program;
+  d.MAXBP = (cfg->max_blocks_per_program + 3) & ~3;
+  d.R = cfg->n_replicas;
+  d.bt = cfg->block_tokens;
+  d.nL = cfg->n_layers; d.Hkv = cfg->n_kv_heads; d.D = cfg->head_dim; d.layout = cfg->layout;
+  d.NB = cfg->hbm_blocks; d.NH = cfg->host_blocks;
+  d.NBW = (int)((d.NB + 31) / 32);
+  d.NHW = (int)((d.NH + 31) / 32);
+  d.dt = cfg->delta_t_ms; d.unit = cfg->decay_unit_ms; d.rate = cfg->decode_tok_per_s;
+  d.flags = cfg->flags; d.compact_every = cfg->compact_every;
+  d.seg_bytes = (i64)cfg->block_tokens * cfg->n_kv_heads * cfg->head_dim * cfg->elem_bytes;
+  d.block_bytes = (i64)x->block_bytes;
+  d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
+  d.api_mode = (cfg->flags & TA_F_TRACE_MODE) ? 0 : 1;
+  for (int r = 0; r < d.R; ++r) {
+    d.cap_max[r] = (i64)(((u64)cfg->lambda_max_q16 * (u64)d.NB) >> 16);
+    d.cap_min[r] = (i64)(((u64)cfg->lambda_min_q16 * (u64)d.NB) >> 16);
+  }
+  for (int k = 0; k < 64; ++k) d.F[k] = cfg->decay_q32[k];
+  for (int r = 0; r < TA_MAX_REPLICAS; ++r) {
+    d.hbm[r] = (char*)bufs->hbm_pool[r];
+    d.host[r] = nullptr;
+    if (bufs->host_pool[r] && cfg->host_blocks > 0) {
+      void* dp = nullptr;
+      cudaError_t e = cudaHostGetDevicePointer(&dp, bufs->host_pool[r], 0);
+      if (e != cudaSuccess) {
+        x->err = std::string("host tier is not page-locked/mapped: ") + cudaGetErrorString(e);
+        delete x;
+        return TA_E_INVAL;
+      }
+      d.host[r] = (char*)dp;
+    }
+  }
+  {
+    void* dp = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dp, bufs->host_workspace, 0);
+    if (e != cudaSuccess) { delete x; return TA_E_INVAL; }
+    char* hb = (char*)dp;
+    d.dec_out = (ta_decision*)(hb + ((char*)x->h.dec - (char*)bufs->host_workspace));
+    d.dec_out_cnt = (u32*)(hb + ((char*)x->h.dec_cnt - (char*)bufs->host_workspace));
+    d.dec_cap = (u32)(4 * (size_t)cfg->max_programs + cfg->n_replicas + 64);
+  }
+  d.n_slots = 0;
+  d.n_initial = 0;
+  x->timing = (cfg->flags & TA_F_TIMING) != 0;
+  size_t dev_bytes = carve(cfg, nullptr, nullptr);
+  cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
+  if (e == cudaSuccess) { k_init<<<148, 256, 0, x->stream>>>(d); e = cudaGetLastError(); }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));
+    delete x;
+    return TA_E_CUDA;
+  }
+  if (x->timing)
+    for (int i = 0; i < 10; ++i) cudaEventCreate(&x->ev[i]);
+  *out = x;
+  return TA_OK;
+}
+
+ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* t) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!t) return TA_E_INVAL;
+  if (ctx->d.api_mode) FAIL(ctx, TA_E_STATE, "ta_load_trace: context is not in trace mode");
+  if (t->n_slots < 0 || t->n_slots > ctx->d.N) FAIL(ctx, TA_E_INVAL, "n_slots %d > max_programs", t->n_slots);
+  if (t->n_initial < 0 || t->n_initial > t->n_slots) FAIL(ctx, TA_E_INVAL, "bad n_initial");
+  const u32 total = t->n_slots ? t->turn_off[t->n_slots] : 0;
+  if (total > (u32)ctx->cfg.max_trace_turns) FAIL(ctx, TA_E_INVAL, "trace has %u turns > max_trace_turns", total);
+  for (int p = 0; p < t->n_slots; ++p) {
+    if (t->turn_off[p + 1] <= t->turn_off[p]) FAIL(ctx, TA_E_INVAL, "slot %d has no turns", p);
+    u64 ctx_max = t->p0[p];
+    for (u32 q = t->turn_off[p]; q < t->turn_off[p + 1]; ++q) ctx_max += (u64)t->g[q] + t->o[q];
+    if ((ctx_max + ctx->d.bt - 1) / ctx->d.bt > (u64)ctx->d.MAXB)
+      FAIL(ctx, TA_E_INVAL, "slot %d reaches %llu tokens > max_blocks_per_program", p, (unsigned long long)ctx_max);
+  }
+  cudaStream_t s = ctx->stream;
+  Dev& d = ctx->d;
+  CK(ctx, cudaMemcpyAsync(d.t_uid, t->uid, sizeof(u32) * t->n_slots, cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaMemcpyAsync(d.t_p0, t->p0, sizeof(u32) * t->n_slots, cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaMemcpyAsync(d.t_off, t->turn_off, sizeof(u32) * (t->n_slots + 1), cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaMemcpyAsync(d.t_g, t->g, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaMemcpyAsync(d.t_d, t->d_ms, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaMemcpyAsync(d.t_o, t->o, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
+  CK(ctx, cudaStreamSynchronize(s));
+  d.n_slots = t->n_slots;
+  d.n_initial = t->n_initial;
+  if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+  ctx->trace_loaded = true;
+  return TA_OK;
+}
+
+ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t n_ev, ta_decision* out,
+                        int32_t out_cap, int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  Dev& d = ctx->d;
+  cudaStream_t s = ctx->stream;
+  if (n_ev < 0 || (n_ev > 0 && !ev) || out_cap < 0) FAIL(ctx, TA_E_INVAL, "bad event/output arguments");
+  if (!d.api_mode) {
+    if (n_ev) FAIL(ctx, TA_E_STATE, "events passed in trace mode");
+    if (!ctx->trace_loaded) FAIL(ctx, TA_E_STATE, "no trace loaded");
+    if (now_ms >= 0) {
+      // must equal tick * delta_t: read the device tick counter
+      CK(ctx, cudaMemcpyAsync(ctx->h.scal, &d.ctr->tick, sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CK(ctx, cudaStreamSynchronize(s));
+      if (now_ms != ctx->h.scal[0] * d.dt) FAIL(ctx, TA_E_INVAL, "now_ms %lld != tick*delta_t", (long long)now_ms);
+    }
+    const bool use_graph = !(ctx->cfg.flags & (TA_F_NO_GRAPH | TA_F_TIMING));
+    if (use_graph) {
+      if (!ctx->graph) {
+        cudaGraph_t g;
+        CK(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t le = launch_tick(ctx, 0);
+        cudaError_t ce = cudaStreamEndCapture(s, &g);
+        CK(ctx, le);
+        CK(ctx, ce);
+        CK(ctx, cudaGraphInstantiate(&ctx->graph, g, 0));
+        cudaGraphDestroy(g);
+      }
+      CK(ctx, cudaGraphLaunch(ctx->graph, s));
+    } else {
+      CK(ctx, launch_tick(ctx, 0));
+    }
+  } else {
+    if (now_ms < 0 || now_ms > (int64_t)AS_MAX) FAIL(ctx, TA_E_INVAL, "API mode needs 0 <= now_ms < 2^40");
+    if (n_ev > kMaxEvents) FAIL(ctx, TA_E_INVAL, "at most %d events per tick", kMaxEvents);
+    memcpy(ctx->h.ev, ev, sizeof(ta_event) * n_ev);
+    ctx->h.scal[0] = now_ms;
+    CK(ctx, cudaMemcpyAsync(ctx->ev_dev, ctx->h.ev, sizeof(ta_event) * n_ev, cudaMemcpyHostToDevice, s));
+    CK(ctx, cudaMemcpyAsync(&d.ctr->now_ms, ctx->h.scal, sizeof(i64), cudaMemcpyHostToDevice, s));
+    // validation pass alone first: a rejected batch leaves the state untouched and
+    // the tick does not run (SURVEY.md §8(c) API table)
+    k_apply_events<<<1, 32, 0, s>>>(d, ctx->ev_dev, n_ev, 0);
+    CK(ctx, cudaGetLastError());
+    CK(ctx, cudaMemcpyAsync(ctx->h.scal + 1, &d.ctr->err, sizeof(i32), cudaMemcpyDeviceToHost, s));
+    CK(ctx, cudaStreamSynchronize(s));
+    int verr = (int)*(i32*)(ctx->h.scal + 1);
+    if (verr != TA_OK) FAIL(ctx, (ta_status)verr, "event batch rejected (first illegal event)");
+    CK(ctx, launch_tick(ctx, n_ev));
+  }
+  if (!out && !n_out) return TA_OK;
+  CK(ctx, cudaStreamSynchronize(s));
+  return copy_out(ctx, out, out_cap, n_out);
+}
+
+ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!out) return TA_E_INVAL;
+  Dev& d = ctx->d;
+  memset(out, 0, sizeof(*out));
+  std::vector<ull> st(ST_N);
+  std::vector<ull> L(d.R);
+  std::vector<u32> hf((size_t)d.R * d.NBW), sf((size_t)d.R * (d.NHW ? d.NHW : 1));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemcpy(st.data(), d.stats, sizeof(ull) * ST_N, cudaMemcpyDeviceToHost));
+  CK(ctx, cudaMemcpy(L.data(), d.L, sizeof(ull) * d.R, cudaMemcpyDeviceToHost));
+  CK(ctx, cudaMemcpy(hf.data(), d.hbm_free, sizeof(u32) * hf.size(), cudaMemcpyDeviceToHost));
+  if (d.NHW) CK(ctx, cudaMemcpy(sf.data(), d.host_free, sizeof(u32) * (size_t)d.R * d.NHW, cudaMemcpyDeviceToHost));
+  memcpy(out, st.data(), sizeof(ull) * ST_N);
+  for (int r = 0; r < d.R; ++r) {
+    out->L[r] = L[r];
+    u64 f = 0, g = 0;
+    for (int w = 0; w < d.NBW; ++w) f += __builtin_popcount(hf[(size_t)r * d.NBW + w]);
+    for (int w = 0; w < d.NHW; ++w) g += __builtin_popcount(sf[(size_t)r * d.NHW + w]);
+    out->hbm_used[r] = d.NB - f;
+    out->host_used[r] = d.NH - g;
+  }
+  out->block_bytes = ctx->block_bytes;
+  return TA_OK;
+}
+
+ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!ctx->timing) FAIL(ctx, TA_E_STATE, "context created without TA_F_TIMING");
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n && i < 9; ++i) {
+    float ms = 0;
+    CK(ctx, cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]));
+    us[i] = ms * 1000.f;
+  }
+  return TA_OK;
+}
+
+ta_status ta_verify_content(ta_ctx* ctx, uint64_t* mismatched, uint64_t* checked) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  Dev& d = ctx->d;
+  CK(ctx, cudaMemsetAsync(d.verify, 0, 2 * sizeof(ull), ctx->stream));
+  k_verify<<<148 * 8, 256, 0, ctx->stream>>>(d, 0);
+  if (d.NH > 0) k_verify<<<148 * 8, 256, 0, ctx->stream>>>(d, 1);
+  CK(ctx, cudaGetLastError());
+  ull v[2];
+  CK(ctx, cudaMemcpyAsync(v, d.verify, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (mismatched) *mismatched = v[0];
+  if (checked) *checked = v[1];
+  return TA_OK;
+}
+
+ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!v || (dir != 0 && dir != 1)) return TA_E_INVAL;
+  Dev& d = ctx->d;
+  cudaStream_t s = ctx->stream;
+  CK(ctx, cudaStreamSynchronize(s));
+  const size_t N = d.N, R = d.R;
+  auto mv = [&](void* host, void* dev, size_t bytes) -> cudaError_t {
+    if (!host) return cudaSuccess;
+    return dir == 0 ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost)
+                    : cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice);
+  };
+  CK(ctx, mv(v->uid, d.uid, N * 4)); CK(ctx, mv(v->c, d.c, N * 4)); CK(ctx, mv(v->c_kv, d.c_kv, N * 4));
+  CK(ctx, mv(v->paused_since, d.paused_since, N * 4)); CK(ctx, mv(v->step_count, d.step_count, N * 4));
+  CK(ctx, mv(v->turn, d.turn, N * 4)); CK(ctx, mv(v->gen_done, d.gen_done, N * 4));
+  CK(ctx, mv(v->status, d.status, N)); CK(ctx, mv(v->phase, d.phase, N)); CK(ctx, mv(v->satisfied, d.satisfied, N));
+  CK(ctx, mv(v->placement, d.placement, N)); CK(ctx, mv(v->home, d.home, N));
+  CK(ctx, mv(v->acting_since, d.acting_since, N * 8)); CK(ctx, mv(v->tool_return, d.tool_return, N * 8));
+  if (v->loc) {
+    size_t w = (size_t)d.MAXB * 4, sp = (size_t)d.MAXBP * 4;
+    if (dir == 0) CK(ctx, cudaMemcpy2D(v->loc, w, d.loc, sp, w, N, cudaMemcpyDeviceToHost));
+    else CK(ctx, cudaMemcpy2D(d.loc, sp, v->loc, w, w, N, cudaMemcpyHostToDevice));
+  }
+  CK(ctx, mv(v->hbm_free, d.hbm_free, R * d.NBW * 4));
+  if (d.NHW) CK(ctx, mv(v->host_free, d.host_free, R * d.NHW * 4));
+  CK(ctx, mv(v->owner_hbm, d.owner_hbm, R * d.NB * 4));
+  if (d.NH) CK(ctx, mv(v->owner_host, d.owner_host, R * d.NH * 4));
+  CK(ctx, mv(v->L, d.L, R * 8));
+  if (dir == 0) {
+    CK(ctx, mv(v->nb, d.nb, N * 4)); CK(ctx, mv(v->n_hbm, d.n_hbm, N * 4));
+    CK(ctx, mv(v->n_host, d.n_host, N * 4)); CK(ctx, mv(v->prefix_hbm, d.prefix_hbm, N * 4));
+    CK(ctx, mv(v->contrib, d.contrib, N * 4));
+  }
+  if (v->scalars) {
+    Ctr c;
+    CK(ctx, cudaMemcpy(&c, d.ctr, sizeof(Ctr), cudaMemcpyDeviceToHost));
+    if (dir == 0) {
+      v->scalars[0] = c.tick; v->scalars[1] = c.next_arrival; v->scalars[2] = c.T; v->scalars[3] = 0;
+    } else {
+      c.tick = v->scalars[0]; c.next_arrival = v->scalars[1]; c.T = v->scalars[2];
+      CK(ctx, cudaMemcpy(d.ctr, &c, sizeof(Ctr), cudaMemcpyHostToDevice));
+    }
+  }
+  return TA_OK;
+}
+
+ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, int32_t out_cap, int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  (void)pid; (void)mode; (void)out; (void)out_cap; (void)n_out;
+  FAIL(ctx, TA_E_STATE, "ta_pause: not implemented yet");
+}
+
+ta_status ta_resume(ta_ctx* ctx, uint32_t pid, int32_t replica, ta_decision* out, int32_t out_cap, int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  (void)pid; (void)replica; (void)out; (void)out_cap; (void)n_out;
+  FAIL(ctx, TA_E_STATE, "ta_resume: not implemented yet");
+}
+
+ta_status ta_migrate(ta_ctx* ctx, uint32_t pid, int32_t dst, ta_decision* out, int32_t out_cap, int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  (void)pid; (void)dst; (void)out; (void)out_cap; (void)n_out;
+  FAIL(ctx, TA_E_STATE, "ta_migrate: not implemented yet");
+}
+
+ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle64) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!handle64) return TA_E_INVAL;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ctx->bufs.hbm_pool[ctx->cfg.first_replica]);
+  if (e != cudaSuccess) { ctx->err = cudaGetErrorString(e); ctx->poisoned = TA_E_PEER; return TA_E_PEER; }
+  memcpy(handle64, &h, sizeof(h));
+  return TA_OK;
+}
+
+ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle64) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!handle64 || replica < 0 || replica >= ctx->d.R) return TA_E_INVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) { ctx->err = cudaGetErrorString(e); ctx->poisoned = TA_E_PEER; return TA_E_PEER; }
+  ctx->bufs.hbm_pool[replica] = p;
+  ctx->d.hbm[replica] = (char*)p;
+  if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+  return TA_OK;
+}
+
+ta_status ta_destroy(ta_ctx* ctx) {
+  if (!ctx) return TA_E_INVAL;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  for (int i = 0; i < 10; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  for (int r = 0; r < ctx->d.R; ++r) {
+    bool local = r >= ctx->cfg.first_replica && r < ctx->cfg.first_replica + ctx->cfg.replicas_here;
+    if (!local && ctx->bufs.hbm_pool[r]) cudaIpcCloseMemHandle(ctx->bufs.hbm_pool[r]);
+  }
+  delete ctx;
+  return TA_OK;
+}
+
+const char* ta_last_error(const ta_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

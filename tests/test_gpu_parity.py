@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, tick by tick,
+on identical seeded traces.  Decisions, program table, block tables, free sets and
+owners must be bit-identical; KV bytes are checked against the content closed form
+(on the GPU for every owned block, and on the CPU for sampled blocks)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import tracegen  # noqa: E402
+from tests.gpu_compare import check_blocks_content, compare_state, dec_tuples, oracle_arrays  # noqa: E402
+from tests.test_oracle_golden import DK, load_w1  # noqa: E402
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_parity(cfg, ticks, state_every=1, content_every=1, samples=4, fill=True, flags=0, seed=0,
+               host_blocks=None):
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    if host_blocks is not None:
+        cfg = dict(cfg, host_blocks=host_blocks)
+    tr = tracegen.make_trace(cfg)
+    o = oracle.Oracle(cfg, tr)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=fill, flags=flags)
+    pool.load_trace(tr)
+    rng = np.random.default_rng(seed)
+    n_dec = 0
+    for k in range(ticks):
+        st_o, dec_o = o.sched_step()
+        st_g, dec_g = pool.step()
+        assert st_o == oracle.OK and st_g == 0
+        got = dec_tuples(dec_g)
+        if got != dec_o:
+            for i, (a, b) in enumerate(zip(dec_o, got)):
+                if a != b:
+                    raise AssertionError(f"tick {k} decision {i}: oracle {a} gpu {b}")
+            raise AssertionError(f"tick {k}: {len(dec_o)} oracle decisions vs {len(got)} gpu")
+        n_dec += len(got)
+        if state_every and (k % state_every == 0 or k == ticks - 1):
+            compare_state(o, pool.debug_download(), where=f"tick {k}")
+        if fill and content_every and (k % content_every == 0 or k == ticks - 1):
+            bad, seen = pool.verify_content()
+            assert bad == 0, f"tick {k}: {bad} of {seen} KV words differ from the closed form"
+            check_blocks_content(o, pool, samples, rng)
+        if o.next_arrival == o.N and all(s == oracle.STOPPED for s in o.status):
+            break
+    s = pool.stats()
+    for key in oracle.ta_oracle.STAT_KEYS:
+        assert s[key] == o.stats[key], (key, s[key], o.stats[key])
+    pool.close()
+    return o, n_dec
+
+
+def stress(seed, R, NB=56, NH=16, n=24, n0=10, compact=3, **kw):
+    return tracegen.get_config("c1_toy", n_replicas=R, hbm_blocks=NB, host_blocks=NH,
+                               compact_every=compact, trace=dict(n=n, n_initial=n0, seed=seed), **kw)
+
+
+def test_gpu_toy_config1_full_run():
+    o, n = run_parity(tracegen.get_config("c1_toy"), 400)
+    assert all(s == oracle.STOPPED for s in o.status) and n > 0
+
+
+@pytest.mark.parametrize("seed,R", [(11, 1), (12, 2), (13, 3), (14, 2), (15, 4)])
+def test_gpu_stress_full_run(seed, R):
+    o, n = run_parity(stress(seed, R, NB=56 if R > 1 else 80), 300, seed=seed)
+    assert o.stats["evict_blocks"] > 0 and o.stats["restores"] > 0
+
+
+def test_gpu_stress_block_major_layout_and_bt1():
+    run_parity(stress(21, 2, layout=1), 200)
+    run_parity(stress(22, 2, NB=600, NH=200, block_tokens=1, compact=5), 120, state_every=5)
+
+
+def test_gpu_no_graph_and_timing_modes():
+    from paper_2602_13692_b200 import binding
+    run_parity(stress(31, 2), 80, flags=binding.F_NO_GRAPH)
+    run_parity(stress(32, 2), 40, flags=binding.F_TIMING)
+
+
+def test_gpu_w1_golden():
+    """Hand-computed two-tick example uploaded into the GPU state (tests/golden/w1.json)."""
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    g, o = load_w1()
+    pool = Pool(o.cfg, o.N, max_turns=o.trace.total_turns, fill=False)
+    pool.load_trace(o.trace)
+    arrs = oracle_arrays(o)
+    arrs["scalars"] = np.array([o.tick, o.next_arrival, 0, 0], np.int64)
+    pool.debug_upload(arrs)
+    for tk in g["ticks"]:
+        st, dec = pool.step()
+        assert st == 0
+        want = [tuple([DK[d[0]]] + d[1:]) for d in tk["decisions"]]
+        assert dec_tuples(dec) == want, tk["tick"]
+        o.sched_step()
+        compare_state(o, pool.debug_download(), where=f"W1 tick {tk['tick']}")
+    pool.close()
+
+
+def test_gpu_determinism():
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = stress(41, 3)
+    outs = []
+    for _ in range(2):
+        tr = tracegen.make_trace(cfg)
+        pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns)
+        pool.load_trace(tr)
+        log = [dec_tuples(pool.step()[1]) for _ in range(150)]
+        st = pool.debug_download()
+        outs.append((log, st["loc"].tobytes(), st["hbm_free"].tobytes(),
+                     bytes(pool.hbm[0].cpu().numpy())))
+        pool.close()
+    assert outs[0] == outs[1]
+
+
+@pytest.mark.slow
+def test_gpu_config2_swe_q32_full_size():
+    """configs[1] at full size (Qwen3-32B KV, 24,576 x 4 MiB blocks, 16,384 host slots)."""
+    run_parity(tracegen.get_config("c2_swe"), 40, state_every=5, content_every=10, samples=3)
+
+
+@pytest.mark.parametrize("name,ticks", [("c3_mixed", 25), ("c4_rlburst", 8)])
+def test_gpu_configs3_4_decisions_full_n(name, ticks):
+    """configs[2]/[3] at their full program counts and per-replica pools, all 8 replicas
+    on one GPU with the decision-only KV shape (bytes per block do not affect decisions)."""
+    cfg = tracegen.get_config(name, kv="mini")
+    run_parity(cfg, ticks, state_every=4, content_every=4, samples=8)
