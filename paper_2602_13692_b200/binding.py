@@ -218,7 +218,8 @@ class Pool:
         b.dev_workspace = self.dev_ws.data_ptr()
         b.host_workspace = self.host_ws.data_ptr()
         self.buffers = b
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # a dedicated (capturable) stream: the legacy default stream cannot host a CUDA graph
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self.ctx = C.c_void_p()
         with torch.cuda.device(self.device):
             st = L.ta_init_pool(C.byref(self.c), C.byref(b), C.c_void_p(self.stream.cuda_stream), None,

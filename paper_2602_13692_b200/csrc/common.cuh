@@ -106,6 +106,7 @@ struct Dev {
   u32* e_pid;                      // [R][N]  eviction order (sorted candidates)
   u32* e_cum;                      // [R][N]  inclusive n_hbm prefix in eviction order
   EvDesc* evd; u32* evd_cnt;       // [R][NB]
+  u32* evx;                        // [R][NB] evicted HBM block per eviction rank
   FeDesc* fed; u32* fed_cnt;       // [R][NB]
   FillDesc* fld; u32* fld_cnt;     // [R][NB]
   u32* dfh; u32* dfh_cnt;          // deferred HBM frees  [R][NB]: (replica << 27) | idx

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     const u32 hfree = s_big[d.NHW];
     EvDesc* evd = d.evd + (size_t)r * d.NB;
-    u32* scr = (u32*)(res ? ka : kb);    // free sort buffer: evicted HBM index per e
+    u32* scr = d.evx + (size_t)r * d.NB; // evicted HBM index per evicted block e (< NB)
     for (u32 e = threadIdx.x; e < X; e += CTA) {
       u32 v = (u32)upper_bound_u32(ec, (int)nv, e);
       u32 excl = v ? ec[v - 1] : 0;
@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   FeDesc* fed = d.fed + (size_t)r * d.NB;
   u32* dfh = d.dfh + (size_t)r * d.NB;
   u32* dfs = d.dfs + (size_t)r * d.NB;
+  u32* qdst = d.evx + (size_t)r * d.NB;  // allocated block per request (eviction use is over)
   for (u32 q = threadIdx.x; q < tot; q += CTA) {
     u32 i = (u32)upper_bound_u32(fc, (int)m, q);
     u32 excl = i ? fc[i - 1] : 0;
@@ -257,10 +258,11 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     }
     row[j] = dst;
     d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
+    qdst[q] = dst;
   }
   __syncthreads();
-  for (u32 q = threadIdx.x; q < tot; q += CTA) {
-    u32 dst = bitmap_select(hf, s_big, d.NBW, q);
+  for (u32 q = threadIdx.x; q < tot; q += CTA) {   // the bitmap changes only after all selects
+    u32 dst = qdst[q];
     atomicAnd(&hf[dst >> 5], ~(1u << (dst & 31)));
   }
 #pragma unroll

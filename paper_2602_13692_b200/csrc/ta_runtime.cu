@@ -136,7 +136,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.dec_fs = L.take<ta_decision>(R * N); x.dec_ev = L.take<ta_decision>(R * N);
   x.ev_cnt = L.take<u32>(R);
   x.e_pid = L.take<u32>(R * N); x.e_cum = L.take<u32>(R * N);
-  x.evd = L.take<EvDesc>(R * NB); x.evd_cnt = L.take<u32>(R);
+  x.evd = L.take<EvDesc>(R * NB); x.evd_cnt = L.take<u32>(R); x.evx = L.take<u32>(R * NB);
   x.fed = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R);
   x.fld = L.take<FillDesc>(R * NB); x.fld_cnt = L.take<u32>(R);
   x.dfh = L.take<u32>(R * NB); x.dfh_cnt = L.take<u32>(R);
