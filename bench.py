@@ -1,0 +1,391 @@
+"""Benchmark of the ThunderAgent KV-manager hot path on B200 (contract: one JSON line).
+
+A step is one scheduler tick through libta (ta_sched_step: ingest, footprint,
+decayed load, pause, restore, materialize, KV block movement, finalize) over the
+bench workload (tracegen config `bench_10k`: configs[3]'s 10k-program RL-burst
+trace, one replica per GPU with a 96 GiB HBM pool of 4 MiB Qwen3-32B blocks and a
+pinned host tier).  `value` = scheduler ticks/s normalised to 10k programs per tick
+(program-ticks/s / 1e4), summed over ranks.  Usage:
+
+  python bench.py [--gpus N] [--steps K] [--warmup W]          # our CUDA path
+  python bench.py --impl reference ...                         # the CPU oracle
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = None
+
+
+def load_metric():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)["metric"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="bench_10k")
+    ap.add_argument("--preroll", type=int, default=8, help="untimed ticks before warm-up")
+    ap.add_argument("--host-gib", type=float, default=64.0, help="cap of the pinned host tier")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback B200_PROFILING.md (6.65 TB/s)"
+
+
+def pcie_peak(torch, dev):
+    """Measured pinned cudaMemcpyAsync peak per direction (1 GiB, best of 5)."""
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = max(best, n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = best
+    del h, d
+    return out
+
+
+def kv_path_microbench(pool, torch, peaks, hbm_peak, n_blocks=2048, reps=3):
+    """Per-mode KV movement through ta_move_blocks with random block lists drawn from a
+    fragmented pool (SURVEY.md §8(d) 'Two movement measurements', 1)."""
+    import numpy as np
+    from paper_2602_13692_b200 import binding
+    rng = np.random.default_rng(7)
+    dev = pool.device
+    bb = pool.block_bytes
+    out = {}
+    NB, NH = pool.NB, pool.NH
+    n_blocks = min(n_blocks, NB // 2, NH if NH else NB // 2)
+    perm = rng.permutation(NB)
+    src = torch.tensor(perm[:n_blocks].astype(np.int32), device=dev)
+    dst = torch.tensor(perm[n_blocks:2 * n_blocks].astype(np.int32), device=dev)
+    modes = [("d2d", binding.MOVE_D2D, src, dst, 2 * bb, hbm_peak, "hbm r+w")]
+    if NH:
+        hs = torch.tensor(rng.permutation(NH)[:n_blocks].astype(np.int32), device=dev)
+        modes += [("d2h", binding.MOVE_D2H, src, hs, bb, peaks["d2h"], "pcie d2h (measured memcpy)"),
+                  ("h2d", binding.MOVE_H2D, hs, dst, bb, peaks["h2d"], "pcie h2d (measured memcpy)")]
+    s = pool.stream
+    for name, kind, a, b, bytes_per_block, peak, pname in modes:
+        best = 0.0
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            pool.move_blocks(kind, 0 if pool.first == 0 else pool.first, pool.first, a, b)
+            e1.record(s)
+            e1.synchronize()
+            gbs = n_blocks * bytes_per_block / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            best = max(best, gbs)
+        out[name] = {"gbs": round(best, 1), "peak_gbs": round(peak, 1), "frac": round(best / peak, 3),
+                     "peak": pname, "blocks": n_blocks, "block_bytes": bb}
+    return out
+
+
+def metadata_bytes(pool_stats_prev, n_programs, sum_nb, moved_blocks):
+    # algorithmic bytes of the decision phase: program records r+w,
+    # one block-table scan, bitmaps, table/owner updates of moved blocks
+    return n_programs * 96 + sum_nb * 4 + moved_blocks * 8
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, metric):
+    import tracegen
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = tracegen.get_config(args.config)
+    tr = tracegen.make_trace(cfg)
+    o = oracle.Oracle(cfg, tr)
+    for _ in range(args.preroll + args.warmup):
+        o.sched_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.sched_step()
+    dt = time.perf_counter() - t0
+    n_prog = tr.n_slots
+    value = args.steps * n_prog / 1e4 / dt
+    line = {
+        "impl": "reference", "metric": metric, "value": round(value, 4),
+        "unit": "ticks/s (10k-program ticks, summed over GPUs)",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.config, "programs": n_prog, "replicas": cfg["n_replicas"],
+                   "ticks": f"{args.preroll + args.warmup}..{args.preroll + args.warmup + args.steps - 1}"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "ticks/s", "cores": 1, "kind": "oracle",
+                         "sample": f"oracle (pure Python, 1 thread) ticks after {args.preroll + args.warmup} untimed"},
+        "e2e": {"value": round(value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, trace, seconds):
+    import oracle
+    o = oracle.Oracle(cfg, trace)
+    o.sched_step()                    # tick 0 (arrivals) untimed
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        o.sched_step()
+        n += 1
+    dt = time.perf_counter() - t0
+    cpu = os.cpu_count()
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": round(n * trace.n_slots / 1e4 / dt, 4), "unit": "ticks/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"ticks 1..{n} of the same trace ({dt:.1f} s, pure-Python oracle, 1 of {cpu} cores, {model})"}
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    metric = load_metric()
+    if args.impl == "reference":
+        return run_reference(args, metric)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import tracegen
+    from paper_2602_13692_b200 import Pool, binding
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = tracegen.get_config(args.config)
+    # weak scaling: every rank runs one replica over its own 10k-program trace
+    # (replicas only)
+    cfg["trace"]["seed"] = cfg["trace"]["seed"] + 1000 * rank
+    tr = tracegen.make_trace(cfg)
+    block_bytes = 2 * 64 * 8 * 128 * 2 * cfg["block_tokens"]
+    nh = min(cfg["host_blocks"], int(args.host_gib * (1 << 30)) // block_bytes)
+    cfg["host_blocks"] = nh
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=binding.F_TIMING, device=local)
+    pool.load_trace(tr)
+    peaks_file, peak_src = measured_peaks()
+    hbm_peak = float(peaks_file.get("hbm_gbs", 6650.0))
+
+    for _ in range(args.preroll + args.warmup):
+        pool.step(decisions=False)
+    torch.cuda.synchronize(dev)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    s = pool.stream
+    st0 = pool.stats()
+    phase_sum = np.zeros(9)
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.zero_()             # L2 flush (256 MiB > 126 MB L2) inside the timed region
+        pool.step(decisions=False)
+        phase_sum += np.array(pool.phase_times())   # syncs the stream: per-kernel CUDA-event times
+    e1.record(s)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    st1 = pool.stats()
+    sum_nb = int(pool.debug_download()["nb"].sum())   # block-table entries scanned per tick
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    progs_total = tr.n_slots * world
+    value = args.steps * progs_total / 1e4 / (ms * 1e-3)
+
+    # ---- e2e: the SAME ticks (fresh context over the same buffers, same untimed
+    # prefix) through the public API, decisions read back to the host every tick
+    pool.reset()
+    pool.load_trace(tr)
+    for _ in range(args.preroll + args.warmup):
+        pool.step(decisions=False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0.record(s)
+    d2h = 0
+    for _ in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        st, dec = pool.step(decisions=True)
+        d2h += 0 if dec is None else dec.nbytes + 4
+    e1.record(s)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = args.steps * progs_total / 1e4 / (e2e_ms * 1e-3)
+
+    # ---- bytes per path in the timed steps, roofline of the dominant kernel
+    dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS if isinstance(st0[k], int)}
+    bb = pool.block_bytes
+    ph = phase_sum / args.steps            # us per step
+    names = ["ingest+footprint", "pause+restore", "plan", "evict_d2h", "fetch_p2p_h2d", "fill",
+             "finalize+compact_plan", "compact_d2d", "assemble"]
+    peaks = pcie_peak(torch, dev) if nh else {"h2d": 1.0, "d2h": 1.0}
+    algo = {
+        "evict_d2h": (dstat["evict_to_host"] * bb / args.steps, peaks["d2h"], "pcie"),
+        "fetch_p2p_h2d": ((dstat["h2d_blocks"] + dstat["p2p_blocks"]) * bb / args.steps, peaks["h2d"], "pcie"),
+        "compact_d2d": (2 * dstat["compact_blocks"] * bb / args.steps, hbm_peak, "hbm"),
+    }
+    dom = int(np.argmax(ph))
+    dname = names[dom]
+    if dname in algo:
+        byt, peak, bound = algo[dname]
+    else:
+        byt = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
+        peak, bound = hbm_peak, "hbm"
+    achieved = byt / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
+    roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
+                "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                "share_of_step": round(float(ph[dom] / ph.sum()), 4),
+                "peak_source": (peak_src if bound == "hbm" else "measured in this run: pinned cudaMemcpyAsync 1 GiB")}
+    kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
+    moved = {
+        "d2h_gb_per_step": round(dstat["evict_to_host"] * bb / args.steps / 1e9, 3),
+        "h2d_gb_per_step": round(dstat["h2d_blocks"] * bb / args.steps / 1e9, 3),
+        "p2p_gb_per_step": round(dstat["p2p_blocks"] * bb / args.steps / 1e9, 3),
+        "d2d_gb_per_step": round(dstat["compact_blocks"] * bb / args.steps / 1e9, 3),
+    }
+    sched_us = float(ph[0] + ph[1] + ph[2] + ph[6] + ph[8])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(tracegen.get_config(args.config), tracegen.make_trace(tracegen.get_config(args.config)),
+                           args.cpu_seconds)
+    line = {
+        "metric": metric, "value": round(value, 4), "unit": "ticks/s (10k-program ticks, summed over GPUs)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": args.config, "programs_per_gpu": tr.n_slots, "replicas_per_gpu": 1,
+                   "kv": "Qwen3-32B GQA L64 H8 D128 bf16, 16-token blocks (4 MiB)",
+                   "hbm_blocks": pool.NB, "host_blocks": pool.NH, "preroll_ticks": args.preroll,
+                   "engine_fill": "off (engine stand-in, not a hot-path row)",
+                   "l2": "256 MiB memset before every timed step (inside the timed region)",
+                   "parallelism": f"dp{world} (one replica per GPU)"},
+        "clocks": clocks,
+        "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(d2h / args.steps),
+                "note": "public API ta_sched_step with decisions read back; trace uploaded once before timing"},
+        "gpu_launches": args.steps * 12,
+        "roofline": roofline,
+        "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
+        "sched_us_per_tick": round(sched_us, 1),
+        "kv_moved": moved,
+        "kv_paths": kv_paths,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pool.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -74,7 +74,7 @@ enum {
   TA_F_TRACE_MODE = 1u << 0,   /* program scripts come from ta_load_trace (closed-loop) */
   TA_F_FILL = 1u << 1,         /* write KV content for new/recomputed tokens (engine stand-in) */
   TA_F_NO_GRAPH = 1u << 2,     /* launch the tick kernel by kernel instead of a CUDA graph */
-  TA_F_TIMING = 1u << 3,       /* record per-phase CUDA events (implies no graph) */
+  TA_F_TIMING = 1u << 3,       /* record per-phase CUDA events (graph event-record nodes) */
   TA_F_COPY_BULK = 1u << 4     /* HBM->HBM copies via cp.async.bulk (TMA) instead of LDG/STG.128 */
 };
 
@@ -93,7 +93,7 @@ typedef struct {
   int64_t host_blocks;         /* NH per replica (0 = no host tier) */
   int64_t delta_t_ms;          /* Delta t of the periodic monitor (reading A1) */
   int64_t decay_unit_ms;       /* time unit of t_q in f(t_q) (reading A2) */
-  uint32_t lambda_max_q16;     /* high watermark, 65536 == 1.0 */
+  uint32_t lambda_max_q16;     /* high watermark, 65536 == 1.0; 0 < min <= max <= 65536 */
   uint32_t lambda_min_q16;     /* low watermark */
   uint64_t decay_q32[64];      /* F[k] = floor(f(k) * 2^32), F[0] = 2^32 (eq. 7) */
   int32_t decode_tok_per_s;    /* synthetic engine decode rate (trace mode) */
@@ -239,6 +239,20 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out);
  * [7] compaction copies [8] decision assembly.  n <= 9. */
 ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
 
+/* Block-list-driven KV movement (the copy engine of step 6, exposed directly):
+ * copy n whole KV blocks, block src_blocks[i] of the source pool to block
+ * dst_blocks[i] of the destination pool.  kind: TA_MOVE_D2D (HBM of src_replica
+ * to HBM of the same replica; dst_replica ignored), TA_MOVE_P2P (HBM of
+ * src_replica to HBM of dst_replica, over NVLink when the pools live on
+ * different GPUs), TA_MOVE_D2H (HBM of src_replica to its host tier),
+ * TA_MOVE_H2D (host tier of src_replica to HBM of dst_replica).
+ * src_blocks / dst_blocks are DEVICE pointers (caller-owned, n u32 each); the
+ * lists must not overlap in the destination.  Block tables and free sets are
+ * not touched.  Enqueued on the context stream.  Errors: TA_E_INVAL. */
+enum { TA_MOVE_D2D = 1, TA_MOVE_P2P = 2, TA_MOVE_D2H = 3, TA_MOVE_H2D = 4 };
+ta_status ta_move_blocks(ta_ctx* ctx, int32_t kind, int32_t src_replica, int32_t dst_replica,
+                         const uint32_t* src_blocks, const uint32_t* dst_blocks, int32_t n);
+
 /* Count KV words that differ from the content closed form
  * over every valid token slot of every owned HBM and host block of the local
  * replicas (test aid; needs TA_F_FILL runs).  Synchronizes. */
@@ -248,10 +262,17 @@ ta_status ta_verify_content(ta_ctx* ctx, uint64_t* mismatched_words, uint64_t* c
  * fields required except the download-only ones).  Synchronizes. */
 ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v);
 
-/* Multi-GPU: export this process's local HBM pool as a 64-byte CUDA IPC handle,
- * and map a peer replica's pool from its handle (sets hbm_pool[replica]). */
-ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle64);
-ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle64);
+/* Multi-GPU, one replica per process (replicas_here == 1, first_replica = rank):
+ * ta_export_pool_handle writes TA_HANDLE_BYTES describing this process's HBM pool
+ * and its barrier mailbox (CUDA IPC handles + offset); every peer passes it to
+ * ta_import_peer_pool, which maps that replica's pool (P2P over NVLink) and
+ * mailbox.  All peers must be imported before the first tick; each tick then
+ * runs two device-side barriers (after evictions, after fetches/pushes) and
+ * pushes host-tier fetches whose destination lives in another process.
+ * Errors: TA_E_INVAL (arguments), TA_E_PEER (IPC failure; poisons the context). */
+#define TA_HANDLE_BYTES 192
+ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle);        /* handle: TA_HANDLE_BYTES */
+ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle);
 
 ta_status ta_destroy(ta_ctx* ctx);
 const char* ta_last_error(const ta_ctx* ctx);

@@ -607,12 +607,19 @@ class Oracle:
         """All-or-nothing validation in order (SURVEY.md §8(c) API table)."""
         status = {}
         phase = {}
+        ctx = {}
+        cap = self.MAXB * self.bt          # contexts are bounded by max_ctx (reading A35)
         for ev in events:
             kind, pid = ev[0], ev[1]
             if pid >= self.N:
                 return E_UNKNOWN_PROGRAM
             st = status.get(pid, self.status[pid])
             ph = phase.get(pid, self.phase[pid])
+            if kind in (E_ARRIVE, E_DECODE, E_TOOL_RESULT):
+                c = ev[3] if kind == E_ARRIVE else ctx.get(pid, self.c[pid]) + ev[3]
+                if c > cap and not (kind == E_ARRIVE and st != UNARRIVED):
+                    return E_INVAL
+                ctx[pid] = c
             if kind == E_ARRIVE:
                 if st != UNARRIVED:
                     return E_DUP_ID                       # SPEC.md:56

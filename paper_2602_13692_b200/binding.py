@@ -115,6 +115,7 @@ def lib():
             "ta_phase_times": [vp, C.POINTER(C.c_float), i32],
             "ta_verify_content": [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
             "ta_debug_state": [vp, i32, vp],
+            "ta_move_blocks": [vp, i32, i32, i32, vp, vp, i32],
             "ta_export_pool_handle": [vp, vp],
             "ta_import_peer_pool": [vp, i32, vp],
             "ta_destroy": [vp],
@@ -133,7 +134,8 @@ def lib():
 EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
-            "ta_last_error", "ta_abi_version")
+            "ta_last_error", "ta_abi_version", "ta_move_blocks")
+MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
 def decay_q32(x: int) -> list:
@@ -227,6 +229,18 @@ class Pool:
         if st != TA_OK:
             raise TAError(st, "ta_init_pool failed")
         self.dec_buf = np.zeros(4 * n_programs + self.R + 64, dtype=DECISION_DTYPE)
+
+    def reset(self):
+        """Destroy the context and create a fresh one over the same buffers (the
+        workspace is re-initialised: every slot UNARRIVED, all blocks free)."""
+        import torch
+        self.close()
+        self.ctx = C.c_void_p()
+        with torch.cuda.device(self.device):
+            st = lib().ta_init_pool(C.byref(self.c), C.byref(self.buffers),
+                                    C.c_void_p(self.stream.cuda_stream), None, C.byref(self.ctx))
+        if st != TA_OK:
+            raise TAError(st, "ta_init_pool (reset) failed")
 
     # ------------------------------------------------------------------ helpers
     def _chk(self, st, what):
@@ -344,6 +358,12 @@ class Pool:
             keep[n] = a
             setattr(v, n, a.ctypes.data_as(C.POINTER(t)))
         self._chk(lib().ta_debug_state(self.ctx, 1, C.byref(v)), "ta_debug_state upload")
+
+    def move_blocks(self, kind: int, src_r: int, dst_r: int, src_idx, dst_idx):
+        """ta_move_blocks with device index tensors (torch int32/uint32 on this device)."""
+        n = int(src_idx.numel())
+        self._chk(lib().ta_move_blocks(self.ctx, kind, src_r, dst_r, src_idx.data_ptr(),
+                                       dst_idx.data_ptr(), n), "ta_move_blocks")
 
     def export_handle(self) -> bytes:
         h = (C.c_char * 64)()

@@ -68,6 +68,7 @@ struct Dev {
   i64 seg_bytes, block_bytes;
   int first_local, n_local;
   int api_mode;
+  u32 nbk, nb_shift;               // coarse-key buckets: nb >> nb_shift < nbk <= 2048
   i64 cap_max[TA_MAX_REPLICAS], cap_min[TA_MAX_REPLICAS];
   ull F[64];
   char* hbm[TA_MAX_REPLICAS];      // device-addressable HBM pool per replica (NULL if not here)
@@ -83,6 +84,7 @@ struct Dev {
   u8* released;                    // released during this tick's ingest
   u8* sat_new;                     // 1 + replica that satisfied the program this tick
   u8* evs;                         // [3N] API-mode validation scratch (kept zero)
+  u32* evc;                        // [N]  API-mode tentative context lengths
   // ---- trace scripts ----
   int n_slots, n_initial;
   u32 *t_uid, *t_p0, *t_off, *t_g, *t_d, *t_o;
@@ -117,6 +119,11 @@ struct Dev {
   u32 dec_cap;
   ull* verify;                     // [2] mismatches, checked
   ta_event* events;                // [kMaxEvents] API-mode event batch
+  // ---- multi-process data plane (one replica per GPU) ----
+  int multi, rank;                 // multi: pools of other replicas live in other processes
+  ull* mbox;                       // [TA_MAX_REPLICAS] this rank's barrier mailbox (epochs)
+  ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
+  ull* epoch;                      // barrier epoch counter (device)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -318,6 +325,45 @@ __device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_
     cur ^= 1;
   }
   return cur;
+}
+
+// ------------------------------------------------------------------ exact prefix selection
+// The pause, restore and eviction passes consume only a PREFIX of their sorted
+// order.  bucket(i) is a coarse key monotone in the full sort key, so the items of
+// buckets [lo, T] are exactly the next stretch of the global order.  One pass
+// builds a weighted histogram in shared memory, a scan finds the smallest T whose
+// cumulative weight reaches `need`, and an ordered gather emits (slot order) the
+// items with lo <= bucket <= T; the caller then sorts only that subset.
+// s_hist: >= nbkt u32 (nbkt <= 8192).  Returns T (nbkt - 1 if need is never reached).
+template <typename Pred, typename Bucket, typename Weight>
+__device__ u32 cta_bucket_threshold(int n, u32 nbkt, u32 lo, ull need, u32* s_hist, u32* s_tmp,
+                                    Pred pred, Bucket bucket, Weight weight) {
+  __shared__ u32 s_T;
+  for (u32 b = threadIdx.x; b < nbkt; b += CTA) s_hist[b] = 0;
+  if (threadIdx.x == 0) s_T = nbkt - 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += CTA) {
+    if (!pred(i)) continue;
+    u32 b = bucket(i);
+    if (b >= lo) atomicAdd(&s_hist[b], weight(i));
+  }
+  __syncthreads();
+  {                                      // inclusive scan, 8 buckets per thread
+    const u32 per = (nbkt + CTA - 1) / CTA;
+    const u32 b0 = threadIdx.x * per;
+    ull s = 0;
+    for (u32 q = 0; q < per && b0 + q < nbkt; ++q) s += s_hist[b0 + q];
+    u32 total;
+    ull run = cta_excl_scan((u32)min(s, 0xFFFFFFFFull), s_tmp, &total);
+    for (u32 q = 0; q < per && b0 + q < nbkt; ++q) {
+      run += s_hist[b0 + q];
+      if (run >= need) { atomicMin(&s_T, b0 + q); break; }
+    }
+  }
+  __syncthreads();
+  const u32 T = s_T;
+  __syncthreads();
+  return T;
 }
 
 // ------------------------------------------------------------------ bitmap rank / select

@@ -85,6 +85,49 @@ __global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
   }
 }
 
+// Multi-process push: H2D fetches whose source is THIS process's host tier but whose
+// destination replica lives in another process: read the local pinned tier, store
+// into the peer's HBM pool over NVLink (mapped with CUDA IPC).
+__global__ void __launch_bounds__(256) k_copy_push(Dev d) {
+  if (!d.multi) return;
+  const int nseg = 2 * d.nL;
+  for (int r = 0; r < d.R; ++r) {
+    if (r >= d.first_local && r < d.first_local + d.n_local) continue;
+    const u32 n = d.fed_cnt[r];
+    const FeDesc* fe = d.fed + (size_t)r * d.NB;
+    for (i64 it = blockIdx.x; it < (i64)n * nseg; it += gridDim.x) {
+      FeDesc x = fe[it / nseg];
+      const int s = (int)(it % nseg);
+      if (x.kind != MV_H2D || d.host[x.src_r] == nullptr || d.hbm[r] == nullptr) continue;
+      const uint4* src = (const uint4*)seg_addr(d.host[x.src_r], d.layout, d.NH, d.seg_bytes, nseg, x.src, s);
+      uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
+      cta_copy16(src, dst, d.seg_bytes >> 4);
+    }
+  }
+  __threadfence_system();                // peer stores visible before the barrier flag
+}
+
+// Cross-process barrier through IPC-mapped mailboxes (one replica per GPU): lane i
+// publishes this rank's epoch into peer i's mailbox, then waits for peer i's epoch
+// in its own.  Bounded spin: a dead peer poisons the context instead of hanging.
+__global__ void k_barrier(Dev d) {
+  if (!d.multi) return;
+  __shared__ ull e;
+  if (threadIdx.x == 0) e = ++(*d.epoch);
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= d.R || i == d.rank) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(d.mbox_peer[i] + d.rank), "l"(e) : "memory");
+  ull v = 0;
+  for (long long spin = 0; spin < (1ll << 26); ++spin) {   // ~15 s worst case
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(d.mbox + i) : "memory");
+    if (v >= e) return;
+    if (spin > 64) __nanosleep(200);
+  }
+  d.ctr->err = TA_E_PEER;
+}
+
 // Two-finger compaction moves inside one replica's HBM pool (D2D).
 __global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
   const int nseg = 2 * d.nL;
@@ -96,6 +139,20 @@ __global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
     const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
     cta_copy16(src, dst, d.seg_bytes >> 4);
+  }
+}
+
+// ta_move_blocks: n whole blocks from one pool to another, block-list driven.
+__global__ void __launch_bounds__(256) k_move(Dev d, const char* sbase, i64 snb, char* dbase, i64 dnb,
+                                              const u32* __restrict__ src, const u32* __restrict__ dst, int n) {
+  const int nseg = 2 * d.nL;
+  const i64 items = (i64)n * nseg;
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    u32 e = (u32)(it / nseg);
+    int s = (int)(it % nseg);
+    const uint4* sp = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, src[e], s);
+    uint4* dp = (uint4*)seg_addr(dbase, d.layout, dnb, d.seg_bytes, nseg, dst[e], s);
+    cta_copy16(sp, dp, d.seg_bytes >> 4);
   }
 }
 

@@ -65,12 +65,22 @@ __global__ void k_apply_events(Dev d, const ta_event* ev, int n_ev, int apply) {
   u8* tst = d.evs;                       // [N] tentative status (zeroed marks between calls)
   u8* tph = tst + d.N;                   // [N] tentative phase
   u8* touched = tph + d.N;               // [N]
+  u32* tc = d.evc;                       // [N] tentative context length
+  const u64 cap = (u64)d.MAXB * (u64)d.bt;   // contexts are bounded by max_ctx (reading A35)
   int err = TA_OK;
   for (int i = 0; i < n_ev && err == TA_OK; ++i) {
     u32 pid = ev[i].pid;
     if (pid >= (u32)d.N) { err = TA_E_UNKNOWN_PROGRAM; break; }
-    if (!touched[pid]) { touched[pid] = 1; tst[pid] = d.status[pid]; tph[pid] = d.phase[pid]; }
+    if (!touched[pid]) {
+      touched[pid] = 1; tst[pid] = d.status[pid]; tph[pid] = d.phase[pid]; tc[pid] = d.c[pid];
+    }
     u8 st = tst[pid], ph = tph[pid];
+    const u32 kd = ev[i].kind;
+    if (kd == TA_EV_ARRIVE || kd == TA_EV_DECODE || kd == TA_EV_TOOL_RESULT) {
+      u64 c = kd == TA_EV_ARRIVE ? (u64)ev[i].tokens : (u64)tc[pid] + ev[i].tokens;
+      if (c > cap && !(kd == TA_EV_ARRIVE && st != TA_UNARRIVED)) { err = TA_E_INVAL; break; }
+      tc[pid] = (u32)c;
+    }
     switch (ev[i].kind) {
       case TA_EV_ARRIVE:
         if (st != TA_UNARRIVED) err = TA_E_DUP_ID; else { tst[pid] = TA_PAUSED; tph[pid] = TA_PHASE_R; }
@@ -139,14 +149,15 @@ __global__ void k_apply_events(Dev d, const ta_event* ev, int n_ev, int apply) {
 // Steps 0 (release frees, closed-loop arrivals) + 1 (footprint) + 2 (contribution,
 // L_eff): one warp per slot.  The block-table row is scanned with 16-byte loads;
 // counts come from ballot/popc, prefix_hbm from the first non-HBM entry.
-__global__ void __launch_bounds__(256) k_footprint(Dev d) {
+__global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const u32 lane = lane_id();
   if (p >= d.N) return;
   u32* row = d.loc + (size_t)p * d.MAXBP;
   const i64 k = d.ctr->tick;
-  const i64 T = d.api_mode ? d.ctr->now_ms : k * d.dt;
-  if (d.released[p]) {                   // free every block of a STOPPED program (A26)
+  // verbs act on the state left by the last tick, at its time T (no ingest, L kept)
+  const i64 T = verb ? d.ctr->T : (d.api_mode ? d.ctr->now_ms : k * d.dt);
+  if (!verb && d.released[p]) {                   // free every block of a STOPPED program (A26)
     const int h = d.home[p];
     const u32 nbv = ceil_div_u32(d.c[p], d.bt);
     for (u32 j = lane; j < nbv; j += 32) {
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(256) k_footprint(Dev d) {
     return;
   }
   u8 st = d.status[p];
-  if (!d.api_mode && st == TA_UNARRIVED) {       // closed-loop arrivals (A12)
+  if (!verb && !d.api_mode && st == TA_UNARRIVED) {       // closed-loop arrivals (A12)
     const i64 na = d.ctr->next_arrival;
     i64 n_arr = trace_arrivals(d);
     if (p >= na && p < na + n_arr && p < d.n_slots) {
@@ -220,6 +231,6 @@ __global__ void __launch_bounds__(256) k_footprint(Dev d) {
     d.prefix_hbm[p] = first == 0xFFFFFFFFu ? nbv : first;
     u32 cb = contrib_of(d, nbv, d.phase[p], d.acting_since[p], T);
     d.contrib[p] = cb;
-    if (st != TA_PAUSED) atomicAdd(&d.L[d.placement[p]], (ull)cb);   // commutative u64 sum
+    if (!verb && st != TA_PAUSED) atomicAdd(&d.L[d.placement[p]], (ull)cb);   // commutative u64 sum
   }
 }

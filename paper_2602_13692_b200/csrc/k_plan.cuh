@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   const int N = d.N;
   const u32 bt = (u32)d.bt;
   const bool fill = (d.flags & TA_F_FILL) != 0;
-  if (verb && r != d.ctr->verb_replica) return;
+  if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
+               d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
   if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
   if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
   u32* fp = d.f_pid + (size_t)r * N;
@@ -82,10 +83,23 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     u64* kb = d.skb + (size_t)r * N;
     u32* va = d.sva + (size_t)r * N;
     u32* vb = d.svb + (size_t)r * N;
+    // exact prefix of E covering X blocks: buckets monotone in the eviction order
+    const u32 NBK = d.nbk, sh = d.nb_shift;
+    auto epred = [&](int i) {
+      u8 s = d.status[i];
+      return d.home[i] == r && d.n_hbm[i] > 0 && (s == TA_PAUSED || s == TA_ACTING);
+    };
+    auto ebucket = [&](int i) -> u32 {
+      if (d.status[i] == TA_PAUSED)      // group 0: A first, nb descending
+        return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> sh));
+      return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> sh);
+    };
+    const u32 T = cta_bucket_threshold(N, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
+                                       [&](int i) { return d.n_hbm[i]; });
     u32 n0 = cta_ordered_gather(N, s_tmp,
         [&](int ii) {
           int i = N - 1 - ii;            // descending slot: ties in group 0 go slot-down
-          return d.home[i] == r && d.n_hbm[i] > 0 && d.status[i] == TA_PAUSED;
+          return epred(i) && d.status[i] == TA_PAUSED && ebucket(i) <= T;
         },
         [&](u32 pos, int ii) {
           int i = N - 1 - ii;
@@ -94,7 +108,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
           va[pos] = (u32)i;
         });
     u32 n12 = cta_ordered_gather(N, s_tmp,
-        [&](int i) { return d.home[i] == r && d.n_hbm[i] > 0 && d.status[i] == TA_ACTING; },
+        [&](int i) { return epred(i) && d.status[i] == TA_ACTING && ebucket(i) <= T; },
         [&](u32 pos, int i) {
           u64 g = d.placement[i] != r ? 1 : 2;
           ka[n0 + pos] = (g << 62) | d.contrib[i];

@@ -1,0 +1,167 @@
+// k_verb.cuh — explicit single-program verbs (ta_pause / ta_resume / ta_migrate).
+// They act on the state left by the last tick, at its time T (SURVEY.md §8(c) "API-mode
+// events and explicit verbs"); resume/migrate reuse k_footprint, k_plan (F = {pid},
+// all-or-nothing), the copy kernels, k_finalize and k_assemble in verb mode.
+#pragma once
+#include "common.cuh"
+
+// Clear every per-call list so the shared copy / assembly kernels see only this verb.
+__global__ void k_verb_reset(Dev d) {
+  int t = threadIdx.x;
+  if (t == 0) { d.ctr->restore_cnt = 0; d.ctr->err = TA_OK; d.ctr->verb_ok = 1; }
+  if (t < d.R) {
+    d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
+    d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
+    d.cpd_cnt[t] = 0;
+  }
+}
+
+// ta_pause: LAZY only unbinds; OFFLOAD evicts every HBM block of the
+// program tail-first into the lowest free host slots of its home (drop when full);
+// DROP frees them.  One CTA.
+__global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  __shared__ int s_err, s_r, s_h;
+  __shared__ u32 s_nh;
+  if (threadIdx.x == 0) {
+    int err = TA_OK;
+    u8 st = pid < (u32)d.N ? d.status[pid] : TA_UNARRIVED;
+    if (pid >= (u32)d.N || st == TA_UNARRIVED) err = TA_E_UNKNOWN_PROGRAM;
+    else if (st != TA_REASONING && st != TA_ACTING) err = TA_E_ILLEGAL_TRANSITION;
+    s_err = err;
+    d.ctr->err = err;
+    if (err == TA_OK) {
+      const int r = d.placement[pid];
+      const u32 nbv = ceil_div_u32(d.c[pid], d.bt);
+      const u32 cb = contrib_of(d, nbv, d.phase[pid], d.acting_since[pid], d.ctr->T);
+      d.L[r] -= cb;
+      d.status[pid] = TA_PAUSED;
+      d.placement[pid] = -1;
+      d.paused_since[pid] = (u32)d.ctr->tick;
+      d.satisfied[pid] = 0;
+      d.pause_list[(size_t)r * d.N] = pid;
+      d.pause_cnt[r] = 1;
+      d.stats[ST_PAUSES] += 1;
+      s_r = r;
+      s_h = d.home[pid];
+      u32 nh = 0;                          // HBM prefix length (I10)
+      const u32* row = d.loc + (size_t)pid * d.MAXBP;
+      while (nh < nbv && is_hbm(row[nh])) ++nh;
+      s_nh = (mode == TA_PAUSE_LAZY || s_h < 0) ? 0 : nh;
+    }
+  }
+  __syncthreads();
+  if (s_err != TA_OK || s_nh == 0) return;
+  const int h = s_h;
+  const u32 X = s_nh;
+  u32* row = d.loc + (size_t)pid * d.MAXBP;
+  const u32* sf = d.host_free + (size_t)h * d.NHW;
+  u32 hfree = 0;
+  if (mode == TA_PAUSE_OFFLOAD) {
+    cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
+    hfree = s_big[d.NHW];
+  }
+  EvDesc* evd = d.evd + (size_t)h * d.NB;
+  u32* scr = d.evx + (size_t)h * d.NB;
+  for (u32 e = threadIdx.x; e < X; e += CTA) {
+    u32 j = X - 1 - e;                    // tail first
+    u32 idx = row[j];
+    scr[e] = idx;
+    if (e < hfree) {
+      u32 slot = bitmap_select(sf, s_big, d.NHW, e);
+      row[j] = LOC_HOST | slot;
+      d.owner_host[(size_t)h * d.NH + slot] = pid * (u32)d.MAXB + j;
+      evd[e].src = idx;
+      evd[e].dst = slot;
+    } else {
+      row[j] = LOC_NONE;
+    }
+  }
+  __syncthreads();
+  u32* hf = d.hbm_free + (size_t)h * d.NBW;
+  u32* shf = d.host_free + (size_t)h * d.NHW;
+  for (u32 e = threadIdx.x; e < X; e += CTA) {
+    u32 idx = scr[e];
+    atomicOr(&hf[idx >> 5], 1u << (idx & 31));
+    if (e < hfree) {
+      u32 slot = evd[e].dst;
+      atomicAnd(&shf[slot >> 5], ~(1u << (slot & 31)));
+    }
+  }
+  if (threadIdx.x == 0) {
+    u32 toh = min(X, hfree);
+    ta_decision rec = {};
+    rec.kind = TA_D_EVICT; rec.pid = pid; rec.src = h; rec.dst = -1; rec.blocks = X;
+    rec.to_host = toh; rec.dropped = X - toh;
+    d.dec_ev[(size_t)h * d.N] = rec;
+    d.ev_cnt[h] = 1;
+    d.evd_cnt[h] = toh;
+    d.stats[ST_EVICT_BLOCKS] += X;
+    d.stats[ST_EVICT_TO_HOST] += toh;
+    d.stats[ST_EVICT_DROPPED] += X - toh;
+  }
+}
+
+// ta_resume / ta_migrate admission (one thread): legality, capacity,
+// target choice (step-4 argmin when replica < 0), tentative activation.  A phase-R
+// program then runs k_plan in verb mode (all-or-nothing); k_verb_commit finishes.
+__global__ void k_verb_admit(Dev d, u32 pid, int replica, int migrate) {
+  if (threadIdx.x != 0) return;
+  int err = TA_OK;
+  u8 st = pid < (u32)d.N ? d.status[pid] : TA_UNARRIVED;
+  if (pid >= (u32)d.N || st == TA_UNARRIVED) err = TA_E_UNKNOWN_PROGRAM;
+  else if (!migrate && st != TA_PAUSED) err = TA_E_ILLEGAL_TRANSITION;
+  else if (migrate && st != TA_REASONING && st != TA_ACTING) err = TA_E_ILLEGAL_TRANSITION;
+  else if (replica >= d.R || replica < -1 || (migrate && (replica < 0 || replica == d.placement[pid])))
+    err = TA_E_INVAL;
+  int t = replica;
+  const ull cr = err == TA_OK ? d.contrib[pid] : 0;
+  if (err == TA_OK) {
+    if (t < 0) {                           // least loaded candidate (step 4 rule)
+      u64 best = ~0ull;
+      for (int r = 0; r < d.R; ++r) {
+        ull L = d.L[r];
+        if (L < (ull)d.cap_min[r] && L + cr <= (ull)d.cap_max[r]) {
+          u64 key = (L << 6) | ((u64)(r != d.home[pid]) << 5) | (u64)r;
+          if (key < best) best = key;
+        }
+      }
+      if (best == ~0ull) err = TA_E_CAPACITY; else t = (int)(best & 31);
+    } else if (d.L[t] + cr > (ull)d.cap_max[t]) {
+      err = TA_E_CAPACITY;
+    }
+  }
+  d.ctr->err = err;
+  if (err != TA_OK) return;
+  const int src = migrate ? d.placement[pid] : d.home[pid];
+  d.ctr->verb_pid = pid;
+  d.ctr->verb_replica = t;
+  d.ctr->n_arr = (u32)(d.placement[pid] + 1) | ((u32)st << 8);   // saved for a revert
+  d.status[pid] = d.phase[pid] == TA_PHASE_R ? TA_REASONING : TA_ACTING;
+  d.placement[pid] = (i8)t;
+  d.restore_pid[0] = pid;
+  d.restore_dst[0] = (u32)t | ((u32)(src + 1) << 8) | ((u32)migrate << 16);
+  d.ctr->restore_cnt = 1;
+  d.ctr->verb_ok = 1;
+}
+
+// After k_plan: revert when the physical fetch could not be satisfied, else book the load.
+__global__ void k_verb_commit(Dev d, int migrate) {
+  if (threadIdx.x != 0 || d.ctr->err != TA_OK) return;
+  const u32 pid = d.ctr->verb_pid;
+  const int t = d.ctr->verb_replica;
+  if (!d.ctr->verb_ok) {
+    u32 saved = d.ctr->n_arr;
+    d.placement[pid] = (i8)((int)(saved & 0xFF) - 1);
+    d.status[pid] = (u8)(saved >> 8);
+    d.ctr->restore_cnt = 0;
+    d.ctr->err = TA_E_CAPACITY;
+    return;
+  }
+  const ull cr = d.contrib[pid];
+  const int old = (int)(d.ctr->n_arr & 0xFF) - 1;
+  if (old >= 0) d.L[old] -= cr;
+  d.L[t] += cr;
+  if (!migrate) d.stats[ST_RESTORES] += 1;
+}

@@ -3,6 +3,8 @@
 // Owns no memory: every buffer comes from the caller (ta_buffers).  The tick is a
 // fixed sequence of kernels on the caller's stream; in trace mode it is captured
 // once into a CUDA graph and replayed (all sizes are read on the device).
+#include <cuda.h>
+
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -14,6 +16,7 @@
 #include "k_ingest.cuh"
 #include "k_plan.cuh"
 #include "k_sched.cuh"
+#include "k_verb.cuh"
 
 namespace {
 
@@ -54,6 +57,9 @@ struct ta_ctx {
   size_t block_bytes = 0;
   cudaEvent_t ev[10] = {};
   bool timing = false;
+  void* mbox_alloc = nullptr;               // barrier mailbox (library-owned, 264 B)
+  void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
+  void* peer_mbox[TA_MAX_REPLICAS] = {};    // IPC-opened peer mailboxes
 };
 
 #define FAIL(ctx, code, ...)                                          \
@@ -97,6 +103,8 @@ static const char* validate(const ta_config* c) {
   if (c->hbm_blocks < 1 || c->hbm_blocks > 131040) return "hbm_blocks must be in [1, 131040]";
   if (c->host_blocks < 0 || c->host_blocks > 262112) return "host_blocks must be in [0, 262112]";
   if (c->delta_t_ms <= 0 || c->decay_unit_ms <= 0) return "delta_t_ms and decay_unit_ms must be > 0";
+  if (c->lambda_min_q16 == 0 || c->lambda_min_q16 > c->lambda_max_q16 || c->lambda_max_q16 > 65536)
+    return "watermarks must satisfy 0 < lambda_min <= lambda_max <= 1 (SPEC.md:190)";
   if (c->decode_tok_per_s < 0 || c->compact_every < 0 || c->max_trace_turns < 0) return "negative rate/compact/turns";
   return nullptr;
 }
@@ -122,6 +130,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.nb = L.take<u32>(N); x.n_hbm = L.take<u32>(N); x.n_host = L.take<u32>(N);
   x.prefix_hbm = L.take<u32>(N); x.contrib = L.take<u32>(N);
   x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
+  x.evc = L.take<u32>(N);
   x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
   x.t_g = L.take<u32>(TT); x.t_d = L.take<u32>(TT); x.t_o = L.take<u32>(TT);
   x.hbm_free = L.take<u32>(R * NBW); x.host_free = L.take<u32>(R * NHW);
@@ -180,7 +189,8 @@ __global__ void k_init(Dev d) {
 
 // ------------------------------------------------------------------ tick launch sequence
 static void rec(ta_ctx* x, int i) {
-  if (x->timing) cudaEventRecord(x->ev[i], x->stream);
+  // external event-record nodes keep working inside the captured CUDA graph
+  if (x->timing) cudaEventRecordWithFlags(x->ev[i], x->stream, cudaEventRecordExternal);
 }
 
 static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
@@ -191,7 +201,7 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   k_begin<<<1, 32, 0, s>>>(d);
   if (d.api_mode) k_apply_events<<<1, 32, 0, s>>>(d, x->ev_dev, n_ev, 1);
   else k_ingest_trace<<<(N + 255) / 256, 256, 0, s>>>(d);
-  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);
+  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 0);
   rec(x, 1);
   k_pause<<<R, CTA, 0, s>>>(d);
   k_restore<<<1, CTA, 0, s>>>(d);
@@ -199,8 +209,13 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   k_plan<<<R, CTA, 0, s>>>(d, 0);
   rec(x, 3);
   k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);   // evicted blocks read before peers refill them
   rec(x, 4);
   k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) {
+    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
+    k_barrier<<<1, 32, 0, s>>>(d);               // fetches landed; P2P sources read
+  }
   rec(x, 5);
   if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
   rec(x, 6);
@@ -217,6 +232,26 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
 static ta_status check_ctx(ta_ctx* ctx) {
   if (!ctx) return TA_E_INVAL;
   if (ctx->poisoned) return (ta_status)ctx->poisoned;
+  return TA_OK;
+}
+
+// Multi-process contexts need every peer's pool and mailbox before any data movement.
+static ta_status check_peers(ta_ctx* ctx) {
+  if (!ctx->d.multi) return TA_OK;
+  for (int r = 0; r < ctx->d.R; ++r)
+    if (r != ctx->d.rank && (!ctx->d.hbm[r] || !ctx->d.mbox_peer[r]))
+      FAIL(ctx, TA_E_STATE, "peer replica %d not imported (ta_import_peer_pool)", r);
+  return TA_OK;
+}
+
+// A barrier that timed out (dead peer) poisons the context.
+static ta_status check_device_err(ta_ctx* ctx) {
+  CK(ctx, cudaMemcpyAsync(ctx->h.scal + 2, &ctx->d.ctr->err, sizeof(i32), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (*(i32*)(ctx->h.scal + 2) == TA_E_PEER) {
+    ctx->poisoned = TA_E_PEER;
+    FAIL(ctx, TA_E_PEER, "cross-process barrier timed out");
+  }
   return TA_OK;
 }
 
@@ -285,6 +320,9 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.seg_bytes = (i64)cfg->block_tokens * cfg->n_kv_heads * cfg->head_dim * cfg->elem_bytes;
   d.block_bytes = (i64)x->block_bytes;
   d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
+  d.nb_shift = 0;
+  while (((u32)d.MAXB >> d.nb_shift) + 1 > 2048) ++d.nb_shift;
+  d.nbk = ((u32)d.MAXB >> d.nb_shift) + 1;
   d.api_mode = (cfg->flags & TA_F_TRACE_MODE) ? 0 : 1;
   for (int r = 0; r < d.R; ++r) {
     d.cap_max[r] = (i64)(((u64)cfg->lambda_max_q16 * (u64)d.NB) >> 16);
@@ -317,6 +355,20 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.n_slots = 0;
   d.n_initial = 0;
   x->timing = (cfg->flags & TA_F_TIMING) != 0;
+  d.multi = cfg->replicas_here < cfg->n_replicas ? 1 : 0;
+  d.rank = cfg->first_replica;
+  if (d.multi && cfg->replicas_here != 1) {
+    fprintf(stderr, "ta_init_pool: multi-process mode needs replicas_here == 1\n");
+    delete x;
+    return TA_E_INVAL;
+  }
+  if (cudaMalloc(&x->mbox_alloc, (TA_MAX_REPLICAS + 1) * sizeof(ull)) != cudaSuccess ||
+      cudaMemset(x->mbox_alloc, 0, (TA_MAX_REPLICAS + 1) * sizeof(ull)) != cudaSuccess) {
+    delete x;
+    return TA_E_CUDA;
+  }
+  d.mbox = (ull*)x->mbox_alloc;
+  d.epoch = d.mbox + TA_MAX_REPLICAS;
   size_t dev_bytes = carve(cfg, nullptr, nullptr);
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
@@ -370,6 +422,7 @@ ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t
   Dev& d = ctx->d;
   cudaStream_t s = ctx->stream;
   if (n_ev < 0 || (n_ev > 0 && !ev) || out_cap < 0) FAIL(ctx, TA_E_INVAL, "bad event/output arguments");
+  if (ta_status ps = check_peers(ctx)) return ps;
   if (!d.api_mode) {
     if (n_ev) FAIL(ctx, TA_E_STATE, "events passed in trace mode");
     if (!ctx->trace_loaded) FAIL(ctx, TA_E_STATE, "no trace loaded");
@@ -379,7 +432,7 @@ ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t
       CK(ctx, cudaStreamSynchronize(s));
       if (now_ms != ctx->h.scal[0] * d.dt) FAIL(ctx, TA_E_INVAL, "now_ms %lld != tick*delta_t", (long long)now_ms);
     }
-    const bool use_graph = !(ctx->cfg.flags & (TA_F_NO_GRAPH | TA_F_TIMING));
+    const bool use_graph = !(ctx->cfg.flags & TA_F_NO_GRAPH);
     if (use_graph) {
       if (!ctx->graph) {
         cudaGraph_t g;
@@ -414,6 +467,8 @@ ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t
   }
   if (!out && !n_out) return TA_OK;
   CK(ctx, cudaStreamSynchronize(s));
+  if (d.multi)
+    if (ta_status de = check_device_err(ctx)) return de;
   return copy_out(ctx, out, out_cap, n_out);
 }
 
@@ -452,6 +507,30 @@ ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n) {
     CK(ctx, cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]));
     us[i] = ms * 1000.f;
   }
+  return TA_OK;
+}
+
+ta_status ta_move_blocks(ta_ctx* ctx, int32_t kind, int32_t src_r, int32_t dst_r, const uint32_t* src_blocks,
+                         const uint32_t* dst_blocks, int32_t n) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  Dev& d = ctx->d;
+  if (n < 0 || (n > 0 && (!src_blocks || !dst_blocks))) FAIL(ctx, TA_E_INVAL, "bad block lists");
+  if (src_r < 0 || src_r >= d.R) FAIL(ctx, TA_E_INVAL, "bad src replica");
+  if (kind == TA_MOVE_D2D || kind == TA_MOVE_D2H) dst_r = src_r;
+  if (dst_r < 0 || dst_r >= d.R) FAIL(ctx, TA_E_INVAL, "bad dst replica");
+  const char* sb = nullptr;
+  char* db = nullptr;
+  i64 snb = d.NB, dnb = d.NB;
+  switch (kind) {
+    case TA_MOVE_D2D: case TA_MOVE_P2P: sb = d.hbm[src_r]; db = d.hbm[dst_r]; break;
+    case TA_MOVE_D2H: sb = d.hbm[src_r]; db = d.host[src_r]; dnb = d.NH; break;
+    case TA_MOVE_H2D: sb = d.host[src_r]; db = d.hbm[dst_r]; snb = d.NH; break;
+    default: FAIL(ctx, TA_E_INVAL, "bad move kind %d", kind);
+  }
+  if (!sb || !db) FAIL(ctx, TA_E_INVAL, "pool not addressable from this process");
+  if (n == 0) return TA_OK;
+  k_move<<<kCopyGrid, 256, 0, ctx->stream>>>(d, sb, snb, db, dnb, src_blocks, dst_blocks, n);
+  CK(ctx, cudaGetLastError());
   return TA_OK;
 }
 
@@ -516,44 +595,118 @@ ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v) {
   return TA_OK;
 }
 
+// Verbs: enqueue, synchronize, read the device-side status, return the decisions.
+static ta_status verb_finish(ta_ctx* ctx, const char* what, ta_decision* out, int32_t out_cap, int32_t* n_out) {
+  Dev& d = ctx->d;
+  CK(ctx, cudaGetLastError());
+  CK(ctx, cudaMemcpyAsync(ctx->h.scal + 1, &d.ctr->err, sizeof(i32), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  int err = (int)*(i32*)(ctx->h.scal + 1);
+  if (n_out) *n_out = 0;
+  if (err != TA_OK) FAIL(ctx, (ta_status)err, "%s rejected", what);
+  return copy_out(ctx, out, out_cap, n_out);
+}
+
 ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, int32_t out_cap, int32_t* n_out) {
   if (ta_status s = check_ctx(ctx)) return s;
-  (void)pid; (void)mode; (void)out; (void)out_cap; (void)n_out;
-  FAIL(ctx, TA_E_STATE, "ta_pause: not implemented yet");
+  if (mode > TA_PAUSE_DROP || out_cap < 0) FAIL(ctx, TA_E_INVAL, "bad pause mode / out_cap");
+  if (ta_status ps = check_peers(ctx)) return ps;
+  Dev& d = ctx->d;
+  cudaStream_t s = ctx->stream;
+  k_verb_reset<<<1, 32, 0, s>>>(d);
+  k_verb_pause<<<1, CTA, 0, s>>>(d, pid, mode);
+  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
+  k_assemble<<<1, CTA, 0, s>>>(d, 1);
+  return verb_finish(ctx, "ta_pause", out, out_cap, n_out);
+}
+
+static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrate, ta_decision* out,
+                          int32_t out_cap, int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (out_cap < 0) FAIL(ctx, TA_E_INVAL, "bad out_cap");
+  if (ta_status ps = check_peers(ctx)) return ps;
+  Dev& d = ctx->d;
+  cudaStream_t s = ctx->stream;
+  const int N = d.N;
+  k_verb_reset<<<1, 32, 0, s>>>(d);
+  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 1);
+  k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
+  k_plan<<<d.R, CTA, 0, s>>>(d, 1);
+  k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
+  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
+  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) {
+    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
+    k_barrier<<<1, 32, 0, s>>>(d);
+  }
+  if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
+  k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 1);
+  k_assemble<<<1, CTA, 0, s>>>(d, 1);
+  return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);
 }
 
 ta_status ta_resume(ta_ctx* ctx, uint32_t pid, int32_t replica, ta_decision* out, int32_t out_cap, int32_t* n_out) {
-  if (ta_status s = check_ctx(ctx)) return s;
-  (void)pid; (void)replica; (void)out; (void)out_cap; (void)n_out;
-  FAIL(ctx, TA_E_STATE, "ta_resume: not implemented yet");
+  return activate(ctx, pid, replica, 0, out, out_cap, n_out);
 }
 
 ta_status ta_migrate(ta_ctx* ctx, uint32_t pid, int32_t dst, ta_decision* out, int32_t out_cap, int32_t* n_out) {
-  if (ta_status s = check_ctx(ctx)) return s;
-  (void)pid; (void)dst; (void)out; (void)out_cap; (void)n_out;
-  FAIL(ctx, TA_E_STATE, "ta_migrate: not implemented yet");
+  return activate(ctx, pid, dst, 1, out, out_cap, n_out);
 }
 
-ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle64) {
+// handle layout: [0,64) pool IPC handle | [64,72) pool offset in its allocation |
+// [72,136) mailbox IPC handle | [136,192) reserved
+ta_status ta_export_pool_handle(ta_ctx* ctx, void* handle) {
   if (ta_status s = check_ctx(ctx)) return s;
-  if (!handle64) return TA_E_INVAL;
+  if (!handle || !ctx->d.multi) FAIL(ctx, TA_E_INVAL, "export needs a multi-process context");
+  char* out = (char*)handle;
+  memset(out, 0, TA_HANDLE_BYTES);
+  void* pool = ctx->bufs.hbm_pool[ctx->cfg.first_replica];
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  // driver entry point through the runtime (no link-time libcuda dependency)
+  typedef CUresult (*range_fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      ((range_fn)fn)(&base, &size, (CUdeviceptr)pool) != CUDA_SUCCESS)
+    { ctx->poisoned = TA_E_PEER; FAIL(ctx, TA_E_PEER, "cuMemGetAddressRange failed"); }
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, ctx->bufs.hbm_pool[ctx->cfg.first_replica]);
-  if (e != cudaSuccess) { ctx->err = cudaGetErrorString(e); ctx->poisoned = TA_E_PEER; return TA_E_PEER; }
-  memcpy(handle64, &h, sizeof(h));
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+  if (e == cudaSuccess) {
+    memcpy(out, &h, 64);
+    u64 off = (u64)((CUdeviceptr)pool - base);
+    memcpy(out + 64, &off, 8);
+    e = cudaIpcGetMemHandle(&h, ctx->mbox_alloc);
+    memcpy(out + 72, &h, 64);
+  }
+  if (e != cudaSuccess) { ctx->poisoned = TA_E_PEER; FAIL(ctx, TA_E_PEER, "%s", cudaGetErrorString(e)); }
   return TA_OK;
 }
 
-ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle64) {
+ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle) {
   if (ta_status s = check_ctx(ctx)) return s;
-  if (!handle64 || replica < 0 || replica >= ctx->d.R) return TA_E_INVAL;
+  if (!handle || replica < 0 || replica >= ctx->d.R || replica == ctx->d.rank || !ctx->d.multi)
+    FAIL(ctx, TA_E_INVAL, "bad peer replica %d", replica);
+  const char* in = (const char*)handle;
   cudaIpcMemHandle_t h;
-  memcpy(&h, handle64, sizeof(h));
+  u64 off;
+  memcpy(&h, in, 64);
+  memcpy(&off, in + 64, 8);
   void* p = nullptr;
+  void* m = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
-  if (e != cudaSuccess) { ctx->err = cudaGetErrorString(e); ctx->poisoned = TA_E_PEER; return TA_E_PEER; }
-  ctx->bufs.hbm_pool[replica] = p;
-  ctx->d.hbm[replica] = (char*)p;
+  if (e == cudaSuccess) {
+    memcpy(&h, in + 72, 64);
+    e = cudaIpcOpenMemHandle(&m, h, cudaIpcMemLazyEnablePeerAccess);
+  }
+  if (e != cudaSuccess) { ctx->poisoned = TA_E_PEER; FAIL(ctx, TA_E_PEER, "%s", cudaGetErrorString(e)); }
+  ctx->peer_base[replica] = p;
+  ctx->peer_mbox[replica] = m;
+  ctx->bufs.hbm_pool[replica] = (char*)p + off;
+  ctx->d.hbm[replica] = (char*)p + off;
+  ctx->d.mbox_peer[replica] = (ull*)m;
   if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
   return TA_OK;
 }
@@ -564,10 +717,11 @@ ta_status ta_destroy(ta_ctx* ctx) {
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   for (int i = 0; i < 10; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
-  for (int r = 0; r < ctx->d.R; ++r) {
-    bool local = r >= ctx->cfg.first_replica && r < ctx->cfg.first_replica + ctx->cfg.replicas_here;
-    if (!local && ctx->bufs.hbm_pool[r]) cudaIpcCloseMemHandle(ctx->bufs.hbm_pool[r]);
+  for (int r = 0; r < TA_MAX_REPLICAS; ++r) {
+    if (ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
+    if (ctx->peer_mbox[r]) cudaIpcCloseMemHandle(ctx->peer_mbox[r]);
   }
+  if (ctx->mbox_alloc) cudaFree(ctx->mbox_alloc);
   delete ctx;
   return TA_OK;
 }

@@ -1,0 +1,120 @@
+"""GPU parity of the API-mode event path and of the explicit verbs (ta_pause /
+ta_resume / ta_migrate) against the oracle, on random legal and illegal inputs."""
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import tracegen  # noqa: E402
+from tests.gpu_compare import compare_state, dec_tuples  # noqa: E402
+from tests.test_gpu_parity import need_gpu, stress  # noqa: E402
+
+A, DEC, TC, TR, REL = (oracle.E_ARRIVE, oracle.E_DECODE, oracle.E_TOOL_CALL, oracle.E_TOOL_RESULT,
+                       oracle.E_RELEASE)
+
+
+def random_events(o, rng, T, n_max=12, illegal_p=0.1):
+    """Events that are legal for the oracle's current state (plus, sometimes, one illegal)."""
+    evs = []
+    used = set()
+    for _ in range(rng.randint(0, n_max)):
+        p = rng.randrange(o.N)
+        if p in used:
+            continue
+        st, ph = o.status[p], o.phase[p]
+        if st == oracle.UNARRIVED:
+            evs.append((A, p, 1000 + p, rng.randint(1, 400), 0))
+        elif st == oracle.REASONING:
+            r = rng.random()
+            if r < 0.5:
+                evs.append((DEC, p, 0, rng.randint(1, 200), 0))
+            elif r < 0.9:
+                evs.append((TC, p, 0, 0, max(0, T - rng.randint(0, 9000))))
+            else:
+                evs.append((REL, p, 0, 0, 0))
+        elif ph == oracle.PHASE_A and st in (oracle.ACTING, oracle.PAUSED):
+            evs.append((TR, p, 0, rng.randint(0, 300), 0) if rng.random() < 0.8 else (REL, p, 0, 0, 0))
+        elif st == oracle.STOPPED and rng.random() < 0.2:
+            evs.append((REL, p, 0, 0, 0))      # idempotent
+        used.add(p)
+    if rng.random() < illegal_p and evs:
+        p = evs[0][1]
+        evs.append((DEC, p, 0, 1, 0) if o.status[p] != oracle.REASONING else (A, p, 1, 1, 0))
+    return evs
+
+
+@pytest.mark.parametrize("seed,R", [(1, 1), (2, 2), (3, 3)])
+def test_gpu_api_mode_events(seed, R):
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = tracegen.get_config("c1_toy", n_replicas=R, hbm_blocks=48, host_blocks=16, max_ctx=4096,
+                              compact_every=4)
+    N = 40
+    o = oracle.Oracle(cfg, api_mode=True, n_slots=N)
+    pool = Pool(cfg, N, trace_mode=False)
+    rng = random.Random(seed)
+    errs = 0
+    for k in range(120):
+        T = 5000 * k
+        evs = random_events(o, rng, T)
+        st_o, dec_o = o.sched_step(T, evs)
+        st_g, dec_g = pool.step(T, evs, raise_on_error=False)
+        assert st_o == st_g, (k, st_o, st_g, evs)
+        if st_o != oracle.OK:
+            errs += 1
+            continue
+        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        if k % 5 == 0:
+            compare_state(o, pool.debug_download(), where=f"api tick {k}")
+        bad, _ = pool.verify_content()
+        assert bad == 0
+    assert errs > 0
+    pool.close()
+
+
+@pytest.mark.parametrize("seed,R", [(5, 2), (6, 3), (7, 1)])
+def test_gpu_verbs_random(seed, R):
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = stress(seed, R, NB=128 if R > 1 else 192)     # some headroom so resumes can succeed
+    tr = tracegen.make_trace(cfg)
+    o = oracle.Oracle(cfg, tr)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns)
+    pool.load_trace(tr)
+    rng = random.Random(seed)
+    n_ok = {"pause": 0, "resume": 0, "migrate": 0}
+    for k in range(80):
+        _, dec_o = o.sched_step()
+        _, dec_g = pool.step()
+        assert dec_tuples(dec_g) == dec_o
+        for _ in range(rng.randint(0, 3)):
+            verb = rng.choice(["pause", "resume", "migrate"])
+            want = {"pause": (oracle.REASONING, oracle.ACTING), "resume": (oracle.PAUSED,),
+                    "migrate": (oracle.REASONING, oracle.ACTING)}[verb]
+            pool_p = [q for q in range(o.N) if o.status[q] in want]
+            p = rng.choice(pool_p) if pool_p and rng.random() < 0.85 else rng.randrange(o.N)
+            if verb == "pause":
+                mode = rng.randrange(3)
+                st_o, d_o = o.pause(p, mode)
+                st_g, d_g = pool.pause(p, mode)
+            elif verb == "resume":
+                rep = rng.randrange(-1, R)
+                st_o, d_o = o.resume(p, rep)
+                st_g, d_g = pool.resume(p, rep)
+            else:
+                rep = rng.randrange(R)
+                st_o, d_o = o.migrate(p, rep)
+                st_g, d_g = pool.migrate(p, rep)
+            assert st_o == st_g, (k, verb, p, st_o, st_g)
+            if st_o == oracle.OK:
+                n_ok[verb] += 1
+                assert dec_tuples(d_g) == d_o, (k, verb, p)
+            compare_state(o, pool.debug_download(), where=f"tick {k} after {verb}({p})")
+        bad, _ = pool.verify_content()
+        assert bad == 0, f"tick {k}: {bad} KV words wrong"
+    assert n_ok["pause"] > 0 and n_ok["resume"] > 0 and (R == 1 or n_ok["migrate"] > 0), n_ok
+    pool.close()

@@ -91,3 +91,13 @@ def test_resume_capacity_when_fetch_cannot_fit():
     o.c[1] = 2
     st, dec = o.resume(1, 0)
     assert st == oracle.OK and dec[-1][0] == oracle.D_FETCH and dec[-1][4] == 2
+
+
+def test_context_bound_rejected():
+    """Reading A35: an event that would grow a context beyond max_ctx is rejected (E_INVAL)."""
+    o = api(max_ctx=300)
+    st, _ = o.sched_step(0, [(A, 0, 11, 301, 0)])
+    assert st == oracle.E_INVAL and o.status[0] == oracle.UNARRIVED
+    o.sched_step(0, [(A, 0, 11, 250, 0)])
+    st, _ = o.sched_step(5000, [(DEC, 0, 0, 40, 0), (DEC, 0, 0, 11, 0)])
+    assert st == oracle.E_INVAL and o.c[0] == 250
