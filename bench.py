@@ -69,7 +69,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
 
     def stop(self):
         if not self.proc:
@@ -82,7 +85,9 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
+        lines = [ln for t, ln in self.lines if t0 - 0.15 <= t <= t1 + 0.15] or [ln for _, ln in self.lines]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -259,29 +264,42 @@ def main():
     peaks_file, peak_src = measured_peaks()
     hbm_peak = float(peaks_file.get("hbm_gbs", 6650.0))
 
+    # the clock sampler starts before warm-up (nvidia-smi start-up can stall the driver);
+    # only samples taken inside the timed window are kept
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.preroll + args.warmup):
         pool.step(decisions=False)
     torch.cuda.synchronize(dev)
+    time.sleep(0.3)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     s = pool.stream
     st0 = pool.stats()
     phase_sum = np.zeros(9)
-    sampler = ClockSampler(local)
-    sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark("t_start")
     e0.record(s)
+    step_ms = []
     for _ in range(args.steps):
+        ea = torch.cuda.Event(enable_timing=True)
+        ea.record(s)
         with torch.cuda.stream(s):
             flush.zero_()             # L2 flush (256 MiB > 126 MB L2) inside the timed region
         pool.step(decisions=False)
-        phase_sum += np.array(pool.phase_times())   # syncs the stream: per-kernel CUDA-event times
+        ph_step = np.array(pool.phase_times())   # syncs the stream: per-kernel CUDA-event times
+        phase_sum += ph_step
+        eb = torch.cuda.Event(enable_timing=True)
+        eb.record(s)
+        eb.synchronize()
+        step_ms.append((round(ea.elapsed_time(eb), 3), round(float(ph_step.sum()) / 1e3, 3)))
     e1.record(s)
     torch.cuda.synchronize(dev)
+    sampler.mark("t_end")
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -379,6 +397,7 @@ def main():
         "kv_moved": moved,
         "kv_paths": kv_paths,
         "cpu_baseline": cpu,
+        "step_ms_and_graph_ms": step_ms,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

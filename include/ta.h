@@ -75,7 +75,8 @@ enum {
   TA_F_FILL = 1u << 1,         /* write KV content for new/recomputed tokens (engine stand-in) */
   TA_F_NO_GRAPH = 1u << 2,     /* launch the tick kernel by kernel instead of a CUDA graph */
   TA_F_TIMING = 1u << 3,       /* record per-phase CUDA events (graph event-record nodes) */
-  TA_F_COPY_BULK = 1u << 4     /* HBM->HBM copies via cp.async.bulk (TMA) instead of LDG/STG.128 */
+  TA_F_COPY_BULK = 1u << 4,    /* HBM->HBM copies via cp.async.bulk (TMA) instead of LDG/STG.128 */
+  TA_F_NO_FUSE = 1u << 5       /* single process: separate evict / fetch / fill kernels (A/B aid) */
 };
 
 typedef struct {

@@ -32,7 +32,9 @@ enum StatIdx {
   ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST, ST_N
 };
 
-enum MoveKind { MV_P2P = 2, MV_H2D = 3 };
+// per-request descriptor kinds (step 5.5): copy from a peer's HBM, copy from a host
+// tier, write new / recomputed tokens, nothing (fills disabled)
+enum MoveKind { MV_NONE = 0, MV_P2P = 2, MV_H2D = 3, MV_FILL = 4 };
 
 struct Ctr {                 // device-resident scalars of the context
   i64 tick;                  // k
@@ -52,7 +54,9 @@ struct Ctr {                 // device-resident scalars of the context
 };
 
 struct EvDesc { u32 src; u32 dst; };                     // HBM block -> host slot (replica r)
-struct FeDesc { u32 kind; u32 src_r; u32 src; u32 dst; };  // P2P / H2D into HBM block dst
+// P2P / H2D into HBM block dst; tokens [t0, t1) of logical block j of program uid are
+// (re)written after the copy when t0 < t1 (new tokens landing in a copied partial block)
+struct FeDesc { u32 kind; u32 src_r; u32 src; u32 dst; u32 uid; u32 t0; u32 t1; u32 j; };
 struct FillDesc { u32 idx; u32 uid; u32 t0; u32 t1; u32 j; u32 pad; };
 struct CpDesc { u32 src; u32 dst; };
 
@@ -109,6 +113,7 @@ struct Dev {
   u32* e_cum;                      // [R][N]  inclusive n_hbm prefix in eviction order
   EvDesc* evd; u32* evd_cnt;       // [R][NB]
   u32* evx;                        // [R][NB] evicted HBM block per eviction rank
+  EvDesc* evt;                     // [R][NB] evictions in victim order (evd: by block index)
   FeDesc* fed; u32* fed_cnt;       // [R][NB]
   FillDesc* fld; u32* fld_cnt;     // [R][NB]
   u32* dfh; u32* dfh_cnt;          // deferred HBM frees  [R][NB]: (replica << 27) | idx
@@ -121,6 +126,8 @@ struct Dev {
   ta_event* events;                // [kMaxEvents] API-mode event batch
   // ---- multi-process data plane (one replica per GPU) ----
   int multi, rank;                 // multi: pools of other replicas live in other processes
+  int fused;                       // single-process: evict / fetch / fill in one kernel
+  u32* evp;                        // [R][NB] segments of a block still to be evicted this tick
   ull* mbox;                       // [TA_MAX_REPLICAS] this rank's barrier mailbox (epochs)
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)

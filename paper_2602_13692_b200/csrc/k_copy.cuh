@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
     int r, s; u32 e;
     locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
     FeDesc x = d.fed[(size_t)r * d.NB + e];
+    if (x.kind != MV_P2P && x.kind != MV_H2D) continue;   // fills: k_fill
     const char* sbase = x.kind == MV_P2P ? d.hbm[x.src_r] : d.host[x.src_r];
     i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
     if (sbase == nullptr) continue;      // executed by the source's owner (multi-process push)
@@ -165,27 +166,114 @@ __device__ __forceinline__ ull splitmix64(ull x) {
   return z ^ (z >> 31);
 }
 
-// Engine stand-in: write the content of tokens [t0, t1) of block j into HBM block idx.
+// Engine stand-in: write the content of tokens [t0, t1) of logical block j of program
+// uid into segment s (= 2l + kv) of HBM block idx of replica r (CTA-wide).
+__device__ __forceinline__ void fill_segment(const Dev& d, int r, u32 idx, int s, u32 uid, u32 j, u32 t0,
+                                             u32 t1) {
+  const int nseg = 2 * d.nL;
+  const u32 wtok = (u32)(d.Hkv * d.D / 4);            // 8-byte words per (token, layer, kv)
+  ull* seg = (ull*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, idx, s);
+  const u32 l = (u32)s >> 1, kv = (u32)s & 1;
+  const u32 slot0 = t0 - j * (u32)d.bt;
+  const u32 nw = (t1 - t0) * wtok;
+  const ull ubase = (ull)uid << 40;
+  for (u32 q = threadIdx.x * 2; q < nw; q += blockDim.x * 2) {
+    u32 t = t0 + q / wtok, rem = q % wtok;            // wtok is even: q, q+1 share t
+    ull i = (((ull)t * d.nL + l) * 2 + kv) * wtok + rem;
+    ull a = splitmix64(ubase + i), b = splitmix64(ubase + i + 1);
+    uint4 v = make_uint4((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32));
+    *reinterpret_cast<uint4*>(seg + (size_t)slot0 * wtok + q) = v;
+  }
+}
+
+// Fills of new / recomputed blocks, then the new-token tails of copied blocks.
 __global__ void __launch_bounds__(256) k_fill(Dev d) {
   const int nseg = 2 * d.nL;
-  const i64 items = local_items(d, d.fld_cnt, nseg);
-  const u32 wtok = (u32)(d.Hkv * d.D / 4);            // 8-byte words per (token, layer, kv)
+  const i64 n1 = local_items(d, d.fld_cnt, nseg);
+  const i64 items = n1 + local_items(d, d.fed_cnt, nseg);
   for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    int r, s; u32 e;
+    if (it < n1) {
+      locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
+      FillDesc x = d.fld[(size_t)r * d.NB + e];
+      fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
+    } else {
+      locate(d, d.fed_cnt, it - n1, nseg, &r, &e, &s);
+      FeDesc x = d.fed[(size_t)r * d.NB + e];
+      if (x.t0 < x.t1) fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
+    }
+  }
+}
+
+__device__ __forceinline__ void wait_evicted(const u32* flag) {
+  if (threadIdx.x == 0) {
+    u32 v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (v) __nanosleep(64);
+    } while (v);
+  }
+  __syncthreads();
+}
+
+// Single-process movement of one tick in ONE kernel (step 6): even CTAs run the D2H
+// evictions, odd CTAs the P2P/H2D fetches (each followed by its new-token tail) and
+// then the fills of new / recomputed blocks.  D2H and H2D therefore share the
+// full-duplex host link instead of running back to back.  A destination block that
+// was evicted in this tick is written only after all its segments were read: the
+// evictor decrements evp[block] per segment (release), the writer waits for 0
+// (acquire).  Evicting CTAs never wait, and the grid is fully resident, so the
+// waits always terminate.
+__global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
+  const int nseg = 2 * d.nL;
+  const int role = blockIdx.x & 1;
+  const int G = gridDim.x >> 1;
+  const int me = blockIdx.x >> 1;
+  if (role == 0) {
+    const i64 items = local_items(d, d.evd_cnt, nseg);
+    for (i64 it = me; it < items; it += G) {
+      int r, s; u32 e;
+      locate(d, d.evd_cnt, it, nseg, &r, &e, &s);
+      EvDesc x = d.evd[(size_t)r * d.NB + e];
+      const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
+      uint4* dst = (uint4*)seg_addr(d.host[r], d.layout, d.NH, d.seg_bytes, nseg, x.dst, s);
+      cta_copy16(src, dst, d.seg_bytes >> 4);
+      __syncthreads();                              // every load of the segment has returned
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicSub(&d.evp[(size_t)r * d.NB + x.src], 1u);
+      }
+    }
+    return;
+  }
+  const i64 nf = local_items(d, d.fed_cnt, nseg);
+  for (i64 it = me; it < nf; it += G) {
+    int r, s; u32 e;
+    locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
+    FeDesc x = d.fed[(size_t)r * d.NB + e];
+    if (x.kind == MV_NONE) continue;
+    wait_evicted(&d.evp[(size_t)r * d.NB + x.dst]);
+    if (x.kind == MV_FILL) {                        // new / recomputed tokens
+      fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
+      continue;
+    }
+    const char* sbase = x.kind == MV_P2P ? d.hbm[x.src_r] : d.host[x.src_r];
+    const i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
+    const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
+    uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
+    cta_copy16(src, dst, d.seg_bytes >> 4);
+    if (x.t0 < x.t1) {
+      __syncthreads();                              // copy done before the tail is overwritten
+      fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
+    }
+  }
+  const i64 nl = local_items(d, d.fld_cnt, nseg);
+  for (i64 it = me; it < nl; it += G) {
     int r, s; u32 e;
     locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
     FillDesc x = d.fld[(size_t)r * d.NB + e];
-    ull* seg = (ull*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.idx, s);
-    const u32 l = (u32)s >> 1, kv = (u32)s & 1;
-    const u32 slot0 = x.t0 - x.j * (u32)d.bt;
-    const u32 nw = (x.t1 - x.t0) * wtok;
-    const ull ubase = (ull)x.uid << 40;
-    for (u32 q = threadIdx.x * 2; q < nw; q += blockDim.x * 2) {
-      u32 t = x.t0 + q / wtok, rem = q % wtok;        // wtok is even: q, q+1 share t
-      ull i = (((ull)t * d.nL + l) * 2 + kv) * wtok + rem;
-      ull a = splitmix64(ubase + i), b = splitmix64(ubase + i + 1);
-      uint4 v = make_uint4((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32));
-      *reinterpret_cast<uint4*>(seg + (size_t)slot0 * wtok + q) = v;
-    }
+    wait_evicted(&d.evp[(size_t)r * d.NB + x.idx]);
+    fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
   }
 }
 

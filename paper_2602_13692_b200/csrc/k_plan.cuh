@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     const u32* sf = d.host_free + (size_t)r * d.NHW;
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     const u32 hfree = s_big[d.NHW];
-    EvDesc* evd = d.evd + (size_t)r * d.NB;
+    EvDesc* evt = d.evt + (size_t)r * d.NB;   // (block, slot) in eviction order
     u32* scr = d.evx + (size_t)r * d.NB; // evicted HBM index per evicted block e (< NB)
     for (u32 e = threadIdx.x; e < X; e += CTA) {
       u32 v = (u32)upper_bound_u32(ec, (int)nv, e);
@@ -137,11 +137,12 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
       u32 idx = row[j];
       scr[e] = idx;
       if (e < hfree) {
+        if (d.fused) d.evp[(size_t)r * d.NB + idx] = 2u * d.nL;  // segments pending their D2H read
         u32 slot = bitmap_select(sf, s_big, d.NHW, e);
         row[j] = LOC_HOST | slot;
         d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
-        evd[e].src = idx;
-        evd[e].dst = slot;
+        evt[e].src = idx;
+        evt[e].dst = slot;
       } else {
         row[j] = LOC_NONE;
       }
@@ -152,8 +153,28 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
       u32 idx = scr[e];
       atomicOr(&hf[idx >> 5], 1u << (idx & 31));
       if (e < hfree) {
-        u32 slot = evd[e].dst;
+        u32 slot = evt[e].dst;
         atomicAnd(&shf[slot >> 5], ~(1u << (slot & 31)));
+      }
+    }
+    // D2H copies are issued in ascending HBM-block order, the order in which the
+    // allocation below hands the freed blocks out again, so a fetch that reuses an
+    // evicted block rarely waits for its eviction (fused movement kernel).
+    {
+      const u32 ntoh = min(X, hfree);
+      u32* sbits = s_big;                 // [NBW] evicted blocks; then [NBW+1] prefix
+      u32* spre = s_big + d.NBW;
+      EvDesc* evd = d.evd + (size_t)r * d.NB;
+      __syncthreads();
+      for (int w = threadIdx.x; w < d.NBW; w += CTA) sbits[w] = 0;
+      __syncthreads();
+      for (u32 e = threadIdx.x; e < ntoh; e += CTA) atomicOr(&sbits[evt[e].src >> 5], 1u << (evt[e].src & 31));
+      __syncthreads();
+      cta_bitmap_prefix(sbits, d.NBW, spre, s_tmp);
+      for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
+        u32 idx = evt[e].src;
+        u32 k = spre[idx >> 5] + __popc(sbits[idx >> 5] & ((1u << (idx & 31)) - 1));
+        evd[k] = evt[e];
       }
     }
     for (u32 v = threadIdx.x; v < nv; v += CTA) {
@@ -247,28 +268,29 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     const u32 ckv = d.c_kv[p], c = d.c[p];
     const u32 hb = ceil_div_u32(ckv, bt);
     const u32 jb = j * bt, je = min(jb + bt, c);
-    bool copied = false;
-    if (is_hbm(old)) {                                  // HBM on h != r: peer copy (P2P)
-      u32 pos = atomicAdd(&s_app[0], 1u);
-      fed[pos] = FeDesc{MV_P2P, (u32)h, old, dst};
-      dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
-      pc[PC_P2P] += 1;
-      copied = true;
-    } else if (is_host(old)) {                          // host tier of h: H2D
-      u32 pos = atomicAdd(&s_app[0], 1u);
-      fed[pos] = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst};
-      dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
-      pc[PC_H2D] += 1;
-      copied = true;
+    if (is_hbm(old) || is_host(old)) {                  // copy: P2P (HBM of h != r) or H2D (tier of h)
+      // a copied partial block that also receives new tokens carries the fill of its
+      // tail [max(jb, c_kv), je) in the same descriptor (written after the copy)
+      u32 t0 = 0, t1 = 0;
+      if (ckv < c && jb + bt > ckv) {
+        t0 = max(jb, ckv);
+        t1 = je;
+        pc[PC_FILLTOK] += t1 - t0;
+        if (!fill) t0 = t1 = 0;
+      }
+      if (is_hbm(old)) {
+        fed[q] = FeDesc{MV_P2P, (u32)h, old, dst, d.uid[p], t0, t1, j};
+        dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
+        pc[PC_P2P] += 1;
+      } else {
+        fed[q] = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst, d.uid[p], t0, t1, j};
+        dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
+        pc[PC_H2D] += 1;
+      }
     } else {                                            // recompute history / brand-new tokens
       if (j < hb) pc[PC_REC] += 1; else pc[PC_NEW] += 1;
       pc[PC_FILLTOK] += je - jb;
-      if (fill) fld[atomicAdd(&s_app[1], 1u)] = FillDesc{dst, d.uid[p], jb, je, j, 0};
-    }
-    if (copied && ckv < c && jb < c && jb + bt > ckv) { // copied block that also gets new tokens
-      u32 t0 = max(jb, ckv);
-      pc[PC_FILLTOK] += je - t0;
-      if (fill) fld[atomicAdd(&s_app[1], 1u)] = FillDesc{dst, d.uid[p], t0, je, j, 0};
+      fed[q] = fill ? FeDesc{MV_FILL, 0, 0, dst, d.uid[p], jb, je, j} : FeDesc{MV_NONE, 0, 0, dst, 0, 0, 0, j};
     }
     row[j] = dst;
     d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
@@ -285,7 +307,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   if (threadIdx.x == 0) {
     d.f_cnt[r] = nF;
     d.s_cnt[r] = m;
-    d.fed_cnt[r] = s_app[0];
+    d.fed_cnt[r] = tot;                  // one descriptor per request, in request order
     d.fld_cnt[r] = s_app[1];
     d.dfh_cnt[r] = s_app[2];
     d.dfs_cnt[r] = s_app[3];

@@ -58,6 +58,7 @@ struct ta_ctx {
   cudaEvent_t ev[10] = {};
   bool timing = false;
   void* mbox_alloc = nullptr;               // barrier mailbox (library-owned, 264 B)
+  int move_grid = 0;                        // resident CTAs of k_move_fused (even)
   void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
   void* peer_mbox[TA_MAX_REPLICAS] = {};    // IPC-opened peer mailboxes
 };
@@ -146,7 +147,8 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.ev_cnt = L.take<u32>(R);
   x.e_pid = L.take<u32>(R * N); x.e_cum = L.take<u32>(R * N);
   x.evd = L.take<EvDesc>(R * NB); x.evd_cnt = L.take<u32>(R); x.evx = L.take<u32>(R * NB);
-  x.fed = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R);
+  x.evt = L.take<EvDesc>(R * NB);
+  x.fed = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R); x.evp = L.take<u32>(R * NB);
   x.fld = L.take<FillDesc>(R * NB); x.fld_cnt = L.take<u32>(R);
   x.dfh = L.take<u32>(R * NB); x.dfh_cnt = L.take<u32>(R);
   x.dfs = L.take<u32>(R * NB); x.dfs_cnt = L.take<u32>(R);
@@ -193,6 +195,29 @@ static void rec(ta_ctx* x, int i) {
   if (x->timing) cudaEventRecordWithFlags(x->ev[i], x->stream, cudaEventRecordExternal);
 }
 
+// Step 6.  Single process: one fused kernel (D2H overlapped with H2D/P2P and fills).
+// Multi-process: evict -> barrier -> fetch (pull) + push -> barrier -> fills.
+static void launch_movement(ta_ctx* x) {
+  Dev& d = x->d;
+  cudaStream_t s = x->stream;
+  if (d.fused) {
+    k_move_fused<<<x->move_grid, 256, 0, s>>>(d);   // persistent: every CTA co-resident
+    rec(x, 4);
+    rec(x, 5);
+    return;
+  }
+  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);   // evicted blocks read before peers refill them
+  rec(x, 4);
+  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
+  if (d.multi) {
+    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
+    k_barrier<<<1, 32, 0, s>>>(d);               // fetches landed; P2P sources read
+  }
+  rec(x, 5);
+  if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
+}
+
 static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   Dev& d = x->d;
   cudaStream_t s = x->stream;
@@ -208,16 +233,7 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   rec(x, 2);
   k_plan<<<R, CTA, 0, s>>>(d, 0);
   rec(x, 3);
-  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
-  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);   // evicted blocks read before peers refill them
-  rec(x, 4);
-  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
-  if (d.multi) {
-    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
-    k_barrier<<<1, 32, 0, s>>>(d);               // fetches landed; P2P sources read
-  }
-  rec(x, 5);
-  if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
+  launch_movement(x);
   rec(x, 6);
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 0);
   k_compact_plan<<<R, CTA, 0, s>>>(d);
@@ -357,6 +373,15 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   x->timing = (cfg->flags & TA_F_TIMING) != 0;
   d.multi = cfg->replicas_here < cfg->n_replicas ? 1 : 0;
   d.rank = cfg->first_replica;
+  d.fused = (!d.multi && !(cfg->flags & TA_F_NO_FUSE)) ? 1 : 0;
+  {   // the fused movement kernel waits across CTAs: launch only as many as are resident
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_move_fused, 256, 0);
+    x->move_grid = (sms * per_sm) & ~1;
+    if (x->move_grid < 2) d.fused = 0;
+  }
   if (d.multi && cfg->replicas_here != 1) {
     fprintf(stderr, "ta_init_pool: multi-process mode needs replicas_here == 1\n");
     delete x;
@@ -615,8 +640,7 @@ ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, i
   cudaStream_t s = ctx->stream;
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_verb_pause<<<1, CTA, 0, s>>>(d, pid, mode);
-  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
-  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
+  launch_movement(ctx);
   k_assemble<<<1, CTA, 0, s>>>(d, 1);
   return verb_finish(ctx, "ta_pause", out, out_cap, n_out);
 }
@@ -634,14 +658,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
   k_plan<<<d.R, CTA, 0, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
-  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
-  if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
-  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
-  if (d.multi) {
-    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
-    k_barrier<<<1, 32, 0, s>>>(d);
-  }
-  if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
+  launch_movement(ctx);
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 1);
   k_assemble<<<1, CTA, 0, s>>>(d, 1);
   return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);
