@@ -151,13 +151,17 @@ def kv_path_microbench(pool, torch, peaks, hbm_peak, n_blocks=2048, reps=3):
         hs = torch.tensor(rng.permutation(NH)[:n_blocks].astype(np.int32), device=dev)
         modes += [("d2h", binding.MOVE_D2H, src, hs, bb, peaks["d2h"], "pcie d2h (measured memcpy)"),
                   ("h2d", binding.MOVE_H2D, hs, dst, bb, peaks["h2d"], "pcie h2d (measured memcpy)")]
+    if pool.R > 1:                      # NVLink: pull blocks from the next rank's HBM pool
+        modes.append(("p2p_pull", binding.MOVE_P2P, src, dst, bb, 770.0,
+                      "nvlink per direction (770 GB/s measured peer copy, B200_PROFILING.md; 900 nominal)"))
     s = pool.stream
     for name, kind, a, b, bytes_per_block, peak, pname in modes:
         best = 0.0
+        srep = (pool.first + 1) % pool.R if kind == binding.MOVE_P2P else pool.first
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            pool.move_blocks(kind, 0 if pool.first == 0 else pool.first, pool.first, a, b)
+            pool.move_blocks(kind, srep, pool.first, a, b)
             e1.record(s)
             e1.synchronize()
             gbs = n_blocks * bytes_per_block / (e0.elapsed_time(e1) * 1e-3) / 1e9
@@ -165,6 +169,27 @@ def kv_path_microbench(pool, torch, peaks, hbm_peak, n_blocks=2048, reps=3):
         out[name] = {"gbs": round(best, 1), "peak_gbs": round(peak, 1), "frac": round(best / peak, 3),
                      "peak": pname, "blocks": n_blocks, "block_bytes": bb}
     return out
+
+
+def workload(name, world):
+    """The bench workload at N GPUs: N replicas, 10k programs per replica (weak scaling)."""
+    import tracegen
+    cfg = tracegen.get_config(name)
+    cfg["n_replicas"] = world
+    cfg["trace"]["n"] = cfg["trace"]["n"] * world
+    return cfg
+
+
+def host_cap_bytes(host_gib, world):
+    """Pinned host tier per rank: at most host_gib, and at most 55% of RAM shared by the ranks."""
+    cap = int(host_gib * (1 << 30))
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal:"):
+                cap = min(cap, int(ln.split()[1]) * 1024 * 55 // 100 // world)
+    except OSError:
+        pass
+    return cap
 
 
 def metadata_bytes(pool_stats_prev, n_programs, sum_nb, moved_blocks):
@@ -180,7 +205,7 @@ def run_reference(args, metric):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = tracegen.get_config(args.config)
+    cfg = workload(args.config, int(os.environ.get("WORLD_SIZE", "1")))
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     for _ in range(args.preroll + args.warmup):
@@ -249,17 +274,22 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=dev)
 
-    cfg = tracegen.get_config(args.config)
-    # weak scaling: every rank runs one replica over its own 10k-program trace
-    # (replicas only)
-    cfg["trace"]["seed"] = cfg["trace"]["seed"] + 1000 * rank
+    # weak scaling: N replicas (one per GPU) share one global queue over 10k * N
+    # programs; every rank runs the replicated control plane, moves its own replica's
+    # bytes, and pulls / pushes migrated blocks over NVLink
+    cfg = workload(args.config, world)
     tr = tracegen.make_trace(cfg)
     block_bytes = 2 * 64 * 8 * 128 * 2 * cfg["block_tokens"]
-    nh = min(cfg["host_blocks"], int(args.host_gib * (1 << 30)) // block_bytes)
+    nh = min(cfg["host_blocks"], host_cap_bytes(args.host_gib, world) // block_bytes)
     cfg["host_blocks"] = nh
-    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=binding.F_TIMING, device=local)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=binding.F_TIMING, device=local,
+                replicas_here=1, first_replica=rank)
+    if world > 1:
+        from paper_2602_13692_b200.dist import connect
+        connect(pool)
     pool.load_trace(tr)
     peaks_file, peak_src = measured_peaks()
     hbm_peak = float(peaks_file.get("hbm_gbs", 6650.0))
@@ -274,6 +304,9 @@ def main():
     time.sleep(0.3)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(pool.stream):
+        flush.zero_()                    # first touch of the flush buffer outside the timed region
+    torch.cuda.synchronize(dev)
     s = pool.stream
     st0 = pool.stats()
     phase_sum = np.zeros(9)
@@ -285,6 +318,7 @@ def main():
     sampler.mark("t_start")
     e0.record(s)
     step_ms = []
+    ticks_info = []
     for _ in range(args.steps):
         ea = torch.cuda.Event(enable_timing=True)
         ea.record(s)
@@ -293,6 +327,7 @@ def main():
         pool.step(decisions=False)
         ph_step = np.array(pool.phase_times())   # syncs the stream: per-kernel CUDA-event times
         phase_sum += ph_step
+        ticks_info.append((pool.last_tick(), ph_step))   # host-mapped telemetry, no extra copy
         eb = torch.cuda.Event(enable_timing=True)
         eb.record(s)
         eb.synchronize()
@@ -311,12 +346,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    progs_total = tr.n_slots * world
+    progs_total = tr.n_slots
     value = args.steps * progs_total / 1e4 / (ms * 1e-3)
 
     # ---- e2e: the SAME ticks (fresh context over the same buffers, same untimed
     # prefix) through the public API, decisions read back to the host every tick
     pool.reset()
+    if world > 1:
+        connect(pool)                    # fresh context: fresh mailboxes to map
     pool.load_trace(tr)
     for _ in range(args.preroll + args.warmup):
         pool.step(decisions=False)
@@ -343,27 +380,61 @@ def main():
     dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS if isinstance(st0[k], int)}
     bb = pool.block_bytes
     ph = phase_sum / args.steps            # us per step
-    names = ["ingest+footprint", "pause+restore", "plan", "evict_d2h", "fetch_p2p_h2d", "fill",
-             "finalize+compact_plan", "compact_d2d", "assemble"]
-    peaks = pcie_peak(torch, dev) if nh else {"h2d": 1.0, "d2h": 1.0}
-    algo = {
-        "evict_d2h": (dstat["evict_to_host"] * bb / args.steps, peaks["d2h"], "pcie"),
-        "fetch_p2p_h2d": ((dstat["h2d_blocks"] + dstat["p2p_blocks"]) * bb / args.steps, peaks["h2d"], "pcie"),
-        "compact_d2d": (2 * dstat["compact_blocks"] * bb / args.steps, hbm_peak, "hbm"),
-    }
+    if world == 1:
+        names = ["ingest+footprint", "pause+restore", "plan", "movement_fused(d2h+h2d+p2p+fill)", "-", "-",
+                 "finalize+compact_plan", "compact_d2d", "assemble"]
+    else:
+        names = ["ingest+footprint", "pause+restore", "plan", "evict_d2h+barrier",
+                 "fetch_p2p_h2d+push+barrier", "fill", "finalize+compact_plan", "compact_d2d", "assemble"]
+    # the host-link peak of ONE GPU's link, measured by rank 0 while the others wait
+    peaks = pcie_peak(torch, dev) if (nh and rank == 0) else {"h2d": 1.0, "d2h": 1.0}
+    if world > 1:
+        dist.barrier()
+    # algorithmic bytes per GPU, tick by tick (telemetry counts are cluster totals; the
+    # replicas are symmetric, so per GPU = total / N).  A movement phase's time floor is
+    # the slowest link it must cross in that tick (PCIe is full duplex).
+    nvl = 770.0 if world > 1 else hbm_peak / 2     # co-located "P2P" is an HBM read+write
+    G = 1e9
+    tmin = {3: 0.0, 4: 0.0, 7: 0.0}
+    byts = {3: 0.0, 4: 0.0, 7: 0.0}
+    for ti, _ in ticks_info:
+        d2h_b = ti["d2h_blocks"] * bb / world
+        h2d_b = ti["h2d_blocks"] * bb / world
+        p2p_b = ti["p2p_blocks"] * bb / world
+        d2d_b = 2 * ti["d2d_blocks"] * bb / world
+        if world == 1:
+            tmin[3] += max(d2h_b / peaks["d2h"], h2d_b / peaks["h2d"], p2p_b / nvl) / G
+            byts[3] += d2h_b + h2d_b + p2p_b
+        else:
+            tmin[3] += d2h_b / peaks["d2h"] / G
+            byts[3] += d2h_b
+            tmin[4] += max(h2d_b / peaks["h2d"], p2p_b / nvl) / G
+            byts[4] += h2d_b + p2p_b
+        tmin[7] += d2d_b / hbm_peak / G
+        byts[7] += d2d_b
+    for k in tmin:                       # per step
+        tmin[k] /= args.steps
+        byts[k] /= args.steps
     dom = int(np.argmax(ph))
     dname = names[dom]
-    if dname in algo:
-        byt, peak, bound = algo[dname]
+    if dom in tmin and ph[dom] > 0 and byts[dom] > 0:
+        t = ph[dom] * 1e-6
+        achieved = byts[dom] / t / 1e9
+        peak = byts[dom] / tmin[dom] / G if tmin[dom] > 0 else achieved
+        bound = "hbm" if dom == 7 else "pcie (full duplex)" if world == 1 else ("pcie" if dom == 3 else "pcie/nvlink")
+        psrc = (peak_src if dom == 7 else
+                f"measured in this run: pinned cudaMemcpyAsync 1 GiB (d2h {peaks['d2h']:.1f}, h2d {peaks['h2d']:.1f}"
+                f" GB/s); peak = bytes / max over links of (link bytes / link peak)")
     else:
-        byt = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
-        peak, bound = hbm_peak, "hbm"
-    achieved = byt / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
+        byts_d = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
+        achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
+        peak, bound, psrc = hbm_peak, "hbm", peak_src
     roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
                 "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
-                "share_of_step": round(float(ph[dom] / ph.sum()), 4),
-                "peak_source": (peak_src if bound == "hbm" else "measured in this run: pinned cudaMemcpyAsync 1 GiB")}
+                "share_of_step": round(float(ph[dom] / ph.sum()), 4), "peak_source": psrc}
     kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
+    if world > 1:
+        dist.barrier()                   # peers keep their pools mapped until rank 0 is done
     moved = {
         "d2h_gb_per_step": round(dstat["evict_to_host"] * bb / args.steps / 1e9, 3),
         "h2d_gb_per_step": round(dstat["h2d_blocks"] * bb / args.steps / 1e9, 3),
@@ -380,7 +451,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": args.config, "programs_per_gpu": tr.n_slots, "replicas_per_gpu": 1,
+        "config": {"workload": args.config, "programs": tr.n_slots, "replicas": world, "replicas_per_gpu": 1,
                    "kv": "Qwen3-32B GQA L64 H8 D128 bf16, 16-token blocks (4 MiB)",
                    "hbm_blocks": pool.NB, "host_blocks": pool.NH, "preroll_ticks": args.preroll,
                    "engine_fill": "off (engine stand-in, not a hot-path row)",
@@ -390,7 +461,9 @@ def main():
         "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(d2h / args.steps),
                 "note": "public API ta_sched_step with decisions read back; trace uploaded once before timing"},
-        "gpu_launches": args.steps * 12,
+        # per tick: begin, ingest, footprint, pause, restore, plan, movement (1 fused kernel;
+        # multi-GPU: evict, barrier, fetch, push, barrier), finalize, compact plan/copy, assemble
+        "gpu_launches": args.steps * (11 if world == 1 else 15),
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),

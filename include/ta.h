@@ -234,6 +234,19 @@ ta_status ta_migrate(ta_ctx* ctx, uint32_t pid, int32_t dst_replica, ta_decision
 /* Cumulative counters and per-replica occupancy (synchronizes the stream). */
 ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out);
 
+typedef struct {               /* what the last tick did (written by the device into host-mapped memory) */
+  int64_t tick;                /* index of the tick */
+  uint32_t decisions;          /* decisions emitted */
+  uint32_t d2h_blocks;         /* evicted to the host tier (all replicas) */
+  uint32_t h2d_blocks;         /* fetched from host tiers */
+  uint32_t p2p_blocks;         /* fetched from another replica's HBM */
+  uint32_t d2d_blocks;         /* moved by compaction */
+  uint32_t fetch_blocks;       /* all allocated blocks (copies + fills) */
+} ta_tick_info;
+
+/* Telemetry of the last ta_sched_step (synchronizes the stream). */
+ta_status ta_last_tick(ta_ctx* ctx, ta_tick_info* out);
+
 /* Per-phase device times of the last tick in microseconds (TA_F_TIMING only):
  * [0] ingest+footprint [1] pause+restore [2] plan [3] D2H evict copies
  * [4] fetch copies (P2P/H2D) [5] fills [6] finalize+compaction plan

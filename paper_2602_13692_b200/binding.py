@@ -14,6 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libta.so")
 MAXR = 32
+HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 
 TA_OK, TA_E_INVAL, TA_E_NOMEM, TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM = 0, 1, 2, 3, 4
 TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA_E_STATE = 5, 6, 7, 8, 9, 10
@@ -70,6 +71,11 @@ class Stats(C.Structure):
         ("block_bytes", C.c_uint64)]
 
 
+class TickInfo(C.Structure):
+    _fields_ = [("tick", C.c_int64)] + [(k, C.c_uint32) for k in (
+        "decisions", "d2h_blocks", "h2d_blocks", "p2p_blocks", "d2d_blocks", "fetch_blocks")]
+
+
 class TraceView(C.Structure):
     _fields_ = [("n_slots", C.c_int32), ("n_initial", C.c_int32)] + [
         (k, C.POINTER(C.c_uint32)) for k in ("uid", "p0", "turn_off", "g", "d_ms", "o")]
@@ -116,6 +122,7 @@ def lib():
             "ta_verify_content": [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
             "ta_debug_state": [vp, i32, vp],
             "ta_move_blocks": [vp, i32, i32, i32, vp, vp, i32],
+            "ta_last_tick": [vp, vp],
             "ta_export_pool_handle": [vp, vp],
             "ta_import_peer_pool": [vp, i32, vp],
             "ta_destroy": [vp],
@@ -134,7 +141,7 @@ def lib():
 EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
-            "ta_last_error", "ta_abi_version", "ta_move_blocks")
+            "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
@@ -317,6 +324,11 @@ class Pool:
         out["block_bytes"] = s.block_bytes
         return out
 
+    def last_tick(self) -> dict:
+        t = TickInfo()
+        self._chk(lib().ta_last_tick(self.ctx, C.byref(t)), "ta_last_tick")
+        return {k: getattr(t, k) for k, _ in TickInfo._fields_}
+
     def phase_times(self):
         a = (C.c_float * 9)()
         self._chk(lib().ta_phase_times(self.ctx, a, 9), "ta_phase_times")
@@ -366,12 +378,12 @@ class Pool:
                                        dst_idx.data_ptr(), n), "ta_move_blocks")
 
     def export_handle(self) -> bytes:
-        h = (C.c_char * 64)()
+        h = (C.c_char * HANDLE_BYTES)()
         self._chk(lib().ta_export_pool_handle(self.ctx, h), "ta_export_pool_handle")
         return bytes(h)
 
     def import_peer(self, replica: int, handle: bytes):
-        h = (C.c_char * 64).from_buffer_copy(handle)
+        h = (C.c_char * HANDLE_BYTES).from_buffer_copy(handle)
         self._chk(lib().ta_import_peer_pool(self.ctx, replica, h), "ta_import_peer_pool")
 
     def read_block(self, r: int, tier: str, idx: int) -> np.ndarray:

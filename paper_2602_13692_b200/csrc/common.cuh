@@ -50,7 +50,7 @@ struct Ctr {                 // device-resident scalars of the context
   u32 verb_pid;              // single-program materialize (verbs)
   i32 verb_replica;
   i32 verb_ok;
-  u32 pad[5];
+  u32 t_d2h, t_h2d, t_p2p, t_d2d, t_fetch;   // this tick's block moves (telemetry)
 };
 
 struct EvDesc { u32 src; u32 dst; };                     // HBM block -> host slot (replica r)
@@ -121,6 +121,7 @@ struct Dev {
   CpDesc* cpd; u32* cpd_cnt;       // [R][NB/2+1]
   ta_decision* dec_out;            // host-mapped decision buffer (canonical order)
   u32* dec_out_cnt;                // host-mapped count
+  ta_tick_info* tick_info;         // host-mapped telemetry of the last tick
   u32 dec_cap;
   ull* verify;                     // [2] mismatches, checked
   ta_event* events;                // [kMaxEvents] API-mode event batch

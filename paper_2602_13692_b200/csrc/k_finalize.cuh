@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(CTA, 1) k_compact_plan(Dev d) {
   if (threadIdx.x == 0) {
     d.cpd_cnt[r] = K;
     atomicAdd(&d.stats[ST_COMPACT], (ull)K);
+    atomicAdd(&d.ctr->t_d2d, K);
   }
 }
 
@@ -166,6 +167,15 @@ __global__ void __launch_bounds__(CTA, 1) k_assemble(Dev d, int verb) {
   }
   if (threadIdx.x == 0) {
     *d.dec_out_cnt = pos;
+    ta_tick_info ti;
+    ti.tick = d.ctr->tick;
+    ti.decisions = pos;
+    ti.d2h_blocks = d.ctr->t_d2h;
+    ti.h2d_blocks = d.ctr->t_h2d;
+    ti.p2p_blocks = d.ctr->t_p2p;
+    ti.d2d_blocks = d.ctr->t_d2d;
+    ti.fetch_blocks = d.ctr->t_fetch;
+    *d.tick_info = ti;
     d.ctr->n_dec = pos;
     if (!verb) {
       ull imb = umax - umin;

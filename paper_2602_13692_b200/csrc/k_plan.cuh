@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
       d.evd_cnt[r] = toh;
       atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
       atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)toh);
+      atomicAdd(&d.ctr->t_d2h, toh);
       atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - toh));
     }
     __syncthreads();
@@ -314,6 +315,9 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     atomicAdd(&d.stats[ST_FETCH_BLOCKS], (ull)tot);
     atomicAdd(&d.stats[ST_P2P], s_pc[PC_P2P]);
     atomicAdd(&d.stats[ST_H2D], s_pc[PC_H2D]);
+    atomicAdd(&d.ctr->t_fetch, tot);
+    atomicAdd(&d.ctr->t_p2p, (u32)s_pc[PC_P2P]);
+    atomicAdd(&d.ctr->t_h2d, (u32)s_pc[PC_H2D]);
     atomicAdd(&d.stats[ST_RECOMPUTE], s_pc[PC_REC]);
     atomicAdd(&d.stats[ST_NEW_BLOCKS], s_pc[PC_NEW]);
     atomicAdd(&d.stats[ST_FILL_TOK], s_pc[PC_FILLTOK]);

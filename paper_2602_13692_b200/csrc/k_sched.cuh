@@ -12,6 +12,7 @@ __global__ void k_begin(Dev d) {
     d.ctr->restore_cnt = 0;
     d.ctr->n_arr = 0;
     d.ctr->T = d.api_mode ? d.ctr->now_ms : d.ctr->tick * d.dt;
+    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
   }
   if (t < d.R) {
     d.L[t] = 0;

@@ -8,7 +8,10 @@
 // Clear every per-call list so the shared copy / assembly kernels see only this verb.
 __global__ void k_verb_reset(Dev d) {
   int t = threadIdx.x;
-  if (t == 0) { d.ctr->restore_cnt = 0; d.ctr->err = TA_OK; d.ctr->verb_ok = 1; }
+  if (t == 0) {
+    d.ctr->restore_cnt = 0; d.ctr->err = TA_OK; d.ctr->verb_ok = 1;
+    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
+  }
   if (t < d.R) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
     d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
     d.evd_cnt[h] = toh;
     d.stats[ST_EVICT_BLOCKS] += X;
     d.stats[ST_EVICT_TO_HOST] += toh;
+    d.ctr->t_d2h += toh;
     d.stats[ST_EVICT_DROPPED] += X - toh;
   }
 }

@@ -37,6 +37,7 @@ struct Layout {                  // workspace carving (dry run when base == null
 struct HostWs {
   ta_decision* dec;              // [dec_cap]
   u32* dec_cnt;
+  ta_tick_info* tick_info;
   ta_event* ev;                  // [kMaxEvents]
   i64* scal;                     // [8] small H2D/D2H staging
 };
@@ -164,6 +165,7 @@ static size_t host_carve(const ta_config* c, char* base, HostWs* h) {
   const size_t cap = 4 * (size_t)c->max_programs + c->n_replicas + 64;
   x.dec = L.take<ta_decision>(cap);
   x.dec_cnt = L.take<u32>(1);
+  x.tick_info = L.take<ta_tick_info>(1);
   x.ev = L.take<ta_event>(kMaxEvents);
   x.scal = L.take<i64>(8);
   if (h) *h = x;
@@ -366,6 +368,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     char* hb = (char*)dp;
     d.dec_out = (ta_decision*)(hb + ((char*)x->h.dec - (char*)bufs->host_workspace));
     d.dec_out_cnt = (u32*)(hb + ((char*)x->h.dec_cnt - (char*)bufs->host_workspace));
+    d.tick_info = (ta_tick_info*)(hb + ((char*)x->h.tick_info - (char*)bufs->host_workspace));
     d.dec_cap = (u32)(4 * (size_t)cfg->max_programs + cfg->n_replicas + 64);
   }
   d.n_slots = 0;
@@ -520,6 +523,14 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
     out->host_used[r] = d.NH - g;
   }
   out->block_bytes = ctx->block_bytes;
+  return TA_OK;
+}
+
+ta_status ta_last_tick(ta_ctx* ctx, ta_tick_info* out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!out) return TA_E_INVAL;
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  *out = *ctx->h.tick_info;
   return TA_OK;
 }
 

@@ -1,0 +1,76 @@
+"""Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
+
+torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs]
+Every rank runs the replicated control plane for all N replicas and moves only its
+own replica's bytes; every rank compares its decisions and full state with its own
+oracle copy, and verifies the KV content of its local pool.  Exit code 0 = parity."""
+import os
+import random
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import tracegen  # noqa: E402
+from paper_2602_13692_b200 import Pool  # noqa: E402
+from paper_2602_13692_b200.dist import connect  # noqa: E402
+from tests.gpu_compare import compare_state, dec_tuples  # noqa: E402
+
+
+def main():
+    ticks = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 150
+    verbs = "--verbs" in sys.argv
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = tracegen.get_config("c1_toy", n_replicas=world, hbm_blocks=64, host_blocks=16, compact_every=3,
+                              trace=dict(n=12 * world, n_initial=5 * world, seed=77))
+    tr = tracegen.make_trace(cfg)
+    o = oracle.Oracle(cfg, tr)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, replicas_here=1, first_replica=rank, device=local)
+    peers = connect(pool)
+    pool.load_trace(tr)
+    rng = random.Random(5)
+    n_dec = n_p2p = n_verbs = 0
+    for k in range(ticks):
+        _, want = o.sched_step()
+        st, got = pool.step()
+        assert st == 0, f"rank {rank} tick {k}: status {st}"
+        got = dec_tuples(got)
+        assert got == want, f"rank {rank} tick {k}: decisions differ"
+        n_dec += len(got)
+        compare_state(o, pool.debug_download(), where=f"rank {rank} tick {k}")
+        bad, seen = pool.verify_content()
+        assert bad == 0, f"rank {rank} tick {k}: {bad} of {seen} local KV words wrong"
+        if verbs and k % 3 == 1:          # collective verbs: same call on every rank
+            p = rng.randrange(o.N)
+            rep = rng.randrange(world)
+            for name, fo, fg, args in (("migrate", o.migrate, pool.migrate, (p, rep)),
+                                       ("resume", o.resume, pool.resume, (p, rep)),
+                                       ("pause", o.pause, pool.pause, (p, 1))):
+                so, do = fo(*args)
+                sg, dg = fg(*args)
+                assert so == sg, (rank, k, name, so, sg)
+                if so == oracle.OK:
+                    assert dec_tuples(dg) == do, (rank, k, name)
+                    n_verbs += 1
+                compare_state(o, pool.debug_download(), where=f"rank {rank} tick {k} {name}")
+        if o.next_arrival == o.N and all(s == oracle.STOPPED for s in o.status):
+            break
+    n_p2p = o.stats["p2p_blocks"]
+    s = pool.stats()
+    for key in oracle.ta_oracle.STAT_KEYS:
+        assert s[key] == o.stats[key], (rank, key, s[key], o.stats[key])
+    dist.barrier()
+    print(f"rank {rank}: OK peers={peers} ticks={k + 1} decisions={n_dec} p2p_blocks={n_p2p} "
+          f"h2d_blocks={o.stats['h2d_blocks']} verbs_ok={n_verbs}", flush=True)
+    pool.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
