@@ -247,6 +247,11 @@ typedef struct {               /* what the last tick did (written by the device 
 /* Telemetry of the last ta_sched_step (synchronizes the stream). */
 ta_status ta_last_tick(ta_ctx* ctx, ta_tick_info* out);
 
+/* Switch the copy engine between TMA bulk copies (cp.async.bulk through a 32 KiB
+ * shared-memory stage, on != 0) and 128-bit loads/stores (on == 0).  Results are
+ * identical; only the speed differs.  Synchronizes the stream. */
+ta_status ta_set_copy_bulk(ta_ctx* ctx, int32_t on);
+
 /* Per-phase device times of the last tick in microseconds (TA_F_TIMING only):
  * [0] ingest+footprint [1] pause+restore [2] plan [3] D2H evict copies
  * [4] fetch copies (P2P/H2D) [5] fills [6] finalize+compaction plan

@@ -19,6 +19,7 @@ HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 TA_OK, TA_E_INVAL, TA_E_NOMEM, TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM = 0, 1, 2, 3, 4
 TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA_E_STATE = 5, 6, 7, 8, 9, 10
 F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE = 1, 2, 4, 8, 16, 32
+F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",
                 9: "E_PEER", 10: "E_STATE"}
@@ -123,6 +124,7 @@ def lib():
             "ta_debug_state": [vp, i32, vp],
             "ta_move_blocks": [vp, i32, i32, i32, vp, vp, i32],
             "ta_last_tick": [vp, vp],
+            "ta_set_copy_bulk": [vp, i32],
             "ta_export_pool_handle": [vp, vp],
             "ta_import_peer_pool": [vp, i32, vp],
             "ta_destroy": [vp],
@@ -141,7 +143,7 @@ def lib():
 EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
-            "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick")
+            "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
@@ -179,7 +181,11 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
         c.decay_q32[k] = v
     c.decode_tok_per_s = cfg["decode_tok_per_s"]
     c.compact_every = cfg.get("compact_every", 0)
-    c.flags = flags | (F_TRACE_MODE if trace_mode else 0) | (F_FILL if fill else 0)
+    # TMA bulk copies are the default engine (measured faster or equal on every path);
+    # pass flags=F_NO_BULK_DEFAULT to keep the 128-bit load/store engine
+    if not flags & F_NO_BULK_DEFAULT:
+        flags |= F_COPY_BULK
+    c.flags = (flags & ~F_NO_BULK_DEFAULT) | (F_TRACE_MODE if trace_mode else 0) | (F_FILL if fill else 0)
     return c
 
 
@@ -323,6 +329,9 @@ class Pool:
         out["host_used"] = list(s.host_used[:self.R])
         out["block_bytes"] = s.block_bytes
         return out
+
+    def set_copy_bulk(self, on: bool):
+        self._chk(lib().ta_set_copy_bulk(self.ctx, 1 if on else 0), "ta_set_copy_bulk")
 
     def last_tick(self) -> dict:
         t = TickInfo()

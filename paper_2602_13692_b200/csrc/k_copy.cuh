@@ -37,6 +37,90 @@ __device__ __forceinline__ void cta_copy16(const uint4* __restrict__ src, uint4*
   for (; i < n16; i += T) st_stream(dst + i, ld_stream(src + i));
 }
 
+// ---- TMA bulk copy (TA_F_COPY_BULK): one elected thread moves the segment through a
+// 32 KiB shared-memory buffer with cp.async.bulk (global -> smem, mbarrier complete_tx)
+// and cp.async.bulk (smem -> global, bulk_group).  Large transfers instead of 16-B
+// accesses; the other threads of the CTA are free for fills.
+#define BULK_CHUNK 32768u
+
+__device__ __forceinline__ void mbar_init(u64* mbar, u32 count) {
+  u32 a = (u32)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* mbar, u32 phase) {
+  u32 a = (u32)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" :: "r"(a), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* src, u32 bytes, u64* mbar) {
+  u32 s = (u32)__cvta_generic_to_shared(smem), m = (u32)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(m), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(s), "l"(src), "r"(bytes), "r"(m) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* smem, u32 bytes) {
+  u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" :: "l"(dst), "r"(s), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct BulkCtx {                 // per-CTA state, used by threadIdx.x == 0 only
+  char* smem;
+  u64* mbar;
+  u32 phase;
+};
+
+// Copy `bytes` (multiple of 16) from src to dst through smem.  `before_store(k)` runs
+// after chunk k has landed in smem and before it is written (used to wait for the
+// destination block's eviction).  Thread 0 only; returns with the smem reusable.
+template <typename BeforeStore>
+__device__ __forceinline__ void bulk_copy(BulkCtx& b, const char* src, char* dst, u32 bytes, BeforeStore before) {
+  for (u32 off = 0; off < bytes; off += BULK_CHUNK) {
+    const u32 n = min(BULK_CHUNK, bytes - off);
+    bulk_load(b.smem, src + off, n, b.mbar);
+    mbar_wait(b.mbar, b.phase);
+    b.phase ^= 1;
+    before(off);
+    bulk_store(dst + off, b.smem, n);
+    bulk_wait_read();
+  }
+}
+
+// Per-kernel setup of the bulk path (dynamic smem of BULK_CHUNK bytes when bulk is on).
+__device__ __forceinline__ BulkCtx bulk_begin(const Dev& d) {
+  extern __shared__ __align__(128) char dyn_smem[];
+  __shared__ u64 mbar;
+  BulkCtx b{dyn_smem, &mbar, 0};
+  if ((d.flags & TA_F_COPY_BULK) && threadIdx.x == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  return b;
+}
+// Copy one segment (CTA-wide call): TMA bulk by thread 0, or 128-bit loads/stores by all.
+__device__ __forceinline__ void seg_copy(const Dev& d, BulkCtx& b, const uint4* src, uint4* dst) {
+  if (d.flags & TA_F_COPY_BULK) {
+    if (threadIdx.x == 0) bulk_copy(b, (const char*)src, (char*)dst, (u32)d.seg_bytes, [](u32) {});
+  } else {
+    cta_copy16(src, dst, d.seg_bytes >> 4);
+  }
+}
+// Make a segment's copy complete and visible to the CTA's generic stores (before a tail fill).
+__device__ __forceinline__ void seg_copy_fence(const Dev& d) {
+  if ((d.flags & TA_F_COPY_BULK) && threadIdx.x == 0) {
+    bulk_wait_all();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void bulk_end(const Dev& d) {
+  if ((d.flags & TA_F_COPY_BULK) && threadIdx.x == 0) bulk_wait_all();
+}
+
 // Map a flat item index onto (local replica, entry, segment) given per-replica counts.
 __device__ __forceinline__ bool locate(const Dev& d, const u32* cnt, i64 item, int nseg, int* r, u32* e, int* s) {
   for (int q = 0; q < d.n_local; ++q) {
@@ -57,14 +141,16 @@ __device__ __forceinline__ i64 local_items(const Dev& d, const u32* cnt, int nse
 __global__ void __launch_bounds__(256) k_copy_evict(Dev d) {
   const int nseg = 2 * d.nL;
   const i64 items = local_items(d, d.evd_cnt, nseg);
+  BulkCtx bk = bulk_begin(d);
   for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
     int r, s; u32 e;
     locate(d, d.evd_cnt, it, nseg, &r, &e, &s);
     EvDesc x = d.evd[(size_t)r * d.NB + e];
     const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.host[r], d.layout, d.NH, d.seg_bytes, nseg, x.dst, s);
-    cta_copy16(src, dst, d.seg_bytes >> 4);
+    seg_copy(d, bk, src, dst);
   }
+  bulk_end(d);
 }
 
 // Fetches into the local replicas' HBM: P2P from a peer (or co-located) replica's
@@ -72,6 +158,7 @@ __global__ void __launch_bounds__(256) k_copy_evict(Dev d) {
 __global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
   const int nseg = 2 * d.nL;
   const i64 items = local_items(d, d.fed_cnt, nseg);
+  BulkCtx bk = bulk_begin(d);
   for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
     int r, s; u32 e;
     locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
@@ -82,8 +169,9 @@ __global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
     if (sbase == nullptr) continue;      // executed by the source's owner (multi-process push)
     const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
-    cta_copy16(src, dst, d.seg_bytes >> 4);
+    seg_copy(d, bk, src, dst);
   }
+  bulk_end(d);
 }
 
 // Multi-process push: H2D fetches whose source is THIS process's host tier but whose
@@ -92,6 +180,7 @@ __global__ void __launch_bounds__(256) k_copy_fetch(Dev d) {
 __global__ void __launch_bounds__(256) k_copy_push(Dev d) {
   if (!d.multi) return;
   const int nseg = 2 * d.nL;
+  BulkCtx bk = bulk_begin(d);
   for (int r = 0; r < d.R; ++r) {
     if (r >= d.first_local && r < d.first_local + d.n_local) continue;
     const u32 n = d.fed_cnt[r];
@@ -102,9 +191,10 @@ __global__ void __launch_bounds__(256) k_copy_push(Dev d) {
       if (x.kind != MV_H2D || d.host[x.src_r] == nullptr || d.hbm[r] == nullptr) continue;
       const uint4* src = (const uint4*)seg_addr(d.host[x.src_r], d.layout, d.NH, d.seg_bytes, nseg, x.src, s);
       uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
-      cta_copy16(src, dst, d.seg_bytes >> 4);
+      seg_copy(d, bk, src, dst);
     }
   }
+  bulk_end(d);
   __threadfence_system();                // peer stores visible before the barrier flag
 }
 
@@ -133,14 +223,16 @@ __global__ void k_barrier(Dev d) {
 __global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
   const int nseg = 2 * d.nL;
   const i64 items = local_items(d, d.cpd_cnt, nseg);
+  BulkCtx bk = bulk_begin(d);
   for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
     int r, s; u32 e;
     locate(d, d.cpd_cnt, it, nseg, &r, &e, &s);
     CpDesc x = d.cpd[(size_t)r * (d.NB / 2 + 1) + e];
     const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
-    cta_copy16(src, dst, d.seg_bytes >> 4);
+    seg_copy(d, bk, src, dst);
   }
+  bulk_end(d);
 }
 
 // ta_move_blocks: n whole blocks from one pool to another, block-list driven.
@@ -148,13 +240,15 @@ __global__ void __launch_bounds__(256) k_move(Dev d, const char* sbase, i64 snb,
                                               const u32* __restrict__ src, const u32* __restrict__ dst, int n) {
   const int nseg = 2 * d.nL;
   const i64 items = (i64)n * nseg;
+  BulkCtx bk = bulk_begin(d);
   for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
     u32 e = (u32)(it / nseg);
     int s = (int)(it % nseg);
     const uint4* sp = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, src[e], s);
     uint4* dp = (uint4*)seg_addr(dbase, d.layout, dnb, d.seg_bytes, nseg, dst[e], s);
-    cta_copy16(sp, dp, d.seg_bytes >> 4);
+    seg_copy(d, bk, sp, dp);
   }
+  bulk_end(d);
 }
 
 // ---- KV content closed form: word(uid, t, l, kv, h, w) =
@@ -229,6 +323,7 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   const int role = blockIdx.x & 1;
   const int G = gridDim.x >> 1;
   const int me = blockIdx.x >> 1;
+  BulkCtx bk = bulk_begin(d);
   if (role == 0) {
     const i64 items = local_items(d, d.evd_cnt, nseg);
     for (i64 it = me; it < items; it += G) {
@@ -237,13 +332,14 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
       EvDesc x = d.evd[(size_t)r * d.NB + e];
       const uint4* src = (const uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.src, s);
       uint4* dst = (uint4*)seg_addr(d.host[r], d.layout, d.NH, d.seg_bytes, nseg, x.dst, s);
-      cta_copy16(src, dst, d.seg_bytes >> 4);
+      seg_copy(d, bk, src, dst);
       __syncthreads();                              // every load of the segment has returned
       if (threadIdx.x == 0) {
         __threadfence();
         atomicSub(&d.evp[(size_t)r * d.NB + x.src], 1u);
       }
     }
+    bulk_end(d);
     return;
   }
   const i64 nf = local_items(d, d.fed_cnt, nseg);
@@ -261,9 +357,9 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
     const i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
     const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
-    cta_copy16(src, dst, d.seg_bytes >> 4);
+    seg_copy(d, bk, src, dst);
     if (x.t0 < x.t1) {
-      __syncthreads();                              // copy done before the tail is overwritten
+      seg_copy_fence(d);                            // copy done before the tail is overwritten
       fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
     }
   }
@@ -275,6 +371,7 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
     wait_evicted(&d.evp[(size_t)r * d.NB + x.idx]);
     fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
   }
+  bulk_end(d);
 }
 
 // Test aid: count words of every owned block (HBM and host tier of the local

@@ -197,23 +197,26 @@ static void rec(ta_ctx* x, int i) {
   if (x->timing) cudaEventRecordWithFlags(x->ev[i], x->stream, cudaEventRecordExternal);
 }
 
+// dynamic shared memory of the copy kernels: the TMA staging buffer in bulk mode
+static inline size_t csm(const Dev& d) { return (d.flags & TA_F_COPY_BULK) ? BULK_CHUNK : 0; }
+
 // Step 6.  Single process: one fused kernel (D2H overlapped with H2D/P2P and fills).
 // Multi-process: evict -> barrier -> fetch (pull) + push -> barrier -> fills.
 static void launch_movement(ta_ctx* x) {
   Dev& d = x->d;
   cudaStream_t s = x->stream;
   if (d.fused) {
-    k_move_fused<<<x->move_grid, 256, 0, s>>>(d);   // persistent: every CTA co-resident
+    k_move_fused<<<x->move_grid, 256, csm(d), s>>>(d);   // persistent: every CTA co-resident
     rec(x, 4);
     rec(x, 5);
     return;
   }
-  k_copy_evict<<<kCopyGrid, 256, 0, s>>>(d);
+  k_copy_evict<<<kCopyGrid, 256, csm(d), s>>>(d);
   if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);   // evicted blocks read before peers refill them
   rec(x, 4);
-  k_copy_fetch<<<kCopyGrid, 256, 0, s>>>(d);
+  k_copy_fetch<<<kCopyGrid, 256, csm(d), s>>>(d);
   if (d.multi) {
-    k_copy_push<<<kCopyGrid, 256, 0, s>>>(d);
+    k_copy_push<<<kCopyGrid, 256, csm(d), s>>>(d);
     k_barrier<<<1, 32, 0, s>>>(d);               // fetches landed; P2P sources read
   }
   rec(x, 5);
@@ -240,7 +243,7 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 0);
   k_compact_plan<<<R, CTA, 0, s>>>(d);
   rec(x, 7);
-  k_copy_compact<<<kCopyGrid, 256, 0, s>>>(d);
+  k_copy_compact<<<kCopyGrid, 256, csm(d), s>>>(d);
   rec(x, 8);
   k_assemble<<<1, CTA, 0, s>>>(d, 0);
   rec(x, 9);
@@ -381,7 +384,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_move_fused, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_move_fused, 256, BULK_CHUNK);
     x->move_grid = (sms * per_sm) & ~1;
     if (x->move_grid < 2) d.fused = 0;
   }
@@ -526,6 +529,14 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
   return TA_OK;
 }
 
+ta_status ta_set_copy_bulk(ta_ctx* ctx, int32_t on) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (on) ctx->d.flags |= TA_F_COPY_BULK; else ctx->d.flags &= ~(u32)TA_F_COPY_BULK;
+  if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }   // params changed
+  return TA_OK;
+}
+
 ta_status ta_last_tick(ta_ctx* ctx, ta_tick_info* out) {
   if (ta_status s = check_ctx(ctx)) return s;
   if (!out) return TA_E_INVAL;
@@ -565,7 +576,7 @@ ta_status ta_move_blocks(ta_ctx* ctx, int32_t kind, int32_t src_r, int32_t dst_r
   }
   if (!sb || !db) FAIL(ctx, TA_E_INVAL, "pool not addressable from this process");
   if (n == 0) return TA_OK;
-  k_move<<<kCopyGrid, 256, 0, ctx->stream>>>(d, sb, snb, db, dnb, src_blocks, dst_blocks, n);
+  k_move<<<kCopyGrid, 256, csm(d), ctx->stream>>>(d, sb, snb, db, dnb, src_blocks, dst_blocks, n);
   CK(ctx, cudaGetLastError());
   return TA_OK;
 }

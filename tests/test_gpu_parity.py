@@ -84,6 +84,13 @@ def test_gpu_no_graph_and_timing_modes():
     run_parity(stress(32, 2), 40, flags=binding.F_TIMING)
 
 
+@pytest.mark.parametrize("flags_name", ["F_NO_BULK_DEFAULT", "F_NO_FUSE"])
+def test_gpu_copy_engine_variants(flags_name):
+    """128-bit load/store engine instead of TMA bulk; split instead of fused movement."""
+    from paper_2602_13692_b200 import binding
+    run_parity(stress(33, 3), 120, flags=getattr(binding, flags_name))
+
+
 def test_gpu_w1_golden():
     """Hand-computed two-tick example uploaded into the GPU state (tests/golden/w1.json)."""
     need_gpu()
