@@ -258,6 +258,12 @@ ta_status ta_set_copy_bulk(ta_ctx* ctx, int32_t on);
  * [7] compaction copies [8] decision assembly.  n <= 9. */
 ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
 
+/* Developer aid (TA_F_TIMING only): raw SM-clock stamps (clock64) taken by thread 0
+ * of CTA 0 at the phase boundaries of the planner kernels during the last tick:
+ * out[32*k + i], k = 0 pause, 1 restore, 2 plan, 3 reserved; 0 = phase not reached.
+ * n <= 128.  Synchronizes the stream.  Errors: TA_E_STATE (no TA_F_TIMING). */
+ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n);
+
 /* Block-list-driven KV movement (the copy engine of step 6, exposed directly):
  * copy n whole KV blocks, block src_blocks[i] of the source pool to block
  * dst_blocks[i] of the destination pool.  kind: TA_MOVE_D2D (HBM of src_replica

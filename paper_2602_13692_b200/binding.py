@@ -120,6 +120,7 @@ def lib():
             "ta_migrate": [vp, u32, i32, vp, i32, C.POINTER(i32)],
             "ta_stats": [vp, vp],
             "ta_phase_times": [vp, C.POINTER(C.c_float), i32],
+            "ta_debug_phase_stamps": [vp, C.POINTER(C.c_uint64), i32],
             "ta_verify_content": [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
             "ta_debug_state": [vp, i32, vp],
             "ta_move_blocks": [vp, i32, i32, i32, vp, vp, i32],
@@ -143,7 +144,8 @@ def lib():
 EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
-            "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk")
+            "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk",
+            "ta_debug_phase_stamps")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
@@ -342,6 +344,19 @@ class Pool:
         a = (C.c_float * 9)()
         self._chk(lib().ta_phase_times(self.ctx, a, 9), "ta_phase_times")
         return list(a)
+
+    def phase_stamps(self):
+        """Raw clock64 stamps of the planner kernels' phases in the last tick (TA_F_TIMING):
+        {kernel: [(phase index, cycles since the kernel's first stamp), ...]}."""
+        a = (C.c_uint64 * 128)()
+        self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 128), "ta_debug_phase_stamps")
+        out = {}
+        for k, name in enumerate(("pause", "restore", "plan")):
+            v = [(i, a[32 * k + i]) for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
+            out[name] = [(i, c - v[0][1]) for i, c in v] if v else []
+            # sizes recorded next to the stamps (bit 62 set): ("n<i>", value)
+            out[name] += [(f"n{i}", a[32 * k + i] & ((1 << 62) - 1)) for i in range(32) if a[32 * k + i] >> 62 == 1]
+        return out
 
     def verify_content(self):
         bad, seen = C.c_uint64(), C.c_uint64()

@@ -95,7 +95,8 @@ struct Dev {
   // ---- replica state (all replicas) ----
   u32 *hbm_free, *host_free;       // [R][NBW], [R][NHW]; bit set = free
   u32 *owner_hbm, *owner_host;     // [R][NB], [R][NH]: pid * MAXB + j
-  ull* L;                          // [R]
+  ull* L;                          // [R]  effective load after the last pause/restore pass
+  ull* Lacc;                       // [R]  footprint accumulator of this tick (zeroed by k_pause)
   Ctr* ctr;
   ull* stats;                      // [ST_N]
   // ---- scratch ----
@@ -132,7 +133,16 @@ struct Dev {
   ull* mbox;                       // [TA_MAX_REPLICAS] this rank's barrier mailbox (epochs)
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)
+  ull* pst;                        // [4][32] in-kernel phase stamps (TA_F_TIMING; developer aid)
 };
+
+// Phase stamp: SM clock of thread 0 of CTA 0 at a phase boundary of a planner kernel
+// (kernel slot kk: 0 pause, 1 restore, 2 plan, 3 other).  Only with TA_F_TIMING.
+#define PSTAMP(kk, i)                                                              \
+  do {                                                                             \
+    if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x == 0)            \
+      d.pst[(kk) * 32 + (i)] = clock64();                                          \
+  } while (0)
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u32 ceil_div_u32(u32 a, u32 b) { return (a + b - 1) / b; }
@@ -333,6 +343,105 @@ __device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_
     cur ^= 1;
   }
   return cur;
+}
+
+// ------------------------------------------------------------------ small sorts
+// The planner's sorts are usually short (a few hundred to a few thousand candidates)
+// and latency-bound.  For n <= SORT_SMALL they run as a bitonic network on
+// (key, input position) pairs held in registers (E = P/1024 pairs per thread):
+// partner distance j < 32 exchanges through warp shuffles, 32 <= j < 1024 through
+// double-buffered shared memory (one barrier per stage), j >= 1024 inside a thread.
+// Positions are unique, so the network's order is the stable order.  Longer inputs
+// fall back to the global-memory radix sort.
+#define SORT_SMALL 4096
+struct SortSmem {                 // 96 KiB of dynamic shared memory
+  u64 k[2][SORT_SMALL];
+  u32 p[2][SORT_SMALL];
+};
+#define PLAN_DSMEM (sizeof(SortSmem) + 3 * 4096 * sizeof(u32))   // sort + staged arrays
+
+// keep the smaller (take_min) or larger pair of self and other; pairs are distinct
+__device__ __forceinline__ void bitonic_pick(u64& k, u32& p, u64 ok, u32 op, bool take_min) {
+  const bool other_less = ok < k || (ok == k && op < p);
+  if (other_less == take_min) { k = ok; p = op; }
+}
+
+// Stable sort of (ka, va)[0, n) by key.  Returns 0 if the result is in (ka, va),
+// 1 if in (kb, vb).  The buffer not holding the result is free scratch afterwards.
+__device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm) {
+  if (n <= 1) return 0;
+  if (n > SORT_SMALL) return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp);
+  int P = 32;
+  while (P < n) P <<= 1;
+  const int E = P > CTA ? P / CTA : 1;        // 1, 2 or 4 pairs per thread
+  const int t = threadIdx.x;
+  const bool act = E > 1 || t < P;            // warp-uniform (P is a multiple of 32)
+  u64 k[SORT_SMALL / CTA];
+  u32 p[SORT_SMALL / CTA];
+#pragma unroll
+  for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+    const int i = t + e * CTA;
+    k[e] = (e < E && i < n) ? ka[i] : ~0ull;   // padding sorts last (positions >= n)
+    p[e] = (u32)i;
+  }
+  int buf = 0;
+  for (int kk = 2; kk <= P; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= CTA) {                         // both elements in this thread
+        // constant register indices only (no local-memory arrays): j / CTA is 1 or 2
+        auto cx = [&](u64& ka_, u32& pa_, u64& kb_, u32& pb_, int e) {
+          const bool up = ((t + e * CTA) & kk) == 0;
+          const bool gt = ka_ > kb_ || (ka_ == kb_ && pa_ > pb_);
+          if (gt == up) {
+            u64 tk = ka_; ka_ = kb_; kb_ = tk;
+            u32 tp = pa_; pa_ = pb_; pb_ = tp;
+          }
+        };
+        if (j == CTA) {
+          cx(k[0], p[0], k[1], p[1], 0);
+          if (E > 2) cx(k[2], p[2], k[3], p[3], 2);
+        } else {
+          cx(k[0], p[0], k[2], p[2], 0);
+          cx(k[1], p[1], k[3], p[3], 1);
+        }
+      } else if (j >= 32) {                   // across warps: shared memory
+        if (act) {
+#pragma unroll
+          for (int e = 0; e < SORT_SMALL / CTA; ++e)
+            if (e < E) { sm->k[buf][t + e * CTA] = k[e]; sm->p[buf][t + e * CTA] = p[e]; }
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+          for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+            if (e >= E) continue;
+            const int i = t + e * CTA, l = i ^ j;
+            bitonic_pick(k[e], p[e], sm->k[buf][l], sm->p[buf][l], ((i & j) == 0) == ((i & kk) == 0));
+          }
+        }
+        buf ^= 1;
+      } else if (act) {                       // inside a warp: shuffles
+#pragma unroll
+        for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+          if (e >= E) continue;
+          const int i = t + e * CTA;
+          const u32 lo = __shfl_xor_sync(FULL_MASK, (u32)k[e], j);
+          const u32 hi = __shfl_xor_sync(FULL_MASK, (u32)(k[e] >> 32), j);
+          const u32 op = __shfl_xor_sync(FULL_MASK, p[e], j);
+          bitonic_pick(k[e], p[e], ((u64)hi << 32) | lo, op, ((i & j) == 0) == ((i & kk) == 0));
+        }
+      }
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+      const int i = t + e * CTA;
+      if (e < E && i < n) { kb[i] = k[e]; vb[i] = va[p[e]]; }
+    }
+  }
+  __syncthreads();
+  return 1;
 }
 
 // ------------------------------------------------------------------ exact prefix selection

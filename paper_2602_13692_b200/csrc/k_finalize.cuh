@@ -189,4 +189,17 @@ __global__ void __launch_bounds__(CTA, 1) k_assemble(Dev d, int verb) {
       d.ctr->tick += 1;
     }
   }
+  // clear the per-tick lists and counters for the next tick / call
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d.ctr->stops = 0;
+    d.ctr->restore_cnt = 0;
+    d.ctr->n_arr = 0;
+    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
+  }
+  for (int t = threadIdx.x; t < R; t += CTA) {
+    d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
+    d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
+    d.cpd_cnt[t] = 0;
+  }
 }

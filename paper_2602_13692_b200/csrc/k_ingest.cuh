@@ -2,14 +2,11 @@
 #pragma once
 #include "common.cuh"
 
-// Step 0, trace mode: one thread per slot.  Decode during the last interval,
-// tool call / tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).
-__global__ void __launch_bounds__(256) k_ingest_trace(Dev d) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= d.N) return;
+// Step 0, trace mode, for one slot: decode during the last interval, tool call /
+// tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).
+__device__ __forceinline__ void ingest_slot(const Dev& d, int p, i64 T) {
   u8 st = d.status[p];
   if (st == TA_UNARRIVED || st == TA_STOPPED) return;
-  const i64 T = d.ctr->tick * d.dt;
   const u32 base = d.t_off[p];
   const u32 nturns = d.t_off[p + 1] - base;
   u32 c = d.c[p];
@@ -146,17 +143,13 @@ __global__ void k_apply_events(Dev d, const ta_event* ev, int n_ev, int apply) {
   d.ctr->n_arr = arr;
 }
 
-// Steps 0 (release frees, closed-loop arrivals) + 1 (footprint) + 2 (contribution,
-// L_eff): one warp per slot.  The block-table row is scanned with 16-byte loads;
-// counts come from ballot/popc, prefix_hbm from the first non-HBM entry.
-__global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Steps 0 (release frees) + 1 (footprint) + 2 (contribution, L_eff) for one slot,
+// by one warp.  The block-table row is scanned with 16-byte loads; counts come from
+// ballot/popc, prefix_hbm from the first non-HBM entry.  Loads accumulate into Lacc
+// (k_pause publishes L).  Closed-loop arrivals are initialised by k_restore.
+__device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int verb) {
   const u32 lane = lane_id();
-  if (p >= d.N) return;
   u32* row = d.loc + (size_t)p * d.MAXBP;
-  const i64 k = d.ctr->tick;
-  // verbs act on the state left by the last tick, at its time T (no ingest, L kept)
-  const i64 T = verb ? d.ctr->T : (d.api_mode ? d.ctr->now_ms : k * d.dt);
   if (!verb && d.released[p]) {                   // free every block of a STOPPED program (A26)
     const int h = d.home[p];
     const u32 nbv = ceil_div_u32(d.c[p], d.bt);
@@ -178,45 +171,37 @@ __global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
     }
     return;
   }
-  u8 st = d.status[p];
-  if (!verb && !d.api_mode && st == TA_UNARRIVED) {       // closed-loop arrivals (A12)
-    const i64 na = d.ctr->next_arrival;
-    i64 n_arr = trace_arrivals(d);
-    if (p >= na && p < na + n_arr && p < d.n_slots) {
-      if (lane == 0) {
-        d.uid[p] = d.t_uid[p]; d.status[p] = TA_PAUSED; d.phase[p] = TA_PHASE_R;
-        d.c[p] = d.t_p0[p]; d.c_kv[p] = 0; d.paused_since[p] = (u32)k;
-        d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
-        d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
-        d.tool_return[p] = INT64_MAX;
-        u32 nbv = ceil_div_u32(d.t_p0[p], d.bt);
-        d.nb[p] = nbv; d.n_hbm[p] = 0; d.n_host[p] = 0; d.prefix_hbm[p] = 0; d.contrib[p] = nbv;
-      }
-      return;
-    }
-  }
+  const u8 st = d.status[p];
   if (st != TA_PAUSED && st != TA_REASONING && st != TA_ACTING) {
     if (lane == 0) d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
     return;
   }
   const u32 nbv = ceil_div_u32(d.c[p], d.bt);
   u32 n_h = 0, n_s = 0, first = 0xFFFFFFFFu;
-  for (u32 j0 = 0; j0 < nbv; j0 += 128) {
-    u32 j = j0 + lane * 4;
-    uint4 q = make_uint4(LOC_NONE, LOC_NONE, LOC_NONE, LOC_NONE);
-    if (j < nbv) q = *reinterpret_cast<const uint4*>(row + j);
-    u32 e[4] = {q.x, q.y, q.z, q.w};
-    u32 lfirst = 0xFFFFFFFFu;
+  for (u32 j0 = 0; j0 < nbv; j0 += 256) {         // two independent 16-B loads per lane in flight
+    uint4 q[2];
 #pragma unroll
-    for (int t = 3; t >= 0; --t) {
-      if (j + t < nbv) {
-        bool h = is_hbm(e[t]);
-        n_h += h;
-        n_s += is_host(e[t]);
-        if (!h) lfirst = j + t;
-      }
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const u32 j = j0 + h2 * 128 + lane * 4;
+      q[h2] = make_uint4(LOC_NONE, LOC_NONE, LOC_NONE, LOC_NONE);
+      if (j < nbv) q[h2] = *reinterpret_cast<const uint4*>(row + j);
     }
-    first = min(first, lfirst);
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const u32 j = j0 + h2 * 128 + lane * 4;
+      u32 e[4] = {q[h2].x, q[h2].y, q[h2].z, q[h2].w};
+      u32 lfirst = 0xFFFFFFFFu;
+#pragma unroll
+      for (int t = 3; t >= 0; --t) {
+        if (j + t < nbv) {
+          bool h = is_hbm(e[t]);
+          n_h += h;
+          n_s += is_host(e[t]);
+          if (!h) lfirst = j + t;
+        }
+      }
+      first = min(first, lfirst);
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -231,6 +216,28 @@ __global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
     d.prefix_hbm[p] = first == 0xFFFFFFFFu ? nbv : first;
     u32 cb = contrib_of(d, nbv, d.phase[p], d.acting_since[p], T);
     d.contrib[p] = cb;
-    if (!verb && st != TA_PAUSED) atomicAdd(&d.L[d.placement[p]], (ull)cb);   // commutative u64 sum
+    if (!verb && st != TA_PAUSED) atomicAdd(&d.Lacc[d.placement[p]], (ull)cb);   // commutative u64 sum
   }
+}
+
+// Trace mode: steps 0-2 of the tick in one kernel, one warp per slot (ingest by
+// lane 0, then the warp's footprint scan of the same slot).
+__global__ void __launch_bounds__(256) k_tick_front(Dev d) {
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= d.N) return;
+  const i64 T = d.ctr->tick * d.dt;
+  if (p == 0 && lane_id() == 0) d.ctr->T = T;
+  if (lane_id() == 0) ingest_slot(d, p, T);
+  __syncwarp();
+  footprint_warp(d, p, T, 0);
+}
+
+// API mode and verbs: steps 1-2 (the events were applied by k_apply_events).  Verbs
+// act on the state left by the last tick, at its time T (no ingest, L kept).
+__global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= d.N) return;
+  const i64 T = verb ? d.ctr->T : d.ctr->now_ms;
+  if (!verb && p == 0 && lane_id() == 0) d.ctr->T = T;
+  footprint_warp(d, p, T, verb);
 }

@@ -26,12 +26,19 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   __shared__ ull s_red[NWARP];
   __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs
   __shared__ ull s_pc[PC_N];
+  extern __shared__ __align__(16) char dsm[];
+  SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
+  u32* s_fc = reinterpret_cast<u32*>(dsm + sizeof(SortSmem));   // staged need prefix  [4096]
+  u32* s_ec = s_fc + 4096;                                         // staged evict prefix [4096]
+  u32* s_hw = s_ec + 4096;                                         // staged HBM free bitmap [4096]
   const int r = blockIdx.x;
   const int N = d.N;
   const u32 bt = (u32)d.bt;
   const bool fill = (d.flags & TA_F_FILL) != 0;
   if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
                d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
+  if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
+  PSTAMP(2, 0);
   if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
   if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
   u32* fp = d.f_pid + (size_t)r * N;
@@ -52,6 +59,13 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
         [&](u32 pos, int i) { fp[pos] = (u32)i; fc[pos] = need_of(d, (u32)i, r); });
     cta_incl_scan_array(fc, (int)nF, s_tmp);
   }
+  // short lists are searched many times below: stage them in shared memory
+  const u32* fcs = fc;
+  if (nF <= 4096) {
+    for (u32 i = threadIdx.x; i < nF; i += CTA) s_fc[i] = fc[i];
+    fcs = s_fc;
+  }
+  PSTAMP(2, 1);
   // ---- free blocks on r and eviction supply
   u32* hf = d.hbm_free + (size_t)r * d.NBW;
   ull fr = 0, es = 0;
@@ -65,7 +79,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   es = cta_reduce<ull>(es, s_red, add, 0ull);
   const ull supply = fr + es;
   // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
-  const u32 m = nF ? (u32)upper_bound_u32(fc, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
+  const u32 m = nF ? (u32)upper_bound_u32(fcs, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
   if (verb) {
     if (m < nF) {                        // all-or-nothing: fail before any mutation
       if (threadIdx.x == 0) d.ctr->verb_ok = 0;
@@ -73,7 +87,8 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     }
     if (threadIdx.x == 0) d.ctr->verb_ok = 1;
   }
-  const u32 tot = m ? fc[m - 1] : 0;
+  PSTAMP(2, 2);
+  const u32 tot = m ? fcs[m - 1] : 0;
   const u32 X = tot > fr ? (u32)(tot - fr) : 0;
   // ---- 5.3 eviction: E_r ordered (group 0 PAUSED, reverse restore order; group 1
   // ACTING placed elsewhere; group 2 ACTING placed on r; groups 1-2 by contrib),
@@ -96,6 +111,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     };
     const u32 T = cta_bucket_threshold(N, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
                                        [&](int i) { return d.n_hbm[i]; });
+    PSTAMP(2, 3);
     u32 n0 = cta_ordered_gather(N, s_tmp,
         [&](int ii) {
           int i = N - 1 - ii;            // descending slot: ties in group 0 go slot-down
@@ -115,71 +131,99 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
           va[n0 + pos] = (u32)i;
         });
     const u32 ne = n0 + n12;
-    int res = cta_radix_sort(ka, va, kb, vb, (int)ne, s_big, s_tmp);
+    PSTAMP(2, 4);
+    if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+      d.pst[2 * 32 + 27] = ne | (1ull << 62);
+      d.pst[2 * 32 + 28] = X | (1ull << 62);
+    }
+    int res = cta_sort(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
     const u32* sv = res ? vb : va;
+    PSTAMP(2, 5);
     u32* ep = d.e_pid + (size_t)r * N;
     u32* ec = d.e_cum + (size_t)r * N;
     for (u32 i = threadIdx.x; i < ne; i += CTA) { ep[i] = sv[i]; ec[i] = d.n_hbm[sv[i]]; }
     __syncthreads();
     cta_incl_scan_array(ec, (int)ne, s_tmp);
-    const u32 nv = (u32)upper_bound_u32(ec, (int)ne, X - 1) + 1;   // victims
-    const u32* sf = d.host_free + (size_t)r * d.NHW;
+    const u32* ecs = ec;
+    if (ne <= 4096) {
+      for (u32 i = threadIdx.x; i < ne; i += CTA) s_ec[i] = ec[i];
+      __syncthreads();
+      ecs = s_ec;
+    }
+    const u32 nv = (u32)upper_bound_u32(ecs, (int)ne, X - 1) + 1;   // victims
+    u32* sf = d.host_free + (size_t)r * d.NHW;
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     const u32 hfree = s_big[d.NHW];
+    // Stage what the per-block loop reads many times in the sort buffers (free now):
+    // the host-tier free words (selects read this snapshot, so the live bitmap can be
+    // updated in the same loop) and the victims' slot and HBM prefix length.
+    u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
+    u32* s_vp = reinterpret_cast<u32*>(sm->k[0]);        // [8192]
+    u32* s_vn = s_vp + 8192;                             // [8192]
+    const bool vst = nv <= 8192;
+    for (int w = threadIdx.x; w < d.NHW; w += CTA) s_sfw[w] = sf[w];
+    if (vst)
+      for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
+    for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
+    __syncthreads();
     EvDesc* evt = d.evt + (size_t)r * d.NB;   // (block, slot) in eviction order
-    u32* scr = d.evx + (size_t)r * d.NB; // evicted HBM index per evicted block e (< NB)
-    for (u32 e = threadIdx.x; e < X; e += CTA) {
-      u32 v = (u32)upper_bound_u32(ec, (int)nv, e);
-      u32 excl = v ? ec[v - 1] : 0;
-      u32 p = ep[v];
-      u32 j = d.n_hbm[p] - 1 - (e - excl);
-      u32* row = d.loc + (size_t)p * d.MAXBP;
-      u32 idx = row[j];
-      scr[e] = idx;
-      if (e < hfree) {
-        if (d.fused) d.evp[(size_t)r * d.NB + idx] = 2u * d.nL;  // segments pending their D2H read
-        u32 slot = bitmap_select(sf, s_big, d.NHW, e);
-        row[j] = LOC_HOST | slot;
-        d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
-        evt[e].src = idx;
-        evt[e].dst = slot;
-      } else {
-        row[j] = LOC_NONE;
+    // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
+    // four per thread per round so their block-table loads are in flight together
+    for (u32 e0 = 0; e0 < X; e0 += 4 * CTA) {
+      u32 pk[4], jk[4], ik[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u32 e = e0 + k * CTA + threadIdx.x;
+        pk[k] = jk[k] = ik[k] = 0;
+        if (e < X) {
+          const u32 v = (u32)upper_bound_u32(ecs, (int)nv, e);
+          const u32 excl = v ? ecs[v - 1] : 0;
+          const u32 p = vst ? s_vp[v] : ep[v];
+          const u32 nh = vst ? s_vn[v] : d.n_hbm[p];
+          pk[k] = p;
+          jk[k] = nh - 1 - (e - excl);
+          ik[k] = d.loc[(size_t)p * d.MAXBP + jk[k]];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u32 e = e0 + k * CTA + threadIdx.x;
+        if (e >= X) continue;
+        const u32 idx = ik[k], j = jk[k], p = pk[k];
+        u32* ent = d.loc + (size_t)p * d.MAXBP + j;
+        atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
+        if (e < hfree) {
+          if (d.fused) d.evp[(size_t)r * d.NB + idx] = 2u * d.nL;  // segments pending their D2H read
+          const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
+          *ent = LOC_HOST | slot;
+          d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
+          evt[e] = EvDesc{idx, slot};
+          atomicAnd(&sf[slot >> 5], ~(1u << (slot & 31)));
+          atomicOr(&s_hw[idx >> 5], 1u << (idx & 31));
+        } else {
+          *ent = LOC_NONE;
+        }
       }
     }
     __syncthreads();
-    u32* shf = d.host_free + (size_t)r * d.NHW;
-    for (u32 e = threadIdx.x; e < X; e += CTA) {
-      u32 idx = scr[e];
-      atomicOr(&hf[idx >> 5], 1u << (idx & 31));
-      if (e < hfree) {
-        u32 slot = evt[e].dst;
-        atomicAnd(&shf[slot >> 5], ~(1u << (slot & 31)));
-      }
-    }
+    PSTAMP(2, 6);
     // D2H copies are issued in ascending HBM-block order, the order in which the
     // allocation below hands the freed blocks out again, so a fetch that reuses an
     // evicted block rarely waits for its eviction (fused movement kernel).
     {
       const u32 ntoh = min(X, hfree);
-      u32* sbits = s_big;                 // [NBW] evicted blocks; then [NBW+1] prefix
-      u32* spre = s_big + d.NBW;
       EvDesc* evd = d.evd + (size_t)r * d.NB;
-      __syncthreads();
-      for (int w = threadIdx.x; w < d.NBW; w += CTA) sbits[w] = 0;
-      __syncthreads();
-      for (u32 e = threadIdx.x; e < ntoh; e += CTA) atomicOr(&sbits[evt[e].src >> 5], 1u << (evt[e].src & 31));
-      __syncthreads();
-      cta_bitmap_prefix(sbits, d.NBW, spre, s_tmp);
+      cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);      // host prefix no longer needed
       for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
-        u32 idx = evt[e].src;
-        u32 k = spre[idx >> 5] + __popc(sbits[idx >> 5] & ((1u << (idx & 31)) - 1));
-        evd[k] = evt[e];
+        const EvDesc x = evt[e];
+        const u32 k = s_big[x.src >> 5] + __popc(s_hw[x.src >> 5] & ((1u << (x.src & 31)) - 1));
+        evd[k] = x;
       }
     }
+    PSTAMP(2, 7);
     for (u32 v = threadIdx.x; v < nv; v += CTA) {
       u32 p = ep[v];
-      u32 excl = v ? ec[v - 1] : 0;
+      u32 excl = v ? ecs[v - 1] : 0;
       u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p];
       u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
       ta_decision rec;
@@ -201,27 +245,50 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     }
     __syncthreads();
   }
+  PSTAMP(2, 8);
   // ---- 5.4 allocation prefix (after the evictions' frees)
   cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
+  const u32* hws = hf;
+  if (d.NBW <= 4096) {
+    for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = hf[w];
+    __syncthreads();
+    hws = s_hw;
+  }
+  PSTAMP(2, 9);
   ull pc[PC_N];
 #pragma unroll
   for (int i = 0; i < PC_N; ++i) pc[i] = 0;
   FillDesc* fld = d.fld + (size_t)r * d.NB;
+  // Per-program values the request loop reads for each of its blocks, staged in the
+  // sort buffers (free now) for S_r programs when they fit: slot, first needed j,
+  // home, c_kv, c, uid.
+  const bool fst = m <= 2048;
+  u32* s_fp = reinterpret_cast<u32*>(sm->k[0]);
+  u32* s_fj = s_fp + 2048;
+  u32* s_fh = s_fp + 4096;
+  u32* s_fk = s_fp + 6144;
+  u32* s_fcn = s_fp + 8192;
+  u32* s_fu = s_fp + 10240;
   // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
   for (u32 i = threadIdx.x; i < nF; i += CTA) {
     u32 p = fp[i];
-    u32 need = fc[i] - (i ? fc[i - 1] : 0);
+    u32 need = fcs[i] - (i ? fcs[i - 1] : 0);
     int h = d.home[p];
     ta_decision rec;
     rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
     rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
     if (i < m) {
       const u32 ckv = d.c_kv[p], c = d.c[p];
+      const u32 nhp = d.n_hbm[p];
+      if (fst) {
+        s_fp[i] = p; s_fj[i] = h == r ? nhp : 0; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
+        s_fu[i] = d.uid[p];
+      }
       const bool resumed = !(d.satisfied[p] && h == r);
       if (resumed && ckv > 0) {
         u32 hb = ceil_div_u32(ckv, bt);
         u32 sh = bt - (ckv - (hb - 1) * bt);           // missing slots of the last block
-        u32 nh = d.n_hbm[p], ns = d.n_host[p], nn = hb - nh - ns;
+        u32 nh = nhp, ns = d.n_host[p], nn = hb - nh - ns;
         ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
         u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
         if (is_hbm(el)) th -= sh; else if (is_host(el)) ts -= sh; else tn -= sh;
@@ -235,7 +302,7 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
       pc[PC_MISS] += rec.miss_tok; pc[PC_NEWTOK] += rec.new_tok;
       if (h == r && c > ckv && (ckv % bt) != 0) {      // partial last block already resident
         u32 j = ckv / bt;
-        if (j < d.n_hbm[p]) {
+        if (j < nhp) {
           u32 t1 = min((j + 1) * bt, c);
           pc[PC_FILLTOK] += t1 - ckv;
           if (fill) {
@@ -252,63 +319,97 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     d.dec_fs[(size_t)r * N + i] = rec;
   }
   __syncthreads();
-  // ---- 5.4 / 5.5 requests: (p in S_r slot order, needed j ascending) -> q-th lowest free block
+  PSTAMP(2, 10);
+  if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+    d.pst[2 * 32 + 29] = nF | (1ull << 62);
+    d.pst[2 * 32 + 30] = tot | (1ull << 62);
+  }
+  // ---- 5.4 / 5.5 requests: (p in S_r slot order, needed j ascending) -> q-th lowest free block.
+  // Selects read the staged snapshot of the free bitmap, so each request clears its
+  // block in the live bitmap at once.  Only requests that move or write bytes get a
+  // descriptor (copies; fills when the engine stand-in is on), compacted in request
+  // order by a CTA scan, so the copy kernels never walk a block that needs nothing.
   FeDesc* fed = d.fed + (size_t)r * d.NB;
   u32* dfh = d.dfh + (size_t)r * d.NB;
   u32* dfs = d.dfs + (size_t)r * d.NB;
-  u32* qdst = d.evx + (size_t)r * d.NB;  // allocated block per request (eviction use is over)
-  for (u32 q = threadIdx.x; q < tot; q += CTA) {
-    u32 i = (u32)upper_bound_u32(fc, (int)m, q);
-    u32 excl = i ? fc[i - 1] : 0;
-    u32 p = fp[i];
-    int h = d.home[p];
-    u32 j = (h == r ? d.n_hbm[p] : 0) + (q - excl);
-    u32 dst = bitmap_select(hf, s_big, d.NBW, q);
-    u32* row = d.loc + (size_t)p * d.MAXBP;
-    u32 old = row[j];
-    const u32 ckv = d.c_kv[p], c = d.c[p];
-    const u32 hb = ceil_div_u32(ckv, bt);
-    const u32 jb = j * bt, je = min(jb + bt, c);
-    if (is_hbm(old) || is_host(old)) {                  // copy: P2P (HBM of h != r) or H2D (tier of h)
-      // a copied partial block that also receives new tokens carries the fill of its
-      // tail [max(jb, c_kv), je) in the same descriptor (written after the copy)
-      u32 t0 = 0, t1 = 0;
-      if (ckv < c && jb + bt > ckv) {
-        t0 = max(jb, ckv);
-        t1 = je;
-        pc[PC_FILLTOK] += t1 - t0;
-        if (!fill) t0 = t1 = 0;
+  u32 nfed = 0;
+  for (u32 q0 = 0; q0 < tot; q0 += 2 * CTA) {
+    u32 ik[2], pk[2], jk[2], dk[2];
+    int hk[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {                       // block-table loads of both in flight
+      const u32 q = q0 + k * CTA + threadIdx.x;
+      ik[k] = pk[k] = jk[k] = dk[k] = 0;
+      hk[k] = 0;
+      if (q < tot) {
+        const u32 i = (u32)upper_bound_u32(fcs, (int)m, q);
+        const u32 excl = i ? fcs[i - 1] : 0;
+        const u32 p = fst ? s_fp[i] : fp[i];
+        const int h = fst ? (int)s_fh[i] : d.home[p];
+        const u32 j = (fst ? s_fj[i] : (h == r ? d.n_hbm[p] : 0)) + (q - excl);
+        pk[k] = fst ? i : p;
+        hk[k] = h;
+        jk[k] = j;
+        dk[k] = bitmap_select(hws, s_big, d.NBW, q);
+        ik[k] = d.loc[(size_t)p * d.MAXBP + j];
       }
-      if (is_hbm(old)) {
-        fed[q] = FeDesc{MV_P2P, (u32)h, old, dst, d.uid[p], t0, t1, j};
-        dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
-        pc[PC_P2P] += 1;
-      } else {
-        fed[q] = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst, d.uid[p], t0, t1, j};
-        dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
-        pc[PC_H2D] += 1;
-      }
-    } else {                                            // recompute history / brand-new tokens
-      if (j < hb) pc[PC_REC] += 1; else pc[PC_NEW] += 1;
-      pc[PC_FILLTOK] += je - jb;
-      fed[q] = fill ? FeDesc{MV_FILL, 0, 0, dst, d.uid[p], jb, je, j} : FeDesc{MV_NONE, 0, 0, dst, 0, 0, 0, j};
     }
-    row[j] = dst;
-    d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
-    qdst[q] = dst;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const u32 q = q0 + k * CTA + threadIdx.x;
+      FeDesc x{MV_NONE, 0, 0, 0, 0, 0, 0, 0};
+      if (q < tot) {
+        const u32 p = fst ? s_fp[pk[k]] : pk[k];
+        const int h = hk[k];
+        const u32 j = jk[k], dst = dk[k], old = ik[k];
+        const u32 ckv = fst ? s_fk[pk[k]] : d.c_kv[p];
+        const u32 c = fst ? s_fcn[pk[k]] : d.c[p];
+        const u32 uid = fst ? s_fu[pk[k]] : d.uid[p];
+        const u32 hb = ceil_div_u32(ckv, bt);
+        const u32 jb = j * bt, je = min(jb + bt, c);
+        if (is_hbm(old) || is_host(old)) {              // copy: P2P (HBM of h != r) or H2D (tier of h)
+          // a copied partial block that also receives new tokens carries the fill of its
+          // tail [max(jb, c_kv), je) in the same descriptor (written after the copy)
+          u32 t0 = 0, t1 = 0;
+          if (ckv < c && jb + bt > ckv) {
+            t0 = max(jb, ckv);
+            t1 = je;
+            pc[PC_FILLTOK] += t1 - t0;
+            if (!fill) t0 = t1 = 0;
+          }
+          if (is_hbm(old)) {
+            x = FeDesc{MV_P2P, (u32)h, old, dst, uid, t0, t1, j};
+            dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
+            pc[PC_P2P] += 1;
+          } else {
+            x = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst, uid, t0, t1, j};
+            dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
+            pc[PC_H2D] += 1;
+          }
+        } else {                                        // recompute history / brand-new tokens
+          if (j < hb) pc[PC_REC] += 1; else pc[PC_NEW] += 1;
+          pc[PC_FILLTOK] += je - jb;
+          if (fill) x = FeDesc{MV_FILL, 0, 0, dst, uid, jb, je, j};
+        }
+        d.loc[(size_t)p * d.MAXBP + j] = dst;
+        d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
+        atomicAnd(&hf[dst >> 5], ~(1u << (dst & 31)));
+      }
+      u32 round_n;
+      const u32 pos = cta_excl_scan(x.kind != MV_NONE ? 1u : 0u, s_tmp, &round_n);
+      if (x.kind != MV_NONE) fed[nfed + pos] = x;
+      nfed += round_n;
+    }
   }
   __syncthreads();
-  for (u32 q = threadIdx.x; q < tot; q += CTA) {   // the bitmap changes only after all selects
-    u32 dst = qdst[q];
-    atomicAnd(&hf[dst >> 5], ~(1u << (dst & 31)));
-  }
+  PSTAMP(2, 11);
 #pragma unroll
   for (int i = 0; i < PC_N; ++i) warp_add_shared(pc[i], &s_pc[i]);
   __syncthreads();
   if (threadIdx.x == 0) {
     d.f_cnt[r] = nF;
     d.s_cnt[r] = m;
-    d.fed_cnt[r] = tot;                  // one descriptor per request, in request order
+    d.fed_cnt[r] = nfed;                 // copy / fill descriptors, in request order
     d.fld_cnt[r] = s_app[1];
     d.dfh_cnt[r] = s_app[2];
     d.dfs_cnt[r] = s_app[3];
@@ -328,4 +429,5 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     atomicAdd(&d.stats[ST_NEW_TOK], s_pc[PC_NEWTOK]);
     atomicAdd(&d.stats[ST_STALLS], s_pc[PC_STALL]);
   }
+  PSTAMP(2, 12);
 }

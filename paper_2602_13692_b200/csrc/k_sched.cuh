@@ -2,25 +2,10 @@
 #pragma once
 #include "common.cuh"
 
-#define RESTORE_CHUNK 512u   // queue entries selected per sorted chunk of the restore loop
-
-// Start of a tick: reset per-tick counters and the load accumulators.
-__global__ void k_begin(Dev d) {
-  int t = threadIdx.x;
-  if (t == 0) {
-    d.ctr->stops = 0;
-    d.ctr->restore_cnt = 0;
-    d.ctr->n_arr = 0;
-    d.ctr->T = d.api_mode ? d.ctr->now_ms : d.ctr->tick * d.dt;
-    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
-  }
-  if (t < d.R) {
-    d.L[t] = 0;
-    d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
-    d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
-    d.cpd_cnt[t] = 0;
-  }
-}
+// Queue entries selected per sorted chunk of the restore loop: the loop usually stops
+// at the head (steady state) or runs long (bursts), so chunks grow geometrically.
+#define RESTORE_CHUNK0 32u
+#define RESTORE_CHUNK_MAX 4096u
 
 // Step 3, one CTA per replica (reading A6): if the decayed
 // load exceeds lambda_max*C, pause the minimal prefix of the actives in S_pause
@@ -30,10 +15,21 @@ __global__ void k_begin(Dev d) {
 __global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
+  extern __shared__ __align__(16) char dsm[];
+  SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
+  __shared__ ull s_L;
   const int r = blockIdx.x;
-  const ull Lr = d.L[r];
+  if (threadIdx.x == 0) {                       // publish this tick's load (eq. 7) of replica r
+    s_L = d.Lacc[r];
+    d.Lacc[r] = 0;
+  }
+  __syncthreads();
+  const ull Lr = s_L;
   const ull cap = (ull)d.cap_max[r];
-  if (Lr <= cap) return;
+  if (Lr <= cap) {
+    if (threadIdx.x == 0) d.L[r] = Lr;
+    return;
+  }
   const u32 dC = (u32)(Lr - cap);
   const int N = d.N;
   const u32 NBK = d.nbk, sh = d.nb_shift;
@@ -54,7 +50,7 @@ __global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
         ka[pos] = pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
         va[pos] = (u32)i;
       });
-  int res = cta_radix_sort(ka, va, kb, vb, (int)n, s_big, s_tmp);
+  int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
   const u32* sv = res ? vb : va;
   u32* cum = (u32*)(res ? ka : kb);             // free key buffer as u32 scratch
   for (u32 i = threadIdx.x; i < n; i += CTA) cum[i] = d.contrib[sv[i]];
@@ -92,6 +88,8 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   __shared__ u32 s_stop;
+  extern __shared__ __align__(16) char dsm[];
+  SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   const int N = d.N, R = d.R;
   const u32 NBK = d.nbk, sh = d.nb_shift;
   u64* ka = d.ska + (size_t)R * N;
@@ -112,21 +110,43 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
       maxcap = t > maxcap ? t : maxcap;
     }
   }
-  u32 cnt = 0, over = 0;
+  if ((d.flags & TA_F_TIMING) && threadIdx.x < 32) d.pst[1 * 32 + threadIdx.x] = 0;
+  PSTAMP(1, 0);
+  if (!d.api_mode) {                   // closed-loop trace arrivals (reading A12):
+    const i64 na = d.ctr->next_arrival;  // the lowest UNARRIVED slots, one per release
+    const i64 n_arr = trace_arrivals(d);
+    const u32 k = (u32)d.ctr->tick;
+    for (i64 q = threadIdx.x; q < n_arr; q += CTA) {
+      const int p = (int)(na + q);
+      d.uid[p] = d.t_uid[p]; d.status[p] = TA_PAUSED; d.phase[p] = TA_PHASE_R;
+      d.c[p] = d.t_p0[p]; d.c_kv[p] = 0; d.paused_since[p] = k;
+      d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
+      d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
+      d.tool_return[p] = INT64_MAX;
+      const u32 nbv = ceil_div_u32(d.t_p0[p], d.bt);
+      d.nb[p] = nbv; d.n_hbm[p] = 0; d.n_host[p] = 0; d.prefix_hbm[p] = 0; d.contrib[p] = nbv;
+    }
+    __syncthreads();
+  }
+  u32 cnt = 0, over = 0, it = 0;
   auto pred = [&](int i) { return d.status[i] == TA_PAUSED; };
   auto bucket = [&](int i) { return (u32)(d.phase[i] == TA_PHASE_A) * NBK + (d.nb[i] >> sh); };
-  u32 lo = 0;
+  u32 lo = 0, chunk = RESTORE_CHUNK0;
   while (true) {
-    const u32 T = cta_bucket_threshold(N, 2 * NBK, lo, RESTORE_CHUNK, s_big, s_tmp, pred, bucket,
+    const u32 T = cta_bucket_threshold(N, 2 * NBK, lo, chunk, s_big, s_tmp, pred, bucket,
                                        [](int) { return 1u; });
+    if (it < 7) PSTAMP(1, 1 + 4 * it);
     u32 n = cta_ordered_gather(N, s_tmp,
         [&](int i) { if (!pred(i)) return false; u32 b = bucket(i); return b >= lo && b <= T; },
         [&](u32 pos, int i) {
           ka[pos] = restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
           va[pos] = (u32)i;
         });
-    int res = cta_radix_sort(ka, va, kb, vb, (int)n, s_big, s_tmp);
+    if (it < 7) PSTAMP(1, 2 + 4 * it);
+    if ((d.flags & TA_F_TIMING) && threadIdx.x == 0 && it < 4) d.pst[1 * 32 + 27 + it] = n | (1ull << 62);
+    int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
     const u32* q = res ? vb : va;
+    if (it < 7) PSTAMP(1, 3 + 4 * it);
     if (w0) {
       bool stop = false;
       for (u32 base = 0; base < n && !stop; base += 32) {
@@ -157,8 +177,11 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
       if (lane == 0) s_stop = stop || T >= 2 * NBK - 1;
     }
     __syncthreads();
+    if (it < 7) PSTAMP(1, 4 + 4 * it);
+    ++it;
     if (s_stop) break;
     lo = T + 1;
+    chunk = min(chunk * 8, RESTORE_CHUNK_MAX);
     __syncthreads();
   }
   if (w0) {
@@ -169,4 +192,5 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
       atomicAdd(&d.stats[ST_OVERSIZED], (ull)over);
     }
   }
+  PSTAMP(1, 31);
 }

@@ -137,7 +137,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.t_g = L.take<u32>(TT); x.t_d = L.take<u32>(TT); x.t_o = L.take<u32>(TT);
   x.hbm_free = L.take<u32>(R * NBW); x.host_free = L.take<u32>(R * NHW);
   x.owner_hbm = L.take<u32>(R * NB); x.owner_host = L.take<u32>(R * NH);
-  x.L = L.take<ull>(R);
+  x.L = L.take<ull>(R); x.Lacc = L.take<ull>(R);
   x.ska = L.take<u64>((R + 1) * N); x.skb = L.take<u64>((R + 1) * N);
   x.sva = L.take<u32>((R + 1) * N); x.svb = L.take<u32>((R + 1) * N);
   x.pause_list = L.take<u32>(R * N); x.pause_cnt = L.take<u32>(R);
@@ -155,6 +155,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.dfs = L.take<u32>(R * NB); x.dfs_cnt = L.take<u32>(R);
   x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
   x.events = L.take<ta_event>(kMaxEvents);
+  x.pst = L.take<ull>(4 * 32);
   if (d) *d = x;
   return L.off + 256;
 }
@@ -228,15 +229,18 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   cudaStream_t s = x->stream;
   const int N = d.N, R = d.R;
   rec(x, 0);
-  k_begin<<<1, 32, 0, s>>>(d);
-  if (d.api_mode) k_apply_events<<<1, 32, 0, s>>>(d, x->ev_dev, n_ev, 1);
-  else k_ingest_trace<<<(N + 255) / 256, 256, 0, s>>>(d);
-  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 0);
+  // per-tick lists and counters were cleared by the previous tick's k_assemble
+  if (d.api_mode) {
+    k_apply_events<<<1, 32, 0, s>>>(d, x->ev_dev, n_ev, 1);
+    k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 0);
+  } else {
+    k_tick_front<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);   // ingest + footprint + load
+  }
   rec(x, 1);
-  k_pause<<<R, CTA, 0, s>>>(d);
-  k_restore<<<1, CTA, 0, s>>>(d);
+  k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
+  k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
   rec(x, 2);
-  k_plan<<<R, CTA, 0, s>>>(d, 0);
+  k_plan<<<R, CTA, PLAN_DSMEM, s>>>(d, 0);
   rec(x, 3);
   launch_movement(x);
   rec(x, 6);
@@ -404,6 +408,10 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
   if (e == cudaSuccess) { k_init<<<148, 256, 0, x->stream>>>(d); e = cudaGetLastError(); }
+  // planner kernels: small sorts and staged lists in dynamic shared memory
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));
@@ -557,6 +565,15 @@ ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n) {
   return TA_OK;
 }
 
+ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!ctx->timing) FAIL(ctx, TA_E_STATE, "context created without TA_F_TIMING");
+  if (!out || n < 0 || n > 128) FAIL(ctx, TA_E_INVAL, "bad stamp buffer");
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemcpy(out, ctx->d.pst, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TA_OK;
+}
+
 ta_status ta_move_blocks(ta_ctx* ctx, int32_t kind, int32_t src_r, int32_t dst_r, const uint32_t* src_blocks,
                          const uint32_t* dst_blocks, int32_t n) {
   if (ta_status s = check_ctx(ctx)) return s;
@@ -678,7 +695,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 1);
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
-  k_plan<<<d.R, CTA, 0, s>>>(d, 1);
+  k_plan<<<d.R, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
   launch_movement(ctx);
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 1);

@@ -1,5 +1,5 @@
 """Per-step device/host timing of the bench workload (developer tool, GPU box).
-usage: python tools/step_times.py [--no-fuse] [--ticks N]"""
+usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing]"""
 import sys
 import time
 
@@ -10,7 +10,7 @@ sys.path.insert(0, ".")
 import tracegen  # noqa: E402
 from paper_2602_13692_b200 import Pool, binding  # noqa: E402
 
-flags = binding.F_TIMING | (binding.F_NO_FUSE if "--no-fuse" in sys.argv else 0)
+flags = (0 if "--no-timing" in sys.argv else binding.F_TIMING) | (binding.F_NO_FUSE if "--no-fuse" in sys.argv else 0)
 ticks = int(sys.argv[sys.argv.index("--ticks") + 1]) if "--ticks" in sys.argv else 24
 cfg = tracegen.get_config("bench_10k")
 tr = tracegen.make_trace(cfg)
@@ -26,7 +26,7 @@ for k in range(ticks):
     e1.record(s)
     e1.synchronize()
     t1 = time.perf_counter()
-    ph = pool.phase_times()
+    ph = pool.phase_times() if flags & binding.F_TIMING else [0.0] * 9
     st = pool.stats()
     d2h = st["evict_to_host"] - prev["evict_to_host"]
     h2d = st["h2d_blocks"] - prev["h2d_blocks"]
@@ -34,3 +34,8 @@ for k in range(ticks):
     print(f"tick {k:3d} dev {e0.elapsed_time(e1):9.2f} ms host {1e3 * (t1 - t0):9.2f} ms  "
           f"move {ph[3] / 1e3:8.2f} ms  d2h {d2h:5d} h2d {h2d:5d} blocks  sched {sum(ph) / 1e3 - ph[3] / 1e3:6.3f} ms",
           flush=True)
+    if "--phases" in sys.argv:
+        print("   phases us: " + " ".join(f"{x:.1f}" for x in ph))
+        for kname, v in pool.phase_stamps().items():   # in-kernel stamps, cycles -> us at 1965 MHz
+            print(f"   {kname:8s}: " + " ".join(f"{i}:{c / 1965.0:.1f}" if isinstance(i, int) else f"{i}={c}"
+                                                for i, c in v))
