@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--host-gib", type=float, default=64.0, help="cap of the pinned host tier")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--sched-ticks", type=int, default=200, help="ticks of the decision-path latency probe")
     return ap.parse_args()
 
 
@@ -171,6 +172,41 @@ def kv_path_microbench(pool, torch, peaks, hbm_peak, n_blocks=2048, reps=3):
     return out
 
 
+def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
+    """Latency of one scheduler tick at the bench's program count, decision path only:
+    the same trace and pool sizes with the decision-identical `mini` KV shape (4 KiB
+    blocks: no decision depends on bytes per block), so the movement kernels still run
+    but move almost nothing.  One CUDA-event pair per tick on the context stream; L2
+    flushed before every tick (outside the pair).  Ticks [start, start + n_ticks)."""
+    import numpy as np
+    from paper_2602_13692_b200 import Pool
+    c = dict(cfg)
+    c["kv"] = "mini"
+    pool = Pool(c, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0, device=dev.index,
+                replicas_here=1, first_replica=0)
+    pool.load_trace(tr)
+    s = pool.stream
+    for _ in range(start):
+        pool.step(decisions=False)
+    us = []
+    for _ in range(n_ticks):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        pool.step(decisions=False)
+        b.record(s)
+        b.synchronize()
+        us.append(a.elapsed_time(b) * 1e3)
+    pool.close()
+    us = np.array(us)
+    return {"median_us": round(float(np.median(us)), 1), "p99_us": round(float(np.percentile(us, 99)), 1),
+            "mean_us": round(float(us.mean()), 1), "ticks": f"{start}..{start + n_ticks - 1}",
+            "programs": tr.n_slots, "target_us": 100,
+            "kv": "mini (4 KiB blocks; decisions identical to the Q32 run, movement kernels run but move ~0 B)",
+            "note": "one full ta_sched_step CUDA graph (all 9 kernels), L2 flushed before each tick"}
+
+
 def workload(name, world):
     """The bench workload at N GPUs: N replicas, 10k programs per replica (weak scaling)."""
     import tracegen
@@ -285,8 +321,11 @@ def main():
     block_bytes = 2 * 64 * 8 * 128 * 2 * cfg["block_tokens"]
     nh = min(cfg["host_blocks"], host_cap_bytes(args.host_gib, world) // block_bytes)
     cfg["host_blocks"] = nh
-    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=binding.F_TIMING, device=local,
+    # the timed run has no timing nodes in its graph; the per-kernel breakdown comes from
+    # a replay of the same ticks with TA_F_TIMING (event-record nodes cost ~2.7 us each)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0, device=local,
                 replicas_here=1, first_replica=rank)
+    base_flags = pool.c.flags
     if world > 1:
         from paper_2602_13692_b200.dist import connect
         connect(pool)
@@ -309,29 +348,20 @@ def main():
     torch.cuda.synchronize(dev)
     s = pool.stream
     st0 = pool.stats()
-    phase_sum = np.zeros(9)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     sampler.mark("t_start")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     e0.record(s)
-    step_ms = []
-    ticks_info = []
-    for _ in range(args.steps):
-        ea = torch.cuda.Event(enable_timing=True)
-        ea.record(s)
+    for i in range(args.steps):       # enqueued back to back: no host sync inside the region
+        ev[2 * i].record(s)
         with torch.cuda.stream(s):
             flush.zero_()             # L2 flush (256 MiB > 126 MB L2) inside the timed region
         pool.step(decisions=False)
-        ph_step = np.array(pool.phase_times())   # syncs the stream: per-kernel CUDA-event times
-        phase_sum += ph_step
-        ticks_info.append((pool.last_tick(), ph_step))   # host-mapped telemetry, no extra copy
-        eb = torch.cuda.Event(enable_timing=True)
-        eb.record(s)
-        eb.synchronize()
-        step_ms.append((round(ea.elapsed_time(eb), 3), round(float(ph_step.sum()) / 1e3, 3)))
+        ev[2 * i + 1].record(s)
     e1.record(s)
     torch.cuda.synchronize(dev)
     sampler.mark("t_end")
@@ -339,6 +369,7 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
+    step_ms = [round(ev[2 * i].elapsed_time(ev[2 * i + 1]), 3) for i in range(args.steps)]
     st1 = pool.stats()
     sum_nb = int(pool.debug_download()["nb"].sum())   # block-table entries scanned per tick
     if world > 1:
@@ -349,9 +380,29 @@ def main():
     progs_total = tr.n_slots
     value = args.steps * progs_total / 1e4 / (ms * 1e-3)
 
+    # ---- per-kernel breakdown: the SAME ticks again with TA_F_TIMING (fresh context over
+    # the same buffers, same untimed prefix); CUDA-event times of every graph phase
+    pool.reset(flags=base_flags | binding.F_TIMING)
+    if world > 1:
+        connect(pool)
+    pool.load_trace(tr)
+    for _ in range(args.preroll + args.warmup):
+        pool.step(decisions=False)
+    phase_sum = np.zeros(9)
+    ticks_info = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        pool.step(decisions=False)
+        ph_step = np.array(pool.phase_times())   # syncs the stream
+        phase_sum += ph_step
+        ticks_info.append((pool.last_tick(), ph_step))   # host-mapped telemetry
+    if world > 1:
+        dist.barrier()
+
     # ---- e2e: the SAME ticks (fresh context over the same buffers, same untimed
     # prefix) through the public API, decisions read back to the host every tick
-    pool.reset()
+    pool.reset(flags=base_flags)
     if world > 1:
         connect(pool)                    # fresh context: fresh mailboxes to map
     pool.load_trace(tr)
@@ -442,6 +493,8 @@ def main():
         "d2d_gb_per_step": round(dstat["compact_blocks"] * bb / args.steps / 1e9, 3),
     }
     sched_us = float(ph[0] + ph[1] + ph[2] + ph[6] + ph[8])
+    tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.preroll + args.warmup, args.sched_ticks, flush)
+                if rank == 0 and world == 1 and args.sched_ticks > 0 else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(tracegen.get_config(args.config), tracegen.make_trace(tracegen.get_config(args.config)),
@@ -461,16 +514,17 @@ def main():
         "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(d2h / args.steps),
                 "note": "public API ta_sched_step with decisions read back; trace uploaded once before timing"},
-        # per tick: begin, ingest, footprint, pause, restore, plan, movement (1 fused kernel;
-        # multi-GPU: evict, barrier, fetch, push, barrier), finalize, compact plan/copy, assemble
-        "gpu_launches": args.steps * (11 if world == 1 else 15),
+        # per tick: tick_front, pause, restore, plan, movement (1 fused kernel; multi-GPU:
+        # evict, barrier, fetch, push, barrier), finalize, compact plan/copy, assemble
+        "gpu_launches": args.steps * (9 if world == 1 else 13),
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),
+        "sched_tick": tick_lat,
         "kv_moved": moved,
         "kv_paths": kv_paths,
         "cpu_baseline": cpu,
-        "step_ms_and_graph_ms": step_ms,
+        "step_ms": step_ms,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -245,11 +245,14 @@ class Pool:
             raise TAError(st, "ta_init_pool failed")
         self.dec_buf = np.zeros(4 * n_programs + self.R + 64, dtype=DECISION_DTYPE)
 
-    def reset(self):
+    def reset(self, flags: int | None = None):
         """Destroy the context and create a fresh one over the same buffers (the
-        workspace is re-initialised: every slot UNARRIVED, all blocks free)."""
+        workspace is re-initialised: every slot UNARRIVED, all blocks free).
+        `flags` replaces the context's TA_F_* flags (same buffers and workspace size)."""
         import torch
         self.close()
+        if flags is not None:
+            self.c.flags = flags
         self.ctx = C.c_void_p()
         with torch.cuda.device(self.device):
             st = lib().ta_init_pool(C.byref(self.c), C.byref(self.buffers),
