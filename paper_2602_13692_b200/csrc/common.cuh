@@ -134,6 +134,13 @@ struct Dev {
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)
   ull* pst;                        // [4][32] in-kernel phase stamps (TA_F_TIMING; developer aid)
+  // ---- candidate lists built by the footprint pass (grid-parallel; unordered appends),
+  // so the single-CTA planner kernels never scan all N slots except the restore gather
+  u32 *act_list, *act_cnt;         // [R][N], [R]: REASONING/ACTING placed on r
+  u32 *ec_list, *ec_cnt;           // [R][N], [R]: home == r with HBM blocks (eviction candidates)
+  u32* rhist;                      // [2 * nbk] restore-bucket histogram of PAUSED slots
+  u32* rb;                         // [N] restore bucket of a PAUSED slot, else 0xFFFFFFFF
+  i8* fpl;                         // [N] placement at footprint time (-1: not active)
 };
 
 // Phase stamp: SM clock of thread 0 of CTA 0 at a phase boundary of a planner kernel
@@ -170,6 +177,11 @@ __device__ __forceinline__ i64 trace_arrivals(const Dev& d) {
   i64 n = (d.ctr->tick == 0 ? (i64)d.n_initial : 0) + (i64)d.ctr->stops;
   i64 room = (i64)d.n_slots - d.ctr->next_arrival;
   return n < room ? n : room;
+}
+
+// Coarse restore bucket (monotone in the S_restore key): tau = R first, then nb.
+__device__ __forceinline__ u32 restore_bucket(const Dev& d, u8 ph, u32 nbv) {
+  return (u32)(ph == TA_PHASE_A) * d.nbk + (nbv >> d.nb_shift);
 }
 
 // S_restore order (reading A8): R first, nb up, paused_since up; ties by slot
@@ -278,24 +290,37 @@ __device__ __forceinline__ int upper_bound_u32(const u32* a, int n, u32 x) {
 
 // ------------------------------------------------------------------ stable CTA radix sort
 // Sorts (key, val) pairs [0, n) ascending by key, stable.  8-bit digits; only the
-// digits in which keys differ are processed (vary = OR ^ AND over all keys).
+// digits in which keys differ are processed (vary = OR ^ AND over all keys).  With
+// by_val the order is (key, val) lexicographic: the val digits are processed first
+// (LSD), then the key digits.
 // Buffers a -> b -> a ...; returns 0 if the result is in (ka, va), 1 if in (kb, vb).
 // s_hist: NWARP * 256 u32 of shared memory; s_tmp: >= NWARP + 1 u32.
-__device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp) {
+__device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp,
+                              bool by_val = false) {
   if (n <= 1) return 0;
   // which digits vary
-  u64 o = 0, a = ~0ull;
-  for (int i = threadIdx.x; i < n; i += CTA) { u64 k = ka[i]; o |= k; a &= k; }
+  u64 o = 0, a = ~0ull, vo = 0, vand = ~0ull;
+  for (int i = threadIdx.x; i < n; i += CTA) {
+    u64 k = ka[i]; o |= k; a &= k;
+    if (by_val) { u64 v = va[i]; vo |= v; vand &= v; }
+  }
   __shared__ u64 s_red[NWARP];
   o = cta_reduce<u64>(o, s_red, [](u64 x, u64 y) { return x | y; }, 0ull);
   a = cta_reduce<u64>(a, s_red, [](u64 x, u64 y) { return x & y; }, ~0ull);
-  u64 vary = o ^ a;
+  u64 vary = o ^ a, vvary = 0;
+  if (by_val) {
+    vo = cta_reduce<u64>(vo, s_red, [](u64 x, u64 y) { return x | y; }, 0ull);
+    vand = cta_reduce<u64>(vand, s_red, [](u64 x, u64 y) { return x & y; }, ~0ull);
+    vvary = vo ^ vand;
+  }
   const int w = threadIdx.x >> 5, lane = lane_id();
   const int tile = (n + NWARP - 1) / NWARP;
   const int lo = w * tile, hi = min(n, lo + tile);
   int cur = 0;
-  for (int shift = 0; shift < 64; shift += 8) {
-    if (((vary >> shift) & 0xFF) == 0) continue;
+  for (int pass = by_val ? 0 : 4; pass < 12; ++pass) {   // passes 0-3: val bytes; 4-11: key bytes
+    const bool on_val = pass < 4;
+    const int shift = on_val ? 8 * pass : 8 * (pass - 4);
+    if ((((on_val ? vvary : vary) >> shift) & 0xFF) == 0) continue;
     u64* kin = cur ? kb : ka;
     u32* vin = cur ? vb : va;
     u64* kout = cur ? ka : kb;
@@ -305,7 +330,7 @@ __device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_
     for (int base = lo; base < hi; base += 32) {
       int i = base + lane;
       bool v = i < hi;
-      u32 dg = v ? (u32)((kin[i] >> shift) & 0xFF) : 256u + lane;
+      u32 dg = v ? (u32)(((on_val ? (u64)vin[i] : kin[i]) >> shift) & 0xFF) : 256u + lane;
       u32 peers = __match_any_sync(FULL_MASK, dg);
       if (v && (__ffs(peers) - 1) == lane) s_hist[dg * NWARP + w] += __popc(peers);
       __syncwarp();
@@ -327,7 +352,8 @@ __device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_
       int i = base + lane;
       bool v = i < hi;
       u64 k = v ? kin[i] : 0;
-      u32 dg = v ? (u32)((k >> shift) & 0xFF) : 256u + lane;
+      u32 vv = v ? vin[i] : 0;
+      u32 dg = v ? (u32)(((on_val ? (u64)vv : k) >> shift) & 0xFF) : 256u + lane;
       u32 peers = __match_any_sync(FULL_MASK, dg);
       u32 rank = __popc(peers & lanemask_lt());
       if (v) {
@@ -366,11 +392,43 @@ __device__ __forceinline__ void bitonic_pick(u64& k, u32& p, u64 ok, u32 op, boo
   if (other_less == take_min) { k = ok; p = op; }
 }
 
+// Rank sort for short inputs (n <= RANK_SORT_MAX): thread i owns element i and
+// counts the elements that precede it in (key, tie) order, reading all keys as
+// shared-memory broadcasts; no barrier-separated network stages.  tie: unique per
+// element.  Writes (key, out_val) to (kb, vb) at the element's rank.
+#define RANK_SORT_MAX 512
+__device__ __forceinline__ void cta_rank_sort(const u64* ka, u64* kb, u32* vb, int n, SortSmem* sm,
+                                              bool tie_is_val, const u32* va) {
+  const int t = threadIdx.x;
+  if (t < n) {
+    sm->k[0][t] = ka[t];
+    sm->p[0][t] = tie_is_val ? va[t] : (u32)t;
+  }
+  __syncthreads();
+  if (t < n) {
+    const u64 k = sm->k[0][t];
+    const u32 v = sm->p[0][t];
+    u32 rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const u64 kj = sm->k[0][j];
+      const u32 vj = sm->p[0][j];
+      rank += (kj < k) | ((kj == k) & (vj < v));
+    }
+    kb[rank] = k;
+    vb[rank] = tie_is_val ? v : va[t];
+  }
+  __syncthreads();
+}
+
 // Stable sort of (ka, va)[0, n) by key.  Returns 0 if the result is in (ka, va),
 // 1 if in (kb, vb).  The buffer not holding the result is free scratch afterwards.
 __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm) {
   if (n <= 1) return 0;
   if (n > SORT_SMALL) return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp);
+  if (n <= RANK_SORT_MAX) {
+    cta_rank_sort(ka, kb, vb, n, sm, false, va);
+    return 1;
+  }
   int P = 32;
   while (P < n) P <<= 1;
   const int E = P > CTA ? P / CTA : 1;        // 1, 2 or 4 pairs per thread
@@ -444,6 +502,89 @@ __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, 
   return 1;
 }
 
+// Sort (ka, va)[0, n) by (key, val) lexicographic, val unique (a slot or a
+// slot-derived tie-break): the result does not depend on the input order, so inputs
+// may come from unordered (atomic) appends.  Returns 0 / 1 like cta_sort.
+__device__ int cta_sort_kv(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm) {
+  if (n <= 1) return 0;
+  if (n > SORT_SMALL) return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp, true);
+  if (n <= RANK_SORT_MAX) {
+    cta_rank_sort(ka, kb, vb, n, sm, true, va);
+    return 1;
+  }
+  int P = 32;
+  while (P < n) P <<= 1;
+  const int E = P > CTA ? P / CTA : 1;
+  const int t = threadIdx.x;
+  const bool act = E > 1 || t < P;
+  u64 k[SORT_SMALL / CTA];
+  u32 p[SORT_SMALL / CTA];
+#pragma unroll
+  for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+    const int i = t + e * CTA;
+    const bool in = e < E && i < n;
+    k[e] = in ? ka[i] : ~0ull;                 // padding: (max key, max val) sorts last
+    p[e] = in ? va[i] : 0xFFFFFFFFu;
+  }
+  int buf = 0;
+  for (int kk = 2; kk <= P; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= CTA) {
+        auto cx = [&](u64& ka_, u32& pa_, u64& kb_, u32& pb_, int e) {
+          const bool up = ((t + e * CTA) & kk) == 0;
+          const bool gt = ka_ > kb_ || (ka_ == kb_ && pa_ > pb_);
+          if (gt == up) {
+            u64 tk = ka_; ka_ = kb_; kb_ = tk;
+            u32 tp = pa_; pa_ = pb_; pb_ = tp;
+          }
+        };
+        if (j == CTA) {
+          cx(k[0], p[0], k[1], p[1], 0);
+          if (E > 2) cx(k[2], p[2], k[3], p[3], 2);
+        } else {
+          cx(k[0], p[0], k[2], p[2], 0);
+          cx(k[1], p[1], k[3], p[3], 1);
+        }
+      } else if (j >= 32) {
+        if (act) {
+#pragma unroll
+          for (int e = 0; e < SORT_SMALL / CTA; ++e)
+            if (e < E) { sm->k[buf][t + e * CTA] = k[e]; sm->p[buf][t + e * CTA] = p[e]; }
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+          for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+            if (e >= E) continue;
+            const int i = t + e * CTA, l = i ^ j;
+            bitonic_pick(k[e], p[e], sm->k[buf][l], sm->p[buf][l], ((i & j) == 0) == ((i & kk) == 0));
+          }
+        }
+        buf ^= 1;
+      } else if (act) {
+#pragma unroll
+        for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+          if (e >= E) continue;
+          const int i = t + e * CTA;
+          const u32 lo = __shfl_xor_sync(FULL_MASK, (u32)k[e], j);
+          const u32 hi = __shfl_xor_sync(FULL_MASK, (u32)(k[e] >> 32), j);
+          const u32 op = __shfl_xor_sync(FULL_MASK, p[e], j);
+          bitonic_pick(k[e], p[e], ((u64)hi << 32) | lo, op, ((i & j) == 0) == ((i & kk) == 0));
+        }
+      }
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+      const int i = t + e * CTA;
+      if (e < E && i < n) { kb[i] = k[e]; vb[i] = p[e]; }
+    }
+  }
+  __syncthreads();
+  return 1;
+}
+
 // ------------------------------------------------------------------ exact prefix selection
 // The pause, restore and eviction passes consume only a PREFIX of their sorted
 // order.  bucket(i) is a coarse key monotone in the full sort key, so the items of
@@ -483,6 +624,61 @@ __device__ u32 cta_bucket_threshold(int n, u32 nbkt, u32 lo, ull need, u32* s_hi
   return T;
 }
 
+// Bucket threshold from a histogram already in global memory (built by other kernels).
+__device__ u32 cta_hist_threshold(const u32* ghist, u32 nbkt, u32 lo, ull need, u32* s_hist, u32* s_tmp) {
+  __shared__ u32 s_T;
+  for (u32 b = threadIdx.x; b < nbkt; b += CTA) s_hist[b] = b >= lo ? ghist[b] : 0u;
+  if (threadIdx.x == 0) s_T = nbkt - 1;
+  __syncthreads();
+  const u32 per = (nbkt + CTA - 1) / CTA;
+  const u32 b0 = threadIdx.x * per;
+  ull sum = 0;
+  for (u32 q = 0; q < per && b0 + q < nbkt; ++q) sum += s_hist[b0 + q];
+  u32 total;
+  ull run = cta_excl_scan((u32)min(sum, 0xFFFFFFFFull), s_tmp, &total);
+  for (u32 q = 0; q < per && b0 + q < nbkt; ++q) {
+    run += s_hist[b0 + q];
+    if (run >= need) { atomicMin(&s_T, b0 + q); break; }
+  }
+  __syncthreads();
+  const u32 T = s_T;
+  __syncthreads();
+  return T;
+}
+
+// Bucket threshold over an explicit candidate list (lst[0, n), unordered): like
+// cta_bucket_threshold, with pred/bucket/weight evaluated on the listed slots.
+template <typename Pred, typename Bucket, typename Weight>
+__device__ u32 cta_list_threshold(const u32* lst, int n, u32 nbkt, u32 lo, ull need, u32* s_hist, u32* s_tmp,
+                                  Pred pred, Bucket bucket, Weight weight) {
+  return cta_bucket_threshold(n, nbkt, lo, need, s_hist, s_tmp,
+                              [&](int i) { return pred((int)lst[i]); },
+                              [&](int i) { return bucket((int)lst[i]); },
+                              [&](int i) { return weight((int)lst[i]); });
+}
+
+// Append the listed slots that satisfy pred: emit(pos, slot) with pos from a shared
+// counter (unordered).  Returns the count.
+template <typename Pred, typename Emit>
+__device__ u32 cta_list_gather(const u32* lst, int n, u32* s_cnt, Pred pred, Emit emit) {
+  if (threadIdx.x == 0) *s_cnt = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += CTA) {               // uniform trip count (warp ballots)
+    const int i = i0 + threadIdx.x;
+    const int p = i < n ? (int)lst[i] : 0;
+    const bool take = i < n && pred(p);
+    const u32 m = __ballot_sync(FULL_MASK, take);      // warp-aggregated append
+    u32 base = 0;
+    if (lane_id() == 0 && m) base = atomicAdd(s_cnt, (u32)__popc(m));
+    base = __shfl_sync(FULL_MASK, base, 0);
+    if (take) emit(base + __popc(m & lanemask_lt()), p);
+  }
+  __syncthreads();
+  const u32 n_out = *s_cnt;
+  __syncthreads();
+  return n_out;
+}
+
 // ------------------------------------------------------------------ bitmap rank / select
 // s_pre[w] = number of set bits in words [0, w) for w in [0, nw]; built by one CTA.
 __device__ void cta_bitmap_prefix(const u32* words, int nw, u32* s_pre, u32* s_tmp) {
@@ -507,4 +703,24 @@ __device__ __forceinline__ u32 bitmap_select(const u32* words, const u32* s_pre,
   u32 k = q - s_pre[lo];                  // k-th set bit inside w
   u32 pos = __fns(w, 0, (int)k + 1);
   return (u32)lo * 32u + pos;
+}
+
+// Write the listed slots (unique, < N) to out[0, n) in ascending slot order: mark them
+// in a shared-memory slot bitmap, rank each by the bitmap prefix.  s_bits: >= nw
+// words, s_pre: >= nw + 1 words, nw = ceil(N / 32).
+__device__ void cta_slot_order(const u32* lst, int n, int N, u32* out, u32* s_bits, u32* s_pre, u32* s_tmp) {
+  const int nw = (N + 31) / 32;
+  for (int w = threadIdx.x; w < nw; w += CTA) s_bits[w] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += CTA) {
+    const u32 p = lst[i];
+    atomicOr(&s_bits[p >> 5], 1u << (p & 31));
+  }
+  __syncthreads();
+  cta_bitmap_prefix(s_bits, nw, s_pre, s_tmp);
+  for (int i = threadIdx.x; i < n; i += CTA) {
+    const u32 p = lst[i];
+    out[s_pre[p >> 5] + __popc(s_bits[p >> 5] & ((1u << (p & 31)) - 1))] = p;
+  }
+  __syncthreads();
 }

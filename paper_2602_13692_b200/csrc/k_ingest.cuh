@@ -168,12 +168,18 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
       d.home[p] = -1;
       d.released[p] = 0;
       d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
+      d.rb[p] = 0xFFFFFFFFu;
+      d.fpl[p] = -1;
     }
     return;
   }
   const u8 st = d.status[p];
   if (st != TA_PAUSED && st != TA_REASONING && st != TA_ACTING) {
-    if (lane == 0) d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
+    if (lane == 0) {
+      d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
+      d.rb[p] = 0xFFFFFFFFu;
+      d.fpl[p] = -1;
+    }
     return;
   }
   const u32 nbv = ceil_div_u32(d.c[p], d.bt);
@@ -214,9 +220,25 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
     d.n_hbm[p] = n_h;
     d.n_host[p] = n_s;
     d.prefix_hbm[p] = first == 0xFFFFFFFFu ? nbv : first;
-    u32 cb = contrib_of(d, nbv, d.phase[p], d.acting_since[p], T);
+    const u8 ph = d.phase[p];
+    u32 cb = contrib_of(d, nbv, ph, d.acting_since[p], T);
     d.contrib[p] = cb;
-    if (!verb && st != TA_PAUSED) atomicAdd(&d.Lacc[d.placement[p]], (ull)cb);   // commutative u64 sum
+    // candidate lists of the planner kernels (unordered appends; consumers sort by key
+    // and slot, so the append order never reaches a result)
+    u32 rbv = 0xFFFFFFFFu;
+    i8 pl = -1;
+    if (st == TA_PAUSED) {
+      rbv = restore_bucket(d, ph, nbv);
+      atomicAdd(&d.rhist[rbv], 1u);
+    } else {
+      pl = d.placement[p];
+      if (!verb) atomicAdd(&d.Lacc[pl], (ull)cb);     // commutative u64 sum
+      d.act_list[(size_t)pl * d.N + atomicAdd(&d.act_cnt[pl], 1u)] = (u32)p;
+    }
+    const int h = d.home[p];
+    if (n_h > 0 && h >= 0) d.ec_list[(size_t)h * d.N + atomicAdd(&d.ec_cnt[h], 1u)] = (u32)p;
+    d.rb[p] = rbv;
+    d.fpl[p] = pl;
   }
 }
 

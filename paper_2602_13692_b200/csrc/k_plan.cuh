@@ -54,9 +54,31 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     nF = 1;
     __syncthreads();
   } else {
-    nF = cta_ordered_gather(N, s_tmp,
+    // candidates: the footprint pass's actives on r, plus programs restored onto r
+    // this tick that were not active on r at footprint time; sorted by slot
+    u64* fka = d.ska + (size_t)r * N;
+    u64* fkb = d.skb + (size_t)r * N;
+    u32* fva = d.sva + (size_t)r * N;
+    u32* fvb = d.svb + (size_t)r * N;
+    __shared__ u32 s_cnt;
+    const int na = (int)d.act_cnt[r];
+    u32 n1 = cta_list_gather(d.act_list + (size_t)r * N, na, &s_cnt,
         [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r; },
-        [&](u32 pos, int i) { fp[pos] = (u32)i; fc[pos] = need_of(d, (u32)i, r); });
+        [&](u32 pos, int i) { fka[pos] = 0; fva[pos] = (u32)i; });
+    u32 n2 = cta_list_gather(d.restore_pid, (int)d.ctr->restore_cnt, &s_cnt,
+        [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r && d.fpl[i] != r; },
+        [&](u32 pos, int i) { fka[n1 + pos] = 0; fva[n1 + pos] = (u32)i; });
+    nF = n1 + n2;
+    if (N <= 32 * 8192) {                // slot order by rank in a slot bitmap (sort buffers free)
+      cta_slot_order(fva, (int)nF, N, fp, sm->p[0], s_big, s_tmp);
+    } else {
+      const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm);
+      const u32* fs = res ? fvb : fva;
+      for (u32 i = threadIdx.x; i < nF; i += CTA) fp[i] = fs[i];
+      __syncthreads();
+    }
+    for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, fp[i], r);
+    __syncthreads();
     cta_incl_scan_array(fc, (int)nF, s_tmp);
   }
   // short lists are searched many times below: stage them in shared memory
@@ -70,9 +92,12 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   u32* hf = d.hbm_free + (size_t)r * d.NBW;
   ull fr = 0, es = 0;
   for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
-  for (int i = threadIdx.x; i < N; i += CTA) {
-    u8 s = d.status[i];
-    if (d.home[i] == r && (s == TA_PAUSED || s == TA_ACTING)) es += d.n_hbm[i];
+  const u32* el = d.ec_list + (size_t)r * N;        // home == r with HBM blocks (footprint pass)
+  const int nel = (int)d.ec_cnt[r];
+  for (int i = threadIdx.x; i < nel; i += CTA) {
+    const u32 p = el[i];
+    const u8 s = d.status[p];
+    if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p];
   }
   auto add = [](ull a, ull b) { return a + b; };
   fr = cta_reduce<ull>(fr, s_red, add, 0ull);
@@ -100,48 +125,50 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     u32* vb = d.svb + (size_t)r * N;
     // exact prefix of E covering X blocks: buckets monotone in the eviction order
     const u32 NBK = d.nbk, sh = d.nb_shift;
-    auto epred = [&](int i) {
+    auto epred = [&](int i) {            // on the list: home == r and n_hbm > 0 already
       u8 s = d.status[i];
-      return d.home[i] == r && d.n_hbm[i] > 0 && (s == TA_PAUSED || s == TA_ACTING);
+      return s == TA_PAUSED || s == TA_ACTING;
     };
     auto ebucket = [&](int i) -> u32 {
       if (d.status[i] == TA_PAUSED)      // group 0: A first, nb descending
         return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> sh));
       return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> sh);
     };
-    const u32 T = cta_bucket_threshold(N, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
-                                       [&](int i) { return d.n_hbm[i]; });
+    const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
+                                     [&](int i) { return d.n_hbm[i]; });
     PSTAMP(2, 3);
-    u32 n0 = cta_ordered_gather(N, s_tmp,
-        [&](int ii) {
-          int i = N - 1 - ii;            // descending slot: ties in group 0 go slot-down
-          return epred(i) && d.status[i] == TA_PAUSED && ebucket(i) <= T;
-        },
-        [&](u32 pos, int ii) {
-          int i = N - 1 - ii;
-          u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
-          ka[pos] = ((1ull << 56) - 1) - rk;
-          va[pos] = (u32)i;
-        });
-    u32 n12 = cta_ordered_gather(N, s_tmp,
-        [&](int i) { return epred(i) && d.status[i] == TA_ACTING && ebucket(i) <= T; },
+    // keys: group 0 (PAUSED) = exact reverse of the restore order, ties slot-down (the
+    // tie-break value N-1-slot); groups 1-2 (ACTING) = (group, contrib), ties slot-up
+    __shared__ u32 s_cnt2;
+    const u32 ne = cta_list_gather(el, nel, &s_cnt2,
+        [&](int i) { return epred(i) && ebucket(i) <= T; },
         [&](u32 pos, int i) {
-          u64 g = d.placement[i] != r ? 1 : 2;
-          ka[n0 + pos] = (g << 62) | d.contrib[i];
-          va[n0 + pos] = (u32)i;
+          if (d.status[i] == TA_PAUSED) {
+            u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
+            ka[pos] = ((1ull << 56) - 1) - rk;
+            va[pos] = (u32)(N - 1 - i);
+          } else {
+            u64 g = d.placement[i] != r ? 1 : 2;
+            ka[pos] = (g << 62) | d.contrib[i];
+            va[pos] = (u32)i;
+          }
         });
-    const u32 ne = n0 + n12;
     PSTAMP(2, 4);
     if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
       d.pst[2 * 32 + 27] = ne | (1ull << 62);
       d.pst[2 * 32 + 28] = X | (1ull << 62);
     }
-    int res = cta_sort(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
+    int res = cta_sort_kv(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
+    const u64* sk = res ? kb : ka;
     const u32* sv = res ? vb : va;
     PSTAMP(2, 5);
     u32* ep = d.e_pid + (size_t)r * N;
     u32* ec = d.e_cum + (size_t)r * N;
-    for (u32 i = threadIdx.x; i < ne; i += CTA) { ep[i] = sv[i]; ec[i] = d.n_hbm[sv[i]]; }
+    for (u32 i = threadIdx.x; i < ne; i += CTA) {
+      const u32 p = (sk[i] >> 62) == 0 ? (u32)(N - 1) - sv[i] : sv[i];   // undo the group-0 tie-break
+      ep[i] = p;
+      ec[i] = d.n_hbm[p];
+    }
     __syncthreads();
     cta_incl_scan_array(ec, (int)ne, s_tmp);
     const u32* ecs = ec;

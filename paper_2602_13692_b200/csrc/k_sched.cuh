@@ -37,20 +37,21 @@ __global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
   u64* kb = d.skb + (size_t)r * N;
   u32* va = d.sva + (size_t)r * N;
   u32* vb = d.svb + (size_t)r * N;
-  auto pred = [&](int i) {
-    u8 s = d.status[i];
-    return (s == TA_REASONING || s == TA_ACTING) && d.placement[i] == r;
-  };
+  // the actives on r are exactly the footprint pass's list for r (statuses have not
+  // changed since); ordered by (S_pause key, slot) whatever the list order
+  __shared__ u32 s_cnt;
+  const u32* al = d.act_list + (size_t)r * N;
+  const int na = (int)d.act_cnt[r];
   auto bucket = [&](int i) { return (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
-  const u32 T = cta_bucket_threshold(N, 2 * NBK, 0, dC, s_big, s_tmp, pred, bucket,
-                                     [&](int i) { return d.contrib[i]; });
-  u32 n = cta_ordered_gather(N, s_tmp,
-      [&](int i) { return pred(i) && bucket(i) <= T; },
+  const u32 T = cta_list_threshold(al, na, 2 * NBK, 0, dC, s_big, s_tmp, [](int) { return true; }, bucket,
+                                   [&](int i) { return d.contrib[i]; });
+  u32 n = cta_list_gather(al, na, &s_cnt,
+      [&](int i) { return bucket(i) <= T; },
       [&](u32 pos, int i) {
         ka[pos] = pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
         va[pos] = (u32)i;
       });
-  int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
+  int res = cta_sort_kv(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
   const u32* sv = res ? vb : va;
   u32* cum = (u32*)(res ? ka : kb);             // free key buffer as u32 scratch
   for (u32 i = threadIdx.x; i < n; i += CTA) cum[i] = d.contrib[sv[i]];
@@ -68,6 +69,9 @@ __global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
     d.paused_since[p] = k;
     d.satisfied[p] = 0;
     d.pause_list[(size_t)r * N + i] = p;
+    const u32 b = restore_bucket(d, d.phase[p], d.nb[p]);   // joins the restore queue
+    d.rb[p] = b;
+    atomicAdd(&d.rhist[b], 1u);
   }
   if (threadIdx.x == 0) {
     d.pause_cnt[r] = m;
@@ -125,19 +129,21 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
       d.tool_return[p] = INT64_MAX;
       const u32 nbv = ceil_div_u32(d.t_p0[p], d.bt);
       d.nb[p] = nbv; d.n_hbm[p] = 0; d.n_host[p] = 0; d.prefix_hbm[p] = 0; d.contrib[p] = nbv;
+      const u32 b = restore_bucket(d, TA_PHASE_R, nbv);
+      d.rb[p] = b;
+      atomicAdd(&d.rhist[b], 1u);
     }
     __syncthreads();
   }
   u32 cnt = 0, over = 0, it = 0;
-  auto pred = [&](int i) { return d.status[i] == TA_PAUSED; };
-  auto bucket = [&](int i) { return (u32)(d.phase[i] == TA_PHASE_A) * NBK + (d.nb[i] >> sh); };
+  // queue buckets: rb[] / rhist[] from the footprint pass, plus this tick's pauses
+  // (k_pause) and arrivals (above), so no pass over the slots is needed to size a chunk
   u32 lo = 0, chunk = RESTORE_CHUNK0;
   while (true) {
-    const u32 T = cta_bucket_threshold(N, 2 * NBK, lo, chunk, s_big, s_tmp, pred, bucket,
-                                       [](int) { return 1u; });
+    const u32 T = cta_hist_threshold(d.rhist, 2 * NBK, lo, chunk, s_big, s_tmp);
     if (it < 7) PSTAMP(1, 1 + 4 * it);
     u32 n = cta_ordered_gather(N, s_tmp,
-        [&](int i) { if (!pred(i)) return false; u32 b = bucket(i); return b >= lo && b <= T; },
+        [&](int i) { const u32 b = d.rb[i]; return b >= lo && b <= T; },
         [&](u32 pos, int i) {
           ka[pos] = restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
           va[pos] = (u32)i;

@@ -156,6 +156,9 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
   x.events = L.take<ta_event>(kMaxEvents);
   x.pst = L.take<ull>(4 * 32);
+  x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
+  x.ec_list = L.take<u32>(R * N); x.ec_cnt = L.take<u32>(R);
+  x.rhist = L.take<u32>(2 * 2048 + 2); x.rb = L.take<u32>(N); x.fpl = L.take<i8>(N);
   if (d) *d = x;
   return L.off + 256;
 }
@@ -203,9 +206,8 @@ static inline size_t csm(const Dev& d) { return (d.flags & TA_F_COPY_BULK) ? BUL
 
 // Step 6.  Single process: one fused kernel (D2H overlapped with H2D/P2P and fills).
 // Multi-process: evict -> barrier -> fetch (pull) + push -> barrier -> fills.
-static void launch_movement(ta_ctx* x) {
+static void launch_movement(ta_ctx* x, cudaStream_t s) {
   Dev& d = x->d;
-  cudaStream_t s = x->stream;
   if (d.fused) {
     k_move_fused<<<x->move_grid, 256, csm(d), s>>>(d);   // persistent: every CTA co-resident
     rec(x, 4);
@@ -242,7 +244,7 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   rec(x, 2);
   k_plan<<<R, CTA, PLAN_DSMEM, s>>>(d, 0);
   rec(x, 3);
-  launch_movement(x);
+  launch_movement(x, s);
   rec(x, 6);
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 0);
   k_compact_plan<<<R, CTA, 0, s>>>(d);
@@ -679,7 +681,7 @@ ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, i
   cudaStream_t s = ctx->stream;
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_verb_pause<<<1, CTA, 0, s>>>(d, pid, mode);
-  launch_movement(ctx);
+  launch_movement(ctx, ctx->stream);
   k_assemble<<<1, CTA, 0, s>>>(d, 1);
   return verb_finish(ctx, "ta_pause", out, out_cap, n_out);
 }
@@ -697,7 +699,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
   k_plan<<<d.R, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
-  launch_movement(ctx);
+  launch_movement(ctx, ctx->stream);
   k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 1);
   k_assemble<<<1, CTA, 0, s>>>(d, 1);
   return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);

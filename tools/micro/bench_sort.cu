@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(CTA, 1) k_bench(u64* ka, u32* va, u64* kb, u32
 }
 
 int main() {
-  int ns[] = {16, 32, 64, 128, 256, 531, 1024, 2048, 4096, 5000};
+  int ns[] = {16, 32, 64, 128, 256, 384, 512, 513, 1024, 2048, 4096, 5000};
   u64 *ka, *kb; u32 *va, *vb; ull* cyc; int* wh;
   cudaMalloc(&ka, 8 * 8192); cudaMalloc(&kb, 8 * 8192); cudaMalloc(&va, 4 * 8192); cudaMalloc(&vb, 4 * 8192);
   cudaMalloc(&cyc, 8); cudaMalloc(&wh, 4);

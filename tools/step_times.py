@@ -1,5 +1,6 @@
 """Per-step device/host timing of the bench workload (developer tool, GPU box).
-usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing]"""
+usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing] [--flush] [--mini]
+--flush: 256 MiB memset before every tick (outside the timed pair); --mini: 4 KiB-block KV shape"""
 import sys
 import time
 
@@ -13,6 +14,9 @@ from paper_2602_13692_b200 import Pool, binding  # noqa: E402
 flags = (0 if "--no-timing" in sys.argv else binding.F_TIMING) | (binding.F_NO_FUSE if "--no-fuse" in sys.argv else 0)
 ticks = int(sys.argv[sys.argv.index("--ticks") + 1]) if "--ticks" in sys.argv else 24
 cfg = tracegen.get_config("bench_10k")
+if "--mini" in sys.argv:
+    cfg["kv"] = "mini"
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if "--flush" in sys.argv else None
 tr = tracegen.make_trace(cfg)
 pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=flags)
 pool.load_trace(tr)
@@ -20,6 +24,9 @@ s = pool.stream
 prev = pool.stats()
 for k in range(ticks):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if flush is not None:
+        with torch.cuda.stream(s):
+            flush.zero_()
     t0 = time.perf_counter()
     e0.record(s)
     pool.step(decisions=False)
