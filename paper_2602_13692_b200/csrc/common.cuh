@@ -141,7 +141,29 @@ struct Dev {
   u32* rhist;                      // [2 * nbk] restore-bucket histogram of PAUSED slots
   u32* rb;                         // [N] restore bucket of a PAUSED slot, else 0xFFFFFFFF
   i8* fpl;                         // [N] placement at footprint time (-1: not active)
+  ull* gsync;                      // [2] grid-barrier counters of k_decide / k_close (monotone)
 };
+
+// Barrier across the CTAs of a cooperative launch (all co-resident).  Counter k is
+// used by one kernel only and grows by gridDim.x per barrier, so arrival t waits for
+// the next multiple of gridDim.x.  One CTA: just a CTA barrier.
+__device__ __forceinline__ void grid_sync(const Dev& d, int k) {
+  __syncthreads();
+  if (gridDim.x > 1) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      ull* c = d.gsync + k;
+      const ull t = atomicAdd(c, 1ull);
+      const ull target = (t / gridDim.x + 1) * gridDim.x;
+      ull v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+      } while (v < target);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
 
 // Phase stamp: SM clock of thread 0 of CTA 0 at a phase boundary of a planner kernel
 // (kernel slot kk: 0 pause, 1 restore, 2 plan, 3 other).  Only with TA_F_TIMING.

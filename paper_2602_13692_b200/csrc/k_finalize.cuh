@@ -5,7 +5,7 @@
 
 // Deferred frees (P2P sources and fetched host slots become free only after the
 // movement, reading A16) and the per-program results of step 5.7.
-__global__ void __launch_bounds__(256) k_finalize(Dev d, int verb) {
+__device__ __forceinline__ void finalize_part(const Dev& d, int verb) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
   for (int r = 0; r < d.R; ++r) {
@@ -38,11 +38,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d, int verb) {
 // Two-finger compaction (reading A20), one CTA per replica: with U used blocks, the
 // m-th lowest free block below U receives the m-th highest used block (all moves
 // of the sequential two-finger loop, computed at once by rank/select).
-__global__ void __launch_bounds__(CTA, 1) k_compact_plan(Dev d) {
-  __shared__ u32 s_big[8192 + 1];
-  __shared__ u32 s_tmp[NWARP + 1];
-  const int r = blockIdx.x;
-  if (d.compact_every <= 0 || (d.ctr->tick % d.compact_every) != 0) return;
+__device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32* s_big, u32* s_tmp) {
   u32* fw = d.hbm_free + (size_t)r * d.NBW;
   const int nw = d.NBW;
   u32* s_free = s_big;                  // [nw + 1]
@@ -103,8 +99,7 @@ __global__ void __launch_bounds__(CTA, 1) k_compact_plan(Dev d) {
 // Canonical decision list (PAUSE by replica, RESTORE in queue order, EVICT by
 // replica, FETCH/STALL by replica in slot order, COMPACT by replica), written to
 // the host-mapped buffer; tick bookkeeping and occupancy statistics.
-__global__ void __launch_bounds__(CTA, 1) k_assemble(Dev d, int verb) {
-  __shared__ u32 s_tmp[NWARP + 1];
+__device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp) {
   __shared__ ull s_red[NWARP];
   const int N = d.N, R = d.R;
   const u32 cap = d.dec_cap;
@@ -200,7 +195,25 @@ __global__ void __launch_bounds__(CTA, 1) k_assemble(Dev d, int verb) {
   for (int t = threadIdx.x; t < R; t += CTA) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
     d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
-    d.cpd_cnt[t] = 0; d.act_cnt[t] = 0; d.ec_cnt[t] = 0;
+    d.act_cnt[t] = 0; d.ec_cnt[t] = 0;   // cpd_cnt is read by the compaction copies after this kernel
   }
   for (u32 b = threadIdx.x; b < 2 * d.nbk; b += CTA) d.rhist[b] = 0;
+}
+
+// Step 7 in one cooperative launch: deferred frees and per-program results over all
+// CTAs, grid barrier, the two-finger compaction plan (CTA r, on compaction ticks),
+// grid barrier, the canonical decision list and statistics on CTA 0.  The
+// compaction copies (k_copy_compact) run after this kernel.
+__global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d, int verb) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  finalize_part(d, verb);
+  grid_sync(d, 1);
+  if (blockIdx.x < (unsigned)d.R) {
+    const int r = blockIdx.x;
+    if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) compact_plan_pass(d, r, s_big, s_tmp);
+    else if (threadIdx.x == 0) d.cpd_cnt[r] = 0;
+  }
+  grid_sync(d, 1);
+  if (blockIdx.x == 0) assemble_pass(d, verb, s_tmp);
 }

@@ -2,6 +2,7 @@
 // allocation, sources, hit accounting, fill descriptors.  One CTA per replica.
 #pragma once
 #include "common.cuh"
+#include "k_sched.cuh"
 
 // need(p) on replica r = #{j < nb : loc[j] is not HBM on r}.  HBM entries of a
 // program always form the prefix [0, n_hbm) of its row (invariant I10: growth
@@ -20,9 +21,7 @@ __device__ __forceinline__ void warp_add_shared(ull v, ull* s) {
 enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_MISS, PC_NEWTOK,
        PC_STALL, PC_N };
 
-__global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
-  __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
-  __shared__ u32 s_tmp[NWARP + 1];
+__device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int verb, u32* s_big, u32* s_tmp) {
   __shared__ ull s_red[NWARP];
   __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs
   __shared__ ull s_pc[PC_N];
@@ -31,7 +30,6 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
   u32* s_fc = reinterpret_cast<u32*>(dsm + sizeof(SortSmem));   // staged need prefix  [4096]
   u32* s_ec = s_fc + 4096;                                         // staged evict prefix [4096]
   u32* s_hw = s_ec + 4096;                                         // staged HBM free bitmap [4096]
-  const int r = blockIdx.x;
   const int N = d.N;
   const u32 bt = (u32)d.bt;
   const bool fill = (d.flags & TA_F_FILL) != 0;
@@ -457,4 +455,26 @@ __global__ void __launch_bounds__(CTA, 1) k_plan(Dev d, int verb) {
     atomicAdd(&d.stats[ST_STALLS], s_pc[PC_STALL]);
   }
   PSTAMP(2, 12);
+}
+
+// Step 5 per replica (CTA r); verb != 0: ta_resume / ta_migrate, the verb's program only.
+__global__ void __launch_bounds__(CTA, 1) k_plan(const __grid_constant__ Dev d, int verb) {
+  __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
+  __shared__ u32 s_tmp[NWARP + 1];
+  plan_pass(d, blockIdx.x, verb, s_big, s_tmp);
+}
+
+// Steps 3 and 4 as their own kernels (one CTA per replica; one CTA).  Measured: one
+// cooperative kernel for steps 3-5 with grid barriers was slower (register pressure
+// of the merged code outweighs the two launch gaps).
+__global__ void __launch_bounds__(CTA, 1) k_pause(const __grid_constant__ Dev d) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  pause_pass(d, blockIdx.x, s_big, s_tmp);
+}
+
+__global__ void __launch_bounds__(CTA, 1) k_restore(const __grid_constant__ Dev d) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  restore_pass(d, s_big, s_tmp);
 }

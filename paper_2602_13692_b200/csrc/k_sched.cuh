@@ -12,13 +12,10 @@
 // order (acting first, shortest first) whose contributions cover Delta C.  Only the
 // prefix is materialized: buckets (tau, nb) select it exactly, then a stable CTA
 // radix sort orders it by the full key.
-__global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
-  __shared__ u32 s_big[8192 + 1];
-  __shared__ u32 s_tmp[NWARP + 1];
+__device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big, u32* s_tmp) {
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   __shared__ ull s_L;
-  const int r = blockIdx.x;
   if (threadIdx.x == 0) {                       // publish this tick's load (eq. 7) of replica r
     s_L = d.Lacc[r];
     d.Lacc[r] = 0;
@@ -88,9 +85,7 @@ __global__ void __launch_bounds__(CTA, 1) k_pause(Dev d) {
 // loop usually stops early.  Warp 0 runs the loop: lane r holds L[r]; the argmin is
 // one __reduce_min_sync over the packed key (L << 6 | [r != home] << 5 | r), which
 // fits 32 bits because a candidate has L < cap_min <= NB < 2^17.
-__global__ void __launch_bounds__(CTA, 1) k_restore(Dev d) {
-  __shared__ u32 s_big[8192 + 1];
-  __shared__ u32 s_tmp[NWARP + 1];
+__device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tmp) {
   __shared__ u32 s_stop;
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);

@@ -5,6 +5,7 @@
 // once into a CUDA graph and replayed (all sizes are read on the device).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -60,6 +61,7 @@ struct ta_ctx {
   bool timing = false;
   void* mbox_alloc = nullptr;               // barrier mailbox (library-owned, 264 B)
   int move_grid = 0;                        // resident CTAs of k_move_fused (even)
+  int close_grid = 1;                       // CTAs of the cooperative k_close
   void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
   void* peer_mbox[TA_MAX_REPLICAS] = {};    // IPC-opened peer mailboxes
 };
@@ -156,6 +158,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
   x.events = L.take<ta_event>(kMaxEvents);
   x.pst = L.take<ull>(4 * 32);
+  x.gsync = L.take<ull>(2);
   x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
   x.ec_list = L.take<u32>(R * N); x.ec_cnt = L.take<u32>(R);
   x.rhist = L.take<u32>(2 * 2048 + 2); x.rb = L.take<u32>(N); x.fpl = L.take<i8>(N);
@@ -226,6 +229,22 @@ static void launch_movement(ta_ctx* x, cudaStream_t s) {
   if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
 }
 
+// Cooperative launch (all CTAs co-resident: the kernel has grid barriers).
+template <typename... Args>
+static void launch_coop(void (*k)(Args...), int grid, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(CTA);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+
 static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   Dev& d = x->d;
   cudaStream_t s = x->stream;
@@ -246,12 +265,10 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   rec(x, 3);
   launch_movement(x, s);
   rec(x, 6);
-  k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 0);
-  k_compact_plan<<<R, CTA, 0, s>>>(d);
+  launch_coop(k_close, x->close_grid, 0, s, (Dev)d, 0);     // frees, compaction plan, decisions
   rec(x, 7);
-  k_copy_compact<<<kCopyGrid, 256, csm(d), s>>>(d);
+  if (d.compact_every > 0) k_copy_compact<<<kCopyGrid, 256, csm(d), s>>>(d);
   rec(x, 8);
-  k_assemble<<<1, CTA, 0, s>>>(d, 0);
   rec(x, 9);
   return cudaGetLastError();
 }
@@ -393,6 +410,9 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_move_fused, 256, BULK_CHUNK);
     x->move_grid = (sms * per_sm) & ~1;
     if (x->move_grid < 2) d.fused = 0;
+    // k_close: one 1024-thread CTA per 1024 slots (at least R), at most one per SM
+    const int want = (cfg->max_programs + CTA - 1) / CTA;
+    x->close_grid = std::min(std::max(want, cfg->n_replicas), std::max(sms, cfg->n_replicas));
   }
   if (d.multi && cfg->replicas_here != 1) {
     fprintf(stderr, "ta_init_pool: multi-process mode needs replicas_here == 1\n");
@@ -682,7 +702,7 @@ ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, i
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_verb_pause<<<1, CTA, 0, s>>>(d, pid, mode);
   launch_movement(ctx, ctx->stream);
-  k_assemble<<<1, CTA, 0, s>>>(d, 1);
+  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
   return verb_finish(ctx, "ta_pause", out, out_cap, n_out);
 }
 
@@ -700,8 +720,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_plan<<<d.R, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
   launch_movement(ctx, ctx->stream);
-  k_finalize<<<(N + 255) / 256, 256, 0, s>>>(d, 1);
-  k_assemble<<<1, CTA, 0, s>>>(d, 1);
+  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
   return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);
 }
 
