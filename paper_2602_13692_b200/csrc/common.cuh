@@ -116,6 +116,7 @@ struct Dev {
   u32* evx;                        // [R][NB] evicted HBM block per eviction rank
   EvDesc* evt;                     // [R][NB] evictions in victim order (evd: by block index)
   FeDesc* fed; u32* fed_cnt;       // [R][NB]
+  FeDesc* fedt;                    // [R][NB] per-CTA staging of k_plan's descriptors
   FillDesc* fld; u32* fld_cnt;     // [R][NB]
   u32* dfh; u32* dfh_cnt;          // deferred HBM frees  [R][NB]: (replica << 27) | idx
   u32* dfs; u32* dfs_cnt;          // deferred host frees [R][NB]
@@ -317,7 +318,7 @@ __device__ __forceinline__ int upper_bound_u32(const u32* a, int n, u32 x) {
 // (LSD), then the key digits.
 // Buffers a -> b -> a ...; returns 0 if the result is in (ka, va), 1 if in (kb, vb).
 // s_hist: NWARP * 256 u32 of shared memory; s_tmp: >= NWARP + 1 u32.
-__device__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp,
+__device__ __noinline__ int cta_radix_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp,
                               bool by_val = false) {
   if (n <= 1) return 0;
   // which digits vary

@@ -323,6 +323,11 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   const int role = blockIdx.x & 1;
   const int G = gridDim.x >> 1;
   const int me = blockIdx.x >> 1;
+  {   // CTAs without work for their role leave before any setup (ticks that move little)
+    const i64 mine = role == 0 ? local_items(d, d.evd_cnt, nseg)
+                               : max(local_items(d, d.fed_cnt, nseg), local_items(d, d.fld_cnt, nseg));
+    if (me >= mine) return;
+  }
   BulkCtx bk = bulk_begin(d);
   if (role == 0) {
     const i64 items = local_items(d, d.evd_cnt, nseg);

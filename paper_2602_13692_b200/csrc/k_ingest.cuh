@@ -184,16 +184,16 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
   }
   const u32 nbv = ceil_div_u32(d.c[p], d.bt);
   u32 n_h = 0, n_s = 0, first = 0xFFFFFFFFu;
-  for (u32 j0 = 0; j0 < nbv; j0 += 256) {         // two independent 16-B loads per lane in flight
-    uint4 q[2];
+  for (u32 j0 = 0; j0 < nbv; j0 += 512) {         // four independent 16-B loads per lane in flight
+    uint4 q[4];
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
+    for (int h2 = 0; h2 < 4; ++h2) {
       const u32 j = j0 + h2 * 128 + lane * 4;
       q[h2] = make_uint4(LOC_NONE, LOC_NONE, LOC_NONE, LOC_NONE);
       if (j < nbv) q[h2] = *reinterpret_cast<const uint4*>(row + j);
     }
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
+    for (int h2 = 0; h2 < 4; ++h2) {
       const u32 j = j0 + h2 * 128 + lane * 4;
       u32 e[4] = {q[h2].x, q[h2].y, q[h2].z, q[h2].w};
       u32 lfirst = 0xFFFFFFFFu;

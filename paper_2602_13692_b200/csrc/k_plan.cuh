@@ -1,6 +1,8 @@
 // k_plan.cuh — step 5 (materialize): stall cut, program-aware eviction, lowest-free
 // allocation, sources, hit accounting, fill descriptors.  One CTA per replica.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "k_sched.cuh"
 
@@ -21,186 +23,255 @@ __device__ __forceinline__ void warp_add_shared(ull v, ull* s) {
 enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_MISS, PC_NEWTOK,
        PC_STALL, PC_N };
 
+// Step 5 of replica r by a thread-block cluster of PLAN_CL CTAs (SM90+ clusters with
+// distributed shared memory).  The leader CTA (rank 0) runs the inherently serial
+// parts: F_r and the stall cut, the eviction order, host-slot and allocation
+// prefixes, hit accounting.  The two per-block loops (one iteration per evicted block,
+// one per requested block) are split over all CTAs of the cluster: each copies the
+// leader's staged lists into its own shared memory through DSMEM, takes a contiguous
+// range, and appends to the leader's shared counters/bitmap with DSMEM atomics.
+// Copy descriptors keep request order: per-CTA compaction into a staging buffer, then
+// placement at the prefix of the CTAs' counts.
+#define PLAN_CL 8
+
+struct PlanSh {                  // leader's scalars, read by the cluster through DSMEM
+  u32 stop, X, hfree, nv, vst, ecs_sm, m, tot, fst, fcs_sm, nF;
+  u32 fcnt[PLAN_CL];
+};
+
+__device__ __forceinline__ void cl_copy(u32* dst, const u32* src, u32 n) {
+  for (u32 i = threadIdx.x; i < n; i += CTA) dst[i] = src[i];
+}
+
 __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int verb, u32* s_big, u32* s_tmp) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const u32 crank = cl.block_rank();
+  const bool lead = crank == 0;
   __shared__ ull s_red[NWARP];
-  __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs
+  __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs (leader's are the live ones)
   __shared__ ull s_pc[PC_N];
+  __shared__ PlanSh sh;
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   u32* s_fc = reinterpret_cast<u32*>(dsm + sizeof(SortSmem));   // staged need prefix  [4096]
   u32* s_ec = s_fc + 4096;                                         // staged evict prefix [4096]
   u32* s_hw = s_ec + 4096;                                         // staged HBM free bitmap [4096]
+  // sort buffers, reused once the sorts are done: host-tier free words, victims,
+  // per-F-program values of the request loop
+  u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
+  u32* s_vp = reinterpret_cast<u32*>(sm->k[0]);        // [8192]
+  u32* s_vn = s_vp + 8192;                             // [8192]
+  u32* s_fp = reinterpret_cast<u32*>(sm->k[0]);        // [2048] x 6 (after the eviction phase)
+  u32* s_fj = s_fp + 2048;
+  u32* s_fh = s_fp + 4096;
+  u32* s_fk = s_fp + 6144;
+  u32* s_fcn = s_fp + 8192;
+  u32* s_fu = s_fp + 10240;
+  PlanSh* L = cl.map_shared_rank(&sh, 0);              // leader's scalars
   const int N = d.N;
   const u32 bt = (u32)d.bt;
   const bool fill = (d.flags & TA_F_FILL) != 0;
+  // uniform over the cluster (depends on r and global state only)
   if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
                d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
-  if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
+  if ((d.flags & TA_F_TIMING) && r == 0 && lead && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
   PSTAMP(2, 0);
   if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
   if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
   u32* fp = d.f_pid + (size_t)r * N;
   u32* fc = d.f_cum + (size_t)r * N;
-  // ---- 5.1 F_r: REASONING programs placed on r, slot order, with their need
-  u32 nF;
-  if (verb) {
-    if (threadIdx.x == 0) {
-      u32 p = d.ctr->verb_pid;
-      fp[0] = p;
-      fc[0] = need_of(d, p, r);
-    }
-    nF = 1;
-    __syncthreads();
-  } else {
-    // candidates: the footprint pass's actives on r, plus programs restored onto r
-    // this tick that were not active on r at footprint time; sorted by slot
-    u64* fka = d.ska + (size_t)r * N;
-    u64* fkb = d.skb + (size_t)r * N;
-    u32* fva = d.sva + (size_t)r * N;
-    u32* fvb = d.svb + (size_t)r * N;
-    __shared__ u32 s_cnt;
-    const int na = (int)d.act_cnt[r];
-    u32 n1 = cta_list_gather(d.act_list + (size_t)r * N, na, &s_cnt,
-        [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r; },
-        [&](u32 pos, int i) { fka[pos] = 0; fva[pos] = (u32)i; });
-    u32 n2 = cta_list_gather(d.restore_pid, (int)d.ctr->restore_cnt, &s_cnt,
-        [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r && d.fpl[i] != r; },
-        [&](u32 pos, int i) { fka[n1 + pos] = 0; fva[n1 + pos] = (u32)i; });
-    nF = n1 + n2;
-    if (N <= 32 * 8192) {                // slot order by rank in a slot bitmap (sort buffers free)
-      cta_slot_order(fva, (int)nF, N, fp, sm->p[0], s_big, s_tmp);
-    } else {
-      const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm);
-      const u32* fs = res ? fvb : fva;
-      for (u32 i = threadIdx.x; i < nF; i += CTA) fp[i] = fs[i];
-      __syncthreads();
-    }
-    for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, fp[i], r);
-    __syncthreads();
-    cta_incl_scan_array(fc, (int)nF, s_tmp);
-  }
-  // short lists are searched many times below: stage them in shared memory
-  const u32* fcs = fc;
-  if (nF <= 4096) {
-    for (u32 i = threadIdx.x; i < nF; i += CTA) s_fc[i] = fc[i];
-    fcs = s_fc;
-  }
-  PSTAMP(2, 1);
-  // ---- free blocks on r and eviction supply
   u32* hf = d.hbm_free + (size_t)r * d.NBW;
-  ull fr = 0, es = 0;
-  for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
-  const u32* el = d.ec_list + (size_t)r * N;        // home == r with HBM blocks (footprint pass)
-  const int nel = (int)d.ec_cnt[r];
-  for (int i = threadIdx.x; i < nel; i += CTA) {
-    const u32 p = el[i];
-    const u8 s = d.status[p];
-    if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p];
-  }
-  auto add = [](ull a, ull b) { return a + b; };
-  fr = cta_reduce<ull>(fr, s_red, add, 0ull);
-  es = cta_reduce<ull>(es, s_red, add, 0ull);
-  const ull supply = fr + es;
-  // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
-  const u32 m = nF ? (u32)upper_bound_u32(fcs, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
-  if (verb) {
-    if (m < nF) {                        // all-or-nothing: fail before any mutation
-      if (threadIdx.x == 0) d.ctr->verb_ok = 0;
-      return;
-    }
-    if (threadIdx.x == 0) d.ctr->verb_ok = 1;
-  }
-  PSTAMP(2, 2);
-  const u32 tot = m ? fcs[m - 1] : 0;
-  const u32 X = tot > fr ? (u32)(tot - fr) : 0;
-  // ---- 5.3 eviction: E_r ordered (group 0 PAUSED, reverse restore order; group 1
-  // ACTING placed elsewhere; group 2 ACTING placed on r; groups 1-2 by contrib),
-  // whole programs tail-first, last victim partially; host tier first, else drop.
-  if (X > 0) {
-    u64* ka = d.ska + (size_t)r * N;
-    u64* kb = d.skb + (size_t)r * N;
-    u32* va = d.sva + (size_t)r * N;
-    u32* vb = d.svb + (size_t)r * N;
-    // exact prefix of E covering X blocks: buckets monotone in the eviction order
-    const u32 NBK = d.nbk, sh = d.nb_shift;
-    auto epred = [&](int i) {            // on the list: home == r and n_hbm > 0 already
-      u8 s = d.status[i];
-      return s == TA_PAUSED || s == TA_ACTING;
-    };
-    auto ebucket = [&](int i) -> u32 {
-      if (d.status[i] == TA_PAUSED)      // group 0: A first, nb descending
-        return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> sh));
-      return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> sh);
-    };
-    const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
-                                     [&](int i) { return d.n_hbm[i]; });
-    PSTAMP(2, 3);
-    // keys: group 0 (PAUSED) = exact reverse of the restore order, ties slot-down (the
-    // tie-break value N-1-slot); groups 1-2 (ACTING) = (group, contrib), ties slot-up
-    __shared__ u32 s_cnt2;
-    const u32 ne = cta_list_gather(el, nel, &s_cnt2,
-        [&](int i) { return epred(i) && ebucket(i) <= T; },
-        [&](u32 pos, int i) {
-          if (d.status[i] == TA_PAUSED) {
-            u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
-            ka[pos] = ((1ull << 56) - 1) - rk;
-            va[pos] = (u32)(N - 1 - i);
-          } else {
-            u64 g = d.placement[i] != r ? 1 : 2;
-            ka[pos] = (g << 62) | d.contrib[i];
-            va[pos] = (u32)i;
-          }
-        });
-    PSTAMP(2, 4);
-    if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
-      d.pst[2 * 32 + 27] = ne | (1ull << 62);
-      d.pst[2 * 32 + 28] = X | (1ull << 62);
-    }
-    int res = cta_sort_kv(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
-    const u64* sk = res ? kb : ka;
-    const u32* sv = res ? vb : va;
-    PSTAMP(2, 5);
-    u32* ep = d.e_pid + (size_t)r * N;
-    u32* ec = d.e_cum + (size_t)r * N;
-    for (u32 i = threadIdx.x; i < ne; i += CTA) {
-      const u32 p = (sk[i] >> 62) == 0 ? (u32)(N - 1) - sv[i] : sv[i];   // undo the group-0 tie-break
-      ep[i] = p;
-      ec[i] = d.n_hbm[p];
-    }
-    __syncthreads();
-    cta_incl_scan_array(ec, (int)ne, s_tmp);
-    const u32* ecs = ec;
-    if (ne <= 4096) {
-      for (u32 i = threadIdx.x; i < ne; i += CTA) s_ec[i] = ec[i];
+  u32* sf = d.host_free + (size_t)r * d.NHW;
+  u32* ep = d.e_pid + (size_t)r * N;
+  u32* ec = d.e_cum + (size_t)r * N;
+  EvDesc* evt = d.evt + (size_t)r * d.NB;   // (block, slot) in eviction order
+  u32 pc[PC_N];
+#pragma unroll
+  for (int i = 0; i < PC_N; ++i) pc[i] = 0;
+
+  // ================= leader, part A: F_r, stall cut, eviction order, staging
+  if (lead) {
+    // ---- 5.1 F_r: REASONING programs placed on r, slot order, with their need
+    u32 nF;
+    if (verb) {
+      if (threadIdx.x == 0) {
+        u32 p = d.ctr->verb_pid;
+        fp[0] = p;
+        fc[0] = need_of(d, p, r);
+      }
+      nF = 1;
       __syncthreads();
-      ecs = s_ec;
+    } else {
+      // candidates: the footprint pass's actives on r, plus programs restored onto r
+      // this tick that were not active on r at footprint time; in slot order
+      u64* fka = d.ska + (size_t)r * N;
+      u64* fkb = d.skb + (size_t)r * N;
+      u32* fva = d.sva + (size_t)r * N;
+      u32* fvb = d.svb + (size_t)r * N;
+      __shared__ u32 s_cnt;
+      const int na = (int)d.act_cnt[r];
+      u32 n1 = cta_list_gather(d.act_list + (size_t)r * N, na, &s_cnt,
+          [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r; },
+          [&](u32 pos, int i) { fka[pos] = 0; fva[pos] = (u32)i; });
+      u32 n2 = cta_list_gather(d.restore_pid, (int)d.ctr->restore_cnt, &s_cnt,
+          [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r && d.fpl[i] != r; },
+          [&](u32 pos, int i) { fka[n1 + pos] = 0; fva[n1 + pos] = (u32)i; });
+      nF = n1 + n2;
+      if (N <= 32 * 8192) {              // slot order by rank in a slot bitmap (sort buffers free)
+        cta_slot_order(fva, (int)nF, N, fp, sm->p[0], s_big, s_tmp);
+      } else {
+        const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm);
+        const u32* fs = res ? fvb : fva;
+        for (u32 i = threadIdx.x; i < nF; i += CTA) fp[i] = fs[i];
+        __syncthreads();
+      }
+      for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, fp[i], r);
+      __syncthreads();
+      cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
-    const u32 nv = (u32)upper_bound_u32(ecs, (int)ne, X - 1) + 1;   // victims
-    u32* sf = d.host_free + (size_t)r * d.NHW;
-    cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
-    const u32 hfree = s_big[d.NHW];
-    // Stage what the per-block loop reads many times in the sort buffers (free now):
-    // the host-tier free words (selects read this snapshot, so the live bitmap can be
-    // updated in the same loop) and the victims' slot and HBM prefix length.
-    u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
-    u32* s_vp = reinterpret_cast<u32*>(sm->k[0]);        // [8192]
-    u32* s_vn = s_vp + 8192;                             // [8192]
-    const bool vst = nv <= 8192;
-    for (int w = threadIdx.x; w < d.NHW; w += CTA) s_sfw[w] = sf[w];
-    if (vst)
-      for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
-    for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
-    __syncthreads();
-    EvDesc* evt = d.evt + (size_t)r * d.NB;   // (block, slot) in eviction order
+    // short lists are searched many times below: stage them in shared memory
+    const bool fcs_sm = nF <= 4096;
+    if (fcs_sm) cl_copy(s_fc, fc, nF);
+    const u32* fcs = fcs_sm ? s_fc : fc;
+    PSTAMP(2, 1);
+    // ---- free blocks on r and eviction supply
+    ull fr = 0, es = 0;
+    for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
+    const u32* el = d.ec_list + (size_t)r * N;      // home == r with HBM blocks (footprint pass)
+    const int nel = (int)d.ec_cnt[r];
+    for (int i = threadIdx.x; i < nel; i += CTA) {
+      const u32 p = el[i];
+      const u8 s = d.status[p];
+      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p];
+    }
+    auto add = [](ull a, ull b) { return a + b; };
+    fr = cta_reduce<ull>(fr, s_red, add, 0ull);
+    es = cta_reduce<ull>(es, s_red, add, 0ull);
+    const ull supply = fr + es;
+    // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
+    const u32 m = nF ? (u32)upper_bound_u32(fcs, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
+    u32 stop = 0;
+    if (verb) {
+      if (m < nF) {                      // all-or-nothing: fail before any mutation
+        if (threadIdx.x == 0) d.ctr->verb_ok = 0;
+        stop = 1;
+      } else if (threadIdx.x == 0) {
+        d.ctr->verb_ok = 1;
+      }
+    }
+    PSTAMP(2, 2);
+    const u32 tot = m ? fcs[m - 1] : 0;
+    const u32 X = stop ? 0 : (tot > fr ? (u32)(tot - fr) : 0);
+    u32 nv = 0, hfree = 0, vst = 0, ecs_sm = 0;
+    // ---- 5.3 eviction: E_r ordered (group 0 PAUSED, reverse restore order; group 1
+    // ACTING placed elsewhere; group 2 ACTING placed on r; groups 1-2 by contrib),
+    // whole programs tail-first, last victim partially; host tier first, else drop.
+    if (X > 0) {
+      u64* ka = d.ska + (size_t)r * N;
+      u64* kb = d.skb + (size_t)r * N;
+      u32* va = d.sva + (size_t)r * N;
+      u32* vb = d.svb + (size_t)r * N;
+      // exact prefix of E covering X blocks: buckets monotone in the eviction order
+      const u32 NBK = d.nbk, shf = d.nb_shift;
+      auto epred = [&](int i) {          // on the list: home == r and n_hbm > 0 already
+        u8 s = d.status[i];
+        return s == TA_PAUSED || s == TA_ACTING;
+      };
+      auto ebucket = [&](int i) -> u32 {
+        if (d.status[i] == TA_PAUSED)    // group 0: A first, nb descending
+          return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> shf));
+        return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> shf);
+      };
+      const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
+                                       [&](int i) { return d.n_hbm[i]; });
+      PSTAMP(2, 3);
+      // keys: group 0 (PAUSED) = exact reverse of the restore order, ties slot-down (the
+      // tie-break value N-1-slot); groups 1-2 (ACTING) = (group, contrib), ties slot-up
+      __shared__ u32 s_cnt2;
+      const u32 ne = cta_list_gather(el, nel, &s_cnt2,
+          [&](int i) { return epred(i) && ebucket(i) <= T; },
+          [&](u32 pos, int i) {
+            if (d.status[i] == TA_PAUSED) {
+              u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
+              ka[pos] = ((1ull << 56) - 1) - rk;
+              va[pos] = (u32)(N - 1 - i);
+            } else {
+              u64 g = d.placement[i] != r ? 1 : 2;
+              ka[pos] = (g << 62) | d.contrib[i];
+              va[pos] = (u32)i;
+            }
+          });
+      PSTAMP(2, 4);
+      if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+        d.pst[2 * 32 + 27] = ne | (1ull << 62);
+        d.pst[2 * 32 + 28] = X | (1ull << 62);
+      }
+      int res = cta_sort_kv(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
+      const u64* sk = res ? kb : ka;
+      const u32* sv = res ? vb : va;
+      PSTAMP(2, 5);
+      for (u32 i = threadIdx.x; i < ne; i += CTA) {
+        const u32 p = (sk[i] >> 62) == 0 ? (u32)(N - 1) - sv[i] : sv[i];   // undo the group-0 tie-break
+        ep[i] = p;
+        ec[i] = d.n_hbm[p];
+      }
+      __syncthreads();
+      cta_incl_scan_array(ec, (int)ne, s_tmp);
+      ecs_sm = ne <= 4096;
+      if (ecs_sm) {
+        cl_copy(s_ec, ec, ne);
+        __syncthreads();
+      }
+      nv = (u32)upper_bound_u32(ecs_sm ? s_ec : ec, (int)ne, X - 1) + 1;   // victims
+      cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);      // host-slot select prefix
+      hfree = s_big[d.NHW];
+      // host-tier free words snapshot (selects read it, so the live bitmap can be
+      // updated in the same loop); victims' slot and HBM prefix length
+      vst = nv <= 8192;
+      cl_copy(s_sfw, sf, d.NHW);
+      if (vst)
+        for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
+      for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
+    }
+    if (threadIdx.x == 0) {
+      sh.stop = stop; sh.X = X; sh.hfree = hfree; sh.nv = nv; sh.vst = vst; sh.ecs_sm = ecs_sm;
+      sh.m = m; sh.tot = stop ? 0 : tot; sh.nF = nF; sh.fcs_sm = fcs_sm;
+    }
+  }
+  cl.sync();                                           // #1: part A visible to the cluster
+
+  // ================= all CTAs: the eviction loop, split by cluster rank
+  const u32 X = L->X;
+  if (L->stop) {
+    cl.sync();                                         // leader's smem outlives every reader
+    return;
+  }
+  if (X > 0) {
+    const u32 nv = L->nv, hfree = L->hfree, vst = L->vst, ecs_sm = L->ecs_sm;
+    if (!lead) {                                       // stage the leader's lists locally
+      if (ecs_sm) cl_copy(s_ec, cl.map_shared_rank(s_ec, 0), nv);
+      if (vst) {
+        cl_copy(s_vp, cl.map_shared_rank(s_vp, 0), nv);
+        cl_copy(s_vn, cl.map_shared_rank(s_vn, 0), nv);
+      }
+      cl_copy(s_sfw, cl.map_shared_rank(s_sfw, 0), d.NHW);
+      cl_copy(s_big, cl.map_shared_rank(s_big, 0), d.NHW + 1);
+      __syncthreads();
+    }
+    const u32* ecs = ecs_sm ? s_ec : ec;
+    u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
+    const u32 per = (X + PLAN_CL - 1) / PLAN_CL;
+    const u32 e_lo = crank * per, e_hi = min(X, e_lo + per);
     // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
     // four per thread per round so their block-table loads are in flight together
-    for (u32 e0 = 0; e0 < X; e0 += 4 * CTA) {
+    for (u32 e0 = e_lo; e0 < e_hi; e0 += 4 * CTA) {
       u32 pk[4], jk[4], ik[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const u32 e = e0 + k * CTA + threadIdx.x;
         pk[k] = jk[k] = ik[k] = 0;
-        if (e < X) {
+        if (e < e_hi) {
           const u32 v = (u32)upper_bound_u32(ecs, (int)nv, e);
           const u32 excl = v ? ecs[v - 1] : 0;
           const u32 p = vst ? s_vp[v] : ep[v];
@@ -213,7 +284,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const u32 e = e0 + k * CTA + threadIdx.x;
-        if (e >= X) continue;
+        if (e >= e_hi) continue;
         const u32 idx = ik[k], j = jk[k], p = pk[k];
         u32* ent = d.loc + (size_t)p * d.MAXBP + j;
         atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
@@ -224,141 +295,148 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
           evt[e] = EvDesc{idx, slot};
           atomicAnd(&sf[slot >> 5], ~(1u << (slot & 31)));
-          atomicOr(&s_hw[idx >> 5], 1u << (idx & 31));
+          atomicOr(&Lhw[idx >> 5], 1u << (idx & 31));
         } else {
           *ent = LOC_NONE;
         }
       }
     }
-    __syncthreads();
-    PSTAMP(2, 6);
-    // D2H copies are issued in ascending HBM-block order, the order in which the
-    // allocation below hands the freed blocks out again, so a fetch that reuses an
-    // evicted block rarely waits for its eviction (fused movement kernel).
-    {
+  }
+  cl.sync();                                           // #2: evictions done
+  PSTAMP(2, 6);
+
+  // ================= leader, part B: D2H order, victims, allocation prefix, hit accounting
+  FillDesc* fld = d.fld + (size_t)r * d.NB;
+  if (lead) {
+    const u32 nv = sh.nv, hfree = sh.hfree, m = sh.m, nF = sh.nF;
+    const u32* fcs = sh.fcs_sm ? s_fc : fc;
+    if (X > 0) {
+      const u32* ecs = sh.ecs_sm ? s_ec : ec;
+      // D2H copies are issued in ascending HBM-block order, the order in which the
+      // allocation below hands the freed blocks out again, so a fetch that reuses an
+      // evicted block rarely waits for its eviction (fused movement kernel).
       const u32 ntoh = min(X, hfree);
       EvDesc* evd = d.evd + (size_t)r * d.NB;
-      cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);      // host prefix no longer needed
+      cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);    // host prefix no longer needed
       for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
         const EvDesc x = evt[e];
         const u32 k = s_big[x.src >> 5] + __popc(s_hw[x.src >> 5] & ((1u << (x.src & 31)) - 1));
         evd[k] = x;
       }
+      PSTAMP(2, 7);
+      for (u32 v = threadIdx.x; v < nv; v += CTA) {
+        u32 p = ep[v];
+        u32 excl = v ? ecs[v - 1] : 0;
+        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p];
+        u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
+        ta_decision rec;
+        rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
+        rec.to_host = toh; rec.dropped = take - toh;
+        rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
+        d.dec_ev[(size_t)r * N + v] = rec;
+        d.n_hbm[p] -= take;
+        d.n_host[p] += toh;
+      }
+      if (threadIdx.x == 0) {
+        d.ev_cnt[r] = nv;
+        d.evd_cnt[r] = ntoh;
+        atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
+        atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)ntoh);
+        atomicAdd(&d.ctr->t_d2h, ntoh);
+        atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - ntoh));
+      }
+      __syncthreads();
     }
-    PSTAMP(2, 7);
-    for (u32 v = threadIdx.x; v < nv; v += CTA) {
-      u32 p = ep[v];
-      u32 excl = v ? ecs[v - 1] : 0;
-      u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p];
-      u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
+    PSTAMP(2, 8);
+    // ---- 5.4 allocation prefix (after the evictions' frees) and free-word snapshot
+    cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
+    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
+    PSTAMP(2, 9);
+    // per-program values the request loop reads for each of its blocks, staged for
+    // S_r programs when they fit: slot, first needed j, home, c_kv, c, uid
+    const bool fst = m <= 2048;
+    // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
+    for (u32 i = threadIdx.x; i < nF; i += CTA) {
+      u32 p = fp[i];
+      u32 need = fcs[i] - (i ? fcs[i - 1] : 0);
+      int h = d.home[p];
       ta_decision rec;
-      rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
-      rec.to_host = toh; rec.dropped = take - toh;
+      rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
       rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
-      d.dec_ev[(size_t)r * N + v] = rec;
-      d.n_hbm[p] -= take;
-      d.n_host[p] += toh;
-    }
-    if (threadIdx.x == 0) {
-      u32 toh = min(X, hfree);
-      d.ev_cnt[r] = nv;
-      d.evd_cnt[r] = toh;
-      atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
-      atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)toh);
-      atomicAdd(&d.ctr->t_d2h, toh);
-      atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - toh));
-    }
-    __syncthreads();
-  }
-  PSTAMP(2, 8);
-  // ---- 5.4 allocation prefix (after the evictions' frees)
-  cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
-  const u32* hws = hf;
-  if (d.NBW <= 4096) {
-    for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = hf[w];
-    __syncthreads();
-    hws = s_hw;
-  }
-  PSTAMP(2, 9);
-  ull pc[PC_N];
-#pragma unroll
-  for (int i = 0; i < PC_N; ++i) pc[i] = 0;
-  FillDesc* fld = d.fld + (size_t)r * d.NB;
-  // Per-program values the request loop reads for each of its blocks, staged in the
-  // sort buffers (free now) for S_r programs when they fit: slot, first needed j,
-  // home, c_kv, c, uid.
-  const bool fst = m <= 2048;
-  u32* s_fp = reinterpret_cast<u32*>(sm->k[0]);
-  u32* s_fj = s_fp + 2048;
-  u32* s_fh = s_fp + 4096;
-  u32* s_fk = s_fp + 6144;
-  u32* s_fcn = s_fp + 8192;
-  u32* s_fu = s_fp + 10240;
-  // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
-  for (u32 i = threadIdx.x; i < nF; i += CTA) {
-    u32 p = fp[i];
-    u32 need = fcs[i] - (i ? fcs[i - 1] : 0);
-    int h = d.home[p];
-    ta_decision rec;
-    rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
-    rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
-    if (i < m) {
-      const u32 ckv = d.c_kv[p], c = d.c[p];
-      const u32 nhp = d.n_hbm[p];
-      if (fst) {
-        s_fp[i] = p; s_fj[i] = h == r ? nhp : 0; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
-        s_fu[i] = d.uid[p];
-      }
-      const bool resumed = !(d.satisfied[p] && h == r);
-      if (resumed && ckv > 0) {
-        u32 hb = ceil_div_u32(ckv, bt);
-        u32 sh = bt - (ckv - (hb - 1) * bt);           // missing slots of the last block
-        u32 nh = nhp, ns = d.n_host[p], nn = hb - nh - ns;
-        ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
-        u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
-        if (is_hbm(el)) th -= sh; else if (is_host(el)) ts -= sh; else tn -= sh;
-        if (h == r) rec.hit_tok = (u32)th; else rec.peer_tok = (u32)th;
-        rec.host_tok = (u32)ts;
-        rec.miss_tok = (u32)tn;
-      }
-      rec.new_tok = c - ckv;
-      rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
-      pc[PC_HIT] += rec.hit_tok; pc[PC_PEER] += rec.peer_tok; pc[PC_HOST] += rec.host_tok;
-      pc[PC_MISS] += rec.miss_tok; pc[PC_NEWTOK] += rec.new_tok;
-      if (h == r && c > ckv && (ckv % bt) != 0) {      // partial last block already resident
-        u32 j = ckv / bt;
-        if (j < nhp) {
-          u32 t1 = min((j + 1) * bt, c);
-          pc[PC_FILLTOK] += t1 - ckv;
-          if (fill) {
-            u32 pos = atomicAdd(&s_app[1], 1u);
-            fld[pos] = FillDesc{d.loc[(size_t)p * d.MAXBP + j], d.uid[p], ckv, t1, j, 0};
+      if (i < m) {
+        const u32 ckv = d.c_kv[p], c = d.c[p];
+        const u32 nhp = d.n_hbm[p];
+        if (fst) {
+          s_fp[i] = p; s_fj[i] = h == r ? nhp : 0; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
+          s_fu[i] = d.uid[p];
+        }
+        const bool resumed = !(d.satisfied[p] && h == r);
+        if (resumed && ckv > 0) {
+          u32 hb = ceil_div_u32(ckv, bt);
+          u32 shs = bt - (ckv - (hb - 1) * bt);        // missing slots of the last block
+          u32 nh = nhp, ns = d.n_host[p], nn = hb - nh - ns;
+          ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
+          u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
+          if (is_hbm(el)) th -= shs; else if (is_host(el)) ts -= shs; else tn -= shs;
+          if (h == r) rec.hit_tok = (u32)th; else rec.peer_tok = (u32)th;
+          rec.host_tok = (u32)ts;
+          rec.miss_tok = (u32)tn;
+        }
+        rec.new_tok = c - ckv;
+        rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
+        pc[PC_HIT] += rec.hit_tok; pc[PC_PEER] += rec.peer_tok; pc[PC_HOST] += rec.host_tok;
+        pc[PC_MISS] += rec.miss_tok; pc[PC_NEWTOK] += rec.new_tok;
+        if (h == r && c > ckv && (ckv % bt) != 0) {    // partial last block already resident
+          u32 j = ckv / bt;
+          if (j < nhp) {
+            u32 t1 = min((j + 1) * bt, c);
+            pc[PC_FILLTOK] += t1 - ckv;
+            if (fill) {
+              u32 pos = atomicAdd(&s_app[1], 1u);
+              fld[pos] = FillDesc{d.loc[(size_t)p * d.MAXBP + j], d.uid[p], ckv, t1, j, 0};
+            }
           }
         }
+        d.sat_new[p] = (u8)(r + 1);
+      } else {
+        rec.kind = TA_D_STALL;
+        pc[PC_STALL] += 1;
       }
-      d.sat_new[p] = (u8)(r + 1);
-    } else {
-      rec.kind = TA_D_STALL;
-      pc[PC_STALL] += 1;
+      d.dec_fs[(size_t)r * N + i] = rec;
     }
-    d.dec_fs[(size_t)r * N + i] = rec;
+    if (threadIdx.x == 0) sh.fst = fst;
+    PSTAMP(2, 10);
+    if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+      d.pst[2 * 32 + 29] = nF | (1ull << 62);
+      d.pst[2 * 32 + 30] = sh.tot | (1ull << 62);
+    }
   }
-  __syncthreads();
-  PSTAMP(2, 10);
-  if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
-    d.pst[2 * 32 + 29] = nF | (1ull << 62);
-    d.pst[2 * 32 + 30] = tot | (1ull << 62);
+  cl.sync();                                           // #3: allocation inputs staged
+
+  // ================= all CTAs: the request loop, split by cluster rank
+  // (p in S_r slot order, needed j ascending) -> q-th lowest free block.  Selects read
+  // the staged snapshot of the free bitmap, so each request clears its block in the
+  // live bitmap at once.  Only requests that move or write bytes get a descriptor
+  // (copies; fills when the engine stand-in is on), compacted in request order.
+  const u32 m = L->m, tot = L->tot, fst = L->fst, fcs_sm = L->fcs_sm;
+  if (!lead) {
+    if (fcs_sm) cl_copy(s_fc, cl.map_shared_rank(s_fc, 0), m);
+    if (fst)                                           // six arrays of 2048, m used each
+      for (u32 a = 0; a < 6; ++a) cl_copy(s_fp + a * 2048, cl.map_shared_rank(s_fp + a * 2048, 0), m);
+    cl_copy(s_hw, cl.map_shared_rank(s_hw, 0), d.NBW);
+    cl_copy(s_big, cl.map_shared_rank(s_big, 0), d.NBW + 1);
+    __syncthreads();
   }
-  // ---- 5.4 / 5.5 requests: (p in S_r slot order, needed j ascending) -> q-th lowest free block.
-  // Selects read the staged snapshot of the free bitmap, so each request clears its
-  // block in the live bitmap at once.  Only requests that move or write bytes get a
-  // descriptor (copies; fills when the engine stand-in is on), compacted in request
-  // order by a CTA scan, so the copy kernels never walk a block that needs nothing.
-  FeDesc* fed = d.fed + (size_t)r * d.NB;
+  const u32* fcs = fcs_sm ? s_fc : fc;
+  const u32* hws = s_hw;
   u32* dfh = d.dfh + (size_t)r * d.NB;
   u32* dfs = d.dfs + (size_t)r * d.NB;
+  u32* Lapp = cl.map_shared_rank(s_app, 0);            // leader's append counters
+  const u32 per = (tot + PLAN_CL - 1) / PLAN_CL;
+  const u32 q_lo = min(tot, crank * per), q_hi = min(tot, q_lo + per);
+  FeDesc* fstage = d.fedt + (size_t)r * d.NB + q_lo;  // this CTA's descriptors, compacted
   u32 nfed = 0;
-  for (u32 q0 = 0; q0 < tot; q0 += 2 * CTA) {
+  for (u32 q0 = q_lo; q0 < q_hi; q0 += 2 * CTA) {
     u32 ik[2], pk[2], jk[2], dk[2];
     int hk[2];
 #pragma unroll
@@ -366,7 +444,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       const u32 q = q0 + k * CTA + threadIdx.x;
       ik[k] = pk[k] = jk[k] = dk[k] = 0;
       hk[k] = 0;
-      if (q < tot) {
+      if (q < q_hi) {
         const u32 i = (u32)upper_bound_u32(fcs, (int)m, q);
         const u32 excl = i ? fcs[i - 1] : 0;
         const u32 p = fst ? s_fp[i] : fp[i];
@@ -383,7 +461,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     for (int k = 0; k < 2; ++k) {
       const u32 q = q0 + k * CTA + threadIdx.x;
       FeDesc x{MV_NONE, 0, 0, 0, 0, 0, 0, 0};
-      if (q < tot) {
+      if (q < q_hi) {
         const u32 p = fst ? s_fp[pk[k]] : pk[k];
         const int h = hk[k];
         const u32 j = jk[k], dst = dk[k], old = ik[k];
@@ -404,11 +482,11 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           }
           if (is_hbm(old)) {
             x = FeDesc{MV_P2P, (u32)h, old, dst, uid, t0, t1, j};
-            dfh[atomicAdd(&s_app[2], 1u)] = ((u32)h << 27) | old;
+            dfh[atomicAdd(&Lapp[2], 1u)] = ((u32)h << 27) | old;
             pc[PC_P2P] += 1;
           } else {
             x = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst, uid, t0, t1, j};
-            dfs[atomicAdd(&s_app[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
+            dfs[atomicAdd(&Lapp[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
             pc[PC_H2D] += 1;
           }
         } else {                                        // recompute history / brand-new tokens
@@ -422,26 +500,29 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       }
       u32 round_n;
       const u32 pos = cta_excl_scan(x.kind != MV_NONE ? 1u : 0u, s_tmp, &round_n);
-      if (x.kind != MV_NONE) fed[nfed + pos] = x;
+      if (x.kind != MV_NONE) fstage[nfed + pos] = x;
       nfed += round_n;
     }
   }
-  __syncthreads();
-  PSTAMP(2, 11);
+  // per-CTA counters: warp sums (one redux per counter), then shared 64-bit atomics
 #pragma unroll
-  for (int i = 0; i < PC_N; ++i) warp_add_shared(pc[i], &s_pc[i]);
-  __syncthreads();
+  for (int i = 0; i < PC_N; ++i) {
+    const u32 v = __reduce_add_sync(FULL_MASK, pc[i]);
+    if (lane_id() == 0 && v) atomicAdd(&s_pc[i], (ull)v);
+  }
+  if (threadIdx.x == 0) L->fcnt[crank] = nfed;
+  cl.sync();                                           // #4: counts of every CTA known
+  u32 base = 0, total_fed = 0;
+  for (u32 c = 0; c < PLAN_CL; ++c) {
+    const u32 n = L->fcnt[c];
+    if (c < crank) base += n;
+    total_fed += n;
+  }
+  FeDesc* fed = d.fed + (size_t)r * d.NB;
+  for (u32 i = threadIdx.x; i < nfed; i += CTA) fed[base + i] = fstage[i];
   if (threadIdx.x == 0) {
-    d.f_cnt[r] = nF;
-    d.s_cnt[r] = m;
-    d.fed_cnt[r] = nfed;                 // copy / fill descriptors, in request order
-    d.fld_cnt[r] = s_app[1];
-    d.dfh_cnt[r] = s_app[2];
-    d.dfs_cnt[r] = s_app[3];
-    atomicAdd(&d.stats[ST_FETCH_BLOCKS], (ull)tot);
     atomicAdd(&d.stats[ST_P2P], s_pc[PC_P2P]);
     atomicAdd(&d.stats[ST_H2D], s_pc[PC_H2D]);
-    atomicAdd(&d.ctr->t_fetch, tot);
     atomicAdd(&d.ctr->t_p2p, (u32)s_pc[PC_P2P]);
     atomicAdd(&d.ctr->t_h2d, (u32)s_pc[PC_H2D]);
     atomicAdd(&d.stats[ST_RECOMPUTE], s_pc[PC_REC]);
@@ -453,15 +534,20 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     atomicAdd(&d.stats[ST_MISS], s_pc[PC_MISS]);
     atomicAdd(&d.stats[ST_NEW_TOK], s_pc[PC_NEWTOK]);
     atomicAdd(&d.stats[ST_STALLS], s_pc[PC_STALL]);
+    if (lead) {
+      d.f_cnt[r] = sh.nF;
+      d.s_cnt[r] = m;
+      d.fed_cnt[r] = total_fed;          // copy / fill descriptors, in request order
+      d.fld_cnt[r] = s_app[1];
+      d.dfh_cnt[r] = s_app[2];
+      d.dfs_cnt[r] = s_app[3];
+      atomicAdd(&d.stats[ST_FETCH_BLOCKS], (ull)tot);
+      atomicAdd(&d.ctr->t_fetch, tot);
+    }
   }
+  PSTAMP(2, 11);
+  cl.sync();                                           // #5: leader's smem outlives every reader
   PSTAMP(2, 12);
-}
-
-// Step 5 per replica (CTA r); verb != 0: ta_resume / ta_migrate, the verb's program only.
-__global__ void __launch_bounds__(CTA, 1) k_plan(const __grid_constant__ Dev d, int verb) {
-  __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
-  __shared__ u32 s_tmp[NWARP + 1];
-  plan_pass(d, blockIdx.x, verb, s_big, s_tmp);
 }
 
 // Steps 3 and 4 as their own kernels (one CTA per replica; one CTA).  Measured: one
@@ -477,4 +563,13 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(const __grid_constant__ Dev 
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   restore_pass(d, s_big, s_tmp);
+}
+
+// Step 5 per replica: cluster r (PLAN_CL CTAs); verb != 0: ta_resume / ta_migrate,
+// the verb's program only.  Grid = R * PLAN_CL.
+__global__ void __cluster_dims__(PLAN_CL, 1, 1) __launch_bounds__(CTA, 1)
+k_plan(const __grid_constant__ Dev d, int verb) {
+  __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
+  __shared__ u32 s_tmp[NWARP + 1];
+  plan_pass(d, blockIdx.x / PLAN_CL, verb, s_big, s_tmp);
 }

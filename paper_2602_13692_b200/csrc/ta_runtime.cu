@@ -151,7 +151,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.e_pid = L.take<u32>(R * N); x.e_cum = L.take<u32>(R * N);
   x.evd = L.take<EvDesc>(R * NB); x.evd_cnt = L.take<u32>(R); x.evx = L.take<u32>(R * NB);
   x.evt = L.take<EvDesc>(R * NB);
-  x.fed = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R); x.evp = L.take<u32>(R * NB);
+  x.fed = L.take<FeDesc>(R * NB); x.fedt = L.take<FeDesc>(R * NB); x.fed_cnt = L.take<u32>(R); x.evp = L.take<u32>(R * NB);
   x.fld = L.take<FillDesc>(R * NB); x.fld_cnt = L.take<u32>(R);
   x.dfh = L.take<u32>(R * NB); x.dfh_cnt = L.take<u32>(R);
   x.dfs = L.take<u32>(R * NB); x.dfs_cnt = L.take<u32>(R);
@@ -261,7 +261,7 @@ static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
   k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
   k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
   rec(x, 2);
-  k_plan<<<R, CTA, PLAN_DSMEM, s>>>(d, 0);
+  k_plan<<<R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 0);   // one CTA cluster per replica
   rec(x, 3);
   launch_movement(x, s);
   rec(x, 6);
@@ -717,7 +717,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 1);
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
-  k_plan<<<d.R, CTA, PLAN_DSMEM, s>>>(d, 1);
+  k_plan<<<d.R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
   launch_movement(ctx, ctx->stream);
   launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
