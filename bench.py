@@ -204,7 +204,7 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
             "mean_us": round(float(us.mean()), 1), "ticks": f"{start}..{start + n_ticks - 1}",
             "programs": tr.n_slots, "target_us": 100,
             "kv": "mini (4 KiB blocks; decisions identical to the Q32 run, movement kernels run but move ~0 B)",
-            "note": "one full ta_sched_step CUDA graph (all 9 kernels), L2 flushed before each tick"}
+            "note": "one full ta_sched_step CUDA graph (6 kernels), L2 flushed before each tick"}
 
 
 def workload(name, world):
@@ -432,11 +432,11 @@ def main():
     bb = pool.block_bytes
     ph = phase_sum / args.steps            # us per step
     if world == 1:
-        names = ["ingest+footprint", "pause+restore", "plan", "movement_fused(d2h+h2d+p2p+fill)", "-", "-",
-                 "finalize+compact_plan", "compact_d2d", "assemble"]
+        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "movement_fused(d2h+h2d+p2p+fill)",
+                 "-", "-", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
     else:
-        names = ["ingest+footprint", "pause+restore", "plan", "evict_d2h+barrier",
-                 "fetch_p2p_h2d+push+barrier", "fill", "finalize+compact_plan", "compact_d2d", "assemble"]
+        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "evict_d2h+barrier",
+                 "fetch_p2p_h2d+push+barrier", "fill", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
     # the host-link peak of ONE GPU's link, measured by rank 0 while the others wait
     peaks = pcie_peak(torch, dev) if (nh and rank == 0) else {"h2d": 1.0, "d2h": 1.0}
     if world > 1:
@@ -480,8 +480,19 @@ def main():
         byts_d = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
         achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
         peak, bound, psrc = hbm_peak, "hbm", peak_src
+    # traffic: DRAM bytes per launch, from the committed ncu --set full capture of the same
+    # kernel (profiles/r1b_move_traffic.json: measured DRAM / algorithmic bytes of one
+    # launch) applied to this run's algorithmic bytes per launch
+    traffic = None
+    if dom == 3 and world == 1:          # the captured kernel is the single-process fused one
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1b_move_traffic.json")) as f:
+                traffic = round(byts[3] * json.load(f)["ratio_dram_to_algorithmic"])
+        except (OSError, KeyError, ValueError):
+            traffic = None
     roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
-                "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
+                "traffic_source": "ncu --set full capture (profiles/r1b_move_traffic.json) ratio x algorithmic bytes",
                 "share_of_step": round(float(ph[dom] / ph.sum()), 4), "peak_source": psrc}
     kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
     if world > 1:
@@ -514,9 +525,10 @@ def main():
         "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(d2h / args.steps),
                 "note": "public API ta_sched_step with decisions read back; trace uploaded once before timing"},
-        # per tick: tick_front, pause, restore, plan, movement (1 fused kernel; multi-GPU:
-        # evict, barrier, fetch, push, barrier), finalize, compact plan/copy, assemble
-        "gpu_launches": args.steps * (9 if world == 1 else 13),
+        # per tick: tick_front, pause, restore, plan (one launch of R 8-CTA clusters), movement
+        # (1 fused kernel; multi-GPU: evict, barrier, fetch, push, barrier), close
+        # (compaction copies only when compaction is configured; off in this workload)
+        "gpu_launches": args.steps * (6 if world == 1 else 10),
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),

@@ -53,6 +53,9 @@ class Event(C.Structure):
                 ("tokens", C.c_uint32), ("t_ms", C.c_int64)]
 
 
+EVENT_DTYPE = np.dtype([("kind", "<u4"), ("pid", "<u4"), ("uid", "<u4"), ("tokens", "<u4"), ("t_ms", "<i8")])
+assert EVENT_DTYPE.itemsize == C.sizeof(Event) == 24
+
 DECISION_DTYPE = np.dtype([("kind", "<u4"), ("pid", "<u4"), ("src", "<i4"), ("dst", "<i4"),
                            ("blocks", "<u4"), ("to_host", "<u4"), ("dropped", "<u4"),
                            ("hit_tok", "<u4"), ("peer_tok", "<u4"), ("host_tok", "<u4"),
@@ -292,7 +295,12 @@ class Pool:
         """One ta_sched_step.  Returns (status, decisions ndarray or None)."""
         n_ev = 0
         evp = None
-        if events:
+        if isinstance(events, np.ndarray):              # EVENT_DTYPE batch: passed as is
+            if events.dtype != EVENT_DTYPE or not events.flags.c_contiguous:
+                raise ValueError("event arrays must be C-contiguous EVENT_DTYPE")
+            if len(events):
+                evp, n_ev = C.c_void_p(events.ctypes.data), len(events)
+        elif events:
             arr = (Event * len(events))()
             for i, e in enumerate(events):
                 arr[i].kind, arr[i].pid, arr[i].uid, arr[i].tokens, arr[i].t_ms = e
@@ -366,7 +374,7 @@ class Pool:
         self._chk(lib().ta_verify_content(self.ctx, C.byref(bad), C.byref(seen)), "ta_verify_content")
         return bad.value, seen.value
 
-    def _view_arrays(self):
+    def _view_arrays(self, fields=None):
         N, R, NB, NH, MAXB = self.N, self.R, self.NB, self.NH, self.MAXB
         NBW, NHW = -(-NB // 32), -(-NH // 32)
         shapes = dict(uid=N, c=N, c_kv=N, paused_since=N, step_count=N, turn=N, gen_done=N, status=N,
@@ -376,15 +384,18 @@ class Pool:
                       scalars=4)
         npt = {C.c_uint32: np.uint32, C.c_uint8: np.uint8, C.c_int8: np.int8, C.c_int64: np.int64,
                C.c_uint64: np.uint64}
-        return {n: np.zeros(shapes[n], dtype=npt[t]) for n, t in _VIEW_FIELDS}
+        return {n: np.zeros(shapes[n], dtype=npt[t]) for n, t in _VIEW_FIELDS if fields is None or n in fields}
 
-    def debug_download(self) -> dict:
-        arrs = self._view_arrays()
+    def debug_download(self, fields=None) -> dict:
+        """Device state as numpy arrays (all fields, or only the named ones)."""
+        arrs = self._view_arrays(fields)
         v = StateView()
         for n, t in _VIEW_FIELDS:
-            setattr(v, n, arrs[n].ctypes.data_as(C.POINTER(t)))
+            if n in arrs:
+                setattr(v, n, arrs[n].ctypes.data_as(C.POINTER(t)))
         self._chk(lib().ta_debug_state(self.ctx, 0, C.byref(v)), "ta_debug_state")
-        arrs["loc"] = arrs["loc"].reshape(self.N, self.MAXB)
+        if "loc" in arrs:
+            arrs["loc"] = arrs["loc"].reshape(self.N, self.MAXB)
         return arrs
 
     def debug_upload(self, arrs: dict):

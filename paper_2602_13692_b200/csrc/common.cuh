@@ -51,7 +51,11 @@ struct Ctr {                 // device-resident scalars of the context
   i32 verb_replica;
   i32 verb_ok;
   u32 t_d2h, t_h2d, t_p2p, t_d2d, t_fetch;   // this tick's block moves (telemetry)
+  ull ev_err;                // API mode: min over programs of (event index << 8 | code); ~0 = legal
+  u32 ev_multi;              // API mode: events of programs with several events in the batch
 };
+
+struct EvRes;
 
 struct EvDesc { u32 src; u32 dst; };                     // HBM block -> host slot (replica r)
 // P2P / H2D into HBM block dst; tokens [t0, t1) of logical block j of program uid are
@@ -126,7 +130,11 @@ struct Dev {
   ta_tick_info* tick_info;         // host-mapped telemetry of the last tick
   u32 dec_cap;
   ull* verify;                     // [2] mismatches, checked
-  ta_event* events;                // [kMaxEvents] API-mode event batch
+  ta_event* events;                // [ev_cap] API-mode event batch
+  EvRes* evr;                      // [ev_cap] per-event result (owner event of each program)
+  u32* ev_pcnt;                    // [N] events per program in the batch (kept zero between calls)
+  u64 *ev_mk, *ev_mk2;             // [ev_cap] (pid << 32 | index) of multi-event programs
+  u32 *ev_mv, *ev_mv2;             // [ev_cap] sort values (unused payload)
   // ---- multi-process data plane (one replica per GPU) ----
   int multi, rank;                 // multi: pools of other replicas live in other processes
   int fused;                       // single-process: evict / fetch / fill in one kernel

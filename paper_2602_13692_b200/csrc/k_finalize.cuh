@@ -207,6 +207,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
 __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d, int verb) {
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
+  if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
   finalize_part(d, verb);
   grid_sync(d, 1);
   if (blockIdx.x < (unsigned)d.R) {

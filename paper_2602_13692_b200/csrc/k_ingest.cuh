@@ -54,93 +54,165 @@ __device__ __forceinline__ void ingest_slot(const Dev& d, int p, i64 T) {
   d.status[p] = st;
 }
 
-// Step 0, API mode: validate the event batch in order, all-or-nothing, then apply
-// it (one thread: event batches are short and order-dependent).  Tentative
-// status/phase of touched pids are tracked in the ska scratch (pid-indexed).
-__global__ void k_apply_events(Dev d, const ta_event* ev, int n_ev, int apply) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  u8* tst = d.evs;                       // [N] tentative status (zeroed marks between calls)
-  u8* tph = tst + d.N;                   // [N] tentative phase
-  u8* touched = tph + d.N;               // [N]
-  u32* tc = d.evc;                       // [N] tentative context length
+// Step 0, API mode (SURVEY.md §8(c) event table): the batch
+// ev[0, n) is validated in order, all-or-nothing, then applied, in parallel over
+// programs.  Events of different programs commute; a program's events are a small
+// state machine over (status, phase, c) run in batch order.  The first illegal event
+// of the batch (lowest index) is the first illegal event of some program's sequence,
+// so the batch error is the minimum over programs of (index, code).
+//   k_ev_count   per event: events per pid; out-of-range pids are errors
+//   k_ev_single  pids with one event run it at once; the rest go to a list
+//   k_ev_multi   one CTA: the list sorted by (pid, index); each pid's sequence run
+//                in order; the batch status is decided (ctr->err)
+//   k_ev_apply   per event: the owner of each pid writes the final state (only if
+//                the batch is legal); per-pid counters are cleared
+// Later kernels of the tick return at once when ctr->err != TA_OK (state unchanged).
+struct EvRes {                 // final state of one program after its events (owner event)
+  i64 as;                      // acting_since (if a TOOL_CALL ran)
+  u32 c, uid, calls;
+  u8 st, ph, fl, pad;          // fl: EVF_*
+};
+static_assert(sizeof(EvRes) == 24, "EvRes layout (workspace carving)");
+enum { EVF_OWNER = 1, EVF_ARRIVE = 2, EVF_CALL = 4 };
+
+// Run the events of pid `p` (indices idx[0, n)) from its current state; returns the
+// (index << 8 | code) of the first illegal event, or ~0 and the final state in *o.
+template <typename Idx>
+__device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, EvRes* o) {
   const u64 cap = (u64)d.MAXB * (u64)d.bt;   // contexts are bounded by max_ctx (reading A35)
-  int err = TA_OK;
-  for (int i = 0; i < n_ev && err == TA_OK; ++i) {
-    u32 pid = ev[i].pid;
-    if (pid >= (u32)d.N) { err = TA_E_UNKNOWN_PROGRAM; break; }
-    if (!touched[pid]) {
-      touched[pid] = 1; tst[pid] = d.status[pid]; tph[pid] = d.phase[pid]; tc[pid] = d.c[pid];
+  u8 st = d.status[p], ph = d.phase[p];
+  u64 c = d.c[p];
+  u32 uid = d.uid[p], calls = 0, fl = 0;
+  i64 as = 0;
+  for (int q = 0; q < n; ++q) {
+    const u32 i = idx(q);
+    const ta_event e = ev[i];
+    if (e.kind == TA_EV_ARRIVE || e.kind == TA_EV_DECODE || e.kind == TA_EV_TOOL_RESULT) {
+      const u64 cn = e.kind == TA_EV_ARRIVE ? (u64)e.tokens : c + e.tokens;
+      if (cn > cap && !(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) return ((ull)i << 8) | TA_E_INVAL;
+      if (!(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) c = cn;
     }
-    u8 st = tst[pid], ph = tph[pid];
-    const u32 kd = ev[i].kind;
-    if (kd == TA_EV_ARRIVE || kd == TA_EV_DECODE || kd == TA_EV_TOOL_RESULT) {
-      u64 c = kd == TA_EV_ARRIVE ? (u64)ev[i].tokens : (u64)tc[pid] + ev[i].tokens;
-      if (c > cap && !(kd == TA_EV_ARRIVE && st != TA_UNARRIVED)) { err = TA_E_INVAL; break; }
-      tc[pid] = (u32)c;
-    }
-    switch (ev[i].kind) {
+    switch (e.kind) {
       case TA_EV_ARRIVE:
-        if (st != TA_UNARRIVED) err = TA_E_DUP_ID; else { tst[pid] = TA_PAUSED; tph[pid] = TA_PHASE_R; }
+        if (st != TA_UNARRIVED) return ((ull)i << 8) | TA_E_DUP_ID;
+        st = TA_PAUSED; ph = TA_PHASE_R; uid = e.uid; fl |= EVF_ARRIVE; calls = 0; fl &= ~EVF_CALL;
         break;
       case TA_EV_DECODE:
-        if (st != TA_REASONING) err = TA_E_ILLEGAL_TRANSITION;
+        if (st != TA_REASONING) return ((ull)i << 8) | TA_E_ILLEGAL_TRANSITION;
         break;
       case TA_EV_TOOL_CALL:
-        if (st != TA_REASONING) err = TA_E_ILLEGAL_TRANSITION;
-        else if (ev[i].t_ms < 0 || ev[i].t_ms > (i64)AS_MAX) err = TA_E_INVAL;
-        else { tst[pid] = TA_ACTING; tph[pid] = TA_PHASE_A; }
+        if (st != TA_REASONING) return ((ull)i << 8) | TA_E_ILLEGAL_TRANSITION;
+        if (e.t_ms < 0 || e.t_ms > (i64)AS_MAX) return ((ull)i << 8) | TA_E_INVAL;
+        st = TA_ACTING; ph = TA_PHASE_A; as = e.t_ms; ++calls; fl |= EVF_CALL;
         break;
       case TA_EV_TOOL_RESULT:
-        if (ph != TA_PHASE_A || (st != TA_ACTING && st != TA_PAUSED)) err = TA_E_ILLEGAL_TRANSITION;
-        else { tph[pid] = TA_PHASE_R; if (st == TA_ACTING) tst[pid] = TA_REASONING; }
+        if (ph != TA_PHASE_A || (st != TA_ACTING && st != TA_PAUSED)) return ((ull)i << 8) | TA_E_ILLEGAL_TRANSITION;
+        ph = TA_PHASE_R;
+        if (st == TA_ACTING) st = TA_REASONING;
         break;
       case TA_EV_RELEASE:
-        if (st == TA_UNARRIVED) err = TA_E_UNKNOWN_PROGRAM; else tst[pid] = TA_STOPPED;
+        if (st == TA_UNARRIVED) return ((ull)i << 8) | TA_E_UNKNOWN_PROGRAM;
+        st = TA_STOPPED;
         break;
       default:
-        err = TA_E_INVAL;
+        return ((ull)i << 8) | TA_E_INVAL;
     }
   }
-  for (int i = 0; i < n_ev; ++i) {       // clear scratch marks
-    u32 pid = ev[i].pid;
-    if (pid < (u32)d.N) touched[pid] = 0;
+  o->as = as; o->c = (u32)c; o->uid = uid; o->calls = calls;
+  o->st = st; o->ph = ph; o->fl = (u8)(fl | EVF_OWNER);
+  return ~0ull;
+}
+
+__global__ void __launch_bounds__(256) k_ev_count(const __grid_constant__ Dev d) {
+  const int n = d.ctr->n_events;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u32 p = d.events[i].pid;
+    d.evr[i].fl = 0;
+    if (p >= (u32)d.N) atomicMin(&d.ctr->ev_err, ((ull)i << 8) | TA_E_UNKNOWN_PROGRAM);
+    else atomicAdd(&d.ev_pcnt[p], 1u);
   }
-  d.ctr->err = err;
-  if (err != TA_OK || !apply) return;
-  const i64 k = d.ctr->tick;
-  u32 arr = 0;
-  for (int i = 0; i < n_ev; ++i) {
-    u32 p = ev[i].pid;
-    switch (ev[i].kind) {
-      case TA_EV_ARRIVE:
-        d.uid[p] = ev[i].uid; d.status[p] = TA_PAUSED; d.phase[p] = TA_PHASE_R;
-        d.c[p] = ev[i].tokens; d.c_kv[p] = 0; d.paused_since[p] = (u32)k;
-        d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
-        d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
-        d.tool_return[p] = INT64_MAX;
-        ++arr;
-        break;
-      case TA_EV_DECODE:
-        d.c[p] += ev[i].tokens;
-        break;
-      case TA_EV_TOOL_CALL:
-        d.phase[p] = TA_PHASE_A; d.status[p] = TA_ACTING; d.acting_since[p] = ev[i].t_ms;
-        d.step_count[p] += 1;
-        break;
-      case TA_EV_TOOL_RESULT:
-        d.c[p] += ev[i].tokens; d.phase[p] = TA_PHASE_R;
-        if (d.status[p] == TA_ACTING) d.status[p] = TA_REASONING;
-        break;
-      case TA_EV_RELEASE:
-        if (d.status[p] != TA_STOPPED) {
-          d.status[p] = TA_STOPPED; d.placement[p] = -1; d.satisfied[p] = 0;
-          d.released[p] = 1;
-          d.ctr->stops += 1;
-        }
-        break;
+}
+
+__global__ void __launch_bounds__(256) k_ev_single(const __grid_constant__ Dev d) {
+  const int n = d.ctr->n_events;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u32 p = d.events[i].pid;
+    if (p >= (u32)d.N) continue;
+    if (d.ev_pcnt[p] == 1) {
+      EvRes o;
+      const ull err = ev_run(d, d.events, p, 1, [&](int) { return (u32)i; }, &o);
+      if (err != ~0ull) atomicMin(&d.ctr->ev_err, err);
+      else d.evr[i] = o;
+    } else {
+      const u32 pos = atomicAdd(&d.ctr->ev_multi, 1u);
+      d.ev_mk[pos] = ((u64)p << 32) | (u32)i;
     }
   }
-  d.ctr->n_arr = arr;
+}
+
+__global__ void __launch_bounds__(CTA, 1) k_ev_multi(const __grid_constant__ Dev d) {
+  __shared__ u32 s_big[8192 + 1];
+  __shared__ u32 s_tmp[NWARP + 1];
+  extern __shared__ __align__(16) char dsm[];
+  SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
+  const int nm = (int)d.ctr->ev_multi;
+  if (nm > 0) {
+    for (int i = threadIdx.x; i < nm; i += CTA) d.ev_mv[i] = 0;
+    __syncthreads();
+    const int res = cta_sort(d.ev_mk, d.ev_mv, d.ev_mk2, d.ev_mv2, nm, s_big, s_tmp, sm);
+    const u64* k = res ? d.ev_mk2 : d.ev_mk;
+    for (int q = threadIdx.x; q < nm; q += CTA) {     // one thread per program: its events in order
+      const u32 p = (u32)(k[q] >> 32);
+      if (q > 0 && (u32)(k[q - 1] >> 32) == p) continue;
+      int len = 1;
+      while (q + len < nm && (u32)(k[q + len] >> 32) == p) ++len;
+      EvRes o;
+      const ull err = ev_run(d, d.events, p, len, [&](int t) { return (u32)k[q + t]; }, &o);
+      if (err != ~0ull) atomicMin(&d.ctr->ev_err, err);
+      else d.evr[(u32)k[q]] = o;                       // owner: the program's first event
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const ull e = d.ctr->ev_err;
+    d.ctr->err = e == ~0ull ? TA_OK : (i32)(e & 0xFF);
+    d.ctr->ev_err = ~0ull;
+    d.ctr->ev_multi = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d) {
+  const int n = d.ctr->n_events;
+  const bool ok = d.ctr->err == TA_OK;
+  const u32 k = (u32)d.ctr->tick;
+  u32 arr = 0, stops = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u32 p = d.events[i].pid;
+    if (p >= (u32)d.N) continue;
+    d.ev_pcnt[p] = 0;
+    const EvRes o = d.evr[i];
+    if (!ok || !(o.fl & EVF_OWNER)) continue;
+    const u8 st0 = d.status[p];
+    if (o.fl & EVF_ARRIVE) {              // _arrive (reading A12)
+      d.uid[p] = o.uid; d.c_kv[p] = 0; d.paused_since[p] = k;
+      d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
+      d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
+      d.tool_return[p] = INT64_MAX;
+      ++arr;
+    }
+    if (o.fl & EVF_CALL) d.acting_since[p] = o.as;
+    d.step_count[p] = ((o.fl & EVF_ARRIVE) ? 0u : d.step_count[p]) + o.calls;
+    d.c[p] = o.c;
+    d.phase[p] = o.ph;
+    d.status[p] = o.st;
+    if (o.st == TA_STOPPED && st0 != TA_STOPPED) {   // release
+      d.placement[p] = -1; d.satisfied[p] = 0;
+      d.released[p] = 1;
+      ++stops;
+    }
+  }
+  if (arr) atomicAdd(&d.ctr->n_arr, arr);
+  if (stops) atomicAdd(&d.ctr->stops, stops);
 }
 
 // Steps 0 (release frees) + 1 (footprint) + 2 (contribution, L_eff) for one slot,
@@ -248,17 +320,20 @@ __global__ void __launch_bounds__(256) k_tick_front(Dev d) {
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= d.N) return;
   const i64 T = d.ctr->tick * d.dt;
-  if (p == 0 && lane_id() == 0) d.ctr->T = T;
+  if (p == 0 && lane_id() == 0) {
+    d.ctr->T = T;
+    if (d.ctr->err != TA_E_PEER) d.ctr->err = TA_OK;   // a failed verb's status does not stop the tick
+  }
   if (lane_id() == 0) ingest_slot(d, p, T);
   __syncwarp();
   footprint_warp(d, p, T, 0);
 }
 
-// API mode and verbs: steps 1-2 (the events were applied by k_apply_events).  Verbs
+// API mode and verbs: steps 1-2 (the events were applied by k_ev_*).  Verbs
 // act on the state left by the last tick, at its time T (no ingest, L kept).
 __global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= d.N) return;
+  if (p >= d.N || (!verb && d.ctr->err != TA_OK)) return;
   const i64 T = verb ? d.ctr->T : d.ctr->now_ms;
   if (!verb && p == 0 && lane_id() == 0) d.ctr->T = T;
   footprint_warp(d, p, T, verb);

@@ -73,6 +73,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   const u32 bt = (u32)d.bt;
   const bool fill = (d.flags & TA_F_FILL) != 0;
   // uniform over the cluster (depends on r and global state only)
+  if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
   if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
                d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
   if ((d.flags & TA_F_TIMING) && r == 0 && lead && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;

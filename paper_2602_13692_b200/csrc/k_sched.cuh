@@ -16,6 +16,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   __shared__ ull s_L;
+  if (d.ctr->err != TA_OK) return;              // API batch rejected: the tick does not run
   if (threadIdx.x == 0) {                       // publish this tick's load (eq. 7) of replica r
     s_L = d.Lacc[r];
     d.Lacc[r] = 0;
@@ -87,6 +88,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
 // fits 32 bits because a candidate has L < cap_min <= NB < 2^17.
 __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tmp) {
   __shared__ u32 s_stop;
+  if (d.ctr->err != TA_OK) return;              // API batch rejected: the tick does not run
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   const int N = d.N, R = d.R;

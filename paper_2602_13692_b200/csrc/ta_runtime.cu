@@ -22,7 +22,10 @@
 namespace {
 
 const int kCopyGrid = 148 * 8;   // copy kernels: 8 resident 256-thread CTAs per SM
-const int kMaxEvents = 4096;
+// API-mode event batch capacity: 4 events per program slot (at least 4096)
+static inline size_t ev_capacity(const ta_config* c) {
+  return std::max<size_t>(4096, 4 * (size_t)c->max_programs);
+}
 
 struct Layout {                  // workspace carving (dry run when base == nullptr)
   char* base;
@@ -39,7 +42,7 @@ struct HostWs {
   ta_decision* dec;              // [dec_cap]
   u32* dec_cnt;
   ta_tick_info* tick_info;
-  ta_event* ev;                  // [kMaxEvents]
+  ta_event* ev;                  // [ev_capacity] pinned staging of the event batch
   i64* scal;                     // [8] small H2D/D2H staging
 };
 
@@ -156,7 +159,12 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.dfh = L.take<u32>(R * NB); x.dfh_cnt = L.take<u32>(R);
   x.dfs = L.take<u32>(R * NB); x.dfs_cnt = L.take<u32>(R);
   x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
-  x.events = L.take<ta_event>(kMaxEvents);
+  const size_t EC = ev_capacity(c);
+  x.events = L.take<ta_event>(EC);
+  x.evr = reinterpret_cast<EvRes*>(L.take<char>(EC * 24));
+  x.ev_pcnt = L.take<u32>(N);
+  x.ev_mk = L.take<u64>(EC); x.ev_mk2 = L.take<u64>(EC);
+  x.ev_mv = L.take<u32>(EC); x.ev_mv2 = L.take<u32>(EC);
   x.pst = L.take<ull>(4 * 32);
   x.gsync = L.take<ull>(2);
   x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
@@ -173,7 +181,7 @@ static size_t host_carve(const ta_config* c, char* base, HostWs* h) {
   x.dec = L.take<ta_decision>(cap);
   x.dec_cnt = L.take<u32>(1);
   x.tick_info = L.take<ta_tick_info>(1);
-  x.ev = L.take<ta_event>(kMaxEvents);
+  x.ev = L.take<ta_event>(ev_capacity(c));
   x.scal = L.take<i64>(8);
   if (h) *h = x;
   return L.off + 256;
@@ -191,6 +199,7 @@ __global__ void k_init(Dev d) {
       d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
     }
   }
+  if (t == 0) d.ctr->ev_err = ~0ull;
   for (int p = t; p < d.N; p += stride) {
     d.tool_return[p] = INT64_MAX;
     d.placement[p] = -1;
@@ -245,14 +254,19 @@ static void launch_coop(void (*k)(Args...), int grid, size_t smem, cudaStream_t 
   cudaLaunchKernelEx(&lc, k, args...);
 }
 
-static cudaError_t launch_tick(ta_ctx* x, int n_ev) {
+static cudaError_t launch_tick(ta_ctx* x, int) {
   Dev& d = x->d;
   cudaStream_t s = x->stream;
   const int N = d.N, R = d.R;
   rec(x, 0);
   // per-tick lists and counters were cleared by the previous tick's k_assemble
   if (d.api_mode) {
-    k_apply_events<<<1, 32, 0, s>>>(d, x->ev_dev, n_ev, 1);
+    // events: validate + apply in parallel over programs (n_events read on the device)
+    const int eg = (int)std::min<size_t>(148 * 4, (ev_capacity(&x->cfg) + 255) / 256);
+    k_ev_count<<<eg, 256, 0, s>>>(d);
+    k_ev_single<<<eg, 256, 0, s>>>(d);
+    k_ev_multi<<<1, CTA, PLAN_DSMEM, s>>>(d);
+    k_ev_apply<<<eg, 256, 0, s>>>(d);
     k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 0);
   } else {
     k_tick_front<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);   // ingest + footprint + load
@@ -434,6 +448,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ev_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));
@@ -477,6 +492,27 @@ ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* t) {
   return TA_OK;
 }
 
+// One tick on the context stream: the captured CUDA graph (built on first use; the
+// same kernels in both modes, API-mode ones reading the batch size on the device), or
+// kernel by kernel with TA_F_NO_GRAPH.
+static cudaError_t run_tick(ta_ctx* ctx) {
+  cudaStream_t s = ctx->stream;
+  if (ctx->cfg.flags & TA_F_NO_GRAPH) return launch_tick(ctx, 0);
+  if (!ctx->graph) {
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    cudaError_t le = launch_tick(ctx, 0);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (le != cudaSuccess) return le;
+    if (ce != cudaSuccess) return ce;
+    e = cudaGraphInstantiate(&ctx->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGraphLaunch(ctx->graph, s);
+}
+
 ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t n_ev, ta_decision* out,
                         int32_t out_cap, int32_t* n_out) {
   if (ta_status s = check_ctx(ctx)) return s;
@@ -493,38 +529,24 @@ ta_status ta_sched_step(ta_ctx* ctx, int64_t now_ms, const ta_event* ev, int32_t
       CK(ctx, cudaStreamSynchronize(s));
       if (now_ms != ctx->h.scal[0] * d.dt) FAIL(ctx, TA_E_INVAL, "now_ms %lld != tick*delta_t", (long long)now_ms);
     }
-    const bool use_graph = !(ctx->cfg.flags & TA_F_NO_GRAPH);
-    if (use_graph) {
-      if (!ctx->graph) {
-        cudaGraph_t g;
-        CK(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        cudaError_t le = launch_tick(ctx, 0);
-        cudaError_t ce = cudaStreamEndCapture(s, &g);
-        CK(ctx, le);
-        CK(ctx, ce);
-        CK(ctx, cudaGraphInstantiate(&ctx->graph, g, 0));
-        cudaGraphDestroy(g);
-      }
-      CK(ctx, cudaGraphLaunch(ctx->graph, s));
-    } else {
-      CK(ctx, launch_tick(ctx, 0));
-    }
+    CK(ctx, run_tick(ctx));
   } else {
     if (now_ms < 0 || now_ms > (int64_t)AS_MAX) FAIL(ctx, TA_E_INVAL, "API mode needs 0 <= now_ms < 2^40");
-    if (n_ev > kMaxEvents) FAIL(ctx, TA_E_INVAL, "at most %d events per tick", kMaxEvents);
-    memcpy(ctx->h.ev, ev, sizeof(ta_event) * n_ev);
+    if ((size_t)n_ev > ev_capacity(&ctx->cfg))
+      FAIL(ctx, TA_E_INVAL, "at most %zu events per tick", ev_capacity(&ctx->cfg));
+    // the batch and its header go to the device; validation, application and the tick
+    // run as one graph; a rejected batch makes every later kernel return at once
+    if (n_ev) memcpy(ctx->h.ev, ev, sizeof(ta_event) * n_ev);
     ctx->h.scal[0] = now_ms;
-    CK(ctx, cudaMemcpyAsync(ctx->ev_dev, ctx->h.ev, sizeof(ta_event) * n_ev, cudaMemcpyHostToDevice, s));
+    *(i32*)(ctx->h.scal + 1) = n_ev;
+    if (n_ev) CK(ctx, cudaMemcpyAsync(ctx->ev_dev, ctx->h.ev, sizeof(ta_event) * n_ev, cudaMemcpyHostToDevice, s));
     CK(ctx, cudaMemcpyAsync(&d.ctr->now_ms, ctx->h.scal, sizeof(i64), cudaMemcpyHostToDevice, s));
-    // validation pass alone first: a rejected batch leaves the state untouched and
-    // the tick does not run (SURVEY.md §8(c) API table)
-    k_apply_events<<<1, 32, 0, s>>>(d, ctx->ev_dev, n_ev, 0);
-    CK(ctx, cudaGetLastError());
-    CK(ctx, cudaMemcpyAsync(ctx->h.scal + 1, &d.ctr->err, sizeof(i32), cudaMemcpyDeviceToHost, s));
+    CK(ctx, cudaMemcpyAsync(&d.ctr->n_events, ctx->h.scal + 1, sizeof(i32), cudaMemcpyHostToDevice, s));
+    CK(ctx, run_tick(ctx));
+    CK(ctx, cudaMemcpyAsync(ctx->h.scal + 2, &d.ctr->err, sizeof(i32), cudaMemcpyDeviceToHost, s));
     CK(ctx, cudaStreamSynchronize(s));
-    int verr = (int)*(i32*)(ctx->h.scal + 1);
-    if (verr != TA_OK) FAIL(ctx, (ta_status)verr, "event batch rejected (first illegal event)");
-    CK(ctx, launch_tick(ctx, n_ev));
+    const int verr = *(i32*)(ctx->h.scal + 2);
+    if (verr != TA_OK) FAIL(ctx, (ta_status)verr, "event batch rejected (first illegal event); nothing applied");
   }
   if (!out && !n_out) return TA_OK;
   CK(ctx, cudaStreamSynchronize(s));

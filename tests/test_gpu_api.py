@@ -118,3 +118,109 @@ def test_gpu_verbs_random(seed, R):
         assert bad == 0, f"tick {k}: {bad} KV words wrong"
     assert n_ok["pause"] > 0 and n_ok["resume"] > 0 and (R == 1 or n_ok["migrate"] > 0), n_ok
     pool.close()
+
+
+def random_event_sequences(o, rng, T, n_max=16, illegal_p=0.15):
+    """Batches with SEVERAL events per program (legal sequences in batch order, programs
+    interleaved), plus sometimes one illegal event somewhere in the batch."""
+    per = {}
+    for _ in range(rng.randint(0, n_max)):
+        p = rng.randrange(o.N)
+        if p in per:
+            continue
+        st, ph = o.status[p], o.phase[p]
+        seq = []
+        if st == oracle.UNARRIVED:
+            seq = [(A, p, 1000 + p, rng.randint(1, 300), 0)]
+            if rng.random() < 0.2:
+                seq.append((REL, p, 0, 0, 0))
+        elif st == oracle.REASONING:
+            seq = [(DEC, p, 0, rng.randint(1, 100), 0)]
+            r = rng.random()
+            if r < 0.4:
+                seq.append((TC, p, 0, 0, max(0, T - rng.randint(0, 4000))))
+                if rng.random() < 0.5:
+                    seq.append((TR, p, 0, rng.randint(0, 200), 0))
+                    seq.append((DEC, p, 0, rng.randint(1, 50), 0))
+            elif r < 0.5:
+                seq.append((REL, p, 0, 0, 0))
+                seq.append((REL, p, 0, 0, 0))      # idempotent
+        elif ph == oracle.PHASE_A and st in (oracle.ACTING, oracle.PAUSED):
+            seq = [(TR, p, 0, rng.randint(0, 300), 0)]
+            if st == oracle.ACTING and rng.random() < 0.5:
+                seq.append((DEC, p, 0, rng.randint(1, 60), 0))
+        per[p] = seq
+    # interleave the programs' sequences, keeping each program's order
+    evs = []
+    queues = [list(s) for s in per.values() if s]
+    while queues:
+        q = rng.choice(queues)
+        evs.append(q.pop(0))
+        if not q:
+            queues.remove(q)
+    if rng.random() < illegal_p and evs:
+        p = evs[rng.randrange(len(evs))][1]
+        bad = (DEC, p, 0, 1, 0) if o.status[p] != oracle.REASONING else (A, p, 1, 1, 0)
+        evs.insert(rng.randrange(len(evs) + 1), bad)
+    return evs
+
+
+@pytest.mark.parametrize("seed,R", [(21, 1), (22, 2), (23, 3)])
+def test_gpu_api_mode_event_sequences(seed, R):
+    """Several events per program in one batch (the parallel per-program state machines
+    and the multi-event sort path) against the oracle's sequential validation."""
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = tracegen.get_config("c1_toy", n_replicas=R, hbm_blocks=48, host_blocks=16, max_ctx=4096,
+                              compact_every=5)
+    N = 48
+    o = oracle.Oracle(cfg, api_mode=True, n_slots=N)
+    pool = Pool(cfg, N, trace_mode=False)
+    rng = random.Random(seed)
+    errs = multi = 0
+    for k in range(150):
+        T = 5000 * k
+        evs = random_event_sequences(o, rng, T)
+        pids = [e[1] for e in evs]
+        multi += len(pids) - len(set(pids))
+        st_o, dec_o = o.sched_step(T, evs)
+        st_g, dec_g = pool.step(T, evs, raise_on_error=False)
+        assert st_o == st_g, (k, st_o, st_g, evs)
+        if st_o != oracle.OK:
+            errs += 1
+            continue
+        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        if k % 7 == 0:
+            compare_state(o, pool.debug_download(), where=f"api tick {k}")
+        bad, _ = pool.verify_content()
+        assert bad == 0
+    assert errs > 0 and multi > 50, (errs, multi)
+    pool.close()
+
+
+@pytest.mark.parametrize("name,n,ticks", [("c1_toy", 24, 60), ("bench_10k", 2000, 30)])
+def test_gpu_api_replay_equals_trace_mode(name, n, ticks):
+    """The engine's event batches recorded from a trace-mode run (tools/api_events.py),
+    replayed through an API-mode context, give the same decisions every tick: the API
+    event path and the trace engine are the same step 0."""
+    need_gpu()
+    import numpy as np
+    from paper_2602_13692_b200 import Pool
+    from tools.api_events import record
+    over = dict(trace=dict(n=n, n_initial=n // 2 if name == "c1_toy" else None))
+    if name == "bench_10k":
+        over["kv"] = "mini"
+    else:
+        over.update(hbm_blocks=56, host_blocks=16)
+    cfg = tracegen.get_config(name, **over)
+    tr = tracegen.make_trace(cfg)
+    batches, want = record(cfg, tr, ticks)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, trace_mode=False, fill=False)
+    n_ev = 0
+    for k in range(ticks):
+        st, got = pool.step(k * cfg["delta_t_ms"], batches[k])
+        assert st == 0, (k, st)
+        n_ev += len(batches[k])
+        assert np.array_equal(got, want[k]), f"tick {k}: API replay differs from trace mode"
+    assert n_ev > 0
+    pool.close()
