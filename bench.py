@@ -400,24 +400,37 @@ def main():
     if world > 1:
         dist.barrier()
 
-    # ---- e2e: the SAME ticks (fresh context over the same buffers, same untimed
-    # prefix) through the public API, decisions read back to the host every tick
-    pool.reset(flags=base_flags)
+    # ---- e2e: the SAME ticks through the public API as a serving engine drives it: an
+    # API-mode context over the same buffers; every step copies that tick's event batch
+    # from host memory to the device (ta_event array, H2D inside ta_sched_step) and
+    # reads the decisions back (D2H).  The batches are the engine's view of the trace
+    # (tools/api_events.py), recorded untimed beforehand on a decision-identical
+    # small-KV context; API replay == trace mode is a GPU test (test_gpu_api.py).
+    from tools.api_events import record
+    rec_cfg = dict(cfg)
+    rec_cfg["kv"] = "mini"
+    n_pre = args.preroll + args.warmup
+    batches, _ = record(rec_cfg, tr, n_pre + args.steps, device=local)
+    pool.reset(flags=base_flags & ~binding.F_TRACE_MODE)
     if world > 1:
         connect(pool)                    # fresh context: fresh mailboxes to map
-    pool.load_trace(tr)
-    for _ in range(args.preroll + args.warmup):
-        pool.step(decisions=False)
+    dt_ms = cfg["delta_t_ms"]
+    for k in range(n_pre):
+        pool.step(k * dt_ms, batches[k], decisions=False)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    h2d = d2h = n_events = 0
     e0.record(s)
-    d2h = 0
-    for _ in range(args.steps):
+    for k in range(n_pre, n_pre + args.steps):
         with torch.cuda.stream(s):
             flush.zero_()
-        st, dec = pool.step(decisions=True)
-        d2h += 0 if dec is None else dec.nbytes + 4
+        st, dec = pool.step(k * dt_ms, batches[k], decisions=True)
+        if st != 0:
+            raise RuntimeError(f"e2e replay: ta_sched_step status {st} at tick {k}")
+        h2d += batches[k].nbytes + 12    # events + header (now_ms, n_events)
+        d2h += dec.nbytes + 8            # decisions + count + status
+        n_events += len(batches[k])
     e1.record(s)
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1)
@@ -522,9 +535,10 @@ def main():
                    "l2": "256 MiB memset before every timed step (inside the timed region)",
                    "parallelism": f"dp{world} (one replica per GPU)"},
         "clocks": clocks,
-        "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": int(d2h / args.steps),
-                "note": "public API ta_sched_step with decisions read back; trace uploaded once before timing"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": int(h2d / args.steps),
+                "d2h_bytes_per_step": int(d2h / args.steps), "events_per_step": round(n_events / args.steps, 1),
+                "note": "API mode (serving-engine path): per step the tick's event batch H2D from host memory, "
+                        "validation + apply + tick on the device, decisions D2H; same ticks as value"},
         # per tick: tick_front, pause, restore, plan (one launch of R 8-CTA clusters), movement
         # (1 fused kernel; multi-GPU: evict, barrier, fetch, push, barrier), close
         # (compaction copies only when compaction is configured; off in this workload)
