@@ -447,6 +447,10 @@ def main():
     if world == 1:
         names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "movement_fused(d2h+h2d+p2p+fill)",
                  "-", "-", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
+    elif pool.c.flags & binding.F_NO_FUSE == 0:
+        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)",
+                 "barrier+movement_fused(d2h+pull+push)+barrier", "-", "fill", "close(finalize+compact_plan+assemble)",
+                 "compact_d2d", "-"]
     else:
         names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "evict_d2h+barrier",
                  "fetch_p2p_h2d+push+barrier", "fill", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
@@ -466,8 +470,12 @@ def main():
         h2d_b = ti["h2d_blocks"] * bb / world
         p2p_b = ti["p2p_blocks"] * bb / world
         d2d_b = 2 * ti["d2d_blocks"] * bb / world
-        if world == 1:
-            tmin[3] += max(d2h_b / peaks["d2h"], h2d_b / peaks["h2d"], p2p_b / nvl) / G
+        if world == 1 or not pool.c.flags & binding.F_NO_FUSE:   # one fused kernel: links in parallel
+            # floor = the slowest replica's own links (PCIe out / in of its tier, NVLink in);
+            # every rank waits for it at the closing barrier
+            floor = max(max(ti["d2h_of"][r] * bb / peaks["d2h"], ti["h2d_of"][r] * bb / peaks["h2d"],
+                            ti["p2p_to"][r] * bb / nvl) for r in range(len(ti["d2h_of"])))
+            tmin[3] += floor / G
             byts[3] += d2h_b + h2d_b + p2p_b
         else:
             tmin[3] += d2h_b / peaks["d2h"] / G
@@ -485,10 +493,11 @@ def main():
         t = ph[dom] * 1e-6
         achieved = byts[dom] / t / 1e9
         peak = byts[dom] / tmin[dom] / G if tmin[dom] > 0 else achieved
-        bound = "hbm" if dom == 7 else "pcie (full duplex)" if world == 1 else ("pcie" if dom == 3 else "pcie/nvlink")
+        bound = ("hbm" if dom == 7 else "pcie (full duplex)" if (world == 1 or not pool.c.flags & binding.F_NO_FUSE)
+                 else ("pcie" if dom == 3 else "pcie/nvlink"))
         psrc = (peak_src if dom == 7 else
                 f"measured in this run: pinned cudaMemcpyAsync 1 GiB (d2h {peaks['d2h']:.1f}, h2d {peaks['h2d']:.1f}"
-                f" GB/s); peak = bytes / max over links of (link bytes / link peak)")
+                f" GB/s); peak = bytes / floor, floor = max over replicas and links of (link bytes / link peak)")
     else:
         byts_d = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
         achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
@@ -540,9 +549,9 @@ def main():
                 "note": "API mode (serving-engine path): per step the tick's event batch H2D from host memory, "
                         "validation + apply + tick on the device, decisions D2H; same ticks as value"},
         # per tick: tick_front, pause, restore, plan (one launch of R 8-CTA clusters), movement
-        # (1 fused kernel; multi-GPU: evict, barrier, fetch, push, barrier), close
+        # (1 fused kernel; multi-GPU: barrier, fused kernel, barrier), close
         # (compaction copies only when compaction is configured; off in this workload)
-        "gpu_launches": args.steps * (6 if world == 1 else 10),
+        "gpu_launches": args.steps * (6 if world == 1 else 8),
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),

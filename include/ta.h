@@ -242,6 +242,10 @@ typedef struct {               /* what the last tick did (written by the device 
   uint32_t p2p_blocks;         /* fetched from another replica's HBM */
   uint32_t d2d_blocks;         /* moved by compaction */
   uint32_t fetch_blocks;       /* all allocated blocks (copies + fills) */
+  /* per replica r (what crosses r's own links; a phase's time floor is the max over r): */
+  uint32_t d2h_of[TA_MAX_REPLICAS];   /* blocks evicted into r's host tier (PCIe, out of r's GPU) */
+  uint32_t h2d_of[TA_MAX_REPLICAS];   /* blocks fetched from r's host tier (PCIe, into r's GPU) */
+  uint32_t p2p_to[TA_MAX_REPLICAS];   /* blocks fetched into r's HBM from a peer's HBM (NVLink) */
 } ta_tick_info;
 
 /* Telemetry of the last ta_sched_step (synchronizes the stream). */

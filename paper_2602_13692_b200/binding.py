@@ -77,7 +77,8 @@ class Stats(C.Structure):
 
 class TickInfo(C.Structure):
     _fields_ = [("tick", C.c_int64)] + [(k, C.c_uint32) for k in (
-        "decisions", "d2h_blocks", "h2d_blocks", "p2p_blocks", "d2d_blocks", "fetch_blocks")]
+        "decisions", "d2h_blocks", "h2d_blocks", "p2p_blocks", "d2d_blocks", "fetch_blocks")] + [
+        (k, C.c_uint32 * 32) for k in ("d2h_of", "h2d_of", "p2p_to")]
 
 
 class TraceView(C.Structure):
@@ -349,7 +350,8 @@ class Pool:
     def last_tick(self) -> dict:
         t = TickInfo()
         self._chk(lib().ta_last_tick(self.ctx, C.byref(t)), "ta_last_tick")
-        return {k: getattr(t, k) for k, _ in TickInfo._fields_}
+        return {k: (list(getattr(t, k))[:self.R] if k.endswith(("_of", "_to")) else getattr(t, k))
+                for k, _ in TickInfo._fields_}
 
     def phase_times(self):
         a = (C.c_float * 9)()

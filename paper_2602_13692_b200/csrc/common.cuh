@@ -135,10 +135,14 @@ struct Dev {
   u32* ev_pcnt;                    // [N] events per program in the batch (kept zero between calls)
   u64 *ev_mk, *ev_mk2;             // [ev_cap] (pid << 32 | index) of multi-event programs
   u32 *ev_mv, *ev_mv2;             // [ev_cap] sort values (unused payload)
+  u32* t_rep;                      // [3][R] this tick's blocks per replica: d2h into, h2d from, p2p into
   // ---- multi-process data plane (one replica per GPU) ----
   int multi, rank;                 // multi: pools of other replicas live in other processes
   int fused;                       // single-process: evict / fetch / fill in one kernel
   u32* evp;                        // [R][NB] segments of a block still to be evicted this tick
+                                   // (multi-process: [NB] of the local replica, in the IPC-shared
+                                   // mailbox allocation)
+  u32* evp_peer[TA_MAX_REPLICAS];  // multi-process: peers' eviction flags (CUDA IPC)
   ull* mbox;                       // [TA_MAX_REPLICAS] this rank's barrier mailbox (epochs)
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)
@@ -173,6 +177,14 @@ __device__ __forceinline__ void grid_sync(const Dev& d, int k) {
     __syncthreads();
   }
 }
+
+// Eviction flags of replica r's HBM blocks (the owner's copy in multi-process mode).
+__device__ __forceinline__ u32* evp_of(const Dev& d, int r) {
+  if (!d.multi) return d.evp + (size_t)r * d.NB;
+  return r == d.rank ? d.evp : d.evp_peer[r];
+}
+// Only the process that will read an evicted block sets its flag.
+__device__ __forceinline__ bool evp_owner(const Dev& d, int r) { return d.fused && (!d.multi || r == d.rank); }
 
 // Phase stamp: SM clock of thread 0 of CTA 0 at a phase boundary of a planner kernel
 // (kernel slot kk: 0 pause, 1 restore, 2 plan, 3 other).  Only with TA_F_TIMING.

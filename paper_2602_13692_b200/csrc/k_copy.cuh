@@ -299,33 +299,44 @@ __global__ void __launch_bounds__(256) k_fill(Dev d) {
   }
 }
 
-__device__ __forceinline__ void wait_evicted(const u32* flag) {
+__device__ __forceinline__ void wait_evicted(const u32* flag, bool sys) {
   if (threadIdx.x == 0) {
     u32 v;
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
       if (v) __nanosleep(64);
     } while (v);
   }
   __syncthreads();
 }
 
-// Single-process movement of one tick in ONE kernel (step 6): even CTAs run the D2H
-// evictions, odd CTAs the P2P/H2D fetches (each followed by its new-token tail) and
-// then the fills of new / recomputed blocks.  D2H and H2D therefore share the
+// The movement of one tick in ONE kernel (step 6): even CTAs run the D2H evictions,
+// odd CTAs the fetches into this process's replicas (P2P pulls over NVLink, H2D from
+// its own host tiers, each followed by its new-token tail), then -- one process per
+// GPU -- the pushes of this process's host tier into peers' pools over NVLink, then
+// the fills of new / recomputed blocks.  D2H and H2D therefore share the
 // full-duplex host link instead of running back to back.  A destination block that
 // was evicted in this tick is written only after all its segments were read: the
-// evictor decrements evp[block] per segment (release), the writer waits for 0
-// (acquire).  Evicting CTAs never wait, and the grid is fully resident, so the
-// waits always terminate.
+// evictor (the block's owner) decrements its flag per segment (release), writers
+// wait for 0 (acquire; over NVLink for pushes).  Evicting CTAs never wait, and the
+// grid is fully resident, so the waits always terminate.  Multi-process: fills and
+// new-token tails run in k_fill after the closing barrier (a pushed block's tail is
+// written by its destination process).
 __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   const int nseg = 2 * d.nL;
   const int role = blockIdx.x & 1;
   const int G = gridDim.x >> 1;
   const int me = blockIdx.x >> 1;
+  if (d.api_mode && d.ctr->err != TA_OK) return;       // rejected API batch
+  i64 n_push = 0;
+  if (d.multi)
+    for (int r = 0; r < d.R; ++r)
+      if (r != d.rank) n_push += (i64)d.fed_cnt[r] * nseg;
   {   // CTAs without work for their role leave before any setup (ticks that move little)
+    const i64 fl = d.multi ? 0 : local_items(d, d.fld_cnt, nseg);
     const i64 mine = role == 0 ? local_items(d, d.evd_cnt, nseg)
-                               : max(local_items(d, d.fed_cnt, nseg), local_items(d, d.fld_cnt, nseg));
+                               : max(local_items(d, d.fed_cnt, nseg) + n_push, fl);
     if (me >= mine) return;
   }
   BulkCtx bk = bulk_begin(d);
@@ -340,43 +351,63 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
       seg_copy(d, bk, src, dst);
       __syncthreads();                              // every load of the segment has returned
       if (threadIdx.x == 0) {
-        __threadfence();
-        atomicSub(&d.evp[(size_t)r * d.NB + x.src], 1u);
+        __threadfence_system();
+        atomicSub(&evp_of(d, r)[x.src], 1u);
       }
     }
     bulk_end(d);
     return;
   }
   const i64 nf = local_items(d, d.fed_cnt, nseg);
-  for (i64 it = me; it < nf; it += G) {
+  for (i64 it = me; it < nf + n_push; it += G) {
     int r, s; u32 e;
-    locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
+    bool push = it >= nf;
+    if (!push) {
+      locate(d, d.fed_cnt, it, nseg, &r, &e, &s);
+    } else {                                        // remote replicas' fetches, in replica order
+      i64 q = it - nf;
+      for (r = 0; r < d.R; ++r) {
+        if (r == d.rank) continue;
+        const i64 n = (i64)d.fed_cnt[r] * nseg;
+        if (q < n) break;
+        q -= n;
+      }
+      e = (u32)(q / nseg);
+      s = (int)(q % nseg);
+    }
     FeDesc x = d.fed[(size_t)r * d.NB + e];
     if (x.kind == MV_NONE) continue;
-    wait_evicted(&d.evp[(size_t)r * d.NB + x.dst]);
-    if (x.kind == MV_FILL) {                        // new / recomputed tokens
+    if (push && (x.kind != MV_H2D || d.host[x.src_r] == nullptr)) continue;   // not from this tier
+    if (x.kind == MV_FILL) {                        // new / recomputed tokens (single process)
+      if (d.multi) continue;
+      wait_evicted(&evp_of(d, r)[x.dst], false);
       fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
       continue;
     }
     const char* sbase = x.kind == MV_P2P ? d.hbm[x.src_r] : d.host[x.src_r];
+    if (sbase == nullptr) continue;                 // H2D from a peer's tier: pushed by its owner
+    wait_evicted(&evp_of(d, r)[x.dst], push);
     const i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
     const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
     seg_copy(d, bk, src, dst);
-    if (x.t0 < x.t1) {
+    if (x.t0 < x.t1 && !d.multi) {
       seg_copy_fence(d);                            // copy done before the tail is overwritten
       fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
     }
   }
-  const i64 nl = local_items(d, d.fld_cnt, nseg);
-  for (i64 it = me; it < nl; it += G) {
-    int r, s; u32 e;
-    locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
-    FillDesc x = d.fld[(size_t)r * d.NB + e];
-    wait_evicted(&d.evp[(size_t)r * d.NB + x.idx]);
-    fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
+  if (!d.multi) {
+    const i64 nl = local_items(d, d.fld_cnt, nseg);
+    for (i64 it = me; it < nl; it += G) {
+      int r, s; u32 e;
+      locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
+      FillDesc x = d.fld[(size_t)r * d.NB + e];
+      wait_evicted(&evp_of(d, r)[x.idx], false);
+      fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
+    }
   }
   bulk_end(d);
+  if (d.multi) __threadfence_system();             // pushed bytes visible before the barrier
 }
 
 // Test aid: count words of every owned block (HBM and host tier of the local

@@ -170,6 +170,11 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     ti.p2p_blocks = d.ctr->t_p2p;
     ti.d2d_blocks = d.ctr->t_d2d;
     ti.fetch_blocks = d.ctr->t_fetch;
+    for (int r = 0; r < TA_MAX_REPLICAS; ++r) {
+      ti.d2h_of[r] = r < R ? d.t_rep[r] : 0;
+      ti.h2d_of[r] = r < R ? d.t_rep[R + r] : 0;
+      ti.p2p_to[r] = r < R ? d.t_rep[2 * R + r] : 0;
+    }
     *d.tick_info = ti;
     d.ctr->n_dec = pos;
     if (!verb) {
@@ -198,6 +203,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     d.act_cnt[t] = 0; d.ec_cnt[t] = 0;   // cpd_cnt is read by the compaction copies after this kernel
   }
   for (u32 b = threadIdx.x; b < 2 * d.nbk; b += CTA) d.rhist[b] = 0;
+  for (int t = threadIdx.x; t < 3 * R; t += CTA) d.t_rep[t] = 0;
 }
 
 // Step 7 in one cooperative launch: deferred frees and per-program results over all

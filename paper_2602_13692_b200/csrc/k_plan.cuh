@@ -52,6 +52,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   __shared__ u32 s_app[4];              // appends: fed, fld, dfh, dfs (leader's are the live ones)
   __shared__ ull s_pc[PC_N];
   __shared__ PlanSh sh;
+  __shared__ u32 s_h2d_src[TA_MAX_REPLICAS];  // H2D requests by source tier (telemetry)
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   u32* s_fc = reinterpret_cast<u32*>(dsm + sizeof(SortSmem));   // staged need prefix  [4096]
@@ -80,6 +81,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   PSTAMP(2, 0);
   if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
   if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
+  if (threadIdx.x < TA_MAX_REPLICAS) s_h2d_src[threadIdx.x] = 0;
   u32* fp = d.f_pid + (size_t)r * N;
   u32* fc = d.f_cum + (size_t)r * N;
   u32* hf = d.hbm_free + (size_t)r * d.NBW;
@@ -290,7 +292,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         u32* ent = d.loc + (size_t)p * d.MAXBP + j;
         atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
         if (e < hfree) {
-          if (d.fused) d.evp[(size_t)r * d.NB + idx] = 2u * d.nL;  // segments pending their D2H read
+          if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
           const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
           *ent = LOC_HOST | slot;
           d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
@@ -341,6 +343,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       if (threadIdx.x == 0) {
         d.ev_cnt[r] = nv;
         d.evd_cnt[r] = ntoh;
+        d.t_rep[r] = ntoh;
         atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
         atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)ntoh);
         atomicAdd(&d.ctr->t_d2h, ntoh);
@@ -488,6 +491,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           } else {
             x = FeDesc{MV_H2D, (u32)h, old & ~LOC_HOST, dst, uid, t0, t1, j};
             dfs[atomicAdd(&Lapp[3], 1u)] = ((u32)h << 27) | (old & ~LOC_HOST);
+            atomicAdd(&s_h2d_src[h], 1u);
             pc[PC_H2D] += 1;
           }
         } else {                                        // recompute history / brand-new tokens
@@ -521,7 +525,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   }
   FeDesc* fed = d.fed + (size_t)r * d.NB;
   for (u32 i = threadIdx.x; i < nfed; i += CTA) fed[base + i] = fstage[i];
+  if (threadIdx.x < d.R && s_h2d_src[threadIdx.x]) atomicAdd(&d.t_rep[d.R + threadIdx.x], s_h2d_src[threadIdx.x]);
   if (threadIdx.x == 0) {
+    if (s_pc[PC_P2P]) atomicAdd(&d.t_rep[2 * d.R + r], (u32)s_pc[PC_P2P]);
     atomicAdd(&d.stats[ST_P2P], s_pc[PC_P2P]);
     atomicAdd(&d.stats[ST_H2D], s_pc[PC_H2D]);
     atomicAdd(&d.ctr->t_p2p, (u32)s_pc[PC_P2P]);

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
     u32 idx = row[j];
     scr[e] = idx;
     if (e < hfree) {
-      if (d.fused) d.evp[(size_t)h * d.NB + idx] = 2u * d.nL;
+      if (evp_owner(d, h)) evp_of(d, h)[idx] = 2u * d.nL;
       u32 slot = bitmap_select(sf, s_big, d.NHW, e);
       row[j] = LOC_HOST | slot;
       d.owner_host[(size_t)h * d.NH + slot] = pid * (u32)d.MAXB + j;

@@ -22,6 +22,7 @@
 namespace {
 
 const int kCopyGrid = 148 * 8;   // copy kernels: 8 resident 256-thread CTAs per SM
+const size_t kEvpOffset = 512;   // eviction flags inside the mailbox allocation
 // API-mode event batch capacity: 4 events per program slot (at least 4096)
 static inline size_t ev_capacity(const ta_config* c) {
   return std::max<size_t>(4096, 4 * (size_t)c->max_programs);
@@ -62,7 +63,7 @@ struct ta_ctx {
   size_t block_bytes = 0;
   cudaEvent_t ev[10] = {};
   bool timing = false;
-  void* mbox_alloc = nullptr;               // barrier mailbox (library-owned, 264 B)
+  void* mbox_alloc = nullptr;               // barrier mailbox + (multi) eviction flags, library-owned
   int move_grid = 0;                        // resident CTAs of k_move_fused (even)
   int close_grid = 1;                       // CTAs of the cooperative k_close
   void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
@@ -167,6 +168,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.ev_mv = L.take<u32>(EC); x.ev_mv2 = L.take<u32>(EC);
   x.pst = L.take<ull>(4 * 32);
   x.gsync = L.take<ull>(2);
+  x.t_rep = L.take<u32>(3 * R);
   x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
   x.ec_list = L.take<u32>(R * N); x.ec_cnt = L.take<u32>(R);
   x.rhist = L.take<u32>(2 * 2048 + 2); x.rb = L.take<u32>(N); x.fpl = L.take<i8>(N);
@@ -221,9 +223,14 @@ static inline size_t csm(const Dev& d) { return (d.flags & TA_F_COPY_BULK) ? BUL
 static void launch_movement(ta_ctx* x, cudaStream_t s) {
   Dev& d = x->d;
   if (d.fused) {
+    // one process per GPU: every peer's plan (and its eviction flags) is in place before
+    // anyone pushes, and every transfer has landed before anyone reuses a block
+    if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
     k_move_fused<<<x->move_grid, 256, csm(d), s>>>(d);   // persistent: every CTA co-resident
+    if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
     rec(x, 4);
     rec(x, 5);
+    if (d.multi && (d.flags & TA_F_FILL)) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
     return;
   }
   k_copy_evict<<<kCopyGrid, 256, csm(d), s>>>(d);
@@ -416,7 +423,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   x->timing = (cfg->flags & TA_F_TIMING) != 0;
   d.multi = cfg->replicas_here < cfg->n_replicas ? 1 : 0;
   d.rank = cfg->first_replica;
-  d.fused = (!d.multi && !(cfg->flags & TA_F_NO_FUSE)) ? 1 : 0;
+  d.fused = !(cfg->flags & TA_F_NO_FUSE) ? 1 : 0;
   {   // the fused movement kernel waits across CTAs: launch only as many as are resident
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -433,13 +440,17 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     delete x;
     return TA_E_INVAL;
   }
-  if (cudaMalloc(&x->mbox_alloc, (TA_MAX_REPLICAS + 1) * sizeof(ull)) != cudaSuccess ||
-      cudaMemset(x->mbox_alloc, 0, (TA_MAX_REPLICAS + 1) * sizeof(ull)) != cudaSuccess) {
+  // mailbox epochs [0, 264) and, one process per GPU, the local replica's eviction
+  // flags at kEvpOffset: one IPC handle shares both with the peers
+  const size_t mbox_bytes = kEvpOffset + (size_t)cfg->hbm_blocks * sizeof(u32);
+  if (cudaMalloc(&x->mbox_alloc, mbox_bytes) != cudaSuccess ||
+      cudaMemset(x->mbox_alloc, 0, mbox_bytes) != cudaSuccess) {
     delete x;
     return TA_E_CUDA;
   }
   d.mbox = (ull*)x->mbox_alloc;
   d.epoch = d.mbox + TA_MAX_REPLICAS;
+  if (d.multi) d.evp = (u32*)((char*)x->mbox_alloc + kEvpOffset);
   size_t dev_bytes = carve(cfg, nullptr, nullptr);
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
@@ -806,6 +817,7 @@ ta_status ta_import_peer_pool(ta_ctx* ctx, int32_t replica, const void* handle) 
   ctx->bufs.hbm_pool[replica] = (char*)p + off;
   ctx->d.hbm[replica] = (char*)p + off;
   ctx->d.mbox_peer[replica] = (ull*)m;
+  ctx->d.evp_peer[replica] = (u32*)((char*)m + kEvpOffset);
   if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
   return TA_OK;
 }
