@@ -364,7 +364,7 @@ class Pool:
         a = (C.c_uint64 * 128)()
         self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 128), "ta_debug_phase_stamps")
         out = {}
-        for k, name in enumerate(("pause", "restore", "plan")):
+        for k, name in enumerate(("pause", "restore", "plan", "close")):
             v = [(i, a[32 * k + i]) for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
             out[name] = [(i, c - v[0][1]) for i, c in v] if v else []
             # sizes recorded next to the stamps (bit 62 set): ("n<i>", value)

@@ -132,6 +132,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     for (u32 i = threadIdx.x; i < n; i += CTA) put(pos + i, d.dec_ev[(size_t)r * N + i]);
     pos += n;
   }
+  PSTAMP(3, 5);
   for (int r = 0; r < R; ++r) {          // FETCH / STALL (kind 0 = no decision)
     const ta_decision* fs = d.dec_fs + (size_t)r * N;
     u32 n = cta_ordered_gather((int)d.f_cnt[r], s_tmp,
@@ -150,6 +151,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
       pos += 1;
     }
   }
+  PSTAMP(3, 6);
   // occupancy / imbalance (SPEC.md:151-157 at block granularity)
   ull umax = 0, umin = ~0ull;
   for (int r = 0; r < R; ++r) {
@@ -160,22 +162,23 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     umax = used > umax ? used : umax;
     umin = used < umin ? used : umin;
   }
+  PSTAMP(3, 7);
+  if (threadIdx.x < TA_MAX_REPLICAS) {   // per-replica link telemetry (host-mapped), one lane each
+    const int r = threadIdx.x;
+    d.tick_info->d2h_of[r] = r < R ? d.t_rep[r] : 0;
+    d.tick_info->h2d_of[r] = r < R ? d.t_rep[R + r] : 0;
+    d.tick_info->p2p_to[r] = r < R ? d.t_rep[2 * R + r] : 0;
+  }
   if (threadIdx.x == 0) {
     *d.dec_out_cnt = pos;
-    ta_tick_info ti;
-    ti.tick = d.ctr->tick;
-    ti.decisions = pos;
-    ti.d2h_blocks = d.ctr->t_d2h;
-    ti.h2d_blocks = d.ctr->t_h2d;
-    ti.p2p_blocks = d.ctr->t_p2p;
-    ti.d2d_blocks = d.ctr->t_d2d;
-    ti.fetch_blocks = d.ctr->t_fetch;
-    for (int r = 0; r < TA_MAX_REPLICAS; ++r) {
-      ti.d2h_of[r] = r < R ? d.t_rep[r] : 0;
-      ti.h2d_of[r] = r < R ? d.t_rep[R + r] : 0;
-      ti.p2p_to[r] = r < R ? d.t_rep[2 * R + r] : 0;
-    }
-    *d.tick_info = ti;
+    ta_tick_info* ti = d.tick_info;
+    ti->tick = d.ctr->tick;
+    ti->decisions = pos;
+    ti->d2h_blocks = d.ctr->t_d2h;
+    ti->h2d_blocks = d.ctr->t_h2d;
+    ti->p2p_blocks = d.ctr->t_p2p;
+    ti->d2d_blocks = d.ctr->t_d2d;
+    ti->fetch_blocks = d.ctr->t_fetch;
     d.ctr->n_dec = pos;
     if (!verb) {
       ull imb = umax - umin;
@@ -191,6 +194,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
   }
   // clear the per-tick lists and counters for the next tick / call
   __syncthreads();
+  PSTAMP(3, 8);
   if (threadIdx.x == 0) {
     d.ctr->stops = 0;
     d.ctr->restore_cnt = 0;
@@ -214,13 +218,21 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
+  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[3 * 32 + threadIdx.x] = 0;
+  PSTAMP(3, 0);
   finalize_part(d, verb);
+  PSTAMP(3, 1);
   grid_sync(d, 1);
+  PSTAMP(3, 2);
   if (blockIdx.x < (unsigned)d.R) {
     const int r = blockIdx.x;
     if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) compact_plan_pass(d, r, s_big, s_tmp);
     else if (threadIdx.x == 0) d.cpd_cnt[r] = 0;
   }
-  grid_sync(d, 1);
+  PSTAMP(3, 3);
+  if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) grid_sync(d, 1);   // plans -> decisions
+  else __syncthreads();
+  PSTAMP(3, 4);
   if (blockIdx.x == 0) assemble_pass(d, verb, s_tmp);
+  PSTAMP(3, 9);
 }

@@ -2,56 +2,80 @@
 #pragma once
 #include "common.cuh"
 
+// A slot's values after step 0, handed from the ingesting lane to its warp.
+struct SlotNow {
+  u32 c;
+  i64 as;          // acting_since
+  int st, ph, pl, home, released;
+};
+
 // Step 0, trace mode, for one slot: decode during the last interval, tool call /
-// tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).
-__device__ __forceinline__ void ingest_slot(const Dev& d, int p, i64 T) {
+// tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).  Every
+// field is loaded up front (one memory round trip), the trace script entries of the
+// current turn in a second one.
+__device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
   u8 st = d.status[p];
-  if (st == TA_UNARRIVED || st == TA_STOPPED) return;
-  const u32 base = d.t_off[p];
-  const u32 nturns = d.t_off[p + 1] - base;
-  u32 c = d.c[p];
+  const u8 sat = d.satisfied[p];
   u8 ph = d.phase[p];
-  if (st == TA_REASONING && d.satisfied[p]) {
+  u32 c = d.c[p];
+  const u32 t = d.turn[p];
+  const u32 gd0 = d.gen_done[p];
+  const i64 tr0 = d.tool_return[p];
+  i64 as = d.acting_since[p];
+  const u32 base = d.t_off[p], base1 = d.t_off[p + 1];
+  SlotNow o{c, as, st, ph, d.placement[p], d.home[p], 0};
+  if (st == TA_UNARRIVED || st == TA_STOPPED) return o;
+  const u32 nturns = base1 - base;
+  const u32 g = d.t_g[base + t], dtool = d.t_d[base + t], res = d.t_o[base + t];
+  i64 tr = tr0;
+  u32 tt = t, gd = gd0;
+  bool wrote_gd = false, wrote_tool = false;
+  if (st == TA_REASONING && sat) {
     const u32 d_tick = (u32)(((i64)d.rate * d.dt) / 1000);
-    u32 t = d.turn[p];
-    u32 g = d.t_g[base + t];
-    u32 gd = d.gen_done[p];
-    u32 left = g - gd;
-    u32 dd = min(d_tick, left);
+    const u32 left = g - gd;
+    const u32 dd = min(d_tick, left);
     c += dd;
     gd += dd;
-    d.gen_done[p] = gd;
+    wrote_gd = true;
     if (gd == g) {
       if (t == nturns - 1) {             // last turn: release
+        d.gen_done[p] = gd;
         d.c[p] = c;
         d.status[p] = TA_STOPPED;
         d.placement[p] = -1;
         d.satisfied[p] = 0;
-        d.released[p] = 1;
         atomicAdd(&d.ctr->stops, 1u);
-        return;
+        o.c = c; o.st = TA_STOPPED; o.pl = -1; o.released = 1;
+        return o;
       }
       ph = TA_PHASE_A;                   // tool call: Reasoning -> Acting
       st = TA_ACTING;
-      i64 took = d.rate == 0 ? 0 : ((i64)left * 1000 + d.rate - 1) / d.rate;
-      i64 as = T - d.dt + took;
+      const i64 took = d.rate == 0 ? 0 : ((i64)left * 1000 + d.rate - 1) / d.rate;
+      as = T - d.dt + took;
+      tr = as + (i64)dtool;
       d.acting_since[p] = as;
-      d.tool_return[p] = as + (i64)d.t_d[base + t];
       d.step_count[p] += 1;
+      wrote_tool = true;
     }
   }
-  if (ph == TA_PHASE_A && (st == TA_ACTING || st == TA_PAUSED) && T >= d.tool_return[p]) {
-    u32 t = d.turn[p];
-    c += d.t_o[base + t];                 // tool result (tools run while paused)
-    d.turn[p] = t + 1;
-    d.gen_done[p] = 0;
+  if (ph == TA_PHASE_A && (st == TA_ACTING || st == TA_PAUSED) && T >= tr) {
+    c += res;                            // tool result (tools run while paused)
+    tt = t + 1;
+    gd = 0;
+    wrote_gd = true;
     ph = TA_PHASE_R;
-    d.tool_return[p] = INT64_MAX;
+    tr = INT64_MAX;
+    wrote_tool = true;
     if (st == TA_ACTING) st = TA_REASONING;
+    d.turn[p] = tt;
   }
+  if (wrote_gd) d.gen_done[p] = gd;
+  if (wrote_tool) d.tool_return[p] = tr;
   d.c[p] = c;
   d.phase[p] = ph;
   d.status[p] = st;
+  o.c = c; o.as = as; o.st = st; o.ph = ph;
+  return o;
 }
 
 // Step 0, API mode (SURVEY.md §8(c) event table): the batch
@@ -216,15 +240,16 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 }
 
 // Steps 0 (release frees) + 1 (footprint) + 2 (contribution, L_eff) for one slot,
-// by one warp.  The block-table row is scanned with 16-byte loads; counts come from
-// ballot/popc, prefix_hbm from the first non-HBM entry.  Loads accumulate into Lacc
-// (k_pause publishes L).  Closed-loop arrivals are initialised by k_restore.
-__device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int verb) {
+// by one warp, given the slot's values after step 0 (identical in every lane).  The
+// block-table row is scanned with 16-byte loads; counts come from ballot/popc,
+// prefix_hbm from the first non-HBM entry.  Loads accumulate into Lacc (k_pause
+// publishes L).  Closed-loop arrivals are initialised by k_restore.
+__device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int verb, const SlotNow& v) {
   const u32 lane = lane_id();
   u32* row = d.loc + (size_t)p * d.MAXBP;
-  if (!verb && d.released[p]) {                   // free every block of a STOPPED program (A26)
-    const int h = d.home[p];
-    const u32 nbv = ceil_div_u32(d.c[p], d.bt);
+  if (!verb && v.released) {                      // free every block of a STOPPED program (A26)
+    const int h = v.home;
+    const u32 nbv = ceil_div_u32(v.c, d.bt);
     for (u32 j = lane; j < nbv; j += 32) {
       u32 e = row[j];
       if (e == LOC_NONE) continue;
@@ -245,7 +270,7 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
     }
     return;
   }
-  const u8 st = d.status[p];
+  const u8 st = (u8)v.st;
   if (st != TA_PAUSED && st != TA_REASONING && st != TA_ACTING) {
     if (lane == 0) {
       d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
@@ -254,7 +279,7 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
     }
     return;
   }
-  const u32 nbv = ceil_div_u32(d.c[p], d.bt);
+  const u32 nbv = ceil_div_u32(v.c, d.bt);
   u32 n_h = 0, n_s = 0, first = 0xFFFFFFFFu;
   for (u32 j0 = 0; j0 < nbv; j0 += 512) {         // four independent 16-B loads per lane in flight
     uint4 q[4];
@@ -292,8 +317,8 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
     d.n_hbm[p] = n_h;
     d.n_host[p] = n_s;
     d.prefix_hbm[p] = first == 0xFFFFFFFFu ? nbv : first;
-    const u8 ph = d.phase[p];
-    u32 cb = contrib_of(d, nbv, ph, d.acting_since[p], T);
+    const u8 ph = (u8)v.ph;
+    u32 cb = contrib_of(d, nbv, ph, v.as, T);
     d.contrib[p] = cb;
     // candidate lists of the planner kernels (unordered appends; consumers sort by key
     // and slot, so the append order never reaches a result)
@@ -303,15 +328,32 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
       rbv = restore_bucket(d, ph, nbv);
       atomicAdd(&d.rhist[rbv], 1u);
     } else {
-      pl = d.placement[p];
+      pl = (i8)v.pl;
       if (!verb) atomicAdd(&d.Lacc[pl], (ull)cb);     // commutative u64 sum
       d.act_list[(size_t)pl * d.N + atomicAdd(&d.act_cnt[pl], 1u)] = (u32)p;
     }
-    const int h = d.home[p];
+    const int h = v.home;
     if (n_h > 0 && h >= 0) d.ec_list[(size_t)h * d.N + atomicAdd(&d.ec_cnt[h], 1u)] = (u32)p;
     d.rb[p] = rbv;
     d.fpl[p] = pl;
   }
+}
+
+// The slot's current values (API mode, verbs: step 0 already applied or absent).
+__device__ __forceinline__ SlotNow slot_now(const Dev& d, int p) {
+  return SlotNow{d.c[p], d.acting_since[p], d.status[p], d.phase[p], d.placement[p], d.home[p], d.released[p]};
+}
+
+// broadcast lane 0's SlotNow to the warp
+__device__ __forceinline__ SlotNow bcast(SlotNow v) {
+  v.c = __shfl_sync(FULL_MASK, v.c, 0);
+  v.as = (i64)__shfl_sync(FULL_MASK, (ull)v.as, 0);
+  v.st = __shfl_sync(FULL_MASK, v.st, 0);
+  v.ph = __shfl_sync(FULL_MASK, v.ph, 0);
+  v.pl = __shfl_sync(FULL_MASK, v.pl, 0);
+  v.home = __shfl_sync(FULL_MASK, v.home, 0);
+  v.released = __shfl_sync(FULL_MASK, v.released, 0);
+  return v;
 }
 
 // Trace mode: steps 0-2 of the tick in one kernel, one warp per slot (ingest by
@@ -324,9 +366,9 @@ __global__ void __launch_bounds__(256) k_tick_front(Dev d) {
     d.ctr->T = T;
     if (d.ctr->err != TA_E_PEER) d.ctr->err = TA_OK;   // a failed verb's status does not stop the tick
   }
-  if (lane_id() == 0) ingest_slot(d, p, T);
-  __syncwarp();
-  footprint_warp(d, p, T, 0);
+  SlotNow v{};
+  if (lane_id() == 0) v = ingest_slot(d, p, T);
+  footprint_warp(d, p, T, 0, bcast(v));
 }
 
 // API mode and verbs: steps 1-2 (the events were applied by k_ev_*).  Verbs
@@ -336,5 +378,7 @@ __global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
   if (p >= d.N || (!verb && d.ctr->err != TA_OK)) return;
   const i64 T = verb ? d.ctr->T : d.ctr->now_ms;
   if (!verb && p == 0 && lane_id() == 0) d.ctr->T = T;
-  footprint_warp(d, p, T, verb);
+  SlotNow v{};
+  if (lane_id() == 0) v = slot_now(d, p);
+  footprint_warp(d, p, T, verb, bcast(v));
 }

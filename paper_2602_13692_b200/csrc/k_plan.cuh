@@ -227,6 +227,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         __syncthreads();
       }
       nv = (u32)upper_bound_u32(ecs_sm ? s_ec : ec, (int)ne, X - 1) + 1;   // victims
+      PSTAMP(2, 13);
       cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);      // host-slot select prefix
       hfree = s_big[d.NHW];
       // host-tier free words snapshot (selects read it, so the live bitmap can be
@@ -237,6 +238,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
       for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
     }
+    PSTAMP(2, 14);
     if (threadIdx.x == 0) {
       sh.stop = stop; sh.X = X; sh.hfree = hfree; sh.nv = nv; sh.vst = vst; sh.ecs_sm = ecs_sm;
       sh.m = m; sh.tot = stop ? 0 : tot; sh.nF = nF; sh.fcs_sm = fcs_sm;
@@ -245,6 +247,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   cl.sync();                                           // #1: part A visible to the cluster
 
   // ================= all CTAs: the eviction loop, split by cluster rank
+  PSTAMP(2, 15);
   const u32 X = L->X;
   if (L->stop) {
     cl.sync();                                         // leader's smem outlives every reader
@@ -305,6 +308,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       }
     }
   }
+  PSTAMP(2, 16);
   cl.sync();                                           // #2: evictions done
   PSTAMP(2, 6);
 
@@ -417,6 +421,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   }
   cl.sync();                                           // #3: allocation inputs staged
 
+  PSTAMP(2, 17);
   // ================= all CTAs: the request loop, split by cluster rank
   // (p in S_r slot order, needed j ascending) -> q-th lowest free block.  Selects read
   // the staged snapshot of the free bitmap, so each request clears its block in the
@@ -509,6 +514,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       nfed += round_n;
     }
   }
+  PSTAMP(2, 18);
   // per-CTA counters: warp sums (one redux per counter), then shared 64-bit atomics
 #pragma unroll
   for (int i = 0; i < PC_N; ++i) {
