@@ -231,6 +231,17 @@ ta_status ta_resume(ta_ctx* ctx, uint32_t pid, int32_t replica, ta_decision* out
 ta_status ta_migrate(ta_ctx* ctx, uint32_t pid, int32_t dst_replica, ta_decision* out,
                      int32_t out_cap, int32_t* n_out);
 
+/* Backend health mask with failover (PAPER.md:699 BackendState.healthy; SPEC.md:499-506:
+ * "unhealthy backends flagged, their programs force-Paused back to the global queue").
+ * healthy == 0: replica's KV (HBM pool and host tier) is considered lost: programs
+ * active on it are paused (PAUSE records, slot order), programs homed on it drop every
+ * block (EVICT records, all blocks dropped, slot order), its watermarks become 0 so no
+ * restore, resume or migration targets it.  healthy != 0: back in service, empty (no
+ * decisions).  No change: TA_OK, no decisions.  Collective in multi-process mode.
+ * Errors: TA_E_INVAL (replica).  Synchronizes. */
+ta_status ta_set_health(ta_ctx* ctx, int32_t replica, int32_t healthy, ta_decision* out, int32_t out_cap,
+                        int32_t* n_out);
+
 /* Cumulative counters and per-replica occupancy (synchronizes the stream). */
 ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out);
 

@@ -119,6 +119,7 @@ class Oracle:
         self.cap_max = [(self.lmax * self.NB) >> 16 for _ in range(self.R)]
         self.cap_min = [(self.lmin * self.NB) >> 16 for _ in range(self.R)]
         self.L = [0] * self.R
+        self.healthy = [True] * self.R     # BackendState.healthy
         self.tick = 0
         self.last_T = 0
         self.next_arrival = 0
@@ -735,8 +736,8 @@ class Oracle:
             if not cand:
                 return E_CAPACITY, []
             replica = min(cand, key=lambda r: (self.L[r], 0 if r == self.home[pid] else 1, r))
-        elif self.L[replica] + cr > self.cap_max[replica]:
-            return E_CAPACITY, []
+        elif not self.healthy[replica] or self.L[replica] + cr > self.cap_max[replica]:
+            return E_CAPACITY, []                         # unhealthy: no capacity (reading A39)
         return self._activate(pid, replica, cr, D_RESTORE)
 
     def migrate(self, pid: int, dst: int):
@@ -750,7 +751,7 @@ class Oracle:
             return E_INVAL, []
         self._verb_prepare()
         cr = self.contrib[pid]
-        if self.L[dst] + cr > self.cap_max[dst]:
+        if not self.healthy[dst] or self.L[dst] + cr > self.cap_max[dst]:
             return E_CAPACITY, []
         return self._activate(pid, dst, cr, D_MIGRATE)
 
@@ -775,6 +776,46 @@ class Oracle:
         if kind == D_RESTORE:
             self.stats["restores"] += 1
         return OK, [decision(kind, pid, src=src, dst=r)] + evicts + fetches
+
+    def set_health(self, r: int, healthy: bool):
+        """Backend health mask with failover (NEXT-4; PAPER.md:699 BackendState.healthy;
+        SPEC.md:502 "unhealthy backends flagged, their programs force-Paused back to the
+        global queue").  Readings A37-A39: a replica marked unhealthy loses
+        its KV -- its HBM pool and its host tier -- so every program homed there drops
+        all its blocks (home -1; the history is recomputed where it resumes); every
+        program active on it is paused (paused_since = the current tick); its
+        watermarks become 0, so no restore targets it until it is marked healthy again
+        (empty).  Decisions: PAUSE (slot order), then EVICT with all blocks dropped
+        (slot order, programs that held blocks on r).  Idempotent: no change, no
+        decisions."""
+        if r < 0 or r >= self.R:
+            return E_INVAL, []
+        healthy = bool(healthy)
+        if healthy == self.healthy[r]:
+            return OK, []
+        self.healthy[r] = healthy
+        if healthy:
+            self.cap_max[r] = (self.lmax * self.NB) >> 16
+            self.cap_min[r] = (self.lmin * self.NB) >> 16
+            return OK, []
+        self.cap_max[r] = self.cap_min[r] = 0
+        pauses, evicts = [], []
+        for p in range(self.N):
+            if self.status[p] in (REASONING, ACTING) and self.placement[p] == r:
+                self._pause(p, self.tick)
+                pauses.append(decision(D_PAUSE, p, src=r))
+        for p in range(self.N):
+            if self.home[p] != r:
+                continue
+            lost = sum(1 for e in self.loc[p] if e != NONE)
+            self._free_all(p)
+            self.home[p] = -1
+            if lost:
+                self.stats["evict_blocks"] += lost
+                self.stats["evict_dropped"] += lost
+                evicts.append(decision(D_EVICT, p, src=r, blocks=lost, dropped=lost))
+        self.L[r] = 0
+        return OK, pauses + evicts
 
     # ------------------------------------------------------------------ invariants
     def check_invariants(self):

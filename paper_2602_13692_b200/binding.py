@@ -122,6 +122,7 @@ def lib():
             "ta_pause": [vp, u32, u32, vp, i32, C.POINTER(i32)],
             "ta_resume": [vp, u32, i32, vp, i32, C.POINTER(i32)],
             "ta_migrate": [vp, u32, i32, vp, i32, C.POINTER(i32)],
+            "ta_set_health": [vp, i32, i32, vp, i32, C.POINTER(i32)],
             "ta_stats": [vp, vp],
             "ta_phase_times": [vp, C.POINTER(C.c_float), i32],
             "ta_debug_phase_stamps": [vp, C.POINTER(C.c_uint64), i32],
@@ -149,7 +150,7 @@ EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_tra
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
             "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk",
-            "ta_debug_phase_stamps")
+            "ta_debug_phase_stamps", "ta_set_health")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
@@ -333,6 +334,9 @@ class Pool:
 
     def migrate(self, pid, dst):
         return self._verb(lib().ta_migrate, pid, dst)
+
+    def set_health(self, replica, healthy):
+        return self._verb(lib().ta_set_health, replica, 1 if healthy else 0)
 
     def stats(self) -> dict:
         s = Stats()

@@ -77,7 +77,8 @@ struct Dev {
   int first_local, n_local;
   int api_mode;
   u32 nbk, nb_shift;               // coarse-key buckets: nb >> nb_shift < nbk <= 2048
-  i64 cap_max[TA_MAX_REPLICAS], cap_min[TA_MAX_REPLICAS];
+  i64 cap_max[TA_MAX_REPLICAS], cap_min[TA_MAX_REPLICAS];   // 0 while a replica is unhealthy
+  u32 healthy;                     // bit r: replica r healthy (BackendState.healthy)
   ull F[64];
   char* hbm[TA_MAX_REPLICAS];      // device-addressable HBM pool per replica (NULL if not here)
   char* host[TA_MAX_REPLICAS];     // device alias of the pinned host tier (local replicas)

@@ -134,8 +134,8 @@ __global__ void k_verb_admit(Dev d, u32 pid, int replica, int migrate) {
         }
       }
       if (best == ~0ull) err = TA_E_CAPACITY; else t = (int)(best & 31);
-    } else if (d.L[t] + cr > (ull)d.cap_max[t]) {
-      err = TA_E_CAPACITY;
+    } else if (!((d.healthy >> t) & 1u) || d.L[t] + cr > (ull)d.cap_max[t]) {
+      err = TA_E_CAPACITY;                 // an unhealthy replica has no capacity (reading A39)
     }
   }
   d.ctr->err = err;
@@ -170,4 +170,72 @@ __global__ void k_verb_commit(Dev d, int migrate) {
   if (old >= 0) d.L[old] -= cr;
   d.L[t] += cr;
   if (!migrate) d.stats[ST_RESTORES] += 1;
+}
+
+// ta_set_health(r, unhealthy) (NEXT-4; readings A37-A39),
+// one CTA: the replica's KV is lost.  Programs active on r are force-paused (PAUSE
+// records, slot order); programs homed on r drop every block (EVICT records with all
+// blocks dropped, slot order, only those that held blocks); r's HBM and host-tier
+// bitmaps become all free; its load is 0.  The caller already set its watermarks to 0.
+__global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ Dev d, int r) {
+  __shared__ u32 s_tmp[NWARP + 1];
+  const int N = d.N;
+  const u32 k = (u32)d.ctr->tick;
+  u32* pl = d.pause_list + (size_t)r * N;
+  const u32 np = cta_ordered_gather(N, s_tmp,
+      [&](int i) { const u8 s = d.status[i]; return (s == TA_REASONING || s == TA_ACTING) && d.placement[i] == r; },
+      [&](u32 pos, int i) { pl[pos] = (u32)i; });
+  for (u32 q = threadIdx.x; q < np; q += CTA) {
+    const u32 p = pl[q];
+    d.status[p] = TA_PAUSED;
+    d.placement[p] = -1;
+    d.paused_since[p] = k;
+    d.satisfied[p] = 0;
+  }
+  u32* hl = d.e_pid + (size_t)r * N;                  // programs homed on r, slot order
+  const u32 nh = cta_ordered_gather(N, s_tmp, [&](int i) { return d.home[i] == r; },
+                                    [&](u32 pos, int i) { hl[pos] = (u32)i; });
+  u32* lost = d.e_cum + (size_t)r * N;
+  const u32 warp = threadIdx.x >> 5, lane = lane_id();
+  for (u32 q = warp; q < nh; q += NWARP) {            // one warp per program: drop its row
+    const u32 p = hl[q];
+    u32* row = d.loc + (size_t)p * d.MAXBP;
+    const u32 nbv = ceil_div_u32(d.c[p], d.bt);
+    u32 cnt = 0;
+    for (u32 j = lane; j < nbv; j += 32) {
+      if (row[j] != LOC_NONE) { ++cnt; row[j] = LOC_NONE; }
+    }
+    cnt = __reduce_add_sync(FULL_MASK, cnt);
+    if (lane == 0) { lost[q] = cnt; d.home[p] = -1; }
+  }
+  __syncthreads();
+  ta_decision* ev = d.dec_ev + (size_t)r * N;
+  __shared__ ull s_lost;
+  if (threadIdx.x == 0) s_lost = 0;
+  __syncthreads();
+  const u32 ne = cta_ordered_gather((int)nh, s_tmp, [&](int q) { return lost[q] > 0; },
+      [&](u32 pos, int q) {
+        ta_decision rec = {};
+        rec.kind = TA_D_EVICT; rec.pid = hl[q]; rec.src = r; rec.dst = -1;
+        rec.blocks = lost[q]; rec.dropped = lost[q];
+        ev[pos] = rec;
+        atomicAdd(&s_lost, (ull)lost[q]);
+      });
+  // every block of r belonged to a program homed on r: the pools are empty now
+  for (int w = threadIdx.x; w < d.NBW; w += CTA) {
+    const i64 lo = (i64)w * 32, n = d.NB - lo;
+    d.hbm_free[(size_t)r * d.NBW + w] = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1);
+  }
+  for (int w = threadIdx.x; w < d.NHW; w += CTA) {
+    const i64 lo = (i64)w * 32, n = d.NH - lo;
+    d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
+  }
+  if (threadIdx.x == 0) {
+    d.pause_cnt[r] = np;
+    d.ev_cnt[r] = ne;
+    d.L[r] = 0;
+    d.stats[ST_PAUSES] += np;
+    d.stats[ST_EVICT_BLOCKS] += s_lost;
+    d.stats[ST_EVICT_DROPPED] += s_lost;
+  }
 }

@@ -393,6 +393,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     d.cap_max[r] = (i64)(((u64)cfg->lambda_max_q16 * (u64)d.NB) >> 16);
     d.cap_min[r] = (i64)(((u64)cfg->lambda_min_q16 * (u64)d.NB) >> 16);
   }
+  d.healthy = d.R >= 32 ? 0xFFFFFFFFu : ((1u << d.R) - 1);
   for (int k = 0; k < 64; ++k) d.F[k] = cfg->decay_q32[k];
   for (int r = 0; r < TA_MAX_REPLICAS; ++r) {
     d.hbm[r] = (char*)bufs->hbm_pool[r];
@@ -755,6 +756,33 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   launch_movement(ctx, ctx->stream);
   launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
   return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);
+}
+
+ta_status ta_set_health(ta_ctx* ctx, int32_t replica, int32_t healthy, ta_decision* out, int32_t out_cap,
+                        int32_t* n_out) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  Dev& d = ctx->d;
+  if (replica < 0 || replica >= d.R || out_cap < 0) FAIL(ctx, TA_E_INVAL, "bad replica %d / out_cap", replica);
+  if (ta_status ps = check_peers(ctx)) return ps;
+  if (n_out) *n_out = 0;
+  const u32 bit = 1u << replica;
+  if (((d.healthy & bit) != 0) == (healthy != 0)) return TA_OK;    // no change, no decisions
+  // watermarks and the health mask are kernel parameters: the tick graph is re-captured
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+  if (healthy) {                         // back in service, empty
+    d.healthy |= bit;
+    d.cap_max[replica] = (i64)(((u64)ctx->cfg.lambda_max_q16 * (u64)d.NB) >> 16);
+    d.cap_min[replica] = (i64)(((u64)ctx->cfg.lambda_min_q16 * (u64)d.NB) >> 16);
+    return TA_OK;
+  }
+  d.healthy &= ~bit;
+  d.cap_max[replica] = d.cap_min[replica] = 0;
+  cudaStream_t s = ctx->stream;
+  k_verb_reset<<<1, 32, 0, s>>>(d);
+  k_verb_health<<<1, CTA, 0, s>>>(d, replica);
+  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
+  return verb_finish(ctx, "ta_set_health", out, out_cap, n_out);
 }
 
 ta_status ta_resume(ta_ctx* ctx, uint32_t pid, int32_t replica, ta_decision* out, int32_t out_cap, int32_t* n_out) {

@@ -224,3 +224,48 @@ def test_gpu_api_replay_equals_trace_mode(name, n, ticks):
         assert np.array_equal(got, want[k]), f"tick {k}: API replay differs from trace mode"
     assert n_ev > 0
     pool.close()
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_gpu_health_failover_random(seed):
+    """NEXT-4 health mask: replicas fail and come back between ticks (ta_set_health),
+    interleaved with the other verbs; decisions, status codes and full state equal the
+    oracle's; the KV left on the healthy replicas stays byte-exact."""
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = tracegen.get_config("c1_toy", n_replicas=3, hbm_blocks=64, host_blocks=16, compact_every=4,
+                              trace=dict(n=30, n_initial=12, seed=seed))
+    tr = tracegen.make_trace(cfg)
+    o = oracle.Oracle(cfg, tr)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns)
+    pool.load_trace(tr)
+    rng = random.Random(seed)
+    down, n_fail = set(), 0
+    for k in range(90):
+        _, dec_o = o.sched_step()
+        _, dec_g = pool.step()
+        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        if rng.random() < 0.2:
+            r = rng.randrange(3)
+            up = r in down or len(down) == 2
+            if up and r not in down:
+                continue
+            so, do = o.set_health(r, up)
+            sg, dg = pool.set_health(r, up)
+            assert so == sg == oracle.OK
+            assert dec_tuples(dg) == do, (k, r, up)
+            (down.discard if up else down.add)(r)
+            n_fail += not up
+            compare_state(o, pool.debug_download(), where=f"tick {k} after set_health({r}, {up})")
+        if rng.random() < 0.3:                # verbs must refuse unhealthy targets the same way
+            p = rng.randrange(o.N)
+            rep = rng.randrange(3)
+            so, do = o.resume(p, rep)
+            sg, dg = pool.resume(p, rep)
+            assert so == sg, (k, p, rep, so, sg)
+            if so == oracle.OK:
+                assert dec_tuples(dg) == do
+        bad, _ = pool.verify_content()
+        assert bad == 0, f"tick {k}: {bad} KV words wrong"
+    assert n_fail > 0
+    pool.close()
