@@ -441,7 +441,7 @@ def main():
     e2e_value = args.steps * progs_total / 1e4 / (e2e_ms * 1e-3)
 
     # ---- bytes per path in the timed steps, roofline of the dominant kernel
-    dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS if isinstance(st0[k], int)}
+    dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS + binding.LEDGER_KEYS if isinstance(st0[k], int)}
     bb = pool.block_bytes
     ph = phase_sum / args.steps            # us per step
     if world == 1:
@@ -555,6 +555,11 @@ def main():
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),
+        # NEXT-1: STP cost ledger of the timed ticks (token-ms per step) and
+        # the Cost_unused < c_min bound of PAPER.md:415 (replica-ticks checked / violated)
+        "stp_ledger_token_ms_per_step": {k[5:]: int(dstat[k] / args.steps) for k in binding.LEDGER_KEYS
+                                         if k.startswith("cost_")},
+        "unused_bound": {"checks": dstat["unused_bound_checks"], "violations": dstat["unused_bound_violations"]},
         "sched_tick": tick_lat,
         "kv_moved": moved,
         "kv_paths": kv_paths,

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 1
+#define TA_ABI_VERSION 2
 #define TA_MAX_REPLICAS 32
 #define TA_LOC_NONE 0xFFFFFFFFu
 #define TA_LOC_HOST 0x80000000u
@@ -100,6 +100,8 @@ typedef struct {
   int32_t decode_tok_per_s;    /* synthetic engine decode rate (trace mode) */
   int32_t compact_every;       /* two-finger compaction every k ticks; 0 = off */
   uint32_t flags;              /* TA_F_* */
+  int32_t prefill_chunk_tokens; /* STP ledger (NEXT-1): chunked-prefill tokens per engine step (>= 1) */
+  int32_t prefill_chunk_ms;    /* STP ledger: duration of one chunk step in ms (>= 0) */
   int32_t reserved;
 } ta_config;
 
@@ -144,6 +146,13 @@ typedef struct {               /* cumulative counters (order fixed; see DESIGN.m
   uint64_t hbm_used[TA_MAX_REPLICAS];   /* HBM blocks in use */
   uint64_t host_used[TA_MAX_REPLICAS];  /* host-tier slots in use */
   uint64_t block_bytes;                 /* bytes per KV block (bytes moved = blocks * block_bytes) */
+  /* NEXT-1: STP cost ledger in token-ms (Eq. 2-3; readings A40-A44):
+   * for the interval after each tick -- decode: satisfied programs hold c; prefill /
+   * recompute: chunked staircases of new tokens / missed history; caching: resident
+   * tokens of ACTING and PAUSED programs; unused: cap_max - used blocks while programs
+   * wait -- and the Cost_unused < c_min bound of PAPER.md:415 per replica-tick. */
+  uint64_t cost_decode, cost_prefill, cost_recompute, cost_unused, cost_caching;
+  uint64_t unused_bound_checks, unused_bound_violations;
 } ta_stats_t;
 
 typedef struct {               /* trace-mode program scripts (tracegen layout; host pointers) */

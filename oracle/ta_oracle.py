@@ -71,7 +71,23 @@ STAT_KEYS = (
     "h2d_blocks", "recompute_blocks", "new_blocks", "compact_blocks", "stalls",
     "hit_tok", "peer_tok", "host_tok", "miss_tok", "new_tok", "fill_tok",
     "imbalance_max_blocks", "imbalance_last_blocks",
+    # NEXT-1: STP cost ledger (token-ms, Eq. 2-3) and the Cost_unused bound
+    "cost_decode", "cost_prefill", "cost_recompute", "cost_unused", "cost_caching",
+    "unused_bound_checks", "unused_bound_violations",
 )
+
+
+def stair(n: int, q: int, base: int = 0) -> int:
+    """Tokens held, summed over the chunks of a chunked prefill of n tokens on top of a
+    resident base (SPEC.md cost-ledger recompute_cost_of; Appendix E.2:
+    chunked prefill processes a constant number of tokens per step, so memory grows
+    linearly and the STP integral is a staircase): sum_{i=1}^{ceil(n/q)} (base + min(i*q, n))."""
+    total = 0
+    i = 1
+    while (i - 1) * q < n:
+        total += base + min(i * q, n)
+        i += 1
+    return total
 
 
 class Oracle:
@@ -91,6 +107,8 @@ class Oracle:
         self.lmax = int(cfg["lambda_max_q16"])
         self.lmin = int(cfg["lambda_min_q16"])
         self.compact_every = int(cfg.get("compact_every", 0))
+        self.chunk_q = int(cfg.get("prefill_chunk_tokens", 2048))   # chunked-prefill tokens per step
+        self.chunk_ms = int(cfg.get("prefill_chunk_ms", 20))        # time of one chunk step
         self.api_mode = api_mode
         self.trace = trace
         N = trace.n_slots if trace is not None else int(n_slots)
@@ -509,6 +527,7 @@ class Oracle:
             self.home[p] = r
             self.c_kv[p] = c1
             n_hbm[p] = nb[p]
+            self._ledger_s.append((p, c0, c1, miss))
         for p in stalled:
             fx.append(decision(D_STALL, p, src=self.home[p], dst=r, blocks=need[p]))
             self.stats["stalls"] += 1
@@ -520,6 +539,7 @@ class Oracle:
     def _step5(self, evict_out: list, fetch_out: list):
         deferred = []
         self._satisfied_now = set()
+        self._ledger_s = []
         for r in range(self.R):
             F = [p for p in range(self.N) if self.status[p] == REASONING and self.placement[p] == r]
             self._materialize(r, F, evict_out, fetch_out, deferred)
@@ -561,6 +581,37 @@ class Oracle:
             self.stats["compact_blocks"] += moves
             out.append(decision(D_COMPACT, NONE, src=r, dst=r, blocks=moves))
 
+    def _ledger(self):
+        """NEXT-1 STP ledger of this tick (readings A40-A44): for the interval that follows
+        the tick, per replica, in token-ms:
+          decode     satisfied programs hold their context c for the interval
+          prefill    new tokens [c_kv, c) of satisfied programs, chunked on top of the
+                     resident history: chunk_ms * stair(c - c_kv, q, base=c_kv)
+          recompute  missed history of resumed programs: chunk_ms * stair(miss, q)
+          caching    resident tokens of ACTING and PAUSED programs (idle KV), min(n_hbm*bt, c)
+          unused     max(0, cap_max - used blocks) * bt while paused programs wait
+        and the Cost_unused bound of PAPER.md:415: while the queue is non-empty, every
+        replica's idle effective capacity max(0, cap_max - L) after the restore pass
+        should be below c_min, the smallest paused footprint (blocks)."""
+        dt, q, tau = self.dt, self.chunk_q, self.chunk_ms
+        for p, c0, c1, miss in self._ledger_s:
+            self.stats["cost_decode"] += c1 * dt
+            self.stats["cost_prefill"] += tau * stair(c1 - c0, q, c0)
+            self.stats["cost_recompute"] += tau * stair(miss, q)
+        nb, n_hbm = self.fp["nb"], self.fp["n_hbm"]
+        for p in range(self.N):
+            if self.home[p] >= 0 and self.status[p] in (ACTING, PAUSED):
+                self.stats["cost_caching"] += min(n_hbm[p] * self.bt, self.c[p]) * dt
+        paused = [nb[p] for p in range(self.N) if self.status[p] == PAUSED]
+        if paused:
+            c_min = min(paused)
+            for r in range(self.R):
+                used = self.NB - sum(self.hbm_free[r])
+                self.stats["cost_unused"] += max(0, self.cap_max[r] - used) * self.bt * dt
+                self.stats["unused_bound_checks"] += 1
+                if max(0, self.cap_max[r] - self.L[r]) >= c_min:
+                    self.stats["unused_bound_violations"] += 1
+
     def _finalize_stats(self):
         used = [self.NB - sum(self.hbm_free[r]) for r in range(self.R)]
         imb = max(used) - min(used)
@@ -599,6 +650,7 @@ class Oracle:
         if self.compact_every and k % self.compact_every == 0:
             for r in range(self.R):
                 self._compact(r, compacts)
+        self._ledger()
         self._finalize_stats()
         self.tick += 1
         return OK, pauses + restores + evicts + fetches + compacts
@@ -763,6 +815,7 @@ class Oracle:
         evicts, fetches, deferred = [], [], []
         if self.status[pid] == REASONING:
             self._satisfied_now = set()
+            self._ledger_s = []                  # verbs are not ticks: no ledger interval
             # all_or_nothing returns before any mutation when the fetch cannot fit
             ok = self._materialize(r, [pid], evicts, fetches, deferred, all_or_nothing=True)
             if not ok:

@@ -40,7 +40,8 @@ class Config(C.Structure):
                 ("delta_t_ms", C.c_int64), ("decay_unit_ms", C.c_int64),
                 ("lambda_max_q16", C.c_uint32), ("lambda_min_q16", C.c_uint32),
                 ("decay_q32", C.c_uint64 * 64), ("decode_tok_per_s", C.c_int32),
-                ("compact_every", C.c_int32), ("flags", C.c_uint32), ("reserved", C.c_int32)]
+                ("compact_every", C.c_int32), ("flags", C.c_uint32), ("prefill_chunk_tokens", C.c_int32),
+                ("prefill_chunk_ms", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Buffers(C.Structure):
@@ -69,10 +70,14 @@ STAT_KEYS = ("ticks", "arrivals", "stops", "pauses", "restores", "oversized_skip
              "imbalance_max_blocks", "imbalance_last_blocks")
 
 
+LEDGER_KEYS = ("cost_decode", "cost_prefill", "cost_recompute", "cost_unused", "cost_caching",
+               "unused_bound_checks", "unused_bound_violations")
+
+
 class Stats(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in STAT_KEYS] + [
         ("L", C.c_uint64 * MAXR), ("hbm_used", C.c_uint64 * MAXR), ("host_used", C.c_uint64 * MAXR),
-        ("block_bytes", C.c_uint64)]
+        ("block_bytes", C.c_uint64)] + [(k, C.c_uint64) for k in LEDGER_KEYS]
 
 
 class TickInfo(C.Structure):
@@ -188,6 +193,8 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
         c.decay_q32[k] = v
     c.decode_tok_per_s = cfg["decode_tok_per_s"]
     c.compact_every = cfg.get("compact_every", 0)
+    c.prefill_chunk_tokens = cfg.get("prefill_chunk_tokens", 2048)   # STP ledger (NEXT-1)
+    c.prefill_chunk_ms = cfg.get("prefill_chunk_ms", 20)
     # TMA bulk copies are the default engine (measured faster or equal on every path);
     # pass flags=F_NO_BULK_DEFAULT to keep the 128-bit load/store engine
     if not flags & F_NO_BULK_DEFAULT:
@@ -341,7 +348,7 @@ class Pool:
     def stats(self) -> dict:
         s = Stats()
         self._chk(lib().ta_stats(self.ctx, C.byref(s)), "ta_stats")
-        out = {k: getattr(s, k) for k in STAT_KEYS}
+        out = {k: getattr(s, k) for k in STAT_KEYS + LEDGER_KEYS}
         out["L"] = list(s.L[:self.R])
         out["hbm_used"] = list(s.hbm_used[:self.R])
         out["host_used"] = list(s.host_used[:self.R])

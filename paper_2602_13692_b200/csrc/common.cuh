@@ -29,7 +29,10 @@ enum StatIdx {
   ST_TICKS = 0, ST_ARRIVALS, ST_STOPS, ST_PAUSES, ST_RESTORES, ST_OVERSIZED, ST_SHORTFALLS,
   ST_EVICT_BLOCKS, ST_EVICT_TO_HOST, ST_EVICT_DROPPED, ST_FETCH_BLOCKS, ST_P2P, ST_H2D,
   ST_RECOMPUTE, ST_NEW_BLOCKS, ST_COMPACT, ST_STALLS, ST_HIT, ST_PEER, ST_HOST, ST_MISS,
-  ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST, ST_N
+  ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST,
+  ST_BASE_N,                                   // counters before block_bytes in ta_stats_t
+  ST_COST_DECODE = ST_BASE_N, ST_COST_PREFILL, ST_COST_RECOMPUTE, ST_COST_UNUSED, ST_COST_CACHING,
+  ST_UNUSED_CHECKS, ST_UNUSED_VIOL, ST_N
 };
 
 // per-request descriptor kinds (step 5.5): copy from a peer's HBM, copy from a host
@@ -51,6 +54,7 @@ struct Ctr {                 // device-resident scalars of the context
   i32 verb_replica;
   i32 verb_ok;
   u32 t_d2h, t_h2d, t_p2p, t_d2d, t_fetch;   // this tick's block moves (telemetry)
+  u32 cmin;                  // smallest footprint (blocks) among PAUSED programs after step 4 (~0: none)
   ull ev_err;                // API mode: min over programs of (event index << 8 | code); ~0 = legal
   u32 ev_multi;              // API mode: events of programs with several events in the batch
 };
@@ -73,6 +77,7 @@ struct Dev {
   int rate;
   u32 flags;
   int compact_every;
+  int chunk_q, chunk_ms;           // STP ledger: prefill chunk tokens / ms per chunk
   i64 seg_bytes, block_bytes;
   int first_local, n_local;
   int api_mode;
@@ -177,6 +182,20 @@ __device__ __forceinline__ void grid_sync(const Dev& d, int k) {
     }
     __syncthreads();
   }
+}
+
+// STP staircase of a chunked prefill of n tokens over a resident base (
+// SPEC.md recompute_cost_of): sum_{i=1}^{ceil(n/q)} (base + min(i*q, n)), in closed form.
+__device__ __forceinline__ ull stp_stair(ull n, ull q, ull base) {
+  const ull m = (n + q - 1) / q, k = n / q;
+  return m * base + q * k * (k + 1) / 2 + (m > k ? n : 0);
+}
+
+// warp sum of a u64 (all lanes)
+__device__ __forceinline__ ull warp_sum_ull(ull v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
 }
 
 // Eviction flags of replica r's HBM blocks (the owner's copy in multi-process mode).

@@ -21,6 +21,8 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int verb) {
       atomicOr(&d.host_free[(size_t)h * d.NHW + (s >> 5)], 1u << (s & 31));
     }
   }
+  ull cach = 0;                          // NEXT-1: idle resident KV (token count)
+  u32 cmin = 0xFFFFFFFFu;                // smallest paused footprint (blocks)
   for (int p = t; p < d.N; p += stride) {
     u8 s = d.sat_new[p];
     if (s) {
@@ -31,6 +33,19 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int verb) {
       d.sat_new[p] = 0;
     } else if (!verb) {
       d.satisfied[p] = 0;
+      const u8 st = d.status[p];
+      if (st == TA_PAUSED || st == TA_ACTING) {
+        if (d.home[p] >= 0) cach += min((ull)d.n_hbm[p] * (ull)d.bt, (ull)d.c[p]);
+        if (st == TA_PAUSED) cmin = min(cmin, d.nb[p]);
+      }
+    }
+  }
+  if (!verb) {
+    cach = warp_sum_ull(cach);
+    cmin = __reduce_min_sync(FULL_MASK, cmin);
+    if (lane_id() == 0) {
+      if (cach) atomicAdd(&d.stats[ST_COST_CACHING], cach * (ull)d.dt);
+      if (cmin != 0xFFFFFFFFu) atomicMin(&d.ctr->cmin, cmin);
     }
   }
 }
@@ -159,6 +174,13 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(d.hbm_free[(size_t)r * d.NBW + w]);
     fr = cta_reduce<ull>(fr, s_red, [](ull a, ull b) { return a + b; }, 0ull);
     ull used = (ull)d.NB - fr;
+    if (!verb && threadIdx.x == 0 && d.ctr->cmin != 0xFFFFFFFFu) {   // programs wait in the queue
+      const ull cap = (ull)d.cap_max[r];
+      d.stats[ST_COST_UNUSED] += (cap > used ? cap - used : 0) * (ull)d.bt * (ull)d.dt;
+      d.stats[ST_UNUSED_CHECKS] += 1;
+      const ull idle = cap > d.L[r] ? cap - d.L[r] : 0;        // C_unused < c_min
+      if (idle >= d.ctr->cmin) d.stats[ST_UNUSED_VIOL] += 1;
+    }
     umax = used > umax ? used : umax;
     umin = used < umin ? used : umin;
   }
@@ -196,6 +218,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
   __syncthreads();
   PSTAMP(3, 8);
   if (threadIdx.x == 0) {
+    d.ctr->cmin = 0xFFFFFFFFu;
     d.ctr->stops = 0;
     d.ctr->restore_cnt = 0;
     d.ctr->n_arr = 0;

@@ -363,6 +363,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     // per-program values the request loop reads for each of its blocks, staged for
     // S_r programs when they fit: slot, first needed j, home, c_kv, c, uid
     const bool fst = m <= 2048;
+    ull l_dec = 0, l_pre = 0, l_rec = 0;             // NEXT-1 STP ledger (token-ms)
     // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
     for (u32 i = threadIdx.x; i < nF; i += CTA) {
       u32 p = fp[i];
@@ -392,6 +393,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         }
         rec.new_tok = c - ckv;
         rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
+        l_dec += (ull)c * (ull)d.dt;                    // holds c while decoding the interval
+        l_pre += (ull)d.chunk_ms * stp_stair(c - ckv, (ull)d.chunk_q, ckv);
+        l_rec += (ull)d.chunk_ms * stp_stair(rec.miss_tok, (ull)d.chunk_q, 0);
         pc[PC_HIT] += rec.hit_tok; pc[PC_PEER] += rec.peer_tok; pc[PC_HOST] += rec.host_tok;
         pc[PC_MISS] += rec.miss_tok; pc[PC_NEWTOK] += rec.new_tok;
         if (h == r && c > ckv && (ckv % bt) != 0) {    // partial last block already resident
@@ -413,6 +417,14 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       d.dec_fs[(size_t)r * N + i] = rec;
     }
     if (threadIdx.x == 0) sh.fst = fst;
+    if (!verb) {
+      l_dec = warp_sum_ull(l_dec); l_pre = warp_sum_ull(l_pre); l_rec = warp_sum_ull(l_rec);
+      if (lane_id() == 0) {
+        if (l_dec) atomicAdd(&d.stats[ST_COST_DECODE], l_dec);
+        if (l_pre) atomicAdd(&d.stats[ST_COST_PREFILL], l_pre);
+        if (l_rec) atomicAdd(&d.stats[ST_COST_RECOMPUTE], l_rec);
+      }
+    }
     PSTAMP(2, 10);
     if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
       d.pst[2 * 32 + 29] = nF | (1ull << 62);

@@ -114,6 +114,7 @@ static const char* validate(const ta_config* c) {
   if (c->lambda_min_q16 == 0 || c->lambda_min_q16 > c->lambda_max_q16 || c->lambda_max_q16 > 65536)
     return "watermarks must satisfy 0 < lambda_min <= lambda_max <= 1 (SPEC.md:190)";
   if (c->decode_tok_per_s < 0 || c->compact_every < 0 || c->max_trace_turns < 0) return "negative rate/compact/turns";
+  if (c->prefill_chunk_tokens < 1 || c->prefill_chunk_ms < 0) return "prefill_chunk_tokens must be >= 1, prefill_chunk_ms >= 0";
   return nullptr;
 }
 
@@ -201,7 +202,7 @@ __global__ void k_init(Dev d) {
       d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
     }
   }
-  if (t == 0) d.ctr->ev_err = ~0ull;
+  if (t == 0) { d.ctr->ev_err = ~0ull; d.ctr->cmin = 0xFFFFFFFFu; }
   for (int p = t; p < d.N; p += stride) {
     d.tool_return[p] = INT64_MAX;
     d.placement[p] = -1;
@@ -382,6 +383,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.NHW = (int)((d.NH + 31) / 32);
   d.dt = cfg->delta_t_ms; d.unit = cfg->decay_unit_ms; d.rate = cfg->decode_tok_per_s;
   d.flags = cfg->flags; d.compact_every = cfg->compact_every;
+  d.chunk_q = cfg->prefill_chunk_tokens;
+  d.chunk_ms = cfg->prefill_chunk_ms;
   d.seg_bytes = (i64)cfg->block_tokens * cfg->n_kv_heads * cfg->head_dim * cfg->elem_bytes;
   d.block_bytes = (i64)x->block_bytes;
   d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
@@ -580,7 +583,14 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
   CK(ctx, cudaMemcpy(L.data(), d.L, sizeof(ull) * d.R, cudaMemcpyDeviceToHost));
   CK(ctx, cudaMemcpy(hf.data(), d.hbm_free, sizeof(u32) * hf.size(), cudaMemcpyDeviceToHost));
   if (d.NHW) CK(ctx, cudaMemcpy(sf.data(), d.host_free, sizeof(u32) * (size_t)d.R * d.NHW, cudaMemcpyDeviceToHost));
-  memcpy(out, st.data(), sizeof(ull) * ST_N);
+  memcpy(out, st.data(), sizeof(ull) * ST_BASE_N);
+  out->cost_decode = st[ST_COST_DECODE];
+  out->cost_prefill = st[ST_COST_PREFILL];
+  out->cost_recompute = st[ST_COST_RECOMPUTE];
+  out->cost_unused = st[ST_COST_UNUSED];
+  out->cost_caching = st[ST_COST_CACHING];
+  out->unused_bound_checks = st[ST_UNUSED_CHECKS];
+  out->unused_bound_violations = st[ST_UNUSED_VIOL];
   for (int r = 0; r < d.R; ++r) {
     out->L[r] = L[r];
     u64 f = 0, g = 0;
