@@ -78,6 +78,18 @@ def test_gpu_stress_block_major_layout_and_bt1():
     run_parity(stress(22, 2, NB=600, NH=200, block_tokens=1, compact=5), 120, state_every=5)
 
 
+@pytest.mark.parametrize("dt,x,lam", [(1000, 1, 65536), (2500, 4, 65536), (10000, 8, 60000),
+                                       (5000, 2, 52000)])
+def test_gpu_policy_parameters(dt, x, lam):
+    """The ablation axes (NEXT-2): detection period Delta t, decay base
+    x of f(t) = x^-t (x = 1: no decay, eq. 6), and lambda_max < 1 (a watermark band:
+    lambda_min = lambda_max - 4096)."""
+    cfg = stress(40 + x, 2, NB=64, delta_t_ms=dt, decay_x=x, lambda_max_q16=lam,
+                 lambda_min_q16=lam - (4096 if lam < 65536 else 0))
+    o, n = run_parity(cfg, 200, seed=x)
+    assert n > 0
+
+
 def test_gpu_no_graph_and_timing_modes():
     from paper_2602_13692_b200 import binding
     run_parity(stress(31, 2), 80, flags=binding.F_NO_GRAPH)
