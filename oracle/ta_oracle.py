@@ -107,6 +107,9 @@ class Oracle:
         self.lmax = int(cfg["lambda_max_q16"])
         self.lmin = int(cfg["lambda_min_q16"])
         self.compact_every = int(cfg.get("compact_every", 0))
+        # NEXT-2 baseline (SPEC.md BaselinePolicy.PinnedRouting; "sends all
+        # requests from the same agentic workflow to the same node"): no global queue
+        self.pinned = bool(cfg.get("pinned_routing", False))
         self.chunk_q = int(cfg.get("prefill_chunk_tokens", 2048))   # chunked-prefill tokens per step
         self.chunk_ms = int(cfg.get("prefill_chunk_ms", 20))        # time of one chunk step
         self.api_mode = api_mode
@@ -367,6 +370,9 @@ class Oracle:
         Q = [p for p in range(self.N) if self.status[p] == PAUSED]
         Q.sort(key=lambda p: self.restore_key(p, nb[p]))
         self.queue_order = list(Q)
+        if self.pinned:
+            self._step4_pinned(Q, out)
+            return
         maxcap = max(self.cap_max)
         for p in Q:
             cr = contrib[p]
@@ -378,6 +384,33 @@ class Oracle:
             if not cand:
                 break
             t = min(cand, key=lambda r: (self.L[r], 0 if r == self.home[p] else 1, r))
+            self.status[p] = REASONING if self.phase[p] == PHASE_R else ACTING
+            self.placement[p] = t
+            self.L[t] += cr
+            self.stats["restores"] += 1
+            out.append(decision(D_RESTORE, p, src=self.home[p], dst=t))
+
+    def _step4_pinned(self, Q: list, out: list):
+        """PinnedRouting baseline (reading A45): program p is bound to replica p mod R for
+        its lifetime; each replica restores from its own queue (the global S_restore
+        order restricted to its programs) while the head fits there (same watermark
+        test) and stops at its first head that does not; programs that can never fit
+        their replica are skipped.  Decisions in global queue order."""
+        contrib = self.contrib
+        stopped = [False] * self.R
+        for p in Q:
+            t = p % self.R
+            if stopped[t]:
+                continue
+            cr = contrib[p]
+            if cr > self.cap_max[t]:
+                self.stats["oversized_skips"] += 1
+                continue
+            if not (self.L[t] < self.cap_min[t] and self.L[t] + cr <= self.cap_max[t]):
+                stopped[t] = True
+                if all(stopped):
+                    break
+                continue
             self.status[p] = REASONING if self.phase[p] == PHASE_R else ACTING
             self.placement[p] = t
             self.L[t] += cr

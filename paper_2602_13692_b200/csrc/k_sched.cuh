@@ -133,6 +133,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     __syncthreads();
   }
   u32 cnt = 0, over = 0, it = 0;
+  u32 stopped = 0;                      // PinnedRouting: replicas whose queue stopped (warp 0)
   // queue buckets: rb[] / rhist[] from the footprint pass, plus this tick's pauses
   // (k_pause) and arrivals (above), so no pass over the slots is needed to size a chunk
   u32 lo = 0, chunk = RESTORE_CHUNK0;
@@ -152,6 +153,8 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     if (it < 7) PSTAMP(1, 3 + 4 * it);
     if (w0) {
       bool stop = false;
+      const bool pinned = (d.flags & TA_F_PINNED_ROUTING) != 0;
+      const u32 all_r = R >= 32 ? 0xFFFFFFFFu : ((1u << R) - 1);
       for (u32 base = 0; base < n && !stop; base += 32) {
         u32 i = base + lane;
         u32 pl = i < n ? q[i] : 0;
@@ -161,12 +164,25 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
         u32 mcount = min(32u, n - base);
         for (u32 jj = 0; jj < mcount; ++jj) {
           u32 cr = __shfl_sync(FULL_MASK, crl, jj);
-          if (cr > maxcap) { ++over; continue; }       // can never fit (reading A9)
-          bool fits = lane < (u32)R && Lr < cmin && Lr + cr <= cmax;
-          if (__ballot_sync(FULL_MASK, fits) == 0) { stop = true; break; }
-          int hm = __shfl_sync(FULL_MASK, hml, jj);
-          u32 key = fits ? (((u32)Lr << 6) | ((u32)((int)lane != hm) << 5) | lane) : 0xFFFFFFFFu;
-          u32 t = __reduce_min_sync(FULL_MASK, key) & 31;
+          u32 t;
+          if (pinned) {                           // PinnedRouting baseline (reading A45)
+            t = __shfl_sync(FULL_MASK, pl, jj) % (u32)R;
+            if ((stopped >> t) & 1u) continue;    // that replica's queue has stopped
+            if (cr > __shfl_sync(FULL_MASK, cmax, t)) { ++over; continue; }
+            const bool fits = lane == t && Lr < cmin && Lr + cr <= cmax;
+            if (__ballot_sync(FULL_MASK, fits) == 0) {
+              stopped |= 1u << t;
+              if (stopped == all_r) { stop = true; break; }
+              continue;
+            }
+          } else {
+            if (cr > maxcap) { ++over; continue; }       // can never fit (reading A9)
+            bool fits = lane < (u32)R && Lr < cmin && Lr + cr <= cmax;
+            if (__ballot_sync(FULL_MASK, fits) == 0) { stop = true; break; }
+            int hm = __shfl_sync(FULL_MASK, hml, jj);
+            u32 key = fits ? (((u32)Lr << 6) | ((u32)((int)lane != hm) << 5) | lane) : 0xFFFFFFFFu;
+            t = __reduce_min_sync(FULL_MASK, key) & 31;
+          }
           if (lane == t) Lr += cr;
           if (lane == jj) {                       // the lane that holds the entry writes it
             d.status[pl] = phl == TA_PHASE_A ? TA_ACTING : TA_REASONING;

@@ -90,6 +90,13 @@ def test_gpu_policy_parameters(dt, x, lam):
     assert n > 0
 
 
+@pytest.mark.parametrize("R", [2, 3])
+def test_gpu_pinned_routing_baseline(R):
+    """NEXT-2 baseline: per-replica queues (TA_F_PINNED_ROUTING) against the oracle."""
+    o, n = run_parity(stress(50 + R, R, NB=56, pinned_routing=True), 200, seed=R)
+    assert n > 0 and o.stats["restores"] > 0
+
+
 def test_gpu_no_graph_and_timing_modes():
     from paper_2602_13692_b200 import binding
     run_parity(stress(31, 2), 80, flags=binding.F_NO_GRAPH)

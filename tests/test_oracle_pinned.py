@@ -1,0 +1,54 @@
+"""NEXT-2 baseline pins: PinnedRouting (SPEC.md BaselinePolicy; "sends
+all requests from the same agentic workflow to the same node"; reading A45): per-replica
+queues instead of the global program-aware queue."""
+import random
+
+import oracle
+import tracegen
+from tests.helpers import base_cfg, flat_trace, set_program
+
+
+def test_pinned_leaves_a_replica_idle_hand_computed():
+    """R = 2, 10 blocks each (bt = 1); paused slots 0, 2, 4 (all pinned to r0, 6 tokens
+    each), r1 empty.  Global queue: slot 0 -> r0, slot 2 -> r1 (least loaded), slot 4
+    fits nowhere.  Pinned: slot 0 -> r0, slot 2 does not fit r0 -> r0's queue stops; r1
+    has no programs of its own and stays idle (Fig. 2a imbalance)."""
+    def build(pinned):
+        o = oracle.Oracle(base_cfg(n_replicas=2, hbm_blocks=10, pinned_routing=pinned), flat_trace(5))
+        for p in (0, 2, 4):
+            set_program(o, p, oracle.PAUSED, oracle.PHASE_R, 6, c_kv=0, paused_since=0)
+        o.next_arrival = 5
+        o.tick = 1
+        return o
+    g, pn = build(False), build(True)
+    _, dg = g.sched_step()
+    _, dp = pn.sched_step()
+    assert [(d[1], d[3]) for d in dg if d[0] == oracle.D_RESTORE] == [(0, 0), (2, 1)]
+    assert [(d[1], d[3]) for d in dp if d[0] == oracle.D_RESTORE] == [(0, 0)]
+    assert g.stats["imbalance_last_blocks"] == 0 and pn.stats["imbalance_last_blocks"] == 6
+
+
+def test_pinned_equals_global_with_one_replica():
+    cfg = tracegen.get_config("c1_toy", n_replicas=1, hbm_blocks=80, host_blocks=16,
+                              trace=dict(n=24, n_initial=10, seed=77))
+    tr = tracegen.make_trace(cfg)
+    a, b = oracle.Oracle(cfg, tr), oracle.Oracle(dict(cfg, pinned_routing=True), tr)
+    for _ in range(120):
+        assert a.sched_step() == b.sched_step()
+
+
+def test_pinned_random_traces_stay_on_their_replica():
+    for seed in range(3):
+        cfg = tracegen.get_config("c1_toy", n_replicas=3, hbm_blocks=48, host_blocks=16, pinned_routing=True,
+                                  trace=dict(n=24, n_initial=12, seed=400 + seed))
+        o = oracle.Oracle(cfg, tracegen.make_trace(cfg))
+        rng = random.Random(seed)
+        for _ in range(100):
+            st, ds = o.sched_step()
+            assert st == oracle.OK
+            o.check_invariants()
+            for p in range(o.N):
+                if o.placement[p] >= 0:
+                    assert o.placement[p] == p % 3
+            if rng.random() < 0.1:
+                o.check_watermark()
