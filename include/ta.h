@@ -279,9 +279,11 @@ ta_status ta_last_tick(ta_ctx* ctx, ta_tick_info* out);
 ta_status ta_set_copy_bulk(ta_ctx* ctx, int32_t on);
 
 /* Per-phase device times of the last tick in microseconds (TA_F_TIMING only):
- * [0] ingest+footprint [1] pause+restore [2] plan [3] D2H evict copies
- * [4] fetch copies (P2P/H2D) [5] fills [6] finalize+compaction plan
- * [7] compaction copies [8] decision assembly.  n <= 9. */
+ * [0] ingest + footprint (API mode: event kernels + footprint) [1] pause + restore
+ * [2] materialize plan [3] movement (one process: the fused kernel; one process per
+ * GPU, TA_F_NO_FUSE: D2H evictions + barrier) [4] fetch copies + push + barrier
+ * (TA_F_NO_FUSE only) [5] fills (multi-process with TA_F_FILL) [6] finalize +
+ * compaction plan + decision assembly [7] compaction copies [8] unused.  n <= 9. */
 ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
 
 /* Developer aid (TA_F_TIMING only): raw SM-clock stamps (clock64) taken by thread 0

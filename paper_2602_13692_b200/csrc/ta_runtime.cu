@@ -280,8 +280,12 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     k_tick_front<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);   // ingest + footprint + load
   }
   rec(x, 1);
-  k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
-  k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
+  if (getenv("TA_SPLIT_PR")) {             // A/B aid: the two passes as separate kernels
+    k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
+    k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
+  } else {
+    launch_coop(k_pause_restore, R, PLAN_DSMEM, s, (Dev)d);
+  }
   rec(x, 2);
   k_plan<<<R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 0);   // one CTA cluster per replica
   rec(x, 3);
@@ -462,6 +466,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   // planner kernels: small sorts and staged lists in dynamic shared memory
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ev_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);

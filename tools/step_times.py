@@ -38,7 +38,7 @@ for k in range(ticks):
     d2h = st["evict_to_host"] - prev["evict_to_host"]
     h2d = st["h2d_blocks"] - prev["h2d_blocks"]
     prev = st
-    print(f"tick {k:3d} dev {e0.elapsed_time(e1):9.2f} ms host {1e3 * (t1 - t0):9.2f} ms  "
+    print(f"tick {k:3d} dev {e0.elapsed_time(e1):9.4f} ms host {1e3 * (t1 - t0):9.3f} ms  "
           f"move {ph[3] / 1e3:8.2f} ms  d2h {d2h:5d} h2d {h2d:5d} blocks  sched {sum(ph) / 1e3 - ph[3] / 1e3:6.3f} ms",
           flush=True)
     if "--phases" in sys.argv:
