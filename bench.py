@@ -204,7 +204,7 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
             "mean_us": round(float(us.mean()), 1), "ticks": f"{start}..{start + n_ticks - 1}",
             "programs": tr.n_slots, "target_us": 100,
             "kv": "mini (4 KiB blocks; decisions identical to the Q32 run, movement kernels run but move ~0 B)",
-            "note": "one full ta_sched_step CUDA graph (6 kernels), L2 flushed before each tick"}
+            "note": "one full ta_sched_step CUDA graph (5 kernels), L2 flushed before each tick"}
 
 
 def workload(name, world):
@@ -503,18 +503,18 @@ def main():
         achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
         peak, bound, psrc = hbm_peak, "hbm", peak_src
     # traffic: DRAM bytes per launch, from the committed ncu --set full capture of the same
-    # kernel (profiles/r1b_move_traffic.json: measured DRAM / algorithmic bytes of one
+    # kernel (profiles/r1d_move_traffic.json: measured DRAM / algorithmic bytes of two
     # launch) applied to this run's algorithmic bytes per launch
     traffic = None
     if dom == 3 and world == 1:          # the captured kernel is the single-process fused one
         try:
-            with open(os.path.join(ROOT, "profiles", "r1b_move_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r1d_move_traffic.json")) as f:
                 traffic = round(byts[3] * json.load(f)["ratio_dram_to_algorithmic"])
         except (OSError, KeyError, ValueError):
             traffic = None
     roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
                 "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
-                "traffic_source": "ncu --set full capture (profiles/r1b_move_traffic.json) ratio x algorithmic bytes",
+                "traffic_source": "ncu --set full capture (profiles/r1d_move_traffic.json) ratio x algorithmic bytes",
                 "share_of_step": round(float(ph[dom] / ph.sum()), 4), "peak_source": psrc}
     kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
     if world > 1:
@@ -548,10 +548,10 @@ def main():
                 "d2h_bytes_per_step": int(d2h / args.steps), "events_per_step": round(n_events / args.steps, 1),
                 "note": "API mode (serving-engine path): per step the tick's event batch H2D from host memory, "
                         "validation + apply + tick on the device, decisions D2H; same ticks as value"},
-        # per tick: tick_front, pause, restore, plan (one launch of R 8-CTA clusters), movement
-        # (1 fused kernel; multi-GPU: barrier, fused kernel, barrier), close
+        # per tick: tick_front, pause+restore (cooperative), plan (one launch of R 8-CTA
+        # clusters), movement (1 fused kernel; multi-GPU: barrier, fused kernel, barrier), close
         # (compaction copies only when compaction is configured; off in this workload)
-        "gpu_launches": args.steps * (6 if world == 1 else 8),
+        "gpu_launches": args.steps * (5 if world == 1 else 7),
         "roofline": roofline,
         "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
         "sched_us_per_tick": round(sched_us, 1),
