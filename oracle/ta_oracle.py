@@ -103,7 +103,9 @@ class Oracle:
         self.dt = int(cfg["delta_t_ms"])
         self.unit = int(cfg["decay_unit_ms"])
         self.rate = int(cfg["decode_tok_per_s"])
-        self.F = decay_table(int(cfg["decay_x"]))
+        # f(t) as a Q32 table: x^-t, or an explicit table (e.g. the TTL-pin
+        # baseline's step function, NEXT-2 reading A47)
+        self.F = list(cfg["decay_table"]) if cfg.get("decay_table") else decay_table(int(cfg["decay_x"]))
         self.lmax = int(cfg["lambda_max_q16"])
         self.lmin = int(cfg["lambda_min_q16"])
         self.compact_every = int(cfg.get("compact_every", 0))

@@ -189,7 +189,8 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
     c.decay_unit_ms = cfg["decay_unit_ms"]
     c.lambda_max_q16 = cfg["lambda_max_q16"]
     c.lambda_min_q16 = cfg["lambda_min_q16"]
-    for k, v in enumerate(decay_q32(cfg["decay_x"])):
+    table = cfg.get("decay_table") or decay_q32(cfg["decay_x"])
+    for k, v in enumerate(table):
         c.decay_q32[k] = v
     c.decode_tok_per_s = cfg["decode_tok_per_s"]
     c.compact_every = cfg.get("compact_every", 0)

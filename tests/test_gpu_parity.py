@@ -90,6 +90,13 @@ def test_gpu_policy_parameters(dt, x, lam):
     assert n > 0
 
 
+def test_gpu_ttl_pin_baseline():
+    """NEXT-2 baseline: TTL-pin decay table (step function) against the oracle."""
+    from tracegen.configs import ttl_pin_table
+    o, n = run_parity(stress(60, 2, NB=56, decay_table=ttl_pin_table(3)), 200, seed=60)
+    assert n > 0
+
+
 @pytest.mark.parametrize("R", [2, 3])
 def test_gpu_pinned_routing_baseline(R):
     """NEXT-2 baseline: per-replica queues (TA_F_PINNED_ROUTING) against the oracle."""

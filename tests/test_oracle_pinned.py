@@ -52,3 +52,21 @@ def test_pinned_random_traces_stay_on_their_replica():
                     assert o.placement[p] == p % 3
             if rng.random() < 0.1:
                 o.check_watermark()
+
+
+def test_ttl_pin_table_step_contribution():
+    """TTL-pin baseline (reading A47): f(t) = 1 for t < TTL, 0 after: an acting program of
+    10 blocks (bt = 1) contributes 10 before its TTL of 3 s and 0 after (vs 10 >> k for
+    the paper's 2^-t)."""
+    from tracegen.configs import ttl_pin_table
+    o = oracle.Oracle(base_cfg(hbm_blocks=100, decay_table=ttl_pin_table(3)), flat_trace(1, d_ms=10 ** 9))
+    set_program(o, 0, oracle.ACTING, oracle.PHASE_A, 10, placement=0, home=0, acting_since=0,
+                tool_return=10 ** 12, hbm=range(10))
+    o.next_arrival = 1
+    o.tick = 0
+    seen = []
+    for _ in range(3):                         # T = 0, 5000, 10000 ms -> k = 0, 5, 10
+        o.sched_step()
+        seen.append(o.L[0])
+    assert seen == [10, 0, 0]
+    assert o.contrib_at(0, 2999, 10) == 10 and o.contrib_at(0, 3000, 10) == 0

@@ -61,6 +61,14 @@ def sweep_config(n_programs: int, gpus: int, block_tokens: int, point: int) -> d
                 hbm_blocks=(96 << 30) // blk_bytes, host_blocks=0, max_ctx=65536, tick_cap=2000)
 
 
+def ttl_pin_table(ttl_units: int) -> list:
+    """TTL-pin baseline's f(t) (NEXT-2; SPEC.md BaselinePolicy.TtlPin; PAPER.md:2.2 "employs a
+    time-to-live (TTL) mechanism to pin KV caches"): an acting program's KV counts in full
+    for ttl_units decay units after its tool call, then not at all.  A parameter table
+    (Q32, 64 entries), like the decay base x; the policy arithmetic stays on each side."""
+    return [(1 << 32) if k < ttl_units else 0 for k in range(64)]
+
+
 def get_config(name: str, **override) -> dict:
     cfg = copy.deepcopy(CONFIGS[name])
     tr = override.pop("trace", None)
