@@ -12,14 +12,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("verbs", [False, True])
-def test_two_gpu_parity(verbs):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    n = 2
+@pytest.mark.parametrize("n,mode", [(2, "trace"), (2, "verbs"), (2, "api"), (4, "trace"), (4, "api")])
+def test_multi_gpu_parity(n, mode):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    port = 29530 + {"trace": 1, "verbs": 3, "api": 5}[mode] + 10 * n
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533" if verbs else "29531",
-           os.path.join(ROOT, "tools", "mgpu_parity.py"), "120"] + (["--verbs"] if verbs else [])
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tools", "mgpu_parity.py"), "120"] + ({"trace": [], "verbs": ["--verbs"],
+                                                                    "api": ["--api"]}[mode])
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(": OK") == n

@@ -1,9 +1,11 @@
 """Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
 
-torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs]
+torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs] [--api]
 Every rank runs the replicated control plane for all N replicas and moves only its
 own replica's bytes; every rank compares its decisions and full state with its own
-oracle copy, and verifies the KV content of its local pool.  Exit code 0 = parity."""
+oracle copy, and verifies the KV content of its local pool.  --api: the same ticks in
+API mode (the engine's recorded events, tools/api_events.py) against the trace-mode
+oracle.  Exit code 0 = parity."""
 import os
 import random
 import sys
@@ -31,19 +33,29 @@ def main():
                               trace=dict(n=12 * world, n_initial=5 * world, seed=77))
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
-    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, replicas_here=1, first_replica=rank, device=local)
+    api = "--api" in sys.argv
+    batches = None
+    if api:   # the engine's events of this trace, recorded on this rank's GPU (all replicas local)
+        from tools.api_events import record
+        rc = dict(cfg)
+        rc["kv"] = "mini"
+        batches, _ = record(rc, tr, ticks, device=local)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, replicas_here=1, first_replica=rank, device=local,
+                trace_mode=not api)
     peers = connect(pool)
-    pool.load_trace(tr)
+    if not api:
+        pool.load_trace(tr)
     rng = random.Random(5)
     n_dec = n_p2p = n_verbs = 0
     for k in range(ticks):
         _, want = o.sched_step()
-        st, got = pool.step()
+        st, got = pool.step(k * cfg["delta_t_ms"], batches[k]) if api else pool.step()
         assert st == 0, f"rank {rank} tick {k}: status {st}"
         got = dec_tuples(got)
         assert got == want, f"rank {rank} tick {k}: decisions differ"
         n_dec += len(got)
-        compare_state(o, pool.debug_download(), where=f"rank {rank} tick {k}")
+        if not api:                        # API mode keeps no tool_return: decisions + bytes only
+            compare_state(o, pool.debug_download(), where=f"rank {rank} tick {k}")
         bad, seen = pool.verify_content()
         assert bad == 0, f"rank {rank} tick {k}: {bad} of {seen} local KV words wrong"
         if verbs and k % 3 == 1:          # collective verbs: same call on every rank
