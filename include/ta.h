@@ -77,8 +77,11 @@ enum {
   TA_F_TIMING = 1u << 3,       /* record per-phase CUDA events (graph event-record nodes) */
   TA_F_COPY_BULK = 1u << 4,    /* HBM->HBM copies via cp.async.bulk (TMA) instead of LDG/STG.128 */
   TA_F_NO_FUSE = 1u << 5,      /* single process: separate evict / fetch / fill kernels (A/B aid) */
-  TA_F_PINNED_ROUTING = 1u << 6 /* baseline (NEXT-2): program p bound to replica p mod R, per-replica
+  TA_F_PINNED_ROUTING = 1u << 6, /* baseline (NEXT-2): program p bound to replica p mod R, per-replica
                                   queues instead of the global queue (reading A45) */
+  TA_F_REQUEST_AWARE = 1u << 7  /* baseline (NEXT-2): stateless request-level engine -- running
+                                  requests preempted latest program first, FCFS waiting queue, LRU
+                                  eviction of idle caches; pass an all-zero decay table (A46) */
 };
 
 typedef struct {

@@ -106,6 +106,10 @@ class Oracle:
         # f(t) as a Q32 table: x^-t, or an explicit table (e.g. the TTL-pin
         # baseline's step function, NEXT-2 reading A47)
         self.F = list(cfg["decay_table"]) if cfg.get("decay_table") else decay_table(int(cfg["decay_x"]))
+        # NEXT-2 baseline RequestAware (reading A46): a stateless engine, no program view
+        self.request_aware = bool(cfg.get("request_aware", False))
+        if self.request_aware:
+            self.F = [0] * 64                  # a program in a tool call holds no request
         self.lmax = int(cfg["lambda_max_q16"])
         self.lmin = int(cfg["lambda_min_q16"])
         self.compact_every = int(cfg.get("compact_every", 0))
@@ -176,12 +180,17 @@ class Oracle:
 
     def restore_key(self, p: int, nb: int):
         """S_restore = 1/c + I(tau=R) (PAPER.md:400-401): R first, shortest first;
-        ties: earlier paused_since, then slot (A8)."""
+        ties: earlier paused_since, then slot (A8).  RequestAware: FCFS (A46)."""
+        if self.request_aware:
+            return (0, 0, self.paused_since[p], p)
         return (0 if self.phase[p] == PHASE_R else 1, nb, self.paused_since[p], p)
 
     def pause_key(self, p: int, nb: int):
         """S_pause = 1/c + I(tau=A) (PAPER.md:403-406): A first, shortest first;
-        ties: later acting_since first (phase A only), then slot (A7)."""
+        ties: later acting_since first (phase A only), then slot (A7).  RequestAware:
+        running requests, the latest program first (recompute preemption, A46)."""
+        if self.request_aware:
+            return (1 if self.phase[p] == PHASE_A else 0, -p, 0, 0)
         if self.phase[p] == PHASE_A:
             return (0, nb, -self.acting_since[p], p)
         return (1, nb, 0, p)
@@ -433,6 +442,9 @@ class Oracle:
         nb, n_hbm, contrib = self.fp["nb"], self.fp["n_hbm"], self.contrib
         E = [p for p in range(self.N) if self.home[p] == r and n_hbm[p] > 0
              and self.status[p] in (PAUSED, ACTING)]
+        if self.request_aware:                 # LRU over idle caches, not program-aware (A46)
+            return sorted(E, key=lambda p: (self.paused_since[p] * self.dt if self.status[p] == PAUSED
+                                            else self.acting_since[p], p))
         g0 = sorted([p for p in E if self.status[p] == PAUSED],
                     key=lambda p: self.restore_key(p, nb[p]), reverse=True)
         g1 = sorted([p for p in E if self.status[p] == ACTING and self.placement[p] != r],

@@ -19,6 +19,7 @@ HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 TA_OK, TA_E_INVAL, TA_E_NOMEM, TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM = 0, 1, 2, 3, 4
 TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA_E_STATE = 5, 6, 7, 8, 9, 10
 F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE, F_PINNED_ROUTING = 1, 2, 4, 8, 16, 32, 64
+F_REQUEST_AWARE = 128
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",
@@ -190,6 +191,9 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
     c.lambda_max_q16 = cfg["lambda_max_q16"]
     c.lambda_min_q16 = cfg["lambda_min_q16"]
     table = cfg.get("decay_table") or decay_q32(cfg["decay_x"])
+    if cfg.get("request_aware", False):              # baseline: no program view (reading A46)
+        flags |= F_REQUEST_AWARE
+        table = [0] * 64
     for k, v in enumerate(table):
         c.decay_q32[k] = v
     c.decode_tok_per_s = cfg["decode_tok_per_s"]

@@ -244,6 +244,7 @@ __device__ __forceinline__ i64 trace_arrivals(const Dev& d) {
 
 // Coarse restore bucket (monotone in the S_restore key): tau = R first, then nb.
 __device__ __forceinline__ u32 restore_bucket(const Dev& d, u8 ph, u32 nbv) {
+  if (d.flags & TA_F_REQUEST_AWARE) return 0;        // FCFS key: one bucket
   return (u32)(ph == TA_PHASE_A) * d.nbk + (nbv >> d.nb_shift);
 }
 

@@ -181,7 +181,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         u8 s = d.status[i];
         return s == TA_PAUSED || s == TA_ACTING;
       };
+      const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware: LRU (A46)
       auto ebucket = [&](int i) -> u32 {
+        if (ra) return 0u;
         if (d.status[i] == TA_PAUSED)    // group 0: A first, nb descending
           return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> shf));
         return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> shf);
@@ -195,7 +197,12 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       const u32 ne = cta_list_gather(el, nel, &s_cnt2,
           [&](int i) { return epred(i) && ebucket(i) <= T; },
           [&](u32 pos, int i) {
-            if (d.status[i] == TA_PAUSED) {
+            if (ra) {                    // idle since (ms), least recent first; ties slot-up
+              const u64 idle = d.status[i] == TA_PAUSED ? (u64)d.paused_since[i] * (u64)d.dt
+                                                        : (u64)d.acting_since[i];
+              ka[pos] = (1ull << 62) | idle;
+              va[pos] = (u32)i;
+            } else if (d.status[i] == TA_PAUSED) {
               u64 rk = ((u64)(d.phase[i] == TA_PHASE_A) << 55) | ((u64)d.nb[i] << 32) | d.paused_since[i];
               ka[pos] = ((1ull << 56) - 1) - rk;
               va[pos] = (u32)(N - 1 - i);

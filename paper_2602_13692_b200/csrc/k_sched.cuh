@@ -40,13 +40,15 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
   __shared__ u32 s_cnt;
   const u32* al = d.act_list + (size_t)r * N;
   const int na = (int)d.act_cnt[r];
-  auto bucket = [&](int i) { return (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
+  const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware baseline (A46)
+  auto bucket = [&](int i) { return ra ? 0u : (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
   const u32 T = cta_list_threshold(al, na, 2 * NBK, 0, dC, s_big, s_tmp, [](int) { return true; }, bucket,
                                    [&](int i) { return d.contrib[i]; });
   u32 n = cta_list_gather(al, na, &s_cnt,
       [&](int i) { return bucket(i) <= T; },
       [&](u32 pos, int i) {
-        ka[pos] = pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
+        ka[pos] = ra ? (((u64)(d.phase[i] == TA_PHASE_A) << 63) | (u64)(0xFFFFFFFFu - (u32)i))
+                     : pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
         va[pos] = (u32)i;
       });
   int res = cta_sort_kv(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
@@ -143,7 +145,8 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     u32 n = cta_ordered_gather(N, s_tmp,
         [&](int i) { const u32 b = d.rb[i]; return b >= lo && b <= T; },
         [&](u32 pos, int i) {
-          ka[pos] = restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
+          ka[pos] = (d.flags & TA_F_REQUEST_AWARE) ? (u64)d.paused_since[i]            // FCFS (A46)
+                                                   : restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
           va[pos] = (u32)i;
         });
     if (it < 7) PSTAMP(1, 2 + 4 * it);

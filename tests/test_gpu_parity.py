@@ -97,6 +97,13 @@ def test_gpu_ttl_pin_baseline():
     assert n > 0
 
 
+@pytest.mark.parametrize("R", [1, 3])
+def test_gpu_request_aware_baseline(R):
+    """NEXT-2 baseline: stateless request-level policy (TA_F_REQUEST_AWARE) vs the oracle."""
+    o, n = run_parity(stress(70 + R, R, NB=56 if R > 1 else 80, request_aware=True), 200, seed=R)
+    assert n > 0 and o.stats["pauses"] > 0
+
+
 @pytest.mark.parametrize("R", [2, 3])
 def test_gpu_pinned_routing_baseline(R):
     """NEXT-2 baseline: per-replica queues (TA_F_PINNED_ROUTING) against the oracle."""

@@ -70,3 +70,50 @@ def test_ttl_pin_table_step_contribution():
         seen.append(o.L[0])
     assert seen == [10, 0, 0]
     assert o.contrib_at(0, 2999, 10) == 10 and o.contrib_at(0, 3000, 10) == 0
+
+
+def test_request_aware_orders_hand_computed():
+    """RequestAware baseline (reading A46): a stateless request-level engine.  Over
+    capacity it preempts the latest running program (not the shortest or the acting
+    one); acting programs hold no request (load 0); the waiting queue is FCFS; idle
+    caches are evicted least-recently-used first, whatever their size or phase."""
+    # over capacity: REASONING slots 0 (12 blocks) and 2 (10 blocks) on 20 blocks -> the
+    # latest program (slot 2) is preempted
+    cfg = base_cfg(hbm_blocks=20, request_aware=True)
+    o = oracle.Oracle(cfg, flat_trace(5, g=1000, d_ms=10 ** 9))
+    set_program(o, 0, oracle.REASONING, oracle.PHASE_R, 12, placement=0, home=0, satisfied=1, hbm=range(12))
+    set_program(o, 2, oracle.REASONING, oracle.PHASE_R, 10, placement=0, home=0, satisfied=1, hbm=())
+    o.next_arrival = 5
+    o.tick = 3
+    st, ds = o.sched_step()
+    assert [d[1] for d in ds if d[0] == oracle.D_PAUSE] == [2]
+    # an acting program weighs nothing: 12 + 6 blocks resident, load 12, nothing paused
+    o2 = oracle.Oracle(base_cfg(hbm_blocks=20, request_aware=True), flat_trace(5, g=1000, d_ms=10 ** 9))
+    set_program(o2, 0, oracle.REASONING, oracle.PHASE_R, 12, placement=0, home=0, satisfied=1, hbm=range(12))
+    set_program(o2, 1, oracle.ACTING, oracle.PHASE_A, 6, placement=0, home=0, acting_since=14000,
+                tool_return=10 ** 12, hbm=range(12, 18))
+    o2.next_arrival = 5
+    o2.tick = 3
+    o2.sched_step()
+    assert o2.L[0] == 12 and o2.status[1] == oracle.ACTING
+    # FCFS queue: slot 4 (paused at tick 0, 9 blocks) before slot 3 (tick 1, 2 blocks);
+    # the 2-block program then no longer fits 10 blocks and the queue stops
+    o3 = oracle.Oracle(base_cfg(hbm_blocks=10, request_aware=True), flat_trace(5, g=1000, d_ms=10 ** 9))
+    set_program(o3, 3, oracle.PAUSED, oracle.PHASE_R, 2, c_kv=0, paused_since=1)
+    set_program(o3, 4, oracle.PAUSED, oracle.PHASE_R, 9, c_kv=0, paused_since=0)
+    o3.next_arrival = 5
+    o3.tick = 3
+    _, ds = o3.sched_step()
+    assert [d[1] for d in ds if d[0] == oracle.D_RESTORE] == [4]
+    # LRU eviction: two idle caches on r0, the older one goes first regardless of size
+    o4 = oracle.Oracle(base_cfg(hbm_blocks=10, request_aware=True), flat_trace(5, g=1000, d_ms=10 ** 9))
+    set_program(o4, 0, oracle.ACTING, oracle.PHASE_A, 3, placement=0, home=0, acting_since=9000,
+                tool_return=10 ** 12, hbm=range(0, 3))
+    set_program(o4, 1, oracle.ACTING, oracle.PHASE_A, 5, placement=0, home=0, acting_since=4000,
+                tool_return=10 ** 12, hbm=range(3, 8))
+    set_program(o4, 2, oracle.PAUSED, oracle.PHASE_R, 4, c_kv=0, paused_since=0)
+    o4.next_arrival = 5
+    o4.tick = 2
+    _, ds = o4.sched_step()
+    ev = [(d[1], d[4]) for d in ds if d[0] == oracle.D_EVICT]
+    assert ev == [(1, 2)]                      # need 4, 2 free: evict 2 blocks of the older cache (slot 1)

@@ -6,6 +6,7 @@ usage: python tools/baseline_compare.py [--programs 256] [--sim-s 2400] [--seeds
 
 Policies (same kernels; parity of each vs the oracle in tests/test_gpu_parity.py):
   program_aware  f(t) = 2^-t
+  request_aware  stateless request-level engine (latest-first preemption, FCFS, LRU; A46)
   ttl_pin_p50    f = 1 for t < 2 s (the ToolOrchestra tool-latency median), 0 after
   ttl_pin_p95    f = 1 for t < 33 s (the p95: pins long)
   no_decay       f = 1 (eq. 6: acting programs always count in full)
@@ -25,7 +26,8 @@ def arg(name, default):
     return sys.argv[sys.argv.index(name) + 1] if name in sys.argv else default
 
 
-POLICIES = {"program_aware": dict(decay_x=2), "ttl_pin_p50": dict(decay_table=ttl_pin_table(2)),
+POLICIES = {"program_aware": dict(decay_x=2), "request_aware": dict(request_aware=True),
+            "ttl_pin_p50": dict(decay_table=ttl_pin_table(2)),
             "ttl_pin_p95": dict(decay_table=ttl_pin_table(33)), "no_decay": dict(decay_x=1)}
 
 
