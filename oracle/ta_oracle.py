@@ -117,7 +117,7 @@ class Oracle:
         # requests from the same agentic workflow to the same node"): no global queue
         self.pinned = bool(cfg.get("pinned_routing", False))
         self.chunk_q = int(cfg.get("prefill_chunk_tokens", 2048))   # chunked-prefill tokens per step
-        self.chunk_ms = int(cfg.get("prefill_chunk_ms", 20))        # time of one chunk step
+        self.chunk_ms = int(cfg.get("prefill_chunk_ms", 100))       # time of one chunk step
         self.api_mode = api_mode
         self.trace = trace
         N = trace.n_slots if trace is not None else int(n_slots)
@@ -137,6 +137,10 @@ class Oracle:
         self.turn = [0] * N
         self.gen_done = [0] * N
         self.satisfied = [0] * N
+        # synthetic engine (reading A48): tokens waiting to be prefilled (prompt, tool
+        # results) and the engine time the last materialize spent (re)prefilling
+        self.pend = [0] * N
+        self.busy = [0] * N
         self.loc = [array("I", [NONE]) * self.MAXB for _ in range(N)]
         # --- per replica pools (BackendState.cache_config) ---
         self.hbm_free = [bytearray([1]) * self.NB for _ in range(self.R)]
@@ -237,6 +241,8 @@ class Oracle:
         self.step_count[p] = 0
         self.acting_since[p] = 0
         self.tool_return[p] = INT64_MAX
+        self.pend[p] = p0                       # the prompt waits for its prefill
+        self.busy[p] = 0
         self.stats["arrivals"] += 1
 
     def _pause(self, p: int, k: int):
@@ -253,7 +259,6 @@ class Oracle:
         """Trace-mode ingest: decode, tool return, release, closed-loop arrivals
         (reason/act loop PAPER.md:160-162; A18)."""
         tr = self.trace
-        d_tick = (self.rate * self.dt) // 1000
         stops = 0
         for p in range(self.N):
             st = self.status[p]
@@ -261,12 +266,14 @@ class Oracle:
                 continue
             base = int(tr.turn_off[p])
             nturns = int(tr.turn_off[p + 1]) - base
-            # 1. decode during the last interval (only if materialized last tick)
+            # 1. decode during the last interval (only if materialized last tick), after
+            #    the engine's (re)prefill of that materialize (reading A48)
             if st == REASONING and self.satisfied[p]:
                 t = self.turn[p]
                 g = int(tr.g[base + t])
                 left = g - self.gen_done[p]
-                d = min(d_tick, left)
+                busy = min(self.busy[p], self.dt)
+                d = min((self.rate * (self.dt - busy)) // 1000, left)
                 self.c[p] += d
                 self.gen_done[p] += d
                 if self.gen_done[p] == g:
@@ -278,13 +285,14 @@ class Oracle:
                     self.phase[p] = PHASE_A
                     self.status[p] = ACTING
                     took = 0 if self.rate == 0 else ceil_div(left * 1000, self.rate)
-                    self.acting_since[p] = T - self.dt + took
+                    self.acting_since[p] = T - self.dt + busy + took
                     self.tool_return[p] = self.acting_since[p] + int(tr.d_ms[base + t])
                     self.step_count[p] += 1
             # 2. tool result (tools keep running while paused)
             if (self.phase[p] == PHASE_A and self.status[p] in (ACTING, PAUSED)
                     and T >= self.tool_return[p]):
                 self.c[p] += int(tr.o[base + self.turn[p]])
+                self.pend[p] += int(tr.o[base + self.turn[p]])   # the result waits for prefill
                 self.turn[p] += 1
                 self.gen_done[p] = 0
                 self.phase[p] = PHASE_R
@@ -574,6 +582,11 @@ class Oracle:
             self.home[p] = r
             self.c_kv[p] = c1
             n_hbm[p] = nb[p]
+            # engine time of this materialize: recompute of the lost history plus the
+            # prefill of waiting prompt / tool-result tokens, in chunk steps (A48)
+            q = self.chunk_q
+            self.busy[p] = self.chunk_ms * (ceil_div(miss, q) + ceil_div(self.pend[p], q))
+            self.pend[p] = 0
             self._ledger_s.append((p, c0, c1, miss))
         for p in stalled:
             fx.append(decision(D_STALL, p, src=self.home[p], dst=r, blocks=need[p]))
@@ -759,6 +772,7 @@ class Oracle:
                 self.step_count[pid] += 1
             elif kind == E_TOOL_RESULT:
                 self.c[pid] += tokens
+                self.pend[pid] += tokens
                 self.phase[pid] = PHASE_R
                 if self.status[pid] == ACTING:
                     self.status[pid] = REASONING

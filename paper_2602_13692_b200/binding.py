@@ -199,7 +199,7 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
     c.decode_tok_per_s = cfg["decode_tok_per_s"]
     c.compact_every = cfg.get("compact_every", 0)
     c.prefill_chunk_tokens = cfg.get("prefill_chunk_tokens", 2048)   # STP ledger (NEXT-1)
-    c.prefill_chunk_ms = cfg.get("prefill_chunk_ms", 20)
+    c.prefill_chunk_ms = cfg.get("prefill_chunk_ms", 100)
     # TMA bulk copies are the default engine (measured faster or equal on every path);
     # pass flags=F_NO_BULK_DEFAULT to keep the 128-bit load/store engine
     if not flags & F_NO_BULK_DEFAULT:

@@ -97,6 +97,8 @@ struct Dev {
   u32 *nb, *n_hbm, *n_host, *prefix_hbm, *contrib;
   u8* released;                    // released during this tick's ingest
   u8* sat_new;                     // 1 + replica that satisfied the program this tick
+  u32 *pend, *busy;                // [N] synthetic engine (A48): tokens waiting for prefill;
+                                   //     ms the last materialize spent (re)prefilling
   u8* evs;                         // [3N] API-mode validation scratch (kept zero)
   u32* evc;                        // [N]  API-mode tentative context lengths
   // ---- trace scripts ----

@@ -22,6 +22,7 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
   const u32 gd0 = d.gen_done[p];
   const i64 tr0 = d.tool_return[p];
   i64 as = d.acting_since[p];
+  const u32 busy = d.busy[p], pend0 = d.pend[p];
   const u32 base = d.t_off[p], base1 = d.t_off[p + 1];
   SlotNow o{c, as, st, ph, d.placement[p], d.home[p], 0};
   if (st == TA_UNARRIVED || st == TA_STOPPED) return o;
@@ -31,7 +32,9 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
   u32 tt = t, gd = gd0;
   bool wrote_gd = false, wrote_tool = false;
   if (st == TA_REASONING && sat) {
-    const u32 d_tick = (u32)(((i64)d.rate * d.dt) / 1000);
+    // decode after the engine's (re)prefill of the last materialize (reading A48)
+    const i64 b = min((i64)busy, d.dt);
+    const u32 d_tick = (u32)(((i64)d.rate * (d.dt - b)) / 1000);
     const u32 left = g - gd;
     const u32 dd = min(d_tick, left);
     c += dd;
@@ -51,7 +54,7 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
       ph = TA_PHASE_A;                   // tool call: Reasoning -> Acting
       st = TA_ACTING;
       const i64 took = d.rate == 0 ? 0 : ((i64)left * 1000 + d.rate - 1) / d.rate;
-      as = T - d.dt + took;
+      as = T - d.dt + b + took;
       tr = as + (i64)dtool;
       d.acting_since[p] = as;
       d.step_count[p] += 1;
@@ -60,6 +63,7 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
   }
   if (ph == TA_PHASE_A && (st == TA_ACTING || st == TA_PAUSED) && T >= tr) {
     c += res;                            // tool result (tools run while paused)
+    d.pend[p] = pend0 + res;             // ... waits for its prefill
     tt = t + 1;
     gd = 0;
     wrote_gd = true;
@@ -93,10 +97,10 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
 // Later kernels of the tick return at once when ctr->err != TA_OK (state unchanged).
 struct EvRes {                 // final state of one program after its events (owner event)
   i64 as;                      // acting_since (if a TOOL_CALL ran)
-  u32 c, uid, calls;
-  u8 st, ph, fl, pad;          // fl: EVF_*
+  u32 c, uid, calls, pend;     // pend: tokens waiting for prefill (prompt, tool results; A48)
+  u8 st, ph, fl, pad[5];       // fl: EVF_*
 };
-static_assert(sizeof(EvRes) == 24, "EvRes layout (workspace carving)");
+static_assert(sizeof(EvRes) == 32, "EvRes layout (workspace carving)");
 enum { EVF_OWNER = 1, EVF_ARRIVE = 2, EVF_CALL = 4 };
 
 // Run the events of pid `p` (indices idx[0, n)) from its current state; returns the
@@ -106,7 +110,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
   const u64 cap = (u64)d.MAXB * (u64)d.bt;   // contexts are bounded by max_ctx (reading A35)
   u8 st = d.status[p], ph = d.phase[p];
   u64 c = d.c[p];
-  u32 uid = d.uid[p], calls = 0, fl = 0;
+  u32 uid = d.uid[p], calls = 0, fl = 0, pend = d.pend[p];
   i64 as = 0;
   for (int q = 0; q < n; ++q) {
     const u32 i = idx(q);
@@ -120,6 +124,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
       case TA_EV_ARRIVE:
         if (st != TA_UNARRIVED) return ((ull)i << 8) | TA_E_DUP_ID;
         st = TA_PAUSED; ph = TA_PHASE_R; uid = e.uid; fl |= EVF_ARRIVE; calls = 0; fl &= ~EVF_CALL;
+        pend = e.tokens;
         break;
       case TA_EV_DECODE:
         if (st != TA_REASONING) return ((ull)i << 8) | TA_E_ILLEGAL_TRANSITION;
@@ -132,6 +137,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
       case TA_EV_TOOL_RESULT:
         if (ph != TA_PHASE_A || (st != TA_ACTING && st != TA_PAUSED)) return ((ull)i << 8) | TA_E_ILLEGAL_TRANSITION;
         ph = TA_PHASE_R;
+        pend += e.tokens;
         if (st == TA_ACTING) st = TA_REASONING;
         break;
       case TA_EV_RELEASE:
@@ -142,7 +148,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
         return ((ull)i << 8) | TA_E_INVAL;
     }
   }
-  o->as = as; o->c = (u32)c; o->uid = uid; o->calls = calls;
+  o->as = as; o->c = (u32)c; o->uid = uid; o->calls = calls; o->pend = pend;
   o->st = st; o->ph = ph; o->fl = (u8)(fl | EVF_OWNER);
   return ~0ull;
 }
@@ -222,11 +228,13 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
       d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
       d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
       d.tool_return[p] = INT64_MAX;
+      d.busy[p] = 0;
       ++arr;
     }
     if (o.fl & EVF_CALL) d.acting_since[p] = o.as;
     d.step_count[p] = ((o.fl & EVF_ARRIVE) ? 0u : d.step_count[p]) + o.calls;
     d.c[p] = o.c;
+    d.pend[p] = o.pend;
     d.phase[p] = o.ph;
     d.status[p] = o.st;
     if (o.st == TA_STOPPED && st0 != TA_STOPPED) {   // release

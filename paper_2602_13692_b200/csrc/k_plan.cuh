@@ -401,6 +401,10 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         rec.new_tok = c - ckv;
         rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
         l_dec += (ull)c * (ull)d.dt;                    // holds c while decoding the interval
+        // engine time of this materialize: recompute + prefill of waiting tokens (A48)
+        const u32 q = (u32)d.chunk_q;
+        d.busy[p] = (u32)d.chunk_ms * (ceil_div_u32(rec.miss_tok, q) + ceil_div_u32(d.pend[p], q));
+        d.pend[p] = 0;
         l_pre += (ull)d.chunk_ms * stp_stair(c - ckv, (ull)d.chunk_q, ckv);
         l_rec += (ull)d.chunk_ms * stp_stair(rec.miss_tok, (ull)d.chunk_q, 0);
         pc[PC_HIT] += rec.hit_tok; pc[PC_PEER] += rec.peer_tok; pc[PC_HOST] += rec.host_tok;

@@ -138,6 +138,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.loc = L.take<u32>(N * MAXBP);
   x.nb = L.take<u32>(N); x.n_hbm = L.take<u32>(N); x.n_host = L.take<u32>(N);
   x.prefix_hbm = L.take<u32>(N); x.contrib = L.take<u32>(N);
+  x.pend = L.take<u32>(N); x.busy = L.take<u32>(N);
   x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
   x.evc = L.take<u32>(N);
   x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
@@ -163,7 +164,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.cpd = L.take<CpDesc>(R * (NB / 2 + 1)); x.cpd_cnt = L.take<u32>(R);
   const size_t EC = ev_capacity(c);
   x.events = L.take<ta_event>(EC);
-  x.evr = reinterpret_cast<EvRes*>(L.take<char>(EC * 24));
+  x.evr = reinterpret_cast<EvRes*>(L.take<char>(EC * 32));
   x.ev_pcnt = L.take<u32>(N);
   x.ev_mk = L.take<u64>(EC); x.ev_mk2 = L.take<u64>(EC);
   x.ev_mv = L.take<u32>(EC); x.ev_mv2 = L.take<u32>(EC);

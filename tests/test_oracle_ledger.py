@@ -88,3 +88,23 @@ def test_unused_cost_and_bound_hand_computed():
     o.next_arrival = 4
     dl = one_tick(o)
     assert dl["unused_bound_checks"] == 2 and dl["unused_bound_violations"] == 1
+
+
+def test_engine_prefill_time_delays_decode_hand_computed():
+    """Synthetic engine (reading A48): a resumed program whose 4096-token history was lost
+    is recomputed in ceil(4096/2048) = 2 chunk steps of 100 ms, plus its 300 waiting
+    tool-result tokens in 1 step: 300 ms of the next 5 s interval are not decoding, so at
+    40 tokens/s it decodes 40 * 4.7 = 188 tokens instead of 200."""
+    cfg = base_cfg(hbm_blocks=5000, max_ctx=8192, decode_tok_per_s=40, prefill_chunk_tokens=2048,
+                   prefill_chunk_ms=100)
+    o = oracle.Oracle(cfg, flat_trace(1, g=10 ** 6, d_ms=10 ** 9))
+    set_program(o, 0, oracle.PAUSED, oracle.PHASE_R, 4396, c_kv=4096, paused_since=0)
+    o.pend[0] = 300
+    o.next_arrival = 1
+    o.tick = 1
+    one_tick(o)                                   # restored, recomputed, prefilled
+    assert o.busy[0] == 300 and o.pend[0] == 0 and o.satisfied[0] == 1
+    one_tick(o)                                   # decodes during the interval after
+    assert o.c[0] == 4396 + 188
+    one_tick(o)                                   # nothing left to prefill: a full interval
+    assert o.c[0] == 4396 + 188 + 200
