@@ -59,6 +59,9 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
+SHARED = -1        # owner_hbm tag of a shared-prefix block: (SHARED, j)
+
+
 def decision(kind, pid=NONE, src=-1, dst=-1, blocks=0, to_host=0, dropped=0,
              hit=0, peer=0, host=0, miss=0, new=0):
     """Decision record; field order matches ``ta_decision`` in include/ta.h."""
@@ -147,6 +150,22 @@ class Oracle:
         self.host_free = [bytearray([1]) * self.NH for _ in range(self.R)]
         self.owner_hbm = [[None] * self.NB for _ in range(self.R)]
         self.owner_host = [[None] * self.NH for _ in range(self.R)]
+        # NEXT-3 (reading A49): the agents' shared system prompt, the first sb blocks of
+        # every program, is stored once per replica in the top sb HBM blocks (reserved:
+        # never free, never evicted, moved or compacted); a homed program's first sb
+        # entries point at them.  Load accounting still counts every program's full c
+        # ("the shared prompt across programs implicitly reserves
+        # sufficient memory buffer").
+        spt = int(cfg.get("shared_prefix_tokens", 0))
+        assert spt % self.bt == 0 and (spt == 0 or spt // self.bt < self.NB), "shared prefix: whole blocks"
+        self.sb = spt // self.bt
+        self.shared_base = self.NB - self.sb
+        for r in range(self.R):
+            for j in range(self.sb):
+                self.hbm_free[r][self.shared_base + j] = 0
+                self.owner_hbm[r][self.shared_base + j] = (SHARED, j)
+        if trace is not None and self.sb:
+            assert int(min(trace.p0)) >= spt, "every prompt starts with the shared prefix"
         self.cap_max = [(self.lmax * self.NB) >> 16 for _ in range(self.R)]
         self.cap_min = [(self.lmin * self.NB) >> 16 for _ in range(self.R)]
         self.L = [0] * self.R
@@ -207,6 +226,9 @@ class Oracle:
             if e == NONE:
                 continue
             assert h >= 0, "KV without a home replica"
+            if j < self.sb:                    # shared prefix: a reference, not an owner
+                row[j] = NONE
+                continue
             if e & HOST_BIT:
                 s = e & ~HOST_BIT
                 self.host_free[h][s] = 1
@@ -438,17 +460,17 @@ class Oracle:
 
     # ------------------------------------------------------------------ step 5
     def _need(self, p: int, r: int) -> int:
-        """#{j < nb : loc[j] is not HBM on r}."""
+        """#{sb <= j < nb : loc[j] is not HBM on r} (the shared prefix is on every replica)."""
         row = self.loc[p]
         here = self.home[p] == r
-        return sum(1 for j in range(self.fp["nb"][p]) if not (here and self.is_hbm(row[j])))
+        return sum(1 for j in range(self.sb, self.fp["nb"][p]) if not (here and self.is_hbm(row[j])))
 
     def _evict_order(self, r: int):
         """Eviction candidates E_r and their order (reading A21):
         group 0 PAUSED in exact reverse of the restore order; group 1 ACTING placed
         elsewhere; group 2 ACTING placed on r; groups 1-2 by (contrib, slot)."""
         nb, n_hbm, contrib = self.fp["nb"], self.fp["n_hbm"], self.contrib
-        E = [p for p in range(self.N) if self.home[p] == r and n_hbm[p] > 0
+        E = [p for p in range(self.N) if self.home[p] == r and n_hbm[p] > self.sb
              and self.status[p] in (PAUSED, ACTING)]
         if self.request_aware:                 # LRU over idle caches, not program-aware (A46)
             return sorted(E, key=lambda p: (self.paused_since[p] * self.dt if self.status[p] == PAUSED
@@ -469,7 +491,7 @@ class Oracle:
         need = {p: self._need(p, r) for p in F}
         E = self._evict_order(r)
         free_r = sum(self.hbm_free[r])
-        supply = free_r + sum(n_hbm[p] for p in E)
+        supply = free_r + sum(n_hbm[p] - self.sb for p in E)   # private HBM blocks
         # 5.2 stall cut: longest prefix of F with sum(need) <= supply
         S, tot = [], 0
         for p in F:
@@ -488,7 +510,7 @@ class Oracle:
             if X == 0:
                 break
             row = self.loc[p]
-            hbm_js = [j for j in range(nb[p]) if self.is_hbm(row[j])]
+            hbm_js = [j for j in range(self.sb, nb[p]) if self.is_hbm(row[j])]
             take = min(X, len(hbm_js))
             to_host = dropped = 0
             for j in sorted(hbm_js, reverse=True)[:take]:
@@ -527,7 +549,9 @@ class Oracle:
                 for j in range(ceil_div(H, self.bt)):
                     tok = min(self.bt, H - j * self.bt)
                     e = row[j]
-                    if e == NONE:
+                    if j < self.sb:                    # shared prefix: resident on r
+                        hit += tok
+                    elif e == NONE:
                         miss += tok
                     elif e & HOST_BIT:
                         host += tok
@@ -537,7 +561,9 @@ class Oracle:
                         peer += tok
             c0, c1 = self.c_kv[p], self.c[p]
             hist_blocks = ceil_div(c0, self.bt)
-            for j in range(nb[p]):
+            for j in range(self.sb):                   # shared prefix (same index on every replica)
+                row[j] = self.shared_base + j
+            for j in range(self.sb, nb[p]):
                 e = row[j]
                 recompute = False
                 if h == r and self.is_hbm(e):
@@ -621,13 +647,13 @@ class Oracle:
         """Two-finger compaction (reading A20): move the highest used block to the
         lowest free block until the fingers cross."""
         free = self.hbm_free[r]
-        lo, hi, moves = 0, self.NB - 1, 0
+        lo, hi, moves = 0, self.shared_base - 1, 0       # the shared prefix stays put
         while True:
-            while lo < self.NB and not free[lo]:
+            while lo < self.shared_base and not free[lo]:
                 lo += 1
             while hi >= 0 and free[hi]:
                 hi -= 1
-            if lo >= self.NB or hi < 0 or lo > hi:
+            if lo >= self.shared_base or hi < 0 or lo > hi:
                 break
             p, j = self.owner_hbm[r][hi]
             self.loc[p][j] = lo
@@ -732,6 +758,8 @@ class Oracle:
                 c = ev[3] if kind == E_ARRIVE else ctx.get(pid, self.c[pid]) + ev[3]
                 if c > cap and not (kind == E_ARRIVE and st != UNARRIVED):
                     return E_INVAL
+                if kind == E_ARRIVE and st == UNARRIVED and c < self.sb * self.bt:
+                    return E_INVAL                        # the prompt starts with the shared prefix
                 ctx[pid] = c
             if kind == E_ARRIVE:
                 if st != UNARRIVED:
@@ -804,7 +832,7 @@ class Oracle:
         if mode in (PAUSE_OFFLOAD, PAUSE_DROP):
             h = self.home[pid]
             row = self.loc[pid]
-            hbm_js = [j for j in range(self.fp["nb"][pid]) if self.is_hbm(row[j])]
+            hbm_js = [j for j in range(self.sb, self.fp["nb"][pid]) if self.is_hbm(row[j])]
             to_host = dropped = 0
             hslot = 0
             for j in sorted(hbm_js, reverse=True):
@@ -921,7 +949,7 @@ class Oracle:
         for p in range(self.N):
             if self.home[p] != r:
                 continue
-            lost = sum(1 for e in self.loc[p] if e != NONE)
+            lost = sum(1 for j, e in enumerate(self.loc[p]) if e != NONE and j >= self.sb)
             self._free_all(p)
             self.home[p] = -1
             if lost:
@@ -950,6 +978,10 @@ class Oracle:
                 assert j < nb, f"I2: block beyond nb for p={p}"
                 h = self.home[p]
                 assert h >= 0, f"I5: KV without home p={p}"
+                if j < self.sb:                            # NEXT-3: shared prefix reference
+                    assert e == self.shared_base + j, f"shared prefix entry p={p} j={j}"
+                    n_hbm += 1
+                    continue
                 if e & HOST_BIT:
                     s = e & ~HOST_BIT
                     assert used_s[h][s] is None and not self.host_free[h][s], "I2 host"
@@ -964,11 +996,17 @@ class Oracle:
                     n_hbm += 1
             if nb:
                 assert (nb if first_non_hbm is None else first_non_hbm) == n_hbm, f"I10 p={p}"
+                if self.sb and self.home[p] >= 0:
+                    assert n_hbm >= self.sb, f"homed program without its shared prefix p={p}"
             st = self.status[p]
             assert (self.placement[p] >= 0) == (st in (REASONING, ACTING)), f"I5 p={p}"
             if st in (UNARRIVED, STOPPED):
                 assert self.home[p] == -1 and n_hbm == 0
         for r in range(self.R):
+            for j in range(self.sb):
+                b = self.shared_base + j
+                assert not self.hbm_free[r][b] and self.owner_hbm[r][b] == (SHARED, j), "shared block"
+                used_h[r][b] = (SHARED, j)
             for b in range(self.NB):
                 assert (used_h[r][b] is None) == bool(self.hbm_free[r][b]), "I1/I2 hbm free-set"
             for s in range(self.NH):
