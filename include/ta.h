@@ -107,7 +107,17 @@ typedef struct {
   uint32_t flags;              /* TA_F_* */
   int32_t prefill_chunk_tokens; /* STP ledger (NEXT-1): chunked-prefill tokens per engine step (>= 1) */
   int32_t prefill_chunk_ms;    /* STP ledger: duration of one chunk step in ms (>= 0) */
-  int32_t reserved;
+  /* NEXT-3 (reading A49; "agentic system prompts are identical across
+   * workflows"): the first shared_prefix_tokens tokens of every program are
+   * the same system prompt, stored ONCE per replica in its top sb = shared_prefix_tokens
+   * / block_tokens HBM blocks [NB - sb, NB), which are never free, evicted, copied or
+   * compacted (content: uid 0 of the closed form).  A homed program's entries j < sb
+   * point at them; need, eviction supply and allocation cover j >= sb only; resumed
+   * programs count the prefix tokens as hit.  The load (Eq. 7) still counts every
+   * program's full context.  Multiple of block_tokens, < NB * block_tokens; every
+   * prompt (trace p0, ARRIVE tokens) must be at least this long (else TA_E_INVAL).
+   * 0 = off (the former reserved field). */
+  int32_t shared_prefix_tokens;
 } ta_config;
 
 typedef struct {

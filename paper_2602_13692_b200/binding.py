@@ -42,7 +42,7 @@ class Config(C.Structure):
                 ("lambda_max_q16", C.c_uint32), ("lambda_min_q16", C.c_uint32),
                 ("decay_q32", C.c_uint64 * 64), ("decode_tok_per_s", C.c_int32),
                 ("compact_every", C.c_int32), ("flags", C.c_uint32), ("prefill_chunk_tokens", C.c_int32),
-                ("prefill_chunk_ms", C.c_int32), ("reserved", C.c_int32)]
+                ("prefill_chunk_ms", C.c_int32), ("shared_prefix_tokens", C.c_int32)]
 
 
 class Buffers(C.Structure):
@@ -200,6 +200,7 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
     c.compact_every = cfg.get("compact_every", 0)
     c.prefill_chunk_tokens = cfg.get("prefill_chunk_tokens", 2048)   # STP ledger (NEXT-1)
     c.prefill_chunk_ms = cfg.get("prefill_chunk_ms", 100)
+    c.shared_prefix_tokens = cfg.get("shared_prefix_tokens", 0)        # NEXT-3
     # TMA bulk copies are the default engine (measured faster or equal on every path);
     # pass flags=F_NO_BULK_DEFAULT to keep the 128-bit load/store engine
     if not flags & F_NO_BULK_DEFAULT:

@@ -21,6 +21,7 @@ typedef unsigned long long ull;
 
 #define LOC_NONE 0xFFFFFFFFu
 #define LOC_HOST 0x80000000u
+#define OWNER_SHARED 0xFFFFFFFFu         // owner_hbm of a reserved shared-prefix block (NEXT-3)
 #define FULL_MASK 0xFFFFFFFFu
 #define CTA 1024          // threads of the single-CTA planner kernels
 #define NWARP (CTA / 32)
@@ -78,6 +79,7 @@ struct Dev {
   u32 flags;
   int compact_every;
   int chunk_q, chunk_ms;           // STP ledger: prefill chunk tokens / ms per chunk
+  u32 sb, sbase;                   // NEXT-3: shared-prefix blocks, first reserved block (NB - sb)
   i64 seg_bytes, block_bytes;
   int first_local, n_local;
   int api_mode;

@@ -427,13 +427,20 @@ __global__ void __launch_bounds__(256) k_verify(Dev d, int tier) {
     const u32* fw = tier ? d.host_free + (size_t)r * d.NHW : d.hbm_free + (size_t)r * d.NBW;
     if (fw[b >> 5] & (1u << (b & 31))) continue;      // free
     u32 o = tier ? d.owner_host[(size_t)r * d.NH + b] : d.owner_hbm[(size_t)r * d.NB + b];
-    u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
-    u32 t0 = j * (u32)d.bt, t1 = min(t0 + (u32)d.bt, d.c_kv[p]);
+    u32 j, t0, t1, uid;
+    if (!tier && o == OWNER_SHARED) {                   // shared prefix block: uid 0, full
+      j = b - d.sbase;
+      t0 = j * (u32)d.bt; t1 = t0 + (u32)d.bt; uid = 0;
+    } else {
+      const u32 p = o / (u32)d.MAXB;
+      j = o % (u32)d.MAXB;
+      t0 = j * (u32)d.bt; t1 = min(t0 + (u32)d.bt, d.c_kv[p]); uid = d.uid[p];
+    }
     if (t1 <= t0) continue;
     char* base = tier ? d.host[r] : d.hbm[r];
     const ull* seg = (const ull*)seg_addr(base, d.layout, nblk, d.seg_bytes, nseg, b, s);
     const u32 l = (u32)s >> 1, kv = (u32)s & 1;
-    const ull ubase = (ull)d.uid[p] << 40;
+    const ull ubase = (ull)uid << 40;
     const u32 nw = (t1 - t0) * wtok;
     for (u32 w = threadIdx.x; w < nw; w += blockDim.x) {
       u32 t = t0 + w / wtok, rw = w % wtok;

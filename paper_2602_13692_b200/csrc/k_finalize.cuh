@@ -59,15 +59,19 @@ __device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32
   u32* s_free = s_big;                  // [nw + 1]
   u32* s_used = s_big + nw + 1;         // [nw + 1]
   cta_bitmap_prefix(fw, nw, s_free, s_tmp);
-  const u32 U = (u32)d.NB - s_free[nw];
-  // used bitmap prefix (bits >= NB are neither free nor used)
+  // blocks [0, NBc) take part; the shared-prefix blocks above NBc stay put (NEXT-3)
+  const u32 NBc = d.sbase;
+  const u32 U = NBc - s_free[nw];
+  // bits of word w that are blocks below NBc
+  auto valid_of = [&](int w) -> u32 {
+    const i64 n = (i64)NBc - (i64)w * 32;
+    return n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
+  };
+  // used bitmap prefix (bits >= NBc are neither free nor used here)
   {
     int chunk = (nw + CTA - 1) / CTA;
     int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
-    auto used_word = [&](int w) {
-      u32 valid = (w == nw - 1 && (d.NB & 31)) ? ((1u << (d.NB & 31)) - 1) : 0xFFFFFFFFu;
-      return ~fw[w] & valid;
-    };
+    auto used_word = [&](int w) { return ~fw[w] & valid_of(w); };
     u32 s = 0;
     for (int w = lo; w < hi; ++w) s += __popc(used_word(w));
     u32 total;
@@ -89,8 +93,7 @@ __device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32
     u32 q = U - 1 - m;
     int lo = 0, hi = nw;
     while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_used[mid] <= q) lo = mid; else hi = mid; }
-    u32 uw = ~fw[lo];
-    if (lo == nw - 1 && (d.NB & 31)) uw &= (1u << (d.NB & 31)) - 1;
+    u32 uw = ~fw[lo] & valid_of(lo);
     u32 src = (u32)lo * 32u + __fns(uw, 0, (int)(q - s_used[lo]) + 1);
     u32 o = d.owner_hbm[(size_t)r * d.NB + src];
     u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;

@@ -118,6 +118,8 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
     if (e.kind == TA_EV_ARRIVE || e.kind == TA_EV_DECODE || e.kind == TA_EV_TOOL_RESULT) {
       const u64 cn = e.kind == TA_EV_ARRIVE ? (u64)e.tokens : c + e.tokens;
       if (cn > cap && !(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) return ((ull)i << 8) | TA_E_INVAL;
+      if (e.kind == TA_EV_ARRIVE && st == TA_UNARRIVED && (u64)e.tokens < (u64)d.sb * (u64)d.bt)
+        return ((ull)i << 8) | TA_E_INVAL;           // the prompt starts with the shared prefix
       if (!(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) c = cn;
     }
     switch (e.kind) {
@@ -261,6 +263,10 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
     for (u32 j = lane; j < nbv; j += 32) {
       u32 e = row[j];
       if (e == LOC_NONE) continue;
+      if (j < d.sb) {                              // shared prefix: a reference, not owned
+        row[j] = LOC_NONE;
+        continue;
+      }
       if (e & LOC_HOST) {
         u32 s = e & ~LOC_HOST;
         atomicOr(&d.host_free[(size_t)h * d.NHW + (s >> 5)], 1u << (s & 31));
@@ -341,7 +347,7 @@ __device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int v
       d.act_list[(size_t)pl * d.N + atomicAdd(&d.act_cnt[pl], 1u)] = (u32)p;
     }
     const int h = v.home;
-    if (n_h > 0 && h >= 0) d.ec_list[(size_t)h * d.N + atomicAdd(&d.ec_cnt[h], 1u)] = (u32)p;
+    if (n_h > d.sb && h >= 0) d.ec_list[(size_t)h * d.N + atomicAdd(&d.ec_cnt[h], 1u)] = (u32)p;
     d.rb[p] = rbv;
     d.fpl[p] = pl;
   }

@@ -6,11 +6,12 @@
 #include "common.cuh"
 #include "k_sched.cuh"
 
-// need(p) on replica r = #{j < nb : loc[j] is not HBM on r}.  HBM entries of a
+// need(p) on replica r = #{sb <= j < nb : loc[j] is not HBM on r}.  HBM entries of a
 // program always form the prefix [0, n_hbm) of its row (invariant I10: growth
-// appends, eviction is tail-first), so need = nb - n_hbm on the home replica.
+// appends, eviction is tail-first), so need = nb - n_hbm on the home replica; the sb
+// shared-prefix blocks (NEXT-3) are resident on every replica.
 __device__ __forceinline__ u32 need_of(const Dev& d, u32 p, int r) {
-  return d.home[p] == r ? d.nb[p] - d.n_hbm[p] : d.nb[p];
+  return d.home[p] == r ? d.nb[p] - d.n_hbm[p] : d.nb[p] - d.sb;
 }
 
 // warp-aggregated add of a per-thread counter into a shared accumulator
@@ -146,7 +147,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     for (int i = threadIdx.x; i < nel; i += CTA) {
       const u32 p = el[i];
       const u8 s = d.status[p];
-      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p];
+      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p] - d.sb;   // private HBM blocks
     }
     auto add = [](ull a, ull b) { return a + b; };
     fr = cta_reduce<ull>(fr, s_red, add, 0ull);
@@ -189,7 +190,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> shf);
       };
       const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
-                                       [&](int i) { return d.n_hbm[i]; });
+                                       [&](int i) { return d.n_hbm[i] - d.sb; });
       PSTAMP(2, 3);
       // keys: group 0 (PAUSED) = exact reverse of the restore order, ties slot-down (the
       // tie-break value N-1-slot); groups 1-2 (ACTING) = (group, contrib), ties slot-up
@@ -224,7 +225,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       for (u32 i = threadIdx.x; i < ne; i += CTA) {
         const u32 p = (sk[i] >> 62) == 0 ? (u32)(N - 1) - sv[i] : sv[i];   // undo the group-0 tie-break
         ep[i] = p;
-        ec[i] = d.n_hbm[p];
+        ec[i] = d.n_hbm[p] - d.sb;
       }
       __syncthreads();
       cta_incl_scan_array(ec, (int)ne, s_tmp);
@@ -341,7 +342,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       for (u32 v = threadIdx.x; v < nv; v += CTA) {
         u32 p = ep[v];
         u32 excl = v ? ecs[v - 1] : 0;
-        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p];
+        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p] - d.sb;
         u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
         ta_decision rec;
         rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
@@ -383,7 +384,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         const u32 ckv = d.c_kv[p], c = d.c[p];
         const u32 nhp = d.n_hbm[p];
         if (fst) {
-          s_fp[i] = p; s_fj[i] = h == r ? nhp : 0; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
+          s_fp[i] = p; s_fj[i] = h == r ? nhp : d.sb; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
           s_fu[i] = d.uid[p];
         }
         const bool resumed = !(d.satisfied[p] && h == r);
@@ -394,7 +395,12 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
           u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
           if (is_hbm(el)) th -= shs; else if (is_host(el)) ts -= shs; else tn -= shs;
-          if (h == r) rec.hit_tok = (u32)th; else rec.peer_tok = (u32)th;
+          if (d.sb) {                                  // shared prefix: resident on r (hit)
+            const ull sh = (ull)d.sb * bt;             // c_kv >= every prompt >= sb * bt
+            if (h >= 0) th -= sh; else tn -= sh;
+            rec.hit_tok = (u32)sh;
+          }
+          if (h == r) rec.hit_tok += (u32)th; else rec.peer_tok = (u32)th;
           rec.host_tok = (u32)ts;
           rec.miss_tok = (u32)tn;
         }
@@ -420,6 +426,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
             }
           }
         }
+        if (d.sb && h < 0)                             // first materialize: point at the prefix
+          for (u32 j = 0; j < d.sb; ++j) d.loc[(size_t)p * d.MAXBP + j] = d.sbase + j;
         d.sat_new[p] = (u8)(r + 1);
       } else {
         rec.kind = TA_D_STALL;
@@ -481,7 +489,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         const u32 excl = i ? fcs[i - 1] : 0;
         const u32 p = fst ? s_fp[i] : fp[i];
         const int h = fst ? (int)s_fh[i] : d.home[p];
-        const u32 j = (fst ? s_fj[i] : (h == r ? d.n_hbm[p] : 0)) + (q - excl);
+        const u32 j = (fst ? s_fj[i] : (h == r ? d.n_hbm[p] : d.sb)) + (q - excl);
         pk[k] = fst ? i : p;
         hk[k] = h;
         jk[k] = j;

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
       u32 nh = 0;                          // HBM prefix length (I10)
       const u32* row = d.loc + (size_t)pid * d.MAXBP;
       while (nh < nbv && is_hbm(row[nh])) ++nh;
-      s_nh = (mode == TA_PAUSE_LAZY || s_h < 0) ? 0 : nh;
+      s_nh = (mode == TA_PAUSE_LAZY || s_h < 0 || nh <= d.sb) ? 0 : nh - d.sb;   // private blocks
     }
   }
   __syncthreads();
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
   EvDesc* evd = d.evd + (size_t)h * d.NB;
   u32* scr = d.evx + (size_t)h * d.NB;
   for (u32 e = threadIdx.x; e < X; e += CTA) {
-    u32 j = X - 1 - e;                    // tail first
+    u32 j = d.sb + X - 1 - e;             // tail first, down to the shared prefix
     u32 idx = row[j];
     scr[e] = idx;
     if (e < hfree) {
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ 
     u32* row = d.loc + (size_t)p * d.MAXBP;
     const u32 nbv = ceil_div_u32(d.c[p], d.bt);
     u32 cnt = 0;
-    for (u32 j = lane; j < nbv; j += 32) {
-      if (row[j] != LOC_NONE) { ++cnt; row[j] = LOC_NONE; }
+    for (u32 j = lane; j < nbv; j += 32) {          // lost: private blocks (j >= sb)
+      if (row[j] != LOC_NONE) { cnt += j >= d.sb; row[j] = LOC_NONE; }
     }
     cnt = __reduce_add_sync(FULL_MASK, cnt);
     if (lane == 0) { lost[q] = cnt; d.home[p] = -1; }
@@ -222,9 +222,9 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ 
         atomicAdd(&s_lost, (ull)lost[q]);
       });
   // every block of r belonged to a program homed on r: the pools are empty now
-  for (int w = threadIdx.x; w < d.NBW; w += CTA) {
-    const i64 lo = (i64)w * 32, n = d.NB - lo;
-    d.hbm_free[(size_t)r * d.NBW + w] = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1);
+  for (int w = threadIdx.x; w < d.NBW; w += CTA) {   // shared-prefix blocks stay reserved
+    const i64 lo = (i64)w * 32, n = (i64)d.sbase - lo;
+    d.hbm_free[(size_t)r * d.NBW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
   }
   for (int w = threadIdx.x; w < d.NHW; w += CTA) {
     const i64 lo = (i64)w * 32, n = d.NH - lo;

@@ -115,6 +115,9 @@ static const char* validate(const ta_config* c) {
     return "watermarks must satisfy 0 < lambda_min <= lambda_max <= 1 (SPEC.md:190)";
   if (c->decode_tok_per_s < 0 || c->compact_every < 0 || c->max_trace_turns < 0) return "negative rate/compact/turns";
   if (c->prefill_chunk_tokens < 1 || c->prefill_chunk_ms < 0) return "prefill_chunk_tokens must be >= 1, prefill_chunk_ms >= 0";
+  if (c->shared_prefix_tokens < 0 || c->shared_prefix_tokens % c->block_tokens != 0 ||
+      c->shared_prefix_tokens / c->block_tokens >= c->hbm_blocks)
+    return "shared_prefix_tokens must be a multiple of block_tokens, below hbm_blocks blocks";
   return nullptr;
 }
 
@@ -194,10 +197,11 @@ static size_t host_carve(const ta_config* c, char* base, HostWs* h) {
 __global__ void k_init(Dev d) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   for (int r = 0; r < d.R; ++r) {
-    for (int w = t; w < d.NBW; w += stride) {
-      i64 lo = (i64)w * 32, n = d.NB - lo;
-      d.hbm_free[(size_t)r * d.NBW + w] = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1);
+    for (int w = t; w < d.NBW; w += stride) {           // the shared-prefix blocks are never free
+      i64 lo = (i64)w * 32, n = (i64)d.sbase - lo;
+      d.hbm_free[(size_t)r * d.NBW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
     }
+    for (u32 j = t; j < d.sb; j += stride) d.owner_hbm[(size_t)r * d.NB + d.sbase + j] = OWNER_SHARED;
     for (int w = t; w < d.NHW; w += stride) {
       i64 lo = (i64)w * 32, n = d.NH - lo;
       d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
@@ -208,6 +212,19 @@ __global__ void k_init(Dev d) {
     d.tool_return[p] = INT64_MAX;
     d.placement[p] = -1;
     d.home[p] = -1;
+  }
+}
+
+// NEXT-3: the shared system prompt's KV (uid 0 of the closed form) in the reserved top
+// blocks of every local replica (engine stand-in, with TA_F_FILL).
+__global__ void __launch_bounds__(256) k_fill_shared(Dev d) {
+  const int nseg = 2 * d.nL;
+  const i64 per = (i64)d.sb * nseg, items = (i64)d.n_local * per;
+  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
+    const int r = d.first_local + (int)(it / per);
+    const u32 j = (u32)((it % per) / nseg);
+    const int s = (int)(it % nseg);
+    fill_segment(d, r, d.sbase + j, s, 0u, j, j * (u32)d.bt, (j + 1) * (u32)d.bt);
   }
 }
 
@@ -390,6 +407,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.flags = cfg->flags; d.compact_every = cfg->compact_every;
   d.chunk_q = cfg->prefill_chunk_tokens;
   d.chunk_ms = cfg->prefill_chunk_ms;
+  d.sb = (u32)(cfg->shared_prefix_tokens / cfg->block_tokens);
+  d.sbase = (u32)(d.NB - d.sb);
   d.seg_bytes = (i64)cfg->block_tokens * cfg->n_kv_heads * cfg->head_dim * cfg->elem_bytes;
   d.block_bytes = (i64)x->block_bytes;
   d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
@@ -464,6 +483,10 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
   if (e == cudaSuccess) { k_init<<<148, 256, 0, x->stream>>>(d); e = cudaGetLastError(); }
+  if (e == cudaSuccess && d.sb && (d.flags & TA_F_FILL)) {
+    k_fill_shared<<<kCopyGrid, 256, 0, x->stream>>>(d);
+    e = cudaGetLastError();
+  }
   // planner kernels: small sorts and staged lists in dynamic shared memory
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
@@ -492,6 +515,8 @@ ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* t) {
   if (total > (u32)ctx->cfg.max_trace_turns) FAIL(ctx, TA_E_INVAL, "trace has %u turns > max_trace_turns", total);
   for (int p = 0; p < t->n_slots; ++p) {
     if (t->turn_off[p + 1] <= t->turn_off[p]) FAIL(ctx, TA_E_INVAL, "slot %d has no turns", p);
+    if ((u64)t->p0[p] < (u64)ctx->d.sb * (u64)ctx->d.bt)
+      FAIL(ctx, TA_E_INVAL, "slot %d: prompt shorter than the shared prefix", p);
     u64 ctx_max = t->p0[p];
     for (u32 q = t->turn_off[p]; q < t->turn_off[p + 1]; ++q) ctx_max += (u64)t->g[q] + t->o[q];
     if ((ctx_max + ctx->d.bt - 1) / ctx->d.bt > (u64)ctx->d.MAXB)

@@ -37,8 +37,8 @@ def oracle_arrays(o) -> dict:
     own_s = np.zeros(max(1, R * o.NH), np.uint32)
     for r in range(R):
         for b, ow in enumerate(o.owner_hbm[r]):
-            if ow is not None:
-                own_h[r * o.NB + b] = ow[0] * MAXB + ow[1]
+            if ow is not None:       # shared-prefix blocks (NEXT-3): the OWNER_SHARED tag
+                own_h[r * o.NB + b] = 0xFFFFFFFF if ow[0] == oracle.ta_oracle.SHARED else ow[0] * MAXB + ow[1]
         for s, ow in enumerate(o.owner_host[r]):
             if ow is not None:
                 own_s[r * o.NH + s] = ow[0] * MAXB + ow[1]
@@ -96,9 +96,10 @@ def check_blocks_content(o, pool, samples, rng):
     n = 0
     for i in pick:
         tier, r, idx, (p, j) = owned[i]
-        valid = min(bt, o.c_kv[p] - j * bt)
+        shared = p == oracle.ta_oracle.SHARED                     # the shared prompt: uid 0
+        valid = bt if shared else min(bt, o.c_kv[p] - j * bt)
         got = pool.read_block(r, tier, idx)                       # [2L, bt, H, D/4]
-        want = block_words(o.uid[p], j, bt, L, H, D).reshape(2 * L, bt, H, D // 4)
+        want = block_words(0 if shared else o.uid[p], j, bt, L, H, D).reshape(2 * L, bt, H, D // 4)
         assert np.array_equal(got[:, :valid], want[:, :valid]), (tier, r, idx, p, j)
         n += 1
     return n

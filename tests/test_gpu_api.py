@@ -47,12 +47,13 @@ def random_events(o, rng, T, n_max=12, illegal_p=0.1):
     return evs
 
 
-@pytest.mark.parametrize("seed,R", [(1, 1), (2, 2), (3, 3)])
-def test_gpu_api_mode_events(seed, R):
+@pytest.mark.parametrize("seed,R,spt", [(1, 1, 0), (2, 2, 0), (3, 3, 0), (4, 2, 32)])
+def test_gpu_api_mode_events(seed, R, spt):
+    """spt > 0: NEXT-3 shared prefix (arrivals shorter than it are rejected batches)."""
     need_gpu()
     from paper_2602_13692_b200 import Pool
     cfg = tracegen.get_config("c1_toy", n_replicas=R, hbm_blocks=48, host_blocks=16, max_ctx=4096,
-                              compact_every=4)
+                              compact_every=4, shared_prefix_tokens=spt)
     N = 40
     o = oracle.Oracle(cfg, api_mode=True, n_slots=N)
     pool = Pool(cfg, N, trace_mode=False)
@@ -76,11 +77,12 @@ def test_gpu_api_mode_events(seed, R):
     pool.close()
 
 
-@pytest.mark.parametrize("seed,R", [(5, 2), (6, 3), (7, 1)])
-def test_gpu_verbs_random(seed, R):
+@pytest.mark.parametrize("seed,R,spt", [(5, 2, 0), (6, 3, 0), (7, 1, 0), (8, 2, 48)])
+def test_gpu_verbs_random(seed, R, spt):
     need_gpu()
     from paper_2602_13692_b200 import Pool
-    cfg = stress(seed, R, NB=128 if R > 1 else 192)     # some headroom so resumes can succeed
+    cfg = stress(seed, R, NB=128 if R > 1 else 192,     # some headroom so resumes can succeed
+                 shared_prefix_tokens=spt)
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns)
@@ -226,15 +228,15 @@ def test_gpu_api_replay_equals_trace_mode(name, n, ticks):
     pool.close()
 
 
-@pytest.mark.parametrize("seed", [31, 32])
-def test_gpu_health_failover_random(seed):
+@pytest.mark.parametrize("seed,spt", [(31, 0), (32, 0), (33, 48)])
+def test_gpu_health_failover_random(seed, spt):
     """NEXT-4 health mask: replicas fail and come back between ticks (ta_set_health),
     interleaved with the other verbs; decisions, status codes and full state equal the
     oracle's; the KV left on the healthy replicas stays byte-exact."""
     need_gpu()
     from paper_2602_13692_b200 import Pool
     cfg = tracegen.get_config("c1_toy", n_replicas=3, hbm_blocks=64, host_blocks=16, compact_every=4,
-                              trace=dict(n=30, n_initial=12, seed=seed))
+                              trace=dict(n=30, n_initial=12, seed=seed), shared_prefix_tokens=spt)
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns)

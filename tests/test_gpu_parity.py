@@ -173,3 +173,20 @@ def test_gpu_configs3_4_decisions_full_n(name, ticks):
     on one GPU with the decision-only KV shape (bytes per block do not affect decisions)."""
     cfg = tracegen.get_config(name, kv="mini")
     run_parity(cfg, ticks, state_every=4, content_every=4, samples=8)
+
+
+@pytest.mark.parametrize("seed,R,spt", [(81, 1, 48), (82, 2, 48), (83, 3, 64), (84, 2, 16)])
+def test_gpu_shared_prefix(seed, R, spt):
+    """NEXT-3: the shared system prompt stored once per replica (reserved top blocks);
+    tight pools with host tier and compaction; the reserved blocks' bytes (uid 0) are
+    verified with the rest."""
+    o, n = run_parity(stress(seed, R, NB=56 if R > 1 else 80, shared_prefix_tokens=spt), 300, seed=seed)
+    assert o.stats["evict_blocks"] > 0 and o.stats["compact_blocks"] > 0 and o.sb == spt // 16
+
+
+def test_gpu_shared_prefix_swe_decisions_full_n():
+    """configs[1] shape (256 SWE programs) with a 1024-token shared system prompt, the
+    decision-only KV shape."""
+    cfg = tracegen.get_config("c2_swe", kv="mini", shared_prefix_tokens=1024)
+    o, n = run_parity(cfg, 40, state_every=5, content_every=10, samples=8)
+    assert n > 0
