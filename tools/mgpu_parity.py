@@ -1,11 +1,13 @@
 """Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
 
 torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs] [--api]
+    [--shared TOKENS]
 Every rank runs the replicated control plane for all N replicas and moves only its
 own replica's bytes; every rank compares its decisions and full state with its own
 oracle copy, and verifies the KV content of its local pool.  --api: the same ticks in
 API mode (the engine's recorded events, tools/api_events.py) against the trace-mode
-oracle.  Exit code 0 = parity."""
+oracle.  --shared: NEXT-3 shared system prompt of TOKENS tokens (reserved blocks on
+every GPU).  Exit code 0 = parity."""
 import os
 import random
 import sys
@@ -29,8 +31,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spt = int(sys.argv[sys.argv.index("--shared") + 1]) if "--shared" in sys.argv else 0
     cfg = tracegen.get_config("c1_toy", n_replicas=world, hbm_blocks=64, host_blocks=16, compact_every=3,
-                              trace=dict(n=12 * world, n_initial=5 * world, seed=77))
+                              trace=dict(n=12 * world, n_initial=5 * world, seed=77),
+                              shared_prefix_tokens=spt)
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     api = "--api" in sys.argv
