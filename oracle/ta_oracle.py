@@ -77,6 +77,9 @@ STAT_KEYS = (
     # NEXT-1: STP cost ledger (token-ms, Eq. 2-3) and the Cost_unused bound
     "cost_decode", "cost_prefill", "cost_recompute", "cost_unused", "cost_caching",
     "unused_bound_checks", "unused_bound_violations",
+    # NEXT-4 guard: how far memory pressure had grown when the periodic monitor found it
+    # (context growth triggers thrashing mid-execution between checks)
+    "overshoot_blocks", "overshoot_max_blocks",
 )
 
 
@@ -384,6 +387,8 @@ class Oracle:
             if self.L[r] <= self.cap_max[r]:
                 continue
             dC = self.L[r] - self.cap_max[r]
+            self.stats["overshoot_blocks"] += dC          # reading A50
+            self.stats["overshoot_max_blocks"] = max(self.stats["overshoot_max_blocks"], dC)
             act = [p for p in range(self.N)
                    if self.status[p] in (REASONING, ACTING) and self.placement[p] == r]
             act.sort(key=lambda p: self.pause_key(p, nb[p]))
