@@ -168,6 +168,12 @@ typedef struct {               /* cumulative counters (order fixed; see DESIGN.m
    * wait -- and the Cost_unused < c_min bound of PAPER.md:415 per replica-tick. */
   uint64_t cost_decode, cost_prefill, cost_recompute, cost_unused, cost_caching;
   uint64_t unused_bound_checks, unused_bound_violations;
+  /* NEXT-4 guard (reading A50; "context growth ... can trigger memory
+   * thrashing mid-execution"): at each pause pass, the excess L_eff - lambda_max*C the
+   * periodic monitor found on a replica (blocks), summed over replica-ticks, and its
+   * maximum.  Shrinking delta_t_ms to one decode step (1000 / decode rate) bounds it by
+   * one step's growth. */
+  uint64_t overshoot_blocks, overshoot_max_blocks;
 } ta_stats_t;
 
 typedef struct {               /* trace-mode program scripts (tracegen layout; host pointers) */

@@ -72,7 +72,8 @@ STAT_KEYS = ("ticks", "arrivals", "stops", "pauses", "restores", "oversized_skip
 
 
 LEDGER_KEYS = ("cost_decode", "cost_prefill", "cost_recompute", "cost_unused", "cost_caching",
-               "unused_bound_checks", "unused_bound_violations")
+               "unused_bound_checks", "unused_bound_violations",
+               "overshoot_blocks", "overshoot_max_blocks")       # + the NEXT-4 guard counters
 
 
 class Stats(C.Structure):

@@ -33,7 +33,7 @@ enum StatIdx {
   ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST,
   ST_BASE_N,                                   // counters before block_bytes in ta_stats_t
   ST_COST_DECODE = ST_BASE_N, ST_COST_PREFILL, ST_COST_RECOMPUTE, ST_COST_UNUSED, ST_COST_CACHING,
-  ST_UNUSED_CHECKS, ST_UNUSED_VIOL, ST_N
+  ST_UNUSED_CHECKS, ST_UNUSED_VIOL, ST_OVERSHOOT, ST_OVERSHOOT_MAX, ST_N
 };
 
 // per-request descriptor kinds (step 5.5): copy from a peer's HBM, copy from a host

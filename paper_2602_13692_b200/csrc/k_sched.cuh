@@ -29,6 +29,10 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
     return;
   }
   const u32 dC = (u32)(Lr - cap);
+  if (threadIdx.x == 0) {                        // NEXT-4 guard: excess found by the monitor (A50)
+    atomicAdd(&d.stats[ST_OVERSHOOT], (ull)dC);
+    atomicMax(&d.stats[ST_OVERSHOOT_MAX], (ull)dC);
+  }
   const int N = d.N;
   const u32 NBK = d.nbk, sh = d.nb_shift;
   u64* ka = d.ska + (size_t)r * N;

@@ -622,6 +622,8 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
   out->cost_caching = st[ST_COST_CACHING];
   out->unused_bound_checks = st[ST_UNUSED_CHECKS];
   out->unused_bound_violations = st[ST_UNUSED_VIOL];
+  out->overshoot_blocks = st[ST_OVERSHOOT];
+  out->overshoot_max_blocks = st[ST_OVERSHOOT_MAX];
   for (int r = 0; r < d.R; ++r) {
     out->L[r] = L[r];
     u64 f = 0, g = 0;

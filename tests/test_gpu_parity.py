@@ -190,3 +190,10 @@ def test_gpu_shared_prefix_swe_decisions_full_n():
     cfg = tracegen.get_config("c2_swe", kv="mini", shared_prefix_tokens=1024)
     o, n = run_parity(cfg, 40, state_every=5, content_every=10, samples=8)
     assert n > 0
+
+
+def test_gpu_decode_step_guard():
+    """NEXT-4 guard: Delta t = one decode step (25 ms at 40 tok/s), 600 ticks; the
+    overshoot counters are among the compared stats."""
+    o, n = run_parity(stress(85, 2, NB=56, delta_t_ms=25), 600, state_every=10, content_every=20, seed=85)
+    assert n > 0 and o.stats["overshoot_blocks"] > 0
