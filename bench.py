@@ -20,6 +20,8 @@ import sys
 import threading
 import time
 
+JSON_OUT = sys.stdout                    # the one JSON line (fd 1 is redirected to stderr when N > 1)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -208,11 +210,13 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
 
 
 def workload(name, world):
-    """The bench workload at N GPUs: N replicas, 10k programs per replica (weak scaling)."""
+    """The bench workload at N GPUs: N replicas, 10k programs per replica (weak scaling):
+    N interleaved copies of the 1-GPU trace (tracegen.tile_trace), so every replica sees
+    the 1-GPU workload and per-GPU work stays fixed as N grows."""
     import tracegen
     cfg = tracegen.get_config(name)
     cfg["n_replicas"] = world
-    cfg["trace"]["n"] = cfg["trace"]["n"] * world
+    cfg["trace"]["tile"] = world
     return cfg
 
 
@@ -307,6 +311,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:                         # native libraries (NCCL's version banner) print to fd 1:
+        global JSON_OUT                   # send fd 1 to stderr, keep stdout for the JSON line
+        JSON_OUT = os.fdopen(os.dup(1), "w")
+        sys.stdout.flush()
+        os.dup2(2, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -454,9 +463,21 @@ def main():
     else:
         names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "evict_d2h+barrier",
                  "fetch_p2p_h2d+push+barrier", "fill", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
-    # the host-link peak of ONE GPU's link, measured by rank 0 while the others wait
+    # the host-link peak of ONE GPU's link, measured by rank 0 while the others wait; with
+    # N > 1 also with every rank copying at once (GPUs can share host-side PCIe / memory
+    # bandwidth): the floor uses the concurrent figure of the slowest rank, the physical
+    # limit when all replicas stream together
     peaks = pcie_peak(torch, dev) if (nh and rank == 0) else {"h2d": 1.0, "d2h": 1.0}
+    peaks_alone = dict(peaks)
     if world > 1:
+        dist.barrier()
+        if nh:
+            torch.cuda.synchronize()
+            dist.barrier()
+            pc = pcie_peak(torch, dev)
+            tpk = torch.tensor([pc["d2h"], pc["h2d"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(tpk, op=dist.ReduceOp.MIN)
+            peaks = {"d2h": float(tpk[0]), "h2d": float(tpk[1])}
         dist.barrier()
     # algorithmic bytes per GPU, tick by tick (telemetry counts are cluster totals; the
     # replicas are symmetric, so per GPU = total / N).  A movement phase's time floor is
@@ -497,7 +518,8 @@ def main():
                  else ("pcie" if dom == 3 else "pcie/nvlink"))
         psrc = (peak_src if dom == 7 else
                 f"measured in this run: pinned cudaMemcpyAsync 1 GiB (d2h {peaks['d2h']:.1f}, h2d {peaks['h2d']:.1f}"
-                f" GB/s); peak = bytes / floor, floor = max over replicas and links of (link bytes / link peak)")
+                f" GB/s{'' if world == 1 else ' per GPU with all %d GPUs copying at once; one GPU alone: d2h %.1f, h2d %.1f' % (world, peaks_alone['d2h'], peaks_alone['h2d'])}"
+                f"); peak = bytes / floor, floor = max over replicas and links of (link bytes / link peak)")
     else:
         byts_d = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
         achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
@@ -567,7 +589,8 @@ def main():
         "step_ms": step_ms,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        JSON_OUT.write(json.dumps(line) + "\n")
+        JSON_OUT.flush()
     pool.close()
     if world > 1:
         dist.destroy_process_group()

@@ -10,5 +10,5 @@ Shapes follow SURVEY.md §8(d) "Trace presets" (all parameters invented and
 labelled synthetic: the paper only gives qualitative tool-latency shapes,
 PAPER.md:775-808, 433, 445).
 """
-from .presets import PRESETS, Trace, gen_trace  # noqa: F401
+from .presets import PRESETS, Trace, gen_trace, tile_trace  # noqa: F401
 from .configs import CONFIGS, KV_SHAPES, get_config, make_trace  # noqa: F401

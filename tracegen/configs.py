@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import copy
 
-from .presets import gen_trace
+from .presets import gen_trace, tile_trace
 
 # KV shapes (2-byte elements).  toy: BASELINE.json configs[0]; q32: Qwen3-32B GQA
 # (64 layers, 8 KV heads, head dim 128), BASELINE.json configs[1].
@@ -80,4 +80,5 @@ def get_config(name: str, **override) -> dict:
 
 def make_trace(cfg: dict):
     t = cfg["trace"]
-    return gen_trace(t["mix"], t["n"], t["seed"], t["max_ctx"], t.get("n_initial"))
+    tr = gen_trace(t["mix"], t["n"], t["seed"], t["max_ctx"], t.get("n_initial"))
+    return tile_trace(tr, int(t.get("tile", 1)))

@@ -137,3 +137,19 @@ def gen_trace(mix, n: int, seed: int, max_ctx: int, n_initial: int | None = None
         n_initial=n if n_initial is None else int(n_initial),
         preset=names,
     )
+
+
+def tile_trace(tr: Trace, k: int) -> Trace:
+    """k interleaved copies of a trace (slot p*k + c is copy c of slot p, uid = slot + 1):
+    the weak-scaling workload for k replicas, where each replica sees the 1-replica
+    workload (copies of a program are adjacent, so restores alternate between replicas)."""
+    if k == 1:
+        return tr
+    n = tr.n_slots
+    src = np.repeat(np.arange(n), k)                     # slot s -> source slot s // k
+    lens = (tr.turn_off[1:] - tr.turn_off[:-1]).astype(np.int64)[src]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+    take = np.concatenate([np.arange(tr.turn_off[p], tr.turn_off[p + 1]) for p in src]).astype(np.int64)
+    return Trace(uid=np.arange(1, n * k + 1, dtype=np.uint32), p0=tr.p0[src].copy(), turn_off=offs,
+                 g=tr.g[take].copy(), d_ms=tr.d_ms[take].copy(), o=tr.o[take].copy(),
+                 n_initial=tr.n_initial * k, preset=[tr.preset[p] for p in src])
