@@ -30,7 +30,10 @@ enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_
 // prefixes, hit accounting.  The two per-block loops (one iteration per evicted block,
 // one per requested block) are split over all CTAs of the cluster: each copies the
 // leader's staged lists into its own shared memory through DSMEM, takes a contiguous
-// range, and appends to the leader's shared counters/bitmap with DSMEM atomics.
+// range, and appends to the leader's shared counters/bitmap with DSMEM atomics.  The
+// leader stays off both loops and off everything that does not depend on its chain:
+// rank 1 builds the host-tier select prefix (part A) and the allocation prefix (part
+// B), rank 2 orders the D2H copies (part B); the loops run on ranks 1..PLAN_CL-1.
 // Copy descriptors keep request order: per-CTA compaction into a staging buffer, then
 // placement at the prefix of the CTAs' counts.
 #define PLAN_CL 8
@@ -42,6 +45,39 @@ struct PlanSh {                  // leader's scalars, read by the cluster throug
 
 __device__ __forceinline__ void cl_copy(u32* dst, const u32* src, u32 n) {
   for (u32 i = threadIdx.x; i < n; i += CTA) dst[i] = src[i];
+}
+
+// Several (DSMEM) -> shared copies as one index space, four loads in flight per thread
+// (one loop per array would serialise their remote-load latencies).
+struct CpSeg { u32* dst; const u32* src; u32 n; };
+template <int K>
+__device__ __forceinline__ void cl_copy_segs(const CpSeg (&sg)[K]) {
+  u32 tot = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) tot += sg[k].n;
+  for (u32 i0 = threadIdx.x; i0 < tot; i0 += 4 * CTA) {
+    u32 v[4];
+    u32* dp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dp[u] = nullptr;
+      v[u] = 0;
+      u32 off = i0 + u * CTA;
+      if (off >= tot) continue;
+      const u32* sp = nullptr;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (sp == nullptr) {
+          if (off < sg[k].n) { sp = sg[k].src + off; dp[u] = sg[k].dst + off; }
+          else off -= sg[k].n;
+        }
+      }
+      v[u] = *sp;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dp[u]) *dp[u] = v[u];
+  }
 }
 
 __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int verb, u32* s_big, u32* s_tmp) {
@@ -64,12 +100,15 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
   u32* s_vp = reinterpret_cast<u32*>(sm->k[0]);        // [8192]
   u32* s_vn = s_vp + 8192;                             // [8192]
-  u32* s_fp = reinterpret_cast<u32*>(sm->k[0]);        // [2048] x 6 (after the eviction phase)
-  u32* s_fj = s_fp + 2048;
-  u32* s_fh = s_fp + 4096;
-  u32* s_fk = s_fp + 6144;
-  u32* s_fcn = s_fp + 8192;
-  u32* s_fu = s_fp + 10240;
+  // [FST_MAX] x 6 in the host-snapshot buffer: the leader fills them during the eviction
+  // phase (nobody reads the leader's copy of that buffer), the others after #3
+  constexpr u32 FST_MAX = 1024;
+  u32* s_fp = sm->p[0];
+  u32* s_fj = s_fp + FST_MAX;
+  u32* s_fh = s_fp + 2 * FST_MAX;
+  u32* s_fk = s_fp + 3 * FST_MAX;
+  u32* s_fcn = s_fp + 4 * FST_MAX;
+  u32* s_fu = s_fp + 5 * FST_MAX;
   PlanSh* L = cl.map_shared_rank(&sh, 0);              // leader's scalars
   const int N = d.N;
   const u32 bt = (u32)d.bt;
@@ -94,6 +133,12 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
 #pragma unroll
   for (int i = 0; i < PC_N; ++i) pc[i] = 0;
 
+  // ================= rank 1, concurrent with part A: host-tier free-word snapshot and
+  // its select prefix (the host bitmap is not touched before the eviction loop)
+  if (crank == 1) {
+    cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
+    cl_copy(s_sfw, sf, d.NHW);
+  }
   // ================= leader, part A: F_r, stall cut, eviction order, staging
   if (lead) {
     // ---- 5.1 F_r: REASONING programs placed on r, slot order, with their need
@@ -236,12 +281,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       }
       nv = (u32)upper_bound_u32(ecs_sm ? s_ec : ec, (int)ne, X - 1) + 1;   // victims
       PSTAMP(2, 13);
-      cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);      // host-slot select prefix
-      hfree = s_big[d.NHW];
-      // host-tier free words snapshot (selects read it, so the live bitmap can be
-      // updated in the same loop); victims' slot and HBM prefix length
+      // victims' slot and HBM prefix length (the host-tier snapshot and its select
+      // prefix are rank 1's)
       vst = nv <= 8192;
-      cl_copy(s_sfw, sf, d.NHW);
       if (vst)
         for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
       for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
@@ -261,116 +303,16 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     cl.sync();                                         // leader's smem outlives every reader
     return;
   }
-  if (X > 0) {
-    const u32 nv = L->nv, hfree = L->hfree, vst = L->vst, ecs_sm = L->ecs_sm;
-    if (!lead) {                                       // stage the leader's lists locally
-      if (ecs_sm) cl_copy(s_ec, cl.map_shared_rank(s_ec, 0), nv);
-      if (vst) {
-        cl_copy(s_vp, cl.map_shared_rank(s_vp, 0), nv);
-        cl_copy(s_vn, cl.map_shared_rank(s_vn, 0), nv);
-      }
-      cl_copy(s_sfw, cl.map_shared_rank(s_sfw, 0), d.NHW);
-      cl_copy(s_big, cl.map_shared_rank(s_big, 0), d.NHW + 1);
-      __syncthreads();
-    }
-    const u32* ecs = ecs_sm ? s_ec : ec;
-    u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
-    const u32 per = (X + PLAN_CL - 1) / PLAN_CL;
-    const u32 e_lo = crank * per, e_hi = min(X, e_lo + per);
-    // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
-    // four per thread per round so their block-table loads are in flight together
-    for (u32 e0 = e_lo; e0 < e_hi; e0 += 4 * CTA) {
-      u32 pk[4], jk[4], ik[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const u32 e = e0 + k * CTA + threadIdx.x;
-        pk[k] = jk[k] = ik[k] = 0;
-        if (e < e_hi) {
-          const u32 v = (u32)upper_bound_u32(ecs, (int)nv, e);
-          const u32 excl = v ? ecs[v - 1] : 0;
-          const u32 p = vst ? s_vp[v] : ep[v];
-          const u32 nh = vst ? s_vn[v] : d.n_hbm[p];
-          pk[k] = p;
-          jk[k] = nh - 1 - (e - excl);
-          ik[k] = d.loc[(size_t)p * d.MAXBP + jk[k]];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const u32 e = e0 + k * CTA + threadIdx.x;
-        if (e >= e_hi) continue;
-        const u32 idx = ik[k], j = jk[k], p = pk[k];
-        u32* ent = d.loc + (size_t)p * d.MAXBP + j;
-        atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
-        if (e < hfree) {
-          if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
-          const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
-          *ent = LOC_HOST | slot;
-          d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
-          evt[e] = EvDesc{idx, slot};
-          atomicAnd(&sf[slot >> 5], ~(1u << (slot & 31)));
-          atomicOr(&Lhw[idx >> 5], 1u << (idx & 31));
-        } else {
-          *ent = LOC_NONE;
-        }
-      }
-    }
-  }
-  PSTAMP(2, 16);
-  cl.sync();                                           // #2: evictions done
-  PSTAMP(2, 6);
-
-  // ================= leader, part B: D2H order, victims, allocation prefix, hit accounting
   FillDesc* fld = d.fld + (size_t)r * d.NB;
   if (lead) {
-    const u32 nv = sh.nv, hfree = sh.hfree, m = sh.m, nF = sh.nF;
+    // the leader, while the others evict: hit accounting of S_r (reads only S_r's rows
+    // and counters, which the evictions do not touch: victims are PAUSED / ACTING)
+    if (X > 0 && threadIdx.x == 0) sh.hfree = cl.map_shared_rank(s_big, 1)[d.NHW];   // rank 1's, before #2
+    const u32 m = sh.m, nF = sh.nF;
     const u32* fcs = sh.fcs_sm ? s_fc : fc;
-    if (X > 0) {
-      const u32* ecs = sh.ecs_sm ? s_ec : ec;
-      // D2H copies are issued in ascending HBM-block order, the order in which the
-      // allocation below hands the freed blocks out again, so a fetch that reuses an
-      // evicted block rarely waits for its eviction (fused movement kernel).
-      const u32 ntoh = min(X, hfree);
-      EvDesc* evd = d.evd + (size_t)r * d.NB;
-      cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);    // host prefix no longer needed
-      for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
-        const EvDesc x = evt[e];
-        const u32 k = s_big[x.src >> 5] + __popc(s_hw[x.src >> 5] & ((1u << (x.src & 31)) - 1));
-        evd[k] = x;
-      }
-      PSTAMP(2, 7);
-      for (u32 v = threadIdx.x; v < nv; v += CTA) {
-        u32 p = ep[v];
-        u32 excl = v ? ecs[v - 1] : 0;
-        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p] - d.sb;
-        u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
-        ta_decision rec;
-        rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
-        rec.to_host = toh; rec.dropped = take - toh;
-        rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
-        d.dec_ev[(size_t)r * N + v] = rec;
-        d.n_hbm[p] -= take;
-        d.n_host[p] += toh;
-      }
-      if (threadIdx.x == 0) {
-        d.ev_cnt[r] = nv;
-        d.evd_cnt[r] = ntoh;
-        d.t_rep[r] = ntoh;
-        atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
-        atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)ntoh);
-        atomicAdd(&d.ctr->t_d2h, ntoh);
-        atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - ntoh));
-      }
-      __syncthreads();
-    }
-    PSTAMP(2, 8);
-    // ---- 5.4 allocation prefix (after the evictions' frees) and free-word snapshot
-    cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
-    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
-    PSTAMP(2, 9);
     // per-program values the request loop reads for each of its blocks, staged for
     // S_r programs when they fit: slot, first needed j, home, c_kv, c, uid
-    const bool fst = m <= 2048;
+    const bool fst = m <= FST_MAX;
     ull l_dec = 0, l_pre = 0, l_rec = 0;             // NEXT-1 STP ledger (token-ms)
     // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
     for (u32 i = threadIdx.x; i < nF; i += CTA) {
@@ -449,8 +391,123 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       d.pst[2 * 32 + 29] = nF | (1ull << 62);
       d.pst[2 * 32 + 30] = sh.tot | (1ull << 62);
     }
+  } else if (X > 0) {
+    const u32 nv = L->nv, vst = L->vst, ecs_sm = L->ecs_sm;
+    {                                                  // the leader's lists, rank 1's host snapshot
+      const u32 n1 = crank == 1 ? 0u : 1u;
+      CpSeg sg[5] = {{s_ec, cl.map_shared_rank(s_ec, 0), ecs_sm ? nv : 0u},
+                     {s_vp, cl.map_shared_rank(s_vp, 0), vst ? nv : 0u},
+                     {s_vn, cl.map_shared_rank(s_vn, 0), vst ? nv : 0u},
+                     {s_sfw, cl.map_shared_rank(s_sfw, 1), n1 * (u32)d.NHW},
+                     {s_big, cl.map_shared_rank(s_big, 1), n1 * ((u32)d.NHW + 1)}};
+      cl_copy_segs(sg);
+      __syncthreads();
+    }
+    const u32 hfree = s_big[d.NHW];
+    const u32* ecs = ecs_sm ? s_ec : ec;
+    u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
+    const u32 per = (X + PLAN_CL - 2) / (PLAN_CL - 1); // ranks 1..PLAN_CL-1
+    const u32 e_lo = (crank - 1) * per, e_hi = min(X, e_lo + per);
+    // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
+    // four per thread per round so their block-table loads are in flight together
+    for (u32 e0 = e_lo; e0 < e_hi; e0 += 4 * CTA) {
+      u32 pk[4], jk[4], ik[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u32 e = e0 + k * CTA + threadIdx.x;
+        pk[k] = jk[k] = ik[k] = 0;
+        if (e < e_hi) {
+          const u32 v = (u32)upper_bound_u32(ecs, (int)nv, e);
+          const u32 excl = v ? ecs[v - 1] : 0;
+          const u32 p = vst ? s_vp[v] : ep[v];
+          const u32 nh = vst ? s_vn[v] : d.n_hbm[p];
+          pk[k] = p;
+          jk[k] = nh - 1 - (e - excl);
+          ik[k] = d.loc[(size_t)p * d.MAXBP + jk[k]];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u32 e = e0 + k * CTA + threadIdx.x;
+        if (e >= e_hi) continue;
+        const u32 idx = ik[k], j = jk[k], p = pk[k];
+        u32* ent = d.loc + (size_t)p * d.MAXBP + j;
+        atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
+        if (e < hfree) {
+          if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
+          const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
+          *ent = LOC_HOST | slot;
+          d.owner_host[(size_t)r * d.NH + slot] = p * (u32)d.MAXB + j;
+          evt[e] = EvDesc{idx, slot};
+          atomicAnd(&sf[slot >> 5], ~(1u << (slot & 31)));
+          atomicOr(&Lhw[idx >> 5], 1u << (idx & 31));
+        } else {
+          *ent = LOC_NONE;
+        }
+      }
+    }
   }
-  cl.sync();                                           // #3: allocation inputs staged
+  PSTAMP(2, 16);
+  cl.sync();                                           // #2: evictions done
+  PSTAMP(2, 6);
+
+  // ================= part B.  Rank 1: the allocation prefix, the only input of the
+  // request loop still missing; it is published by a split cluster barrier (#3), so
+  // the leader's victims and D2H order run beside the request loop, and the other ranks
+  // stage the leader's lists before they wait for it.
+  if (crank == 1) {
+    // ---- 5.4 allocation prefix (after the evictions' frees) and free-word snapshot
+    cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
+    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
+    __syncthreads();
+  }
+  cl.barrier_arrive();                                 // #3 (arrive; release)
+  if (lead && X > 0) {
+    // D2H copies are issued in ascending HBM-block order, the order in which the
+    // allocation hands the freed blocks out again, so a fetch that reuses an evicted
+    // block rarely waits for its eviction (fused movement kernel).
+    const u32 ntoh = min(X, sh.hfree);
+    EvDesc* evd = d.evd + (size_t)r * d.NB;
+    cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);      // s_hw: blocks evicted to host (bitmap)
+    for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
+      const EvDesc x = evt[e];
+      const u32 k = s_big[x.src >> 5] + __popc(s_hw[x.src >> 5] & ((1u << (x.src & 31)) - 1));
+      evd[k] = x;
+    }
+  }
+  if (lead) {
+    const u32 nv = sh.nv, hfree = sh.hfree;
+    if (X > 0) {
+      const u32* ecs = sh.ecs_sm ? s_ec : ec;
+      const u32 ntoh = min(X, hfree);
+      PSTAMP(2, 7);
+      for (u32 v = threadIdx.x; v < nv; v += CTA) {
+        u32 p = ep[v];
+        u32 excl = v ? ecs[v - 1] : 0;
+        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p] - d.sb;
+        u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
+        ta_decision rec;
+        rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
+        rec.to_host = toh; rec.dropped = take - toh;
+        rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
+        d.dec_ev[(size_t)r * N + v] = rec;
+        d.n_hbm[p] -= take;
+        d.n_host[p] += toh;
+      }
+      if (threadIdx.x == 0) {
+        d.ev_cnt[r] = nv;
+        d.evd_cnt[r] = ntoh;
+        d.t_rep[r] = ntoh;
+        atomicAdd(&d.stats[ST_EVICT_BLOCKS], (ull)X);
+        atomicAdd(&d.stats[ST_EVICT_TO_HOST], (ull)ntoh);
+        atomicAdd(&d.ctr->t_d2h, ntoh);
+        atomicAdd(&d.stats[ST_EVICT_DROPPED], (ull)(X - ntoh));
+      }
+      __syncthreads();
+    }
+    PSTAMP(2, 8);
+    PSTAMP(2, 9);
+  }
 
   PSTAMP(2, 17);
   // ================= all CTAs: the request loop, split by cluster rank
@@ -459,21 +516,31 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // live bitmap at once.  Only requests that move or write bytes get a descriptor
   // (copies; fills when the engine stand-in is on), compacted in request order.
   const u32 m = L->m, tot = L->tot, fst = L->fst, fcs_sm = L->fcs_sm;
-  if (!lead) {
-    if (fcs_sm) cl_copy(s_fc, cl.map_shared_rank(s_fc, 0), m);
-    if (fst)                                           // six arrays of 2048, m used each
-      for (u32 a = 0; a < 6; ++a) cl_copy(s_fp + a * 2048, cl.map_shared_rank(s_fp + a * 2048, 0), m);
-    cl_copy(s_hw, cl.map_shared_rank(s_hw, 0), d.NBW);
-    cl_copy(s_big, cl.map_shared_rank(s_big, 0), d.NBW + 1);
-    __syncthreads();
+  if (!lead) {                                         // the leader's lists (complete since #2)
+    const u32 mf = fst ? m : 0u;                       // six arrays of FST_MAX, m used each
+    CpSeg sg[7] = {{s_fc, cl.map_shared_rank(s_fc, 0), fcs_sm ? m : 0u},
+                   {s_fp, cl.map_shared_rank(s_fp, 0), mf},
+                   {s_fj, cl.map_shared_rank(s_fj, 0), mf},
+                   {s_fh, cl.map_shared_rank(s_fh, 0), mf},
+                   {s_fk, cl.map_shared_rank(s_fk, 0), mf},
+                   {s_fcn, cl.map_shared_rank(s_fcn, 0), mf},
+                   {s_fu, cl.map_shared_rank(s_fu, 0), mf}};
+    cl_copy_segs(sg);
   }
+  cl.barrier_wait();                                   // #3 (wait; acquire): rank 1's prefix
+  if (crank >= 2) {                                    // rank 1's free snapshot and prefix
+    CpSeg sg[2] = {{s_hw, cl.map_shared_rank(s_hw, 1), (u32)d.NBW},
+                   {s_big, cl.map_shared_rank(s_big, 1), (u32)d.NBW + 1}};
+    cl_copy_segs(sg);
+  }
+  __syncthreads();
   const u32* fcs = fcs_sm ? s_fc : fc;
   const u32* hws = s_hw;
   u32* dfh = d.dfh + (size_t)r * d.NB;
   u32* dfs = d.dfs + (size_t)r * d.NB;
   u32* Lapp = cl.map_shared_rank(s_app, 0);            // leader's append counters
-  const u32 per = (tot + PLAN_CL - 1) / PLAN_CL;
-  const u32 q_lo = min(tot, crank * per), q_hi = min(tot, q_lo + per);
+  const u32 per = (tot + PLAN_CL - 2) / (PLAN_CL - 1);  // ranks 1..PLAN_CL-1; the leader has none
+  const u32 q_lo = lead ? tot : min(tot, (crank - 1) * per), q_hi = lead ? tot : min(tot, q_lo + per);
   FeDesc* fstage = d.fedt + (size_t)r * d.NB + q_lo;  // this CTA's descriptors, compacted
   u32 nfed = 0;
   for (u32 q0 = q_lo; q0 < q_hi; q0 += 2 * CTA) {
