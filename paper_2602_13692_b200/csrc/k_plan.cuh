@@ -41,6 +41,7 @@ enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_
 struct PlanSh {                  // leader's scalars, read by the cluster through DSMEM
   u32 stop, X, hfree, nv, vst, ecs_sm, m, tot, fst, fcs_sm, nF;
   u32 fcnt[PLAN_CL];
+  ull fr, es;                    // free blocks and eviction supply (rank 2, before #0)
 };
 
 __device__ __forceinline__ void cl_copy(u32* dst, const u32* src, u32 n) {
@@ -139,10 +140,29 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     cl_copy(s_sfw, sf, d.NHW);
   }
+  // ================= rank 2, concurrent with F_r: free blocks on r and eviction supply
+  if (crank == 2) {
+    ull fr = 0, es = 0;
+    for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
+    const u32* el = d.ec_list + (size_t)r * N;      // home == r with HBM blocks (footprint pass)
+    const int nel = (int)d.ec_cnt[r];
+    for (int i = threadIdx.x; i < nel; i += CTA) {
+      const u32 p = el[i];
+      const u8 s = d.status[p];
+      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p] - d.sb;   // private HBM blocks
+    }
+    auto add = [](ull a, ull b) { return a + b; };
+    fr = cta_reduce<ull>(fr, s_red, add, 0ull);
+    es = cta_reduce<ull>(es, s_red, add, 0ull);
+    if (threadIdx.x == 0) { L->fr = fr; L->es = es; }   // into the leader's scalars
+  }
   // ================= leader, part A: F_r, stall cut, eviction order, staging
+  {                                                    // part A scope
+  u32 nF = 0;
+  bool fcs_sm = false;
+  const u32* fcs = fc;
   if (lead) {
     // ---- 5.1 F_r: REASONING programs placed on r, slot order, with their need
-    u32 nF;
     if (verb) {
       if (threadIdx.x == 0) {
         u32 p = d.ctr->verb_pid;
@@ -180,23 +200,16 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
     // short lists are searched many times below: stage them in shared memory
-    const bool fcs_sm = nF <= 4096;
+    fcs_sm = nF <= 4096;
     if (fcs_sm) cl_copy(s_fc, fc, nF);
-    const u32* fcs = fcs_sm ? s_fc : fc;
+    fcs = fcs_sm ? s_fc : fc;
     PSTAMP(2, 1);
-    // ---- free blocks on r and eviction supply
-    ull fr = 0, es = 0;
-    for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
+  }
+  cl.sync();                                           // #0: rank 2's supply reaches the leader
+  if (lead) {
     const u32* el = d.ec_list + (size_t)r * N;      // home == r with HBM blocks (footprint pass)
     const int nel = (int)d.ec_cnt[r];
-    for (int i = threadIdx.x; i < nel; i += CTA) {
-      const u32 p = el[i];
-      const u8 s = d.status[p];
-      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p] - d.sb;   // private HBM blocks
-    }
-    auto add = [](ull a, ull b) { return a + b; };
-    fr = cta_reduce<ull>(fr, s_red, add, 0ull);
-    es = cta_reduce<ull>(es, s_red, add, 0ull);
+    const ull fr = sh.fr, es = sh.es;
     const ull supply = fr + es;
     // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
     const u32 m = nF ? (u32)upper_bound_u32(fcs, (int)nF, supply > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)supply) : 0;
@@ -294,6 +307,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       sh.m = m; sh.tot = stop ? 0 : tot; sh.nF = nF; sh.fcs_sm = fcs_sm;
     }
   }
+  }                                                    // part A scope
   cl.sync();                                           // #1: part A visible to the cluster
 
   // ================= all CTAs: the eviction loop, split by cluster rank
