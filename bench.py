@@ -115,22 +115,28 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback B200_PROFILING.md (6.65 TB/s)"
 
 
-def pcie_peak(torch, dev):
-    """Measured pinned cudaMemcpyAsync peak per direction (1 GiB, best of 5)."""
+def pcie_peak(torch, dev, barrier=None):
+    """Measured pinned cudaMemcpyAsync peak per direction (1 GiB, best of 5).  With a
+    `barrier` (all ranks copying at once) each direction starts together on every rank
+    and the median of 5 copies is kept: a best-of figure would pick a copy that ran
+    while the other ranks were already done (tools/pcie_concurrent.py)."""
     n = 1 << 30
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=dev)
     out = {}
     for name, (dst, src) in (("h2d", (d, h)), ("d2h", (h, d))):
-        best = 0.0
+        if barrier is not None:
+            torch.cuda.synchronize()
+            barrier()
+        vals = []
         for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             dst.copy_(src, non_blocking=True)
             e1.record()
             e1.synchronize()
-            best = max(best, n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
-        out[name] = best
+            vals.append(n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = max(vals) if barrier is None else sorted(vals)[len(vals) // 2]
     del h, d
     return out
 
@@ -480,7 +486,7 @@ def main():
         if nh:
             torch.cuda.synchronize()
             dist.barrier()
-            pc = pcie_peak(torch, dev)
+            pc = pcie_peak(torch, dev, barrier=dist.barrier)
             tpk = torch.tensor([pc["d2h"], pc["h2d"]], dtype=torch.float64, device=dev)
             dist.all_reduce(tpk, op=dist.ReduceOp.MIN)
             peaks = {"d2h": float(tpk[0]), "h2d": float(tpk[1])}
