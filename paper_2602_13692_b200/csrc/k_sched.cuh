@@ -98,7 +98,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
   extern __shared__ __align__(16) char dsm[];
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   const int N = d.N, R = d.R;
-  const u32 NBK = d.nbk, sh = d.nb_shift;
+  const u32 NBK = d.nbk;
   u64* ka = d.ska + (size_t)R * N;
   u64* kb = d.skb + (size_t)R * N;
   u32* va = d.sva + (size_t)R * N;

@@ -26,7 +26,7 @@ __global__ void k_verb_reset(Dev d) {
 __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode) {
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
-  __shared__ int s_err, s_r, s_h;
+  __shared__ int s_err, s_h;
   __shared__ u32 s_nh;
   if (threadIdx.x == 0) {
     int err = TA_OK;
@@ -47,7 +47,6 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
       d.pause_list[(size_t)r * d.N] = pid;
       d.pause_cnt[r] = 1;
       d.stats[ST_PAUSES] += 1;
-      s_r = r;
       s_h = d.home[pid];
       u32 nh = 0;                          // HBM prefix length (I10)
       const u32* row = d.loc + (size_t)pid * d.MAXBP;

@@ -276,7 +276,7 @@ static void launch_coop(void (*k)(Args...), int grid, size_t smem, cudaStream_t 
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
+  lc.numAttrs = grid > 1 ? 1 : 0;       // one CTA needs no co-residency guarantee
   cudaLaunchKernelEx(&lc, k, args...);
 }
 
