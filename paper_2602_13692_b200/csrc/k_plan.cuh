@@ -633,11 +633,13 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     const u32 v = __reduce_add_sync(FULL_MASK, pc[i]);
     if (lane_id() == 0 && v) atomicAdd(&s_pc[i], (ull)v);
   }
-  if (threadIdx.x == 0) L->fcnt[crank] = nfed;
+  // every CTA's count into every CTA's copy, so nothing is read remotely after #4 and
+  // no CTA has to outlive the others (no closing cluster barrier)
+  if (threadIdx.x < PLAN_CL) cl.map_shared_rank(&sh, threadIdx.x)->fcnt[crank] = nfed;
   cl.sync();                                           // #4: counts of every CTA known
   u32 base = 0, total_fed = 0;
   for (u32 c = 0; c < PLAN_CL; ++c) {
-    const u32 n = L->fcnt[c];
+    const u32 n = sh.fcnt[c];
     if (c < crank) base += n;
     total_fed += n;
   }
@@ -671,7 +673,6 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     }
   }
   PSTAMP(2, 11);
-  cl.sync();                                           // #5: leader's smem outlives every reader
   PSTAMP(2, 12);
 }
 
