@@ -37,8 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libta.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:   # registers / spills per kernel
+        f.write("".join(ln for ln in r.stderr.splitlines(True) if "Compile time" not in ln))
     os.replace(LIB + ".tmp", LIB)
     return LIB
 
