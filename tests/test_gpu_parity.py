@@ -197,3 +197,11 @@ def test_gpu_decode_step_guard():
     overshoot counters are among the compared stats."""
     o, n = run_parity(stress(85, 2, NB=56, delta_t_ms=25), 600, state_every=10, content_every=20, seed=85)
     assert n > 0 and o.stats["overshoot_blocks"] > 0
+
+
+def test_gpu_shared_prefix_configs3_full_n():
+    """configs[2] (2k mixed programs, 8 replicas on one GPU, decision-only KV shape) with a
+    960-token shared system prompt (every preset's prompt is at least 1,000 tokens)."""
+    cfg = tracegen.get_config("c3_mixed", kv="mini", shared_prefix_tokens=960)
+    o, n = run_parity(cfg, 20, state_every=4, content_every=4, samples=8)
+    assert n > 0 and o.sb == 60
