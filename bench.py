@@ -537,18 +537,18 @@ def main():
         achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
         peak, bound, psrc = hbm_peak, "hbm", peak_src
     # traffic: DRAM bytes per launch, from the committed ncu --set full capture of the same
-    # kernel (profiles/r1d_move_traffic.json: measured DRAM / algorithmic bytes of two
+    # kernel (profiles/r1e_move_traffic.json: measured DRAM / algorithmic bytes of two
     # launch) applied to this run's algorithmic bytes per launch
     traffic = None
     if dom == 3 and world == 1:          # the captured kernel is the single-process fused one
         try:
-            with open(os.path.join(ROOT, "profiles", "r1d_move_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r1e_move_traffic.json")) as f:
                 traffic = round(byts[3] * json.load(f)["ratio_dram_to_algorithmic"])
         except (OSError, KeyError, ValueError):
             traffic = None
     roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
                 "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
-                "traffic_source": "ncu --set full capture (profiles/r1d_move_traffic.json) ratio x algorithmic bytes",
+                "traffic_source": "ncu --set full capture (profiles/r1e_move_traffic.json) ratio x algorithmic bytes",
                 "share_of_step": round(float(ph[dom] / ph.sum()), 4), "peak_source": psrc}
     kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
     if world > 1:
