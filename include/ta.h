@@ -20,8 +20,14 @@
  *    SPEC.md:82, 283).  All device work is stream-ordered on the context stream.
  *  - Multi-replica: replica state (program table, block tables, bitmaps) is
  *    replicated on every rank; each rank holds the KV pools of
- *    `replicas_here` replicas starting at `first_replica`.  ta_sched_step is
- *    then collective: every rank passes the same now_ms and events.
+ *    `replicas_here` replicas starting at `first_replica`.  In multi-process
+ *    mode (one replica per process) ta_sched_step, ta_pause, ta_resume,
+ *    ta_migrate and ta_set_health are COLLECTIVE: every rank makes the same
+ *    call with the same arguments, in the same order (they change replicated
+ *    state and run the cross-process device barriers of the movement step; a
+ *    call made on one rank only waits ~15 s at the barrier and returns
+ *    TA_E_PEER).  Replicas marked unhealthy (ta_set_health) are skipped by the
+ *    barriers, so the surviving ranks keep ticking after a failover.
  *  - Block-table entry encoding (u32): TA_LOC_NONE = no KV; bit 31 clear =
  *    HBM block index on the program's home replica; bit 31 set = slot index in
  *    the home replica's pinned host tier.
@@ -79,9 +85,15 @@ enum {
   TA_F_NO_FUSE = 1u << 5,      /* single process: separate evict / fetch / fill kernels (A/B aid) */
   TA_F_PINNED_ROUTING = 1u << 6, /* baseline (NEXT-2): program p bound to replica p mod R, per-replica
                                   queues instead of the global queue (reading A45) */
-  TA_F_REQUEST_AWARE = 1u << 7  /* baseline (NEXT-2): stateless request-level engine -- running
+  TA_F_REQUEST_AWARE = 1u << 7, /* baseline (NEXT-2): stateless request-level engine -- running
                                   requests preempted latest program first, FCFS waiting queue, LRU
                                   eviction of idle caches; pass an all-zero decay table (A46) */
+  TA_F_SMALL_PATHS = 1u << 8    /* test aid: lower the size thresholds of the shared-memory fast
+                                  paths (CTA sort 4096 -> 64, rank sort 512 -> 16, staged planner
+                                  lists 4096 / 8192 / 1024 -> 8 / 8 / 4, slot-bitmap ordering off,
+                                  restore chunks 32..4096 -> 4..64, restore buckets <= 8) so that
+                                  small runs take the code paths of full-size runs.  Results are
+                                  identical; only the speed differs. */
 };
 
 typedef struct {
@@ -310,6 +322,16 @@ ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
  * out[32*k + i], k = 0 pause, 1 restore, 2 plan, 3 reserved; 0 = phase not reached.
  * n <= 128.  Synchronizes the stream.  Errors: TA_E_STATE (no TA_F_TIMING). */
 ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n);
+
+/* Developer / test aid: cumulative size-branch counters since ta_init_pool, out[i] =
+ * how many times branch i ran: [0] CTA radix sort (n above the shared-memory sort
+ * limit) [1] bitonic sort [2] rank sort [3] planner F_r ordered by a sort (slot-bitmap
+ * ordering off) [4] planner need prefix in global memory [5] eviction prefix in global
+ * memory [6] victims in global memory [7] request loop reading program values from
+ * global memory [8] restore-pass chunks after the first [9] replica-ticks with
+ * evictions; [10, 16) reserved.  n <= 16.  Synchronizes the stream. */
+#define TA_DEBUG_COUNTERS 16
+ta_status ta_debug_counters(ta_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Block-list-driven KV movement (the copy engine of step 6, exposed directly):
  * copy n whole KV blocks, block src_blocks[i] of the source pool to block

@@ -20,6 +20,7 @@ TA_OK, TA_E_INVAL, TA_E_NOMEM, TA_E_DUP_ID, TA_E_UNKNOWN_PROGRAM = 0, 1, 2, 3, 4
 TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA_E_STATE = 5, 6, 7, 8, 9, 10
 F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE, F_PINNED_ROUTING = 1, 2, 4, 8, 16, 32, 64
 F_REQUEST_AWARE = 128
+F_SMALL_PATHS = 256                  # test aid: small runs take the full-size code paths
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",
@@ -133,6 +134,7 @@ def lib():
             "ta_stats": [vp, vp],
             "ta_phase_times": [vp, C.POINTER(C.c_float), i32],
             "ta_debug_phase_stamps": [vp, C.POINTER(C.c_uint64), i32],
+            "ta_debug_counters": [vp, C.POINTER(C.c_uint64), i32],
             "ta_verify_content": [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
             "ta_debug_state": [vp, i32, vp],
             "ta_move_blocks": [vp, i32, i32, i32, vp, vp, i32],
@@ -157,7 +159,9 @@ EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_tra
             "ta_pause", "ta_resume", "ta_migrate", "ta_stats", "ta_phase_times", "ta_verify_content",
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
             "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk",
-            "ta_debug_phase_stamps", "ta_set_health")
+            "ta_debug_phase_stamps", "ta_set_health", "ta_debug_counters")
+DEBUG_COUNTERS = ("radix_sort", "bitonic_sort", "rank_sort", "plan_f_sort", "plan_f_global", "plan_e_global",
+                  "plan_v_global", "plan_fst_global", "restore_chunks", "evict_ticks")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 
@@ -390,6 +394,12 @@ class Pool:
             # sizes recorded next to the stamps (bit 62 set): ("n<i>", value)
             out[name] += [(f"n{i}", a[32 * k + i] & ((1 << 62) - 1)) for i in range(32) if a[32 * k + i] >> 62 == 1]
         return out
+
+    def debug_counters(self) -> dict:
+        """Size-branch counters (ta_debug_counters): how often each large-size path ran."""
+        a = (C.c_uint64 * 16)()
+        self._chk(lib().ta_debug_counters(self.ctx, a, 16), "ta_debug_counters")
+        return {n: int(a[i]) for i, n in enumerate(DEBUG_COUNTERS)}
 
     def verify_content(self):
         bad, seen = C.c_uint64(), C.c_uint64()

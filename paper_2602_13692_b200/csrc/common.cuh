@@ -165,7 +165,30 @@ struct Dev {
   u32* rb;                         // [N] restore bucket of a PAUSED slot, else 0xFFFFFFFF
   i8* fpl;                         // [N] placement at footprint time (-1: not active)
   ull* gsync;                      // [2] grid-barrier counters of k_decide / k_close (monotone)
+  ull* dbg;                        // [DBG_N] size-branch counters (ta_debug_counters)
 };
+
+// Size-branch counters: how often each large-size / fallback code path ran (test
+// evidence that parity runs reach them; ta_debug_counters).
+enum DbgIdx {
+  DBG_RADIX = 0,        // CTA sort of n > sort limit: global-memory radix sort
+  DBG_BITONIC,          // register/shared bitonic network (rank limit < n <= sort limit)
+  DBG_RANK,             // rank sort (n <= rank limit)
+  DBG_F_SORT,           // k_plan F_r ordered by a sort (N beyond the slot-bitmap limit)
+  DBG_F_GLOBAL,         // k_plan need prefix read from global memory (nF > staging limit)
+  DBG_E_GLOBAL,         // k_plan eviction prefix read from global memory (ne > staging limit)
+  DBG_V_GLOBAL,         // k_plan victims read from global memory (nv > victim staging limit)
+  DBG_FST_GLOBAL,       // k_plan request loop reads per-program values from global (m > FST limit)
+  DBG_RESTORE_CHUNKS,   // restore pass chunks after the first
+  DBG_EVICT_TICKS,      // k_plan replica-ticks with X > 0
+  DBG_N = 16
+};
+__device__ __forceinline__ void dbg_hit(const Dev& d, int i) {
+  if (threadIdx.x == 0) atomicAdd(&d.dbg[i], 1ull);
+}
+// Size thresholds of the shared-memory fast paths.  TA_F_SMALL_PATHS (test aid) lowers
+// them so that toy-sized runs take the branches of full-size runs.
+__device__ __forceinline__ bool small_paths(const Dev& d) { return (d.flags & TA_F_SMALL_PATHS) != 0; }
 
 // Barrier across the CTAs of a cooperative launch (all co-resident).  Counter k is
 // used by one kernel only and grows by gridDim.x per barrier, so arrival t waits for
@@ -488,15 +511,28 @@ __device__ __forceinline__ void cta_rank_sort(const u64* ka, u64* kb, u32* vb, i
   __syncthreads();
 }
 
+// Which sort runs for n items (TA_F_SMALL_PATHS: 64 / 16 instead of 4096 / 512), and
+// the counter of the branch taken.
+struct SortLim { int small, rank; ull* cnt; };
+__device__ __forceinline__ SortLim sort_lim(const Dev& d) {
+  return small_paths(d) ? SortLim{64, 16, d.dbg} : SortLim{SORT_SMALL, RANK_SORT_MAX, d.dbg};
+}
+__device__ __forceinline__ void sort_count(const SortLim& L, int i) {
+  if (threadIdx.x == 0) atomicAdd(&L.cnt[i], 1ull);
+}
+
 // Stable sort of (ka, va)[0, n) by key.  Returns 0 if the result is in (ka, va),
 // 1 if in (kb, vb).  The buffer not holding the result is free scratch afterwards.
-__device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm) {
+__device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm,
+                        const SortLim& L) {
   if (n <= 1) return 0;
-  if (n > SORT_SMALL) return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp);
-  if (n <= RANK_SORT_MAX) {
+  if (n > L.small) { sort_count(L, DBG_RADIX); return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp); }
+  if (n <= L.rank) {
+    sort_count(L, DBG_RANK);
     cta_rank_sort(ka, kb, vb, n, sm, false, va);
     return 1;
   }
+  sort_count(L, DBG_BITONIC);
   int P = 32;
   while (P < n) P <<= 1;
   const int E = P > CTA ? P / CTA : 1;        // 1, 2 or 4 pairs per thread
@@ -573,13 +609,16 @@ __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, 
 // Sort (ka, va)[0, n) by (key, val) lexicographic, val unique (a slot or a
 // slot-derived tie-break): the result does not depend on the input order, so inputs
 // may come from unordered (atomic) appends.  Returns 0 / 1 like cta_sort.
-__device__ int cta_sort_kv(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm) {
+__device__ int cta_sort_kv(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, u32* s_tmp, SortSmem* sm,
+                           const SortLim& L) {
   if (n <= 1) return 0;
-  if (n > SORT_SMALL) return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp, true);
-  if (n <= RANK_SORT_MAX) {
+  if (n > L.small) { sort_count(L, DBG_RADIX); return cta_radix_sort(ka, va, kb, vb, n, s_hist, s_tmp, true); }
+  if (n <= L.rank) {
+    sort_count(L, DBG_RANK);
     cta_rank_sort(ka, kb, vb, n, sm, true, va);
     return 1;
   }
+  sort_count(L, DBG_BITONIC);
   int P = 32;
   while (P < n) P <<= 1;
   const int E = P > CTA ? P / CTA : 1;

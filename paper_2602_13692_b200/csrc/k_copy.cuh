@@ -207,7 +207,7 @@ __global__ void k_barrier(Dev d) {
   if (threadIdx.x == 0) e = ++(*d.epoch);
   __syncthreads();
   const int i = threadIdx.x;
-  if (i >= d.R || i == d.rank) return;
+  if (i >= d.R || i == d.rank || !((d.healthy >> i) & 1u)) return;   // failed replicas are not waited for
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(d.mbox_peer[i] + d.rank), "l"(e) : "memory");
   ull v = 0;
@@ -219,8 +219,12 @@ __global__ void k_barrier(Dev d) {
   d.ctr->err = TA_E_PEER;
 }
 
-// Two-finger compaction moves inside one replica's HBM pool (D2D).
+// Two-finger compaction moves inside one replica's HBM pool (D2D).  A tick that did
+// not run (rejected API batch, peer failure) planned no compaction: the descriptor list
+// still holds the previous tick's moves, whose destinations the engine may have written
+// since, so nothing is copied.
 __global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
+  if (d.ctr->err != TA_OK) return;
   const int nseg = 2 * d.nL;
   const i64 items = local_items(d, d.cpd_cnt, nseg);
   BulkCtx bk = bulk_begin(d);
@@ -299,16 +303,28 @@ __global__ void __launch_bounds__(256) k_fill(Dev d) {
   }
 }
 
-__device__ __forceinline__ void wait_evicted(const u32* flag, bool sys) {
+// Wait until every segment of the destination block has been read by its eviction.
+// The grid is co-resident (cooperative launch), so a local wait always ends; a wait
+// over NVLink on a peer's flag is bounded (~10 s): a dead peer sets TA_E_PEER, and the
+// CTA skips the copy (returns false) instead of hanging.
+__device__ __forceinline__ bool wait_evicted(const Dev& d, const u32* flag, bool sys) {
+  __shared__ int s_ok;
   if (threadIdx.x == 0) {
     u32 v;
+    long long spin = 0;
+    int ok = 1;
     do {
       if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
       else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-      if (v) __nanosleep(64);
+      if (v) {
+        __nanosleep(64);
+        if (++spin > (1ll << 27)) { d.ctr->err = TA_E_PEER; ok = 0; break; }
+      }
     } while (v);
+    s_ok = ok;
   }
   __syncthreads();
+  return s_ok != 0;
 }
 
 // The movement of one tick in ONE kernel (step 6): even CTAs run the D2H evictions,
@@ -328,7 +344,8 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   const int role = blockIdx.x & 1;
   const int G = gridDim.x >> 1;
   const int me = blockIdx.x >> 1;
-  if (d.api_mode && d.ctr->err != TA_OK) return;       // rejected API batch
+  // rejected API batch, or a peer failure in any mode: the lists are not this tick's
+  if (d.ctr->err == TA_E_PEER || (d.api_mode && d.ctr->err != TA_OK)) return;
   i64 n_push = 0;
   if (d.multi)
     for (int r = 0; r < d.R; ++r)
@@ -378,15 +395,16 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
     FeDesc x = d.fed[(size_t)r * d.NB + e];
     if (x.kind == MV_NONE) continue;
     if (push && (x.kind != MV_H2D || d.host[x.src_r] == nullptr)) continue;   // not from this tier
+    if (push && !((d.healthy >> r) & 1u)) continue;   // a failed replica receives nothing
     if (x.kind == MV_FILL) {                        // new / recomputed tokens (single process)
       if (d.multi) continue;
-      wait_evicted(&evp_of(d, r)[x.dst], false);
+      if (!wait_evicted(d, &evp_of(d, r)[x.dst], false)) continue;
       fill_segment(d, r, x.dst, s, x.uid, x.j, x.t0, x.t1);
       continue;
     }
     const char* sbase = x.kind == MV_P2P ? d.hbm[x.src_r] : d.host[x.src_r];
     if (sbase == nullptr) continue;                 // H2D from a peer's tier: pushed by its owner
-    wait_evicted(&evp_of(d, r)[x.dst], push);
+    if (!wait_evicted(d, &evp_of(d, r)[x.dst], push)) continue;
     const i64 snb = x.kind == MV_P2P ? d.NB : d.NH;
     const uint4* src = (const uint4*)seg_addr((char*)sbase, d.layout, snb, d.seg_bytes, nseg, x.src, s);
     uint4* dst = (uint4*)seg_addr(d.hbm[r], d.layout, d.NB, d.seg_bytes, nseg, x.dst, s);
@@ -402,7 +420,7 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
       int r, s; u32 e;
       locate(d, d.fld_cnt, it, nseg, &r, &e, &s);
       FillDesc x = d.fld[(size_t)r * d.NB + e];
-      wait_evicted(&evp_of(d, r)[x.idx], false);
+      if (!wait_evicted(d, &evp_of(d, r)[x.idx], false)) continue;
       fill_segment(d, r, x.idx, s, x.uid, x.j, x.t0, x.t1);
     }
   }

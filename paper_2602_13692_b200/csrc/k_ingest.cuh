@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(CTA, 1) k_ev_multi(const __grid_constant__ Dev
   if (nm > 0) {
     for (int i = threadIdx.x; i < nm; i += CTA) d.ev_mv[i] = 0;
     __syncthreads();
-    const int res = cta_sort(d.ev_mk, d.ev_mv, d.ev_mk2, d.ev_mv2, nm, s_big, s_tmp, sm);
+    const int res = cta_sort(d.ev_mk, d.ev_mv, d.ev_mk2, d.ev_mv2, nm, s_big, s_tmp, sm, sort_lim(d));
     const u64* k = res ? d.ev_mk2 : d.ev_mk;
     for (int q = threadIdx.x; q < nm; q += CTA) {     // one thread per program: its events in order
       const u32 p = (u32)(k[q] >> 32);

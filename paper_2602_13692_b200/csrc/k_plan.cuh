@@ -187,10 +187,11 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r && d.fpl[i] != r; },
           [&](u32 pos, int i) { fka[n1 + pos] = 0; fva[n1 + pos] = (u32)i; });
       nF = n1 + n2;
-      if (N <= 32 * 8192) {              // slot order by rank in a slot bitmap (sort buffers free)
+      if (N <= 32 * 8192 && !small_paths(d)) {   // slot order by rank in a slot bitmap (sort buffers free)
         cta_slot_order(fva, (int)nF, N, fp, sm->p[0], s_big, s_tmp);
       } else {
-        const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm);
+        dbg_hit(d, DBG_F_SORT);
+        const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm, sort_lim(d));
         const u32* fs = res ? fvb : fva;
         for (u32 i = threadIdx.x; i < nF; i += CTA) fp[i] = fs[i];
         __syncthreads();
@@ -200,7 +201,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
     // short lists are searched many times below: stage them in shared memory
-    fcs_sm = nF <= 4096;
+    fcs_sm = nF <= (small_paths(d) ? 8u : 4096u);
+    if (!fcs_sm) dbg_hit(d, DBG_F_GLOBAL);
     if (fcs_sm) cl_copy(s_fc, fc, nF);
     fcs = fcs_sm ? s_fc : fc;
     PSTAMP(2, 1);
@@ -276,7 +278,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         d.pst[2 * 32 + 27] = ne | (1ull << 62);
         d.pst[2 * 32 + 28] = X | (1ull << 62);
       }
-      int res = cta_sort_kv(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm);
+      int res = cta_sort_kv(ka, va, kb, vb, (int)ne, s_big, s_tmp, sm, sort_lim(d));
       const u64* sk = res ? kb : ka;
       const u32* sv = res ? vb : va;
       PSTAMP(2, 5);
@@ -287,7 +289,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       }
       __syncthreads();
       cta_incl_scan_array(ec, (int)ne, s_tmp);
-      ecs_sm = ne <= 4096;
+      ecs_sm = ne <= (small_paths(d) ? 8u : 4096u);
+      if (!ecs_sm) dbg_hit(d, DBG_E_GLOBAL);
+      dbg_hit(d, DBG_EVICT_TICKS);
       if (ecs_sm) {
         cl_copy(s_ec, ec, ne);
         __syncthreads();
@@ -296,7 +300,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       PSTAMP(2, 13);
       // victims' slot and HBM prefix length (the host-tier snapshot and its select
       // prefix are rank 1's)
-      vst = nv <= 8192;
+      vst = nv <= (small_paths(d) ? 8u : 8192u);
+      if (!vst) dbg_hit(d, DBG_V_GLOBAL);
       if (vst)
         for (u32 v = threadIdx.x; v < nv; v += CTA) { const u32 p = ep[v]; s_vp[v] = p; s_vn[v] = d.n_hbm[p]; }
       for (int w = threadIdx.x; w < d.NBW; w += CTA) s_hw[w] = 0;   // blocks evicted to host (bitmap)
@@ -326,7 +331,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     const u32* fcs = sh.fcs_sm ? s_fc : fc;
     // per-program values the request loop reads for each of its blocks, staged for
     // S_r programs when they fit: slot, first needed j, home, c_kv, c, uid
-    const bool fst = m <= FST_MAX;
+    const bool fst = m <= (small_paths(d) ? 4u : FST_MAX);
+    if (!fst) dbg_hit(d, DBG_FST_GLOBAL);
     ull l_dec = 0, l_pre = 0, l_rec = 0;             // NEXT-1 STP ledger (token-ms)
     // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
     for (u32 i = threadIdx.x; i < nF; i += CTA) {

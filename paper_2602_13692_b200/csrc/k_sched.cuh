@@ -55,7 +55,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
                      : pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
         va[pos] = (u32)i;
       });
-  int res = cta_sort_kv(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
+  int res = cta_sort_kv(ka, va, kb, vb, (int)n, s_big, s_tmp, sm, sort_lim(d));
   const u32* sv = res ? vb : va;
   u32* cum = (u32*)(res ? ka : kb);             // free key buffer as u32 scratch
   for (u32 i = threadIdx.x; i < n; i += CTA) cum[i] = d.contrib[sv[i]];
@@ -143,7 +143,8 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
   u32 stopped = 0;                      // PinnedRouting: replicas whose queue stopped (warp 0)
   // queue buckets: rb[] / rhist[] from the footprint pass, plus this tick's pauses
   // (k_pause) and arrivals (above), so no pass over the slots is needed to size a chunk
-  u32 lo = 0, chunk = RESTORE_CHUNK0;
+  const u32 chunk_max = small_paths(d) ? 64u : RESTORE_CHUNK_MAX;
+  u32 lo = 0, chunk = small_paths(d) ? 4u : RESTORE_CHUNK0;
   while (true) {
     const u32 T = cta_hist_threshold(d.rhist, 2 * NBK, lo, chunk, s_big, s_tmp);
     if (it < 7) PSTAMP(1, 1 + 4 * it);
@@ -156,7 +157,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
         });
     if (it < 7) PSTAMP(1, 2 + 4 * it);
     if ((d.flags & TA_F_TIMING) && threadIdx.x == 0 && it < 4) d.pst[1 * 32 + 27 + it] = n | (1ull << 62);
-    int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm);
+    int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm, sort_lim(d));
     const u32* q = res ? vb : va;
     if (it < 7) PSTAMP(1, 3 + 4 * it);
     if (w0) {
@@ -208,7 +209,8 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     ++it;
     if (s_stop) break;
     lo = T + 1;
-    chunk = min(chunk * 8, RESTORE_CHUNK_MAX);
+    chunk = min(chunk * 8, chunk_max);
+    dbg_hit(d, DBG_RESTORE_CHUNKS);
     __syncthreads();
   }
   if (w0) {

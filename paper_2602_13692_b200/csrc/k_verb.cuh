@@ -9,7 +9,8 @@
 __global__ void k_verb_reset(Dev d) {
   int t = threadIdx.x;
   if (t == 0) {
-    d.ctr->restore_cnt = 0; d.ctr->err = TA_OK; d.ctr->verb_ok = 1;
+    d.ctr->restore_cnt = 0; d.ctr->verb_ok = 1;
+    if (d.ctr->err != TA_E_PEER) d.ctr->err = TA_OK;   // a peer failure stays until read
     d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
   }
   if (t < d.R) {

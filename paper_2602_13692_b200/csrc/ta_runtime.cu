@@ -68,6 +68,7 @@ struct ta_ctx {
   int close_grid = 1;                       // CTAs of the cooperative k_close
   void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
   void* peer_mbox[TA_MAX_REPLICAS] = {};    // IPC-opened peer mailboxes
+  bool split_pr = false;                    // A/B aid (env TA_SPLIT_PR at init): k_pause + k_restore
 };
 
 #define FAIL(ctx, code, ...)                                          \
@@ -173,6 +174,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.ev_mv = L.take<u32>(EC); x.ev_mv2 = L.take<u32>(EC);
   x.pst = L.take<ull>(4 * 32);
   x.gsync = L.take<ull>(2);
+  x.dbg = L.take<ull>(DBG_N);
   x.t_rep = L.take<u32>(3 * R);
   x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
   x.ec_list = L.take<u32>(R * N); x.ec_cnt = L.take<u32>(R);
@@ -237,6 +239,27 @@ static void rec(ta_ctx* x, int i) {
 // dynamic shared memory of the copy kernels: the TMA staging buffer in bulk mode
 static inline size_t csm(const Dev& d) { return (d.flags & TA_F_COPY_BULK) ? BULK_CHUNK : 0; }
 
+// Cooperative launch (all CTAs co-resident: the kernel has grid barriers or waits
+// across CTAs).
+template <typename... Args>
+static void launch_coop_b(void (*k)(Args...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = grid > 1 ? 1 : 0;       // one CTA needs no co-residency guarantee
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+template <typename... Args>
+static void launch_coop(void (*k)(Args...), int grid, size_t smem, cudaStream_t s, Args... args) {
+  launch_coop_b(k, grid, CTA, smem, s, args...);
+}
+
 // Step 6.  Single process: one fused kernel (D2H overlapped with H2D/P2P and fills).
 // Multi-process: evict -> barrier -> fetch (pull) + push -> barrier -> fills.
 static void launch_movement(ta_ctx* x, cudaStream_t s) {
@@ -245,7 +268,9 @@ static void launch_movement(ta_ctx* x, cudaStream_t s) {
     // one process per GPU: every peer's plan (and its eviction flags) is in place before
     // anyone pushes, and every transfer has landed before anyone reuses a block
     if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
-    k_move_fused<<<x->move_grid, 256, csm(d), s>>>(d);   // persistent: every CTA co-resident
+    // persistent, CTAs wait on each other's evictions: cooperative, so the driver either
+    // makes the whole grid co-resident or fails the launch (never a partial grid)
+    launch_coop_b(k_move_fused, x->move_grid, 256, csm(d), s, (Dev)d);
     if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
     rec(x, 4);
     rec(x, 5);
@@ -262,22 +287,6 @@ static void launch_movement(ta_ctx* x, cudaStream_t s) {
   }
   rec(x, 5);
   if (d.flags & TA_F_FILL) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
-}
-
-// Cooperative launch (all CTAs co-resident: the kernel has grid barriers).
-template <typename... Args>
-static void launch_coop(void (*k)(Args...), int grid, size_t smem, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(CTA);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  lc.attrs = at;
-  lc.numAttrs = grid > 1 ? 1 : 0;       // one CTA needs no co-residency guarantee
-  cudaLaunchKernelEx(&lc, k, args...);
 }
 
 static cudaError_t launch_tick(ta_ctx* x, int) {
@@ -298,7 +307,7 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     k_tick_front<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);   // ingest + footprint + load
   }
   rec(x, 1);
-  if (getenv("TA_SPLIT_PR")) {             // A/B aid: the two passes as separate kernels
+  if (x->split_pr) {                       // A/B aid: the two passes as separate kernels
     k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
     k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
   } else {
@@ -413,7 +422,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.block_bytes = (i64)x->block_bytes;
   d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
   d.nb_shift = 0;
-  while (((u32)d.MAXB >> d.nb_shift) + 1 > 2048) ++d.nb_shift;
+  const u32 nbk_max = (cfg->flags & TA_F_SMALL_PATHS) ? 8u : 2048u;   // restore / pause buckets
+  while (((u32)d.MAXB >> d.nb_shift) + 1 > nbk_max) ++d.nb_shift;
   d.nbk = ((u32)d.MAXB >> d.nb_shift) + 1;
   d.api_mode = (cfg->flags & TA_F_TRACE_MODE) ? 0 : 1;
   for (int r = 0; r < d.R; ++r) {
@@ -449,6 +459,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.n_slots = 0;
   d.n_initial = 0;
   x->timing = (cfg->flags & TA_F_TIMING) != 0;
+  x->split_pr = getenv("TA_SPLIT_PR") != nullptr;
   d.multi = cfg->replicas_here < cfg->n_replicas ? 1 : 0;
   d.rank = cfg->first_replica;
   d.fused = !(cfg->flags & TA_F_NO_FUSE) ? 1 : 0;
@@ -496,6 +507,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));
+    cudaFree(x->mbox_alloc);
     delete x;
     return TA_E_CUDA;
   }
@@ -670,6 +682,14 @@ ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n) {
   if (!out || n < 0 || n > 128) FAIL(ctx, TA_E_INVAL, "bad stamp buffer");
   CK(ctx, cudaStreamSynchronize(ctx->stream));
   CK(ctx, cudaMemcpy(out, ctx->d.pst, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return TA_OK;
+}
+
+ta_status ta_debug_counters(ta_ctx* ctx, uint64_t* out, int32_t n) {
+  if (ta_status s = check_ctx(ctx)) return s;
+  if (!out || n < 0 || n > DBG_N) FAIL(ctx, TA_E_INVAL, "bad counter buffer");
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemcpy(out, ctx->d.dbg, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return TA_OK;
 }
 

@@ -271,3 +271,50 @@ def test_gpu_health_failover_random(seed, spt):
         assert bad == 0, f"tick {k}: {bad} KV words wrong"
     assert n_fail > 0
     pool.close()
+
+
+def test_gpu_rejected_batch_after_compaction_moves_no_bytes():
+    """a rejected batch right after a compaction tick must not replay
+    that tick's compaction copies.  Between ticks the engine writes into blocks (here:
+    every HBM byte is overwritten with noise); the rejected batch must leave every byte
+    as it was, and the oracle-parity run then continues unchanged."""
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = tracegen.get_config("c1_toy", n_replicas=2, hbm_blocks=48, host_blocks=16, max_ctx=4096,
+                              compact_every=1)
+    N = 40
+    o = oracle.Oracle(cfg, api_mode=True, n_slots=N)
+    pool = Pool(cfg, N, trace_mode=False)
+    rng = random.Random(99)
+    hit = 0
+    for k in range(200):
+        T = 5000 * k
+        evs = random_events(o, rng, T, illegal_p=0.0)
+        c0 = o.stats["compact_blocks"]
+        st_o, dec_o = o.sched_step(T, evs)
+        st_g, dec_g = pool.step(T, evs, raise_on_error=False)
+        assert st_o == st_g == oracle.OK
+        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        if o.stats["compact_blocks"] == c0:
+            continue
+        # this tick compacted: the engine now writes; then an illegal batch arrives
+        torch.cuda.synchronize()
+        saved = {r: pool.hbm[r].clone() for r in pool.hbm}
+        for r in pool.hbm:
+            pool.hbm[r].random_(0, 256)
+        noise = {r: pool.hbm[r].clone() for r in pool.hbm}
+        unarrived = [p for p in range(N) if o.status[p] == oracle.UNARRIVED]
+        bad = [(DEC, unarrived[0] if unarrived else 0, 0, 1, 0)] if unarrived else [(A, 0, 1, 1, 0)]
+        st_o, _ = o.sched_step(T + 1, bad)
+        st_g, _ = pool.step(T + 1, bad, raise_on_error=False)
+        assert st_o == st_g != oracle.OK
+        torch.cuda.synchronize()
+        for r in pool.hbm:
+            assert torch.equal(pool.hbm[r], noise[r]), f"tick {k}: a rejected batch moved KV bytes on r{r}"
+            pool.hbm[r].copy_(saved[r])
+        compare_state(o, pool.debug_download(), where=f"after rejected batch, tick {k}")
+        hit += 1
+        if hit >= 3:
+            break
+    assert hit >= 3
+    pool.close()

@@ -20,7 +20,7 @@ def need_gpu():
 
 
 def run_parity(cfg, ticks, state_every=1, content_every=1, samples=4, fill=True, flags=0, seed=0,
-               host_blocks=None):
+               host_blocks=None, counters=None):
     need_gpu()
     from paper_2602_13692_b200 import Pool
     if host_blocks is not None:
@@ -53,6 +53,9 @@ def run_parity(cfg, ticks, state_every=1, content_every=1, samples=4, fill=True,
     s = pool.stats()
     for key in oracle.ta_oracle.STAT_KEYS:
         assert s[key] == o.stats[key], (key, s[key], o.stats[key])
+    if counters is not None:                  # size-branch counters (ta_debug_counters)
+        for k, v in pool.debug_counters().items():
+            counters[k] = counters.get(k, 0) + v
     pool.close()
     return o, n_dec
 
@@ -167,7 +170,7 @@ def test_gpu_config2_swe_q32_full_size():
     run_parity(tracegen.get_config("c2_swe"), 40, state_every=5, content_every=10, samples=3)
 
 
-@pytest.mark.parametrize("name,ticks", [("c3_mixed", 25), ("c4_rlburst", 8)])
+@pytest.mark.parametrize("name,ticks", [("c3_mixed", 25), ("c4_rlburst", 40)])
 def test_gpu_configs3_4_decisions_full_n(name, ticks):
     """configs[2]/[3] at their full program counts and per-replica pools, all 8 replicas
     on one GPU with the decision-only KV shape (bytes per block do not affect decisions)."""
