@@ -4,9 +4,18 @@ A step is one scheduler tick through libta (ta_sched_step: ingest, footprint,
 decayed load, pause, restore, materialize, KV block movement, finalize) over the
 bench workload (tracegen config `bench_10k`: configs[3]'s 10k-program RL-burst
 trace, one replica per GPU with a 96 GiB HBM pool of 4 MiB Qwen3-32B blocks and a
-pinned host tier).  `value` = scheduler ticks/s normalised to 10k programs per tick
-(program-ticks/s / 1e4), summed over ranks.  Usage:
+64 GiB pinned host tier).
 
+The timed window is FIXED: ticks [1, 1 + K) of a fresh context (tick 0, the arrival
+of the 10k programs, runs untimed), whatever W is -- the W warm-up ticks run on a
+throw-away context over the same buffers first.  The window opens with the burst:
+ticks 1-12 offload ~46k blocks (~190 GB) to the host tier and fetch ~13k back, so
+every run at K >= 12 moves KV over every path the workload uses.  Each tick is
+bracketed by its own CUDA-event pair; the 256 MiB L2 flush before each tick sits
+OUTSIDE the pair.  `value` = K ticks / sum of tick times, normalised to 10k programs
+per tick (program-ticks/s / 1e4), summed over ranks (max-over-ranks time).
+
+Usage:
   python bench.py [--gpus N] [--steps K] [--warmup W]          # our CUDA path
   python bench.py --impl reference ...                         # the CPU oracle
 """
@@ -40,11 +49,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bench_10k")
-    ap.add_argument("--preroll", type=int, default=8, help="untimed ticks before warm-up")
+    ap.add_argument("--window-start", dest="start", type=int, default=1, help="first timed tick of the fresh context")
     ap.add_argument("--host-gib", type=float, default=64.0, help="cap of the pinned host tier")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sched-ticks", type=int, default=200, help="ticks of the decision-path latency probe")
+    ap.add_argument("--sched-start", type=int, default=13, help="first tick of the latency probe (after the burst)")
     return ap.parse_args()
 
 
@@ -252,15 +262,21 @@ def metadata_bytes(pool_stats_prev, n_programs, sum_nb, moved_blocks):
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, metric):
+    """The tier's reference arm: the CPU oracle, as it stands, on the same window."""
     import tracegen
     import oracle
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = workload(args.config, int(os.environ.get("WORLD_SIZE", "1")))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = workload(args.config, world)
     tr = tracegen.make_trace(cfg)
+    warm = oracle.Oracle(cfg, tr)            # W warm-up ticks on a throw-away instance
+    for _ in range(args.warmup):
+        warm.sched_step()
+    del warm
     o = oracle.Oracle(cfg, tr)
-    for _ in range(args.preroll + args.warmup):
+    for _ in range(args.start):
         o.sched_step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -275,18 +291,21 @@ def run_reference(args, metric):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.config, "programs": n_prog, "replicas": cfg["n_replicas"],
-                   "ticks": f"{args.preroll + args.warmup}..{args.preroll + args.warmup + args.steps - 1}"},
+                   "ticks": f"{args.start}..{args.start + args.steps - 1}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "ticks/s", "cores": 1, "kind": "oracle",
-                         "sample": f"oracle (pure Python, 1 thread) ticks after {args.preroll + args.warmup} untimed"},
+                         "sample": f"oracle (pure Python, 1 thread), ticks {args.start}..{args.start + args.steps - 1} "
+                                   f"of a fresh run; it tracks block indices, moves no KV bytes"},
         "e2e": {"value": round(value, 4), "unit": "ticks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, trace, seconds):
+def cpu_baseline(cfg, trace, start, seconds):
+    """The oracle on the same trace from the same first tick, for ~`seconds`."""
     import oracle
     o = oracle.Oracle(cfg, trace)
-    o.sched_step()                    # tick 0 (arrivals) untimed
+    for _ in range(start):
+        o.sched_step()                    # untimed, like the GPU window
     t0 = time.perf_counter()
     n = 0
     while time.perf_counter() - t0 < seconds:
@@ -304,7 +323,23 @@ def cpu_baseline(cfg, trace, seconds):
         pass
     return {"value": round(n * trace.n_slots / 1e4 / dt, 4), "unit": "ticks/s", "cores": 1,
             "kind": "oracle",
-            "sample": f"ticks 1..{n} of the same trace ({dt:.1f} s, pure-Python oracle, 1 of {cpu} cores, {model})"}
+            "sample": f"ticks {start}..{start + n - 1} of the same trace ({dt:.1f} s, pure-Python oracle, "
+                      f"1 of {cpu} cores, {model}); the oracle tracks block indices and moves no KV bytes"}
+
+
+# per-tick algorithmic bytes of the kernels: the footprint pass reads a
+# slot's 64-B program record and writes 24 B of derived values, and reads 4 B per
+# block-table entry below nb; the movement kernel moves one block per moved block over
+# its link; compaction reads and writes each moved block in HBM
+FRONT_SLOT_BYTES = 88
+
+
+def fresh(pool, world, flags=None):
+    """A fresh context over the same buffers (every slot UNARRIVED, all blocks free)."""
+    pool.reset(flags=flags)
+    if world > 1:
+        from paper_2602_13692_b200.dist import connect
+        connect(pool)
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -334,6 +369,17 @@ def main():
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=dev)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     # weak scaling: N replicas (one per GPU) share one global queue over 10k * N
     # programs; every rank runs the replicated control plane, moves its own replica's
     # bytes, and pulls / pushes migrated blocks over NVLink
@@ -342,8 +388,7 @@ def main():
     block_bytes = 2 * 64 * 8 * 128 * 2 * cfg["block_tokens"]
     nh = min(cfg["host_blocks"], host_cap_bytes(args.host_gib, world) // block_bytes)
     cfg["host_blocks"] = nh
-    # the timed run has no timing nodes in its graph; the per-kernel breakdown comes from
-    # a replay of the same ticks with TA_F_TIMING (event-record nodes cost ~2.7 us each)
+    K, W, S0 = args.steps, args.warmup, args.start
     pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0, device=local,
                 replicas_here=1, first_replica=rank)
     base_flags = pool.c.flags
@@ -353,252 +398,257 @@ def main():
     pool.load_trace(tr)
     peaks_file, peak_src = measured_peaks()
     hbm_peak = float(peaks_file.get("hbm_gbs", 6650.0))
+    s = pool.stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(s):
+        flush.zero_()                    # first touch of the flush buffer outside the timed region
 
     # the clock sampler starts before warm-up (nvidia-smi start-up can stall the driver);
     # only samples taken inside the timed window are kept
     sampler = ClockSampler(local)
     sampler.start()
-    for _ in range(args.preroll + args.warmup):
+    # ---- W warm-up ticks (ticks 0..W-1 of a throw-away context over the same buffers)
+    for _ in range(W):
+        pool.step(decisions=False)
+    torch.cuda.synchronize(dev)
+    # ---- the timed window: ticks [S0, S0 + K) of a fresh context
+    fresh(pool, world)
+    pool.load_trace(tr)
+    for _ in range(S0):
         pool.step(decisions=False)
     torch.cuda.synchronize(dev)
     time.sleep(0.3)
-
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    with torch.cuda.stream(pool.stream):
-        flush.zero_()                    # first touch of the flush buffer outside the timed region
-    torch.cuda.synchronize(dev)
-    s = pool.stream
     st0 = pool.stats()
-    if world > 1:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     sampler.mark("t_start")
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K)]
     e0.record(s)
-    for i in range(args.steps):       # enqueued back to back: no host sync inside the region
-        ev[2 * i].record(s)
+    for i in range(K):                # enqueued back to back: no host sync inside the region
         with torch.cuda.stream(s):
-            flush.zero_()             # L2 flush (256 MiB > 126 MB L2) inside the timed region
+            flush.zero_()             # L2 flush (256 MiB > 126 MB L2), outside the tick's event pair
+        ev[2 * i].record(s)
         pool.step(decisions=False)
         ev[2 * i + 1].record(s)
     e1.record(s)
     torch.cuda.synchronize(dev)
     sampler.mark("t_end")
-    if world > 1:
-        dist.barrier()
+    barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    step_ms = [round(ev[2 * i].elapsed_time(ev[2 * i + 1]), 3) for i in range(args.steps)]
+    step_ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(K)]
+    ms = max_over_ranks(sum(step_ms))
+    region_ms = max_over_ranks(e0.elapsed_time(e1))
     st1 = pool.stats()
-    sum_nb = int(pool.debug_download()["nb"].sum())   # block-table entries scanned per tick
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
     progs_total = tr.n_slots
-    value = args.steps * progs_total / 1e4 / (ms * 1e-3)
+    value = K * progs_total / 1e4 / (ms * 1e-3)
 
-    # ---- per-kernel breakdown: the SAME ticks again with TA_F_TIMING (fresh context over
-    # the same buffers, same untimed prefix); CUDA-event times of every graph phase
-    pool.reset(flags=base_flags | binding.F_TIMING)
-    if world > 1:
-        connect(pool)
+    # ---- per-kernel breakdown: the SAME window again with TA_F_TIMING (event-record
+    # nodes in the graph, ~2.7 us each) on the context stream; host-mapped telemetry of
+    # every tick (blocks per path and per replica) and the block-table entries scanned
+    fresh(pool, world, flags=base_flags | binding.F_TIMING)
     pool.load_trace(tr)
-    for _ in range(args.preroll + args.warmup):
+    for _ in range(S0):
         pool.step(decisions=False)
-    phase_sum = np.zeros(9)
-    ticks_info = []
-    for _ in range(args.steps):
+    ticks = []
+    nb_prev = pool.debug_download(["nb", "status"])
+    for _ in range(K):
         with torch.cuda.stream(s):
             flush.zero_()
         pool.step(decisions=False)
-        ph_step = np.array(pool.phase_times())   # syncs the stream
-        phase_sum += ph_step
-        ticks_info.append((pool.last_tick(), ph_step))   # host-mapped telemetry
-    if world > 1:
-        dist.barrier()
+        ph = np.array(pool.phase_times())          # syncs the stream
+        ti = pool.last_tick()
+        cur = pool.debug_download(["nb", "status"])
+        # entries scanned by this tick's footprint pass: the rows of the live programs at
+        # the previous tick's end (their nb then; the rows grow only after the scan)
+        live = np.isin(nb_prev["status"], (1, 2, 3))
+        ticks.append((ti, ph, int(nb_prev["nb"][live].sum()), int(live.sum())))
+        nb_prev = cur
+    barrier()
 
-    # ---- e2e: the SAME ticks through the public API as a serving engine drives it: an
-    # API-mode context over the same buffers; every step copies that tick's event batch
-    # from host memory to the device (ta_event array, H2D inside ta_sched_step) and
-    # reads the decisions back (D2H).  The batches are the engine's view of the trace
+    # ---- e2e through the public API as a serving engine drives it: an API-mode context
+    # over the same buffers; every step copies that tick's event batch from pinned host
+    # memory to the device (ta_event array, H2D inside ta_sched_step) and reads the
+    # decisions back (D2H).  The batches are the engine's view of the trace
     # (tools/api_events.py), recorded untimed beforehand on a decision-identical
     # small-KV context; API replay == trace mode is a GPU test (test_gpu_api.py).
     from tools.api_events import record
     rec_cfg = dict(cfg)
     rec_cfg["kv"] = "mini"
-    n_pre = args.preroll + args.warmup
-    batches, _ = record(rec_cfg, tr, n_pre + args.steps, device=local)
-    pool.reset(flags=base_flags & ~binding.F_TRACE_MODE)
-    if world > 1:
-        connect(pool)                    # fresh context: fresh mailboxes to map
+    batches, _ = record(rec_cfg, tr, S0 + K, device=local)
+    fresh(pool, world, flags=base_flags & ~binding.F_TRACE_MODE)
     dt_ms = cfg["delta_t_ms"]
-    for k in range(n_pre):
+    for k in range(S0):
         pool.step(k * dt_ms, batches[k], decisions=False)
     torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+    barrier()
     h2d = d2h = n_events = 0
-    e0.record(s)
-    for k in range(n_pre, n_pre + args.steps):
+    e2e_ms = 0.0
+    for k in range(S0, S0 + K):
         with torch.cuda.stream(s):
             flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
         st, dec = pool.step(k * dt_ms, batches[k], decisions=True)
+        b.record(s)
         if st != 0:
             raise RuntimeError(f"e2e replay: ta_sched_step status {st} at tick {k}")
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
         h2d += batches[k].nbytes + 12    # events + header (now_ms, n_events)
         d2h += dec.nbytes + 8            # decisions + count + status
         n_events += len(batches[k])
-    e1.record(s)
-    torch.cuda.synchronize(dev)
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = args.steps * progs_total / 1e4 / (e2e_ms * 1e-3)
+    e2e_ms = max_over_ranks(e2e_ms)
+    e2e_value = K * progs_total / 1e4 / (e2e_ms * 1e-3)
 
-    # ---- bytes per path in the timed steps, roofline of the dominant kernel
-    dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS + binding.LEDGER_KEYS if isinstance(st0[k], int)}
-    bb = pool.block_bytes
-    ph = phase_sum / args.steps            # us per step
-    if world == 1:
-        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "movement_fused(d2h+h2d+p2p+fill)",
-                 "-", "-", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
-    elif pool.c.flags & binding.F_NO_FUSE == 0:
-        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)",
-                 "barrier+movement_fused(d2h+pull+push)+barrier", "-", "fill", "close(finalize+compact_plan+assemble)",
-                 "compact_d2d", "-"]
-    else:
-        names = ["tick_front(ingest+footprint)", "pause+restore", "plan(cluster)", "evict_d2h+barrier",
-                 "fetch_p2p_h2d+push+barrier", "fill", "close(finalize+compact_plan+assemble)", "compact_d2d", "-"]
-    # the host-link peak of ONE GPU's link, measured by rank 0 while the others wait; with
-    # N > 1 also with every rank copying at once (GPUs can share host-side PCIe / memory
-    # bandwidth): the floor uses the concurrent figure of the slowest rank, the physical
-    # limit when all replicas stream together
+    # ---- host-link peaks of this run: one GPU alone (rank 0), and with N > 1 every rank
+    # copying at once (GPUs share host-side PCIe / memory bandwidth): the movement floor
+    # uses the concurrent figure of the slowest rank
     peaks = pcie_peak(torch, dev) if (nh and rank == 0) else {"h2d": 1.0, "d2h": 1.0}
     peaks_alone = dict(peaks)
     if world > 1:
-        dist.barrier()
+        barrier()
         if nh:
             torch.cuda.synchronize()
-            dist.barrier()
+            barrier()
             pc = pcie_peak(torch, dev, barrier=dist.barrier)
             tpk = torch.tensor([pc["d2h"], pc["h2d"]], dtype=torch.float64, device=dev)
             dist.all_reduce(tpk, op=dist.ReduceOp.MIN)
             peaks = {"d2h": float(tpk[0]), "h2d": float(tpk[1])}
-        dist.barrier()
-    # algorithmic bytes per GPU, tick by tick (telemetry counts are cluster totals; the
-    # replicas are symmetric, so per GPU = total / N).  A movement phase's time floor is
-    # the slowest link it must cross in that tick (PCIe is full duplex).
-    nvl = 770.0 if world > 1 else hbm_peak / 2     # co-located "P2P" is an HBM read+write
+        barrier()
+
+    # ---- movement in the window, per path, and the roofline of every kernel.  Tick
+    # telemetry counts are cluster totals; the replicas are symmetric (per GPU = total/N).
+    bb = pool.block_bytes
     G = 1e9
-    tmin = {3: 0.0, 4: 0.0, 7: 0.0}
-    byts = {3: 0.0, 4: 0.0, 7: 0.0}
-    for ti, _ in ticks_info:
-        d2h_b = ti["d2h_blocks"] * bb / world
-        h2d_b = ti["h2d_blocks"] * bb / world
-        p2p_b = ti["p2p_blocks"] * bb / world
-        d2d_b = 2 * ti["d2d_blocks"] * bb / world
-        if world == 1 or not pool.c.flags & binding.F_NO_FUSE:   # one fused kernel: links in parallel
-            # floor = the slowest replica's own links (PCIe out / in of its tier, NVLink in);
-            # every rank waits for it at the closing barrier
-            floor = max(max(ti["d2h_of"][r] * bb / peaks["d2h"], ti["h2d_of"][r] * bb / peaks["h2d"],
-                            ti["p2p_to"][r] * bb / nvl) for r in range(len(ti["d2h_of"])))
-            tmin[3] += floor / G
-            byts[3] += d2h_b + h2d_b + p2p_b
-        else:
-            tmin[3] += d2h_b / peaks["d2h"] / G
-            byts[3] += d2h_b
-            tmin[4] += max(h2d_b / peaks["h2d"], p2p_b / nvl) / G
-            byts[4] += h2d_b + p2p_b
-        tmin[7] += d2d_b / hbm_peak / G
-        byts[7] += d2d_b
-    for k in tmin:                       # per step
-        tmin[k] /= args.steps
-        byts[k] /= args.steps
-    dom = int(np.argmax(ph))
-    dname = names[dom]
-    if dom in tmin and ph[dom] > 0 and byts[dom] > 0:
-        t = ph[dom] * 1e-6
-        achieved = byts[dom] / t / 1e9
-        peak = byts[dom] / tmin[dom] / G if tmin[dom] > 0 else achieved
-        bound = ("hbm" if dom == 7 else "pcie (full duplex)" if (world == 1 or not pool.c.flags & binding.F_NO_FUSE)
-                 else ("pcie" if dom == 3 else "pcie/nvlink"))
-        psrc = (peak_src if dom == 7 else
-                f"measured in this run: pinned cudaMemcpyAsync 1 GiB (d2h {peaks['d2h']:.1f}, h2d {peaks['h2d']:.1f}"
-                f" GB/s{'' if world == 1 else ' per GPU with all %d GPUs copying at once; one GPU alone: d2h %.1f, h2d %.1f' % (world, peaks_alone['d2h'], peaks_alone['h2d'])}"
-                f"); peak = bytes / floor, floor = max over replicas and links of (link bytes / link peak)")
+    nvl = 770.0 if world > 1 else hbm_peak / 2     # co-located "P2P" is an HBM read+write
+    ph_sum = np.zeros(9)
+    mv = dict(d2h=0.0, h2d=0.0, p2p=0.0, d2d=0.0, floor_s=0.0, d2d_floor_s=0.0)
+    front_bytes = 0.0
+    for ti, ph, sum_nb, n_live in ticks:
+        ph_sum += ph
+        mv["d2h"] += ti["d2h_blocks"] * bb / world
+        mv["h2d"] += ti["h2d_blocks"] * bb / world
+        mv["p2p"] += ti["p2p_blocks"] * bb / world
+        mv["d2d"] += ti["d2d_blocks"] * bb / world
+        # one fused kernel: the links run in parallel; its floor is the slowest replica's
+        # own links (PCIe out / in of its tier, NVLink in); every rank waits for it
+        mv["floor_s"] += max(max(ti["d2h_of"][r] * bb / peaks["d2h"], ti["h2d_of"][r] * bb / peaks["h2d"],
+                                 ti["p2p_to"][r] * bb / nvl) for r in range(len(ti["d2h_of"]))) / G
+        mv["d2d_floor_s"] += 2 * ti["d2d_blocks"] * bb / world / hbm_peak / G
+        front_bytes += (FRONT_SLOT_BYTES * progs_total / world + 4 * sum_nb / world)
+    move_s = ph_sum[3] * 1e-6                         # fused movement kernel, summed over the window
+    move_bytes = mv["d2h"] + mv["h2d"] + mv["p2p"]
+    # kernel names by phase slot (ta_phase_times)
+    if world == 1:
+        names = ["k_tick_front", "k_pause_restore", "k_plan", "k_move_fused", "-", "-", "k_close",
+                 "k_copy_compact", "-"]
     else:
-        byts_d = metadata_bytes(st0, tr.n_slots, sum_nb, 0)
-        achieved = byts_d / (ph[dom] * 1e-6) / 1e9 if ph[dom] > 0 else 0.0
-        peak, bound, psrc = hbm_peak, "hbm", peak_src
-    # traffic: DRAM bytes per launch, from the committed ncu --set full capture of the same
-    # kernel (profiles/r1e_move_traffic.json: measured DRAM / algorithmic bytes of two
-    # launch) applied to this run's algorithmic bytes per launch
+        names = ["k_tick_front", "k_pause_restore", "k_plan", "k_barrier+k_move_fused+k_barrier", "-", "k_fill",
+                 "k_close", "k_copy_compact", "-"]
+    dom = int(np.argmax(ph_sum))
+    per_kernel = []
+    for i, nm in enumerate(names):
+        if nm == "-" or ph_sum[i] <= 0:
+            continue
+        t = ph_sum[i] * 1e-6
+        if i == 3:
+            byts, pk, bnd = move_bytes, (move_bytes / mv["floor_s"] / G if mv["floor_s"] > 0 else None), \
+                "pcie full duplex (+ nvlink)"
+        elif i == 7:
+            byts, pk, bnd = 2 * mv["d2d"], hbm_peak, "hbm"
+        elif i == 0:
+            byts, pk, bnd = front_bytes, hbm_peak, "hbm"
+        else:
+            byts, pk, bnd = None, None, "latency (serial planner chain)"
+        ach = byts / t / G if byts else None
+        per_kernel.append({"kernel": nm, "us_per_launch": round(ph_sum[i] / K, 2),
+                           "share_of_step": round(float(ph_sum[i] / ph_sum.sum()), 4),
+                           "bytes_per_launch": int(byts / K) if byts else None,
+                           "achieved_gbs": round(ach, 2) if ach else None,
+                           "peak_gbs": round(pk, 1) if pk else None,
+                           "frac": round(ach / pk, 4) if (ach and pk) else None, "bound": bnd})
+    # traffic: DRAM bytes per launch from the committed ncu --set full capture of the
+    # movement kernel in this window (ratio of measured DRAM bytes to algorithmic bytes)
     traffic = None
-    if dom == 3 and world == 1:          # the captured kernel is the single-process fused one
-        try:
-            with open(os.path.join(ROOT, "profiles", "r1e_move_traffic.json")) as f:
-                traffic = round(byts[3] * json.load(f)["ratio_dram_to_algorithmic"])
-        except (OSError, KeyError, ValueError):
-            traffic = None
-    roofline = {"bound": bound, "kernel": dname, "achieved": round(achieved, 2), "peak": round(peak, 1),
-                "unit": "GB/s", "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
-                "traffic_source": "ncu --set full capture (profiles/r1e_move_traffic.json) ratio x algorithmic bytes",
-                "share_of_step": round(float(ph[dom] / ph.sum()), 4), "peak_source": psrc}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_move_traffic.json")) as f:
+            traffic = round(move_bytes / K * json.load(f)["ratio_dram_to_algorithmic"])
+    except (OSError, KeyError, ValueError):
+        traffic = None
+    dk = next(k for k in per_kernel if k["kernel"] == names[dom])
+    psrc = (f"measured in this run: pinned cudaMemcpyAsync 1 GiB (d2h {peaks['d2h']:.1f}, h2d {peaks['h2d']:.1f}"
+            f" GB/s{'' if world == 1 else ' per GPU with all %d GPUs copying at once; one GPU alone: d2h %.1f, h2d %.1f' % (world, peaks_alone['d2h'], peaks_alone['h2d'])}"
+            f"); peak = bytes / floor, floor = sum over ticks of max over replicas and links of link bytes / link peak"
+            ) if dom == 3 else peak_src
+    roofline = {"bound": "pcie" if dom == 3 else dk["bound"], "kernel": names[dom],
+                "achieved": dk["achieved_gbs"], "peak": dk["peak_gbs"], "unit": "GB/s", "frac": dk["frac"],
+                "traffic": traffic if dom == 3 else None,
+                "traffic_source": "ncu --set full (profiles/r2_move_traffic.json): DRAM bytes / algorithmic bytes x this run's bytes per launch",
+                "share_of_step": dk["share_of_step"], "peak_source": psrc,
+                "note": "achieved = algorithmic bytes per launch / mean launch time (CUDA events on the context stream, TA_F_TIMING replay of the same window)"}
     kv_paths = kv_path_microbench(pool, torch, peaks, hbm_peak) if rank == 0 else None
-    if world > 1:
-        dist.barrier()                   # peers keep their pools mapped until rank 0 is done
-    moved = {
-        "d2h_gb_per_step": round(dstat["evict_to_host"] * bb / args.steps / 1e9, 3),
-        "h2d_gb_per_step": round(dstat["h2d_blocks"] * bb / args.steps / 1e9, 3),
-        "p2p_gb_per_step": round(dstat["p2p_blocks"] * bb / args.steps / 1e9, 3),
-        "d2d_gb_per_step": round(dstat["compact_blocks"] * bb / args.steps / 1e9, 3),
+    barrier()                            # peers keep their pools mapped until rank 0 is done
+    kv_moved = {
+        "window": f"ticks {S0}..{S0 + K - 1}",
+        "gb": {p: round(mv[p] / 1e9, 3) for p in ("d2h", "h2d", "p2p", "d2d")},
+        "blocks_total_all_replicas": {"d2h": st1["evict_to_host"] - st0["evict_to_host"],
+                                      "h2d": st1["h2d_blocks"] - st0["h2d_blocks"],
+                                      "p2p": st1["p2p_blocks"] - st0["p2p_blocks"],
+                                      "d2d": st1["compact_blocks"] - st0["compact_blocks"],
+                                      "dropped": st1["evict_dropped"] - st0["evict_dropped"]},
+        "movement_kernel_s": round(move_s, 4),
+        "in_trace_gbs": round(move_bytes / move_s / G, 2) if move_s > 0 else None,
+        "link_floor_s": round(mv["floor_s"], 4),
+        "frac_of_link_floor": round(mv["floor_s"] / move_s, 4) if move_s > 0 else None,
+        "compaction": ({"gbs_rw": round(2 * mv["d2d"] / (ph_sum[7] * 1e-6) / G, 1),
+                        "frac_hbm": round(mv["d2d_floor_s"] / (ph_sum[7] * 1e-6), 4)}
+                       if mv["d2d"] > 0 and ph_sum[7] > 0 else None),
+        "host_link_peaks_gbs": peaks,
     }
-    sched_us = float(ph[0] + ph[1] + ph[2] + ph[6] + ph[8])
-    tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.preroll + args.warmup, args.sched_ticks, flush)
+    tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.sched_start, args.sched_ticks, flush)
                 if rank == 0 and world == 1 and args.sched_ticks > 0 else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(tracegen.get_config(args.config), tracegen.make_trace(tracegen.get_config(args.config)),
-                           args.cpu_seconds)
+        c1 = tracegen.get_config(args.config)
+        cpu = cpu_baseline(c1, tracegen.make_trace(c1), S0, args.cpu_seconds)
+    dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS + binding.LEDGER_KEYS if isinstance(st0[k], int)}
+    launches = 5 + (1 if cfg.get("compact_every", 0) > 0 else 0) + (2 if world > 1 else 0)
     line = {
         "metric": metric, "value": round(value, 4), "unit": "ticks/s (10k-program ticks, summed over GPUs)",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic",
         "config": {"workload": args.config, "programs": tr.n_slots, "replicas": world, "replicas_per_gpu": 1,
                    "kv": "Qwen3-32B GQA L64 H8 D128 bf16, 16-token blocks (4 MiB)",
-                   "hbm_blocks": pool.NB, "host_blocks": pool.NH, "preroll_ticks": args.preroll,
+                   "hbm_blocks": pool.NB, "host_blocks": pool.NH,
+                   "window": f"ticks {S0}..{S0 + K - 1} of a fresh context (fixed; the W warm-up ticks run on a "
+                             f"throw-away context first)",
                    "engine_fill": "off (engine stand-in, not a hot-path row)",
-                   "l2": "256 MiB memset before every timed step (inside the timed region)",
+                   "l2": "256 MiB memset before every tick, outside the tick's CUDA-event pair; KV pools and "
+                         "host tier (160 GiB) exceed L2",
                    "parallelism": f"dp{world} (one replica per GPU)"},
         "clocks": clocks,
-        "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": int(h2d / args.steps),
-                "d2h_bytes_per_step": int(d2h / args.steps), "events_per_step": round(n_events / args.steps, 1),
-                "note": "API mode (serving-engine path): per step the tick's event batch H2D from host memory, "
-                        "validation + apply + tick on the device, decisions D2H; same ticks as value"},
-        # per tick: tick_front, pause+restore (cooperative), plan (one launch of R 8-CTA
-        # clusters), movement (1 fused kernel; multi-GPU: barrier, fused kernel, barrier), close
-        # (compaction copies only when compaction is configured; off in this workload)
-        "gpu_launches": args.steps * (5 if world == 1 else 7),
+        "e2e": {"value": round(e2e_value, 4), "unit": "ticks/s", "h2d_bytes_per_step": int(h2d / K),
+                "d2h_bytes_per_step": int(d2h / K), "events_per_step": round(n_events / K, 1),
+                "note": "API mode (serving-engine path): per step the tick's event batch H2D from pinned host "
+                        "memory, validation + apply + tick on the device, decisions D2H; same window as value"},
+        "gpu_launches": K * launches,
         "roofline": roofline,
-        "phases_us_per_step": {n: round(float(v), 1) for n, v in zip(names, ph)},
-        "sched_us_per_tick": round(sched_us, 1),
+        "kernels": per_kernel,
+        "kv_moved": kv_moved,
+        "sched_tick": tick_lat,
+        "phases_us_per_step": {n: round(float(v / K), 1) for n, v in zip(names, ph_sum) if n != "-"},
         # NEXT-1: STP cost ledger of the timed ticks (token-ms per step) and
         # the Cost_unused < c_min bound of PAPER.md:415 (replica-ticks checked / violated)
-        "stp_ledger_token_ms_per_step": {k[5:]: int(dstat[k] / args.steps) for k in binding.LEDGER_KEYS
+        "stp_ledger_token_ms_per_step": {k[5:]: int(dstat[k] / K) for k in binding.LEDGER_KEYS
                                          if k.startswith("cost_")},
         "unused_bound": {"checks": dstat["unused_bound_checks"], "violations": dstat["unused_bound_violations"]},
-        "sched_tick": tick_lat,
-        "kv_moved": moved,
         "kv_paths": kv_paths,
         "cpu_baseline": cpu,
-        "step_ms": step_ms,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "region_ms_incl_flush": round(region_ms, 3),
     }
     if rank == 0:
         JSON_OUT.write(json.dumps(line) + "\n")

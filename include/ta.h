@@ -90,8 +90,8 @@ enum {
                                   eviction of idle caches; pass an all-zero decay table (A46) */
   TA_F_SMALL_PATHS = 1u << 8    /* test aid: lower the size thresholds of the shared-memory fast
                                   paths (CTA sort 4096 -> 64, rank sort 512 -> 16, staged planner
-                                  lists 4096 / 8192 / 1024 -> 8 / 8 / 4, slot-bitmap ordering off,
-                                  restore chunks 32..4096 -> 4..64, restore buckets <= 8) so that
+                                  lists 4096 / 8192 / 1024 -> 8 / 8 / 4, candidate slot lists in
+                                  shared memory 12288 / 8192 -> 8, restore chunks 32..4096 -> 4..64, restore buckets <= 8) so that
                                   small runs take the code paths of full-size runs.  Results are
                                   identical; only the speed differs. */
 };
@@ -325,8 +325,8 @@ ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Developer / test aid: cumulative size-branch counters since ta_init_pool, out[i] =
  * how many times branch i ran: [0] CTA radix sort (n above the shared-memory sort
- * limit) [1] bitonic sort [2] rank sort [3] planner F_r ordered by a sort (slot-bitmap
- * ordering off) [4] planner need prefix in global memory [5] eviction prefix in global
+ * limit) [1] bitonic sort [2] rank sort [3] a candidate set's slot list kept in global
+ * memory (beyond the shared-memory list limit) [4] planner need prefix in global memory [5] eviction prefix in global
  * memory [6] victims in global memory [7] request loop reading program values from
  * global memory [8] restore-pass chunks after the first [9] replica-ticks with
  * evictions; [10, 16) reserved.  n <= 16.  Synchronizes the stream. */

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libta.so")
+# TA_LIB: developer A/B aid (a variant built with build.py --out, inside this package)
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("TA_LIB", "libta.so")))
 MAXR = 32
 HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 
@@ -160,7 +161,7 @@ EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_tra
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
             "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk",
             "ta_debug_phase_stamps", "ta_set_health", "ta_debug_counters")
-DEBUG_COUNTERS = ("radix_sort", "bitonic_sort", "rank_sort", "plan_f_sort", "plan_f_global", "plan_e_global",
+DEBUG_COUNTERS = ("radix_sort", "bitonic_sort", "rank_sort", "list_global", "plan_f_global", "plan_e_global",
                   "plan_v_global", "plan_fst_global", "restore_chunks", "evict_ticks")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 

@@ -8,6 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libta.so")
+# developer A/B aid: extra nvcc flags (e.g. -DROW_PRE=2) and another output name
+EXTRA = os.environ.get("TA_NVCC_EXTRA", "").split()
 SRC = os.path.join(HERE, "csrc", "ta_runtime.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -27,16 +29,19 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    if out is None and not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", SRC]
+    cmd = [NVCC, *FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"), "-o", (out or LIB) + ".tmp", SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libta.so")
     if verbose:
         sys.stderr.write(r.stderr)
+    if out is not None:                   # A/B variant: no log, no default library
+        os.replace(out + ".tmp", out)
+        return out
     with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:   # registers / spills per kernel
         f.write("".join(ln for ln in r.stderr.splitlines(True) if "Compile time" not in ln))
     os.replace(LIB + ".tmp", LIB)
@@ -44,4 +49,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose=True, out=out))

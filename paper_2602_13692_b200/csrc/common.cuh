@@ -157,13 +157,17 @@ struct Dev {
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)
   ull* pst;                        // [4][32] in-kernel phase stamps (TA_F_TIMING; developer aid)
-  // ---- candidate lists built by the footprint pass (grid-parallel; unordered appends),
-  // so the single-CTA planner kernels never scan all N slots except the restore gather
-  u32 *act_list, *act_cnt;         // [R][N], [R]: REASONING/ACTING placed on r
-  u32 *ec_list, *ec_cnt;           // [R][N], [R]: home == r with HBM blocks (eviction candidates)
+  // ---- candidate sets built by the footprint pass as slot bitmaps (one word per 32
+  // slots, written whole by the CTA that owns those slots: no atomics), so the planner
+  // kernels never scan all N slots except the restore gather; consumers turn a bitmap
+  // into a slot-ordered list (cta_bits_to_list)
+  int NW;                          // words per bitmap: ceil(N / 32)
+  u32* act_bits;                   // [R][NW]: REASONING or ACTING placed on r
+  u32* reas_bits;                  // [R][NW]: REASONING placed on r (F_r before steps 3-4)
+  u32* ec_bits;                    // [R][NW]: home == r with private HBM blocks (eviction candidates)
+  u32 *act_list, *ec_list;         // [R][N]: list scratch when a list does not fit shared memory
   u32* rhist;                      // [2 * nbk] restore-bucket histogram of PAUSED slots
   u32* rb;                         // [N] restore bucket of a PAUSED slot, else 0xFFFFFFFF
-  i8* fpl;                         // [N] placement at footprint time (-1: not active)
   ull* gsync;                      // [2] grid-barrier counters of k_decide / k_close (monotone)
   ull* dbg;                        // [DBG_N] size-branch counters (ta_debug_counters)
 };
@@ -174,7 +178,7 @@ enum DbgIdx {
   DBG_RADIX = 0,        // CTA sort of n > sort limit: global-memory radix sort
   DBG_BITONIC,          // register/shared bitonic network (rank limit < n <= sort limit)
   DBG_RANK,             // rank sort (n <= rank limit)
-  DBG_F_SORT,           // k_plan F_r ordered by a sort (N beyond the slot-bitmap limit)
+  DBG_LIST_GLOBAL,      // a candidate bitmap's slot list did not fit shared memory (global list)
   DBG_F_GLOBAL,         // k_plan need prefix read from global memory (nF > staging limit)
   DBG_E_GLOBAL,         // k_plan eviction prefix read from global memory (ne > staging limit)
   DBG_V_GLOBAL,         // k_plan victims read from global memory (nv > victim staging limit)
@@ -810,6 +814,31 @@ __device__ __forceinline__ u32 bitmap_select(const u32* words, const u32* s_pre,
   u32 k = q - s_pre[lo];                  // k-th set bit inside w
   u32 pos = __fns(w, 0, (int)k + 1);
   return (u32)lo * 32u + pos;
+}
+
+// The slots of a bitmap (bit b of word w = slot 32w + b) in ascending slot order: into
+// s_out (shared memory, capacity s_cap) when they fit, else into g_out (global).  One
+// CTA; every thread takes a contiguous run of words.  *out receives the list used.
+__device__ u32 cta_bits_to_list(const u32* words, int nw, u32* s_out, u32 s_cap, u32* g_out, u32* s_tmp,
+                                const u32** out) {
+  const int chunk = (nw + CTA - 1) / CTA;
+  const int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
+  u32 cnt = 0;
+  for (int w = lo; w < hi; ++w) cnt += __popc(words[w]);
+  u32 total;
+  u32 pos = cta_excl_scan(cnt, s_tmp, &total);
+  u32* dst = total <= s_cap ? s_out : g_out;
+  for (int w = lo; w < hi; ++w) {
+    u32 m = words[w];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      dst[pos++] = (u32)(w * 32 + b);
+    }
+  }
+  __syncthreads();
+  *out = dst;
+  return total;
 }
 
 // Write the listed slots (unique, < N) to out[0, n) in ascending slot order: mark them

@@ -137,7 +137,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     for (u32 i = threadIdx.x; i < n; i += CTA) {
       ta_decision rec = {};
       u32 x = d.restore_dst[i];
-      rec.kind = (x >> 16) ? TA_D_MIGRATE : TA_D_RESTORE;
+      rec.kind = ((x >> 16) & 1u) ? TA_D_MIGRATE : TA_D_RESTORE;
       rec.pid = d.restore_pid[i];
       rec.src = (int)((x >> 8) & 0xFF) - 1;
       rec.dst = (int)(x & 0xFF);
@@ -230,7 +230,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
   for (int t = threadIdx.x; t < R; t += CTA) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
     d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
-    d.act_cnt[t] = 0; d.ec_cnt[t] = 0;   // cpd_cnt is read by the compaction copies after this kernel
+    // cpd_cnt is read by the compaction copies after this kernel
   }
   for (u32 b = threadIdx.x; b < 2 * d.nbk; b += CTA) d.rhist[b] = 0;
   for (int t = threadIdx.x; t < 3 * R; t += CTA) d.t_rep[t] = 0;

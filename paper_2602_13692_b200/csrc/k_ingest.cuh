@@ -10,28 +10,41 @@ struct SlotNow {
 };
 
 // Step 0, trace mode, for one slot: decode during the last interval, tool call /
-// tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).  Every
-// field is loaded up front (one memory round trip), the trace script entries of the
-// current turn in a second one.
-__device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
-  u8 st = d.status[p];
-  const u8 sat = d.satisfied[p];
-  u8 ph = d.phase[p];
-  u32 c = d.c[p];
-  const u32 t = d.turn[p];
-  const u32 gd0 = d.gen_done[p];
-  const i64 tr0 = d.tool_return[p];
-  i64 as = d.acting_since[p];
-  const u32 busy = d.busy[p], pend0 = d.pend[p];
-  const u32 base = d.t_off[p], base1 = d.t_off[p + 1];
-  SlotNow o{c, as, st, ph, d.placement[p], d.home[p], 0};
+// tool result, release (PAPER.md:160-162 reason/act loop; readings A3, A18).  Split in
+// two so the block-table row loads can be issued between them: ingest_load issues
+// every program-table load of the slot (one memory round trip), ingest_apply the trace
+// script loads of the current turn (a second one) and the state change.
+struct SlotFields {
+  i64 tr0, as;
+  u32 c, t, gd0, busy, pend0, base, base1;
+  u8 st, sat, ph;
+  i8 pl, home;
+};
+
+__device__ __forceinline__ SlotFields ingest_load(const Dev& d, int p) {
+  SlotFields f;
+  f.st = d.status[p]; f.sat = d.satisfied[p]; f.ph = d.phase[p];
+  f.c = d.c[p]; f.t = d.turn[p]; f.gd0 = d.gen_done[p];
+  f.tr0 = d.tool_return[p]; f.as = d.acting_since[p];
+  f.busy = d.busy[p]; f.pend0 = d.pend[p];
+  f.base = d.t_off[p]; f.base1 = d.t_off[p + 1];
+  f.pl = d.placement[p]; f.home = d.home[p];
+  return f;
+}
+
+__device__ __forceinline__ SlotNow ingest_apply(const Dev& d, int p, i64 T, const SlotFields& f) {
+  u8 st = f.st, ph = f.ph;
+  u32 c = f.c;
+  i64 as = f.as;
+  const u32 t = f.t, gd0 = f.gd0, busy = f.busy, base = f.base;
+  SlotNow o{c, as, st, ph, f.pl, f.home, 0};
   if (st == TA_UNARRIVED || st == TA_STOPPED) return o;
-  const u32 nturns = base1 - base;
+  const u32 nturns = f.base1 - base;
   const u32 g = d.t_g[base + t], dtool = d.t_d[base + t], res = d.t_o[base + t];
-  i64 tr = tr0;
+  i64 tr = f.tr0;
   u32 tt = t, gd = gd0;
   bool wrote_gd = false, wrote_tool = false;
-  if (st == TA_REASONING && sat) {
+  if (st == TA_REASONING && f.sat) {
     // decode after the engine's (re)prefill of the last materialize (reading A48)
     const i64 b = min((i64)busy, d.dt);
     const u32 d_tick = (u32)(((i64)d.rate * (d.dt - b)) / 1000);
@@ -63,7 +76,7 @@ __device__ __forceinline__ SlotNow ingest_slot(const Dev& d, int p, i64 T) {
   }
   if (ph == TA_PHASE_A && (st == TA_ACTING || st == TA_PAUSED) && T >= tr) {
     c += res;                            // tool result (tools run while paused)
-    d.pend[p] = pend0 + res;             // ... waits for its prefill
+    d.pend[p] = f.pend0 + res;           // ... waits for its prefill
     tt = t + 1;
     gd = 0;
     wrote_gd = true;
@@ -249,150 +262,220 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
   if (stops) atomicAdd(&d.ctr->stops, stops);
 }
 
-// Steps 0 (release frees) + 1 (footprint) + 2 (contribution, L_eff) for one slot,
-// by one warp, given the slot's values after step 0 (identical in every lane).  The
-// block-table row is scanned with 16-byte loads; counts come from ballot/popc,
-// prefix_hbm from the first non-HBM entry.  Loads accumulate into Lacc (k_pause
-// publishes L).  Closed-loop arrivals are initialised by k_restore.
-__device__ __forceinline__ void footprint_warp(const Dev& d, int p, i64 T, int verb, const SlotNow& v) {
-  const u32 lane = lane_id();
-  u32* row = d.loc + (size_t)p * d.MAXBP;
-  if (!verb && v.released) {                      // free every block of a STOPPED program (A26)
-    const int h = v.home;
-    const u32 nbv = ceil_div_u32(v.c, d.bt);
-    for (u32 j = lane; j < nbv; j += 32) {
-      u32 e = row[j];
-      if (e == LOC_NONE) continue;
-      if (j < d.sb) {                              // shared prefix: a reference, not owned
-        row[j] = LOC_NONE;
-        continue;
-      }
-      if (e & LOC_HOST) {
-        u32 s = e & ~LOC_HOST;
-        atomicOr(&d.host_free[(size_t)h * d.NHW + (s >> 5)], 1u << (s & 31));
-      } else {
-        atomicOr(&d.hbm_free[(size_t)h * d.NBW + (e >> 5)], 1u << (e & 31));
-      }
-      row[j] = LOC_NONE;
-    }
-    if (lane == 0) {
-      d.home[p] = -1;
-      d.released[p] = 0;
-      d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
-      d.rb[p] = 0xFFFFFFFFu;
-      d.fpl[p] = -1;
-    }
-    return;
-  }
-  const u8 st = (u8)v.st;
-  if (st != TA_PAUSED && st != TA_REASONING && st != TA_ACTING) {
-    if (lane == 0) {
-      d.nb[p] = d.n_hbm[p] = d.n_host[p] = d.prefix_hbm[p] = d.contrib[p] = 0;
-      d.rb[p] = 0xFFFFFFFFu;
-      d.fpl[p] = -1;
-    }
-    return;
-  }
-  const u32 nbv = ceil_div_u32(v.c, d.bt);
-  u32 n_h = 0, n_s = 0, first = 0xFFFFFFFFu;
-  for (u32 j0 = 0; j0 < nbv; j0 += 512) {         // four independent 16-B loads per lane in flight
-    uint4 q[4];
-#pragma unroll
-    for (int h2 = 0; h2 < 4; ++h2) {
-      const u32 j = j0 + h2 * 128 + lane * 4;
-      q[h2] = make_uint4(LOC_NONE, LOC_NONE, LOC_NONE, LOC_NONE);
-      if (j < nbv) q[h2] = *reinterpret_cast<const uint4*>(row + j);
-    }
-#pragma unroll
-    for (int h2 = 0; h2 < 4; ++h2) {
-      const u32 j = j0 + h2 * 128 + lane * 4;
-      u32 e[4] = {q[h2].x, q[h2].y, q[h2].z, q[h2].w};
-      u32 lfirst = 0xFFFFFFFFu;
-#pragma unroll
-      for (int t = 3; t >= 0; --t) {
-        if (j + t < nbv) {
-          bool h = is_hbm(e[t]);
-          n_h += h;
-          n_s += is_host(e[t]);
-          if (!h) lfirst = j + t;
-        }
-      }
-      first = min(first, lfirst);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    n_h += __shfl_xor_sync(FULL_MASK, n_h, o);
-    n_s += __shfl_xor_sync(FULL_MASK, n_s, o);
-    first = min(first, __shfl_xor_sync(FULL_MASK, first, o));
-  }
-  if (lane == 0) {
-    d.nb[p] = nbv;
-    d.n_hbm[p] = n_h;
-    d.n_host[p] = n_s;
-    d.prefix_hbm[p] = first == 0xFFFFFFFFu ? nbv : first;
-    const u8 ph = (u8)v.ph;
-    u32 cb = contrib_of(d, nbv, ph, v.as, T);
-    d.contrib[p] = cb;
-    // candidate lists of the planner kernels (unordered appends; consumers sort by key
-    // and slot, so the append order never reaches a result)
-    u32 rbv = 0xFFFFFFFFu;
-    i8 pl = -1;
-    if (st == TA_PAUSED) {
-      rbv = restore_bucket(d, ph, nbv);
-      atomicAdd(&d.rhist[rbv], 1u);
-    } else {
-      pl = (i8)v.pl;
-      if (!verb) atomicAdd(&d.Lacc[pl], (ull)cb);     // commutative u64 sum
-      d.act_list[(size_t)pl * d.N + atomicAdd(&d.act_cnt[pl], 1u)] = (u32)p;
-    }
-    const int h = v.home;
-    if (n_h > d.sb && h >= 0) d.ec_list[(size_t)h * d.N + atomicAdd(&d.ec_cnt[h], 1u)] = (u32)p;
-    d.rb[p] = rbv;
-    d.fpl[p] = pl;
-  }
+// Steps 0 (release frees) + 1 (footprint) + 2 (contribution, L_eff), one CTA per 32
+// slots (FP_SLOTS), four memory round trips for the whole CTA:
+//   1. warp 0, lane l = slot base + l: the slot's program-table fields (coalesced SoA
+//      loads), hence its row length nbo;
+//   2. every thread: the block-table rows of the 32 slots as one flat list of 16-B
+//      chunks, copied into shared memory with cp.async (LDGSTS: many loads in flight
+//      per thread, no registers held) -- while warp 0 runs the ingest, whose trace
+//      script loads overlap the row traffic;
+//   3. every warp: a contiguous range of the staged chunks, per-slot counts (n_hbm,
+//      n_host, first non-HBM entry) accumulated in registers and flushed to shared
+//      memory when the slot changes; rows of programs released this tick are freed;
+//   4. warp 0: nb, contribution (Eq. 7), and the planners' candidate lists, appended
+//      with one atomic per distinct replica per warp (warp-aggregated).
+// A slot whose chunks do not fit the staging buffer is read straight from global memory.
+//
+// Only entries j < nbo are read: nbo = ceil(c/bt) of the context the row was written
+// for (before this tick's ingest).  A row holds no entry at or beyond nb(c) (invariant
+// I2: blocks are allocated for j < nb only, and c never shrinks), so entries [nbo, nb)
+// are NONE: n_hbm and n_host are the counts over [0, nbo), and the first non-HBM entry
+// is the first one in [0, nbo), else nbo.
+#define FP_SLOTS 32                      // slots per CTA (one lane of warp 0 each)
+#ifndef FP_THREADS
+#define FP_THREADS 256                   // FP_SLOTS / (FP_THREADS / 32) slots per warp
+#endif
+#define FP_STAGE (FP_SLOTS * 80)         // 16-B chunks staged per CTA (320 block-table entries per slot)
+#define FP_SMEM (FP_STAGE * 16)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
 }
 
-// The slot's current values (API mode, verbs: step 0 already applied or absent).
-__device__ __forceinline__ SlotNow slot_now(const Dev& d, int p) {
-  return SlotNow{d.c[p], d.acting_since[p], d.status[p], d.phase[p], d.placement[p], d.home[p], d.released[p]};
+// Entries of a slot's row that can hold KV: nb of its context if it is live.
+__device__ __forceinline__ u32 row_len_of(const Dev& d, u8 st, u32 c) {
+  return (st == TA_PAUSED || st == TA_REASONING || st == TA_ACTING) ? ceil_div_u32(c, d.bt) : 0u;
 }
 
-// broadcast lane 0's SlotNow to the warp
-__device__ __forceinline__ SlotNow bcast(SlotNow v) {
-  v.c = __shfl_sync(FULL_MASK, v.c, 0);
-  v.as = (i64)__shfl_sync(FULL_MASK, (ull)v.as, 0);
-  v.st = __shfl_sync(FULL_MASK, v.st, 0);
-  v.ph = __shfl_sync(FULL_MASK, v.ph, 0);
-  v.pl = __shfl_sync(FULL_MASK, v.pl, 0);
-  v.home = __shfl_sync(FULL_MASK, v.home, 0);
-  v.released = __shfl_sync(FULL_MASK, v.released, 0);
-  return v;
-}
-
-// Trace mode: steps 0-2 of the tick in one kernel, one warp per slot (ingest by
-// lane 0, then the warp's footprint scan of the same slot).
-__global__ void __launch_bounds__(256) k_tick_front(Dev d) {
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= d.N) return;
-  const i64 T = d.ctr->tick * d.dt;
-  if (p == 0 && lane_id() == 0) {
+// mode 0: trace-mode tick (ingest + footprint); 1: API-mode tick (events applied);
+// 2: verbs (state of the last tick, no L accumulation, no release handling)
+template <int MODE>
+__device__ __forceinline__ void footprint_cta(const Dev& d) {
+  extern __shared__ __align__(16) uint4 s_stage[];   // [FP_STAGE], dynamic (FP_SMEM bytes)
+  __shared__ u32 s_off[FP_SLOTS + 1];    // chunk offsets (exclusive prefix of ceil(nbo/4))
+  __shared__ u32 s_nbo[FP_SLOTS], s_nh[FP_SLOTS], s_ns[FP_SLOTS], s_first[FP_SLOTS];
+  __shared__ int s_home[FP_SLOTS];
+  __shared__ u8 s_rel[FP_SLOTS];
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  const int p0 = blockIdx.x * FP_SLOTS;
+  const int p = p0 + lane;
+  const bool w0 = warp == 0;
+  const i64 T = MODE == 0 ? d.ctr->tick * d.dt : (MODE == 1 ? d.ctr->now_ms : d.ctr->T);
+  if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     d.ctr->T = T;
     if (d.ctr->err != TA_E_PEER) d.ctr->err = TA_OK;   // a failed verb's status does not stop the tick
   }
+  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) d.ctr->T = T;
+  // ---- 1. fields (warp 0)
+  SlotFields f{};
   SlotNow v{};
-  if (lane_id() == 0) v = ingest_slot(d, p, T);
-  footprint_warp(d, p, T, 0, bcast(v));
+  if (w0) {
+    u32 nbo = 0;
+    if (p < d.N) {
+      if (MODE == 0) {
+        f = ingest_load(d, p);
+        nbo = row_len_of(d, f.st, f.c);
+      } else {
+        v = SlotNow{d.c[p], d.acting_since[p], d.status[p], d.phase[p], d.placement[p], d.home[p],
+                    MODE == 1 ? (int)d.released[p] : 0};
+        nbo = max(row_len_of(d, (u8)v.st, v.c), v.released ? ceil_div_u32(v.c, d.bt) : 0u);
+      }
+    }
+    const u32 nch = (nbo + 3) >> 2;
+    const u32 inc = warp_incl_scan(nch);
+    s_off[lane] = inc - nch;
+    if (lane == 31) s_off[FP_SLOTS] = inc;
+    s_nbo[lane] = nbo;
+    s_nh[lane] = 0; s_ns[lane] = 0; s_first[lane] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const u32* rows = d.loc + (size_t)p0 * d.MAXBP;
+  // warp w owns slots w, w + 8, w + 16, w + 24 (interleaved for balance); a slot's
+  // chunks go to the staging buffer at s_off[slot] if they fit, else they are read
+  // straight from global memory in step 3
+  constexpr int SPW = FP_SLOTS / (FP_THREADS / 32);
+  // ---- 2. rows -> shared memory (each warp its slots), ingest (warp 0)
+#pragma unroll
+  for (int k = 0; k < SPW; ++k) {
+    const int sl = warp + k * (FP_THREADS / 32);
+    const u32 o = s_off[sl], nch = s_off[sl + 1] - o;
+    if (o + nch <= FP_STAGE)
+      for (u32 c = lane; c < nch; c += 32) cp_async16(&s_stage[o + c], rows + (size_t)sl * d.MAXBP + 4 * c);
+  }
+  if (w0) {
+    if (MODE == 0 && p < d.N) v = ingest_apply(d, p, T, f);
+    s_rel[lane] = (MODE != 2 && p < d.N && v.released) ? 1 : 0;
+    s_home[lane] = v.home;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- 3. per slot (its warp): counts, or the frees of a released row
+#pragma unroll 1
+  for (int k = 0; k < SPW; ++k) {
+    const int sl = warp + k * (FP_THREADS / 32);
+    const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
+    const bool staged = o + nch <= FP_STAGE;
+    const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
+    if (s_rel[sl]) {                     // free every block of a STOPPED program (A26)
+      const int h = s_home[sl];
+      u32* row = d.loc + (size_t)(p0 + sl) * d.MAXBP;
+      for (u32 c = lane; c < nch; c += 32) {
+        const uint4 q = staged ? s_stage[o + c] : grow[c];
+        const u32 e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const u32 j = 4 * c + t;
+          if (j >= nbo || e[t] == LOC_NONE) continue;
+          if (j >= d.sb) {                 // the shared prefix is a reference, not owned
+            if (e[t] & LOC_HOST) {
+              const u32 s2 = e[t] & ~LOC_HOST;
+              atomicOr(&d.host_free[(size_t)h * d.NHW + (s2 >> 5)], 1u << (s2 & 31));
+            } else {
+              atomicOr(&d.hbm_free[(size_t)h * d.NBW + (e[t] >> 5)], 1u << (e[t] & 31));
+            }
+          }
+          row[j] = LOC_NONE;
+        }
+      }
+      continue;
+    }
+    u32 a_h = 0, a_s = 0, a_f = 0xFFFFFFFFu;
+    for (u32 c = lane; c < nch; c += 32) {
+      const uint4 q = staged ? s_stage[o + c] : grow[c];
+      const u32 e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int t = 3; t >= 0; --t) {
+        const u32 j = 4 * c + t;
+        if (j < nbo) {
+          const bool h = is_hbm(e[t]);
+          a_h += h;
+          a_s += is_host(e[t]);
+          if (!h) a_f = j;
+        }
+      }
+    }
+    a_h = __reduce_add_sync(FULL_MASK, a_h);
+    a_s = __reduce_add_sync(FULL_MASK, a_s);
+    a_f = __reduce_min_sync(FULL_MASK, a_f);
+    if (lane == 0) { s_nh[sl] = a_h; s_ns[sl] = a_s; s_first[sl] = a_f; }
+  }
+  __syncthreads();
+  // ---- 4. per slot: derived values and candidate sets (warp 0)
+  if (!w0) return;
+  const bool valid = p < d.N;
+  const u8 st = (u8)v.st;
+  const bool live = valid && !(MODE != 2 && v.released) &&
+                    (st == TA_PAUSED || st == TA_REASONING || st == TA_ACTING);
+  u32 nbv = 0, n_h = 0, n_s = 0, cb = 0, rbv = 0xFFFFFFFFu;
+  int pl = -1;
+  if (live) {
+    nbv = ceil_div_u32(v.c, d.bt);
+    n_h = s_nh[lane];
+    n_s = s_ns[lane];
+    const u32 first = s_first[lane];
+    cb = contrib_of(d, nbv, (u8)v.ph, v.as, T);
+    if (st == TA_PAUSED) {
+      rbv = restore_bucket(d, (u8)v.ph, nbv);
+      atomicAdd(&d.rhist[rbv], 1u);
+    } else {
+      pl = v.pl;
+    }
+    d.prefix_hbm[p] = first == 0xFFFFFFFFu ? s_nbo[lane] : first;   // entries [nbo, nbv) are NONE
+  } else if (valid) {
+    d.prefix_hbm[p] = 0;
+    if (MODE != 2 && v.released) d.home[p] = -1;
+    if (MODE == 1 && v.released) d.released[p] = 0;
+  }
+  if (valid) {
+    d.nb[p] = nbv; d.n_hbm[p] = n_h; d.n_host[p] = n_s; d.contrib[p] = cb;
+    d.rb[p] = rbv;
+  }
+  // candidate bitmaps: this CTA's 32 slots are word blockIdx.x of every replica's maps
+  // (whole-word stores, every word rewritten each pass); the decayed load of the actives
+  // (Eq. 7) summed per replica (one reduction per replica per warp, a commutative u64 add)
+  const int h = v.home;
+  const bool ecand = live && n_h > d.sb && h >= 0;
+  const size_t wi = blockIdx.x;
+  for (int r = 0; r < d.R; ++r) {
+    const bool on_r = pl == r;
+    const u32 wa = __ballot_sync(FULL_MASK, on_r);
+    const u32 wr = __ballot_sync(FULL_MASK, on_r && st == TA_REASONING);
+    const u32 we = __ballot_sync(FULL_MASK, ecand && h == r);
+    const u32 sum = __reduce_add_sync(FULL_MASK, on_r ? cb : 0u);   // < 32 lanes x 2^23
+    if (lane == 0) {
+      d.act_bits[(size_t)r * d.NW + wi] = wa;
+      d.reas_bits[(size_t)r * d.NW + wi] = wr;
+      d.ec_bits[(size_t)r * d.NW + wi] = we;
+      if (MODE != 2 && sum) atomicAdd(&d.Lacc[r], (ull)sum);
+    }
+  }
 }
 
-// API mode and verbs: steps 1-2 (the events were applied by k_ev_*).  Verbs
-// act on the state left by the last tick, at its time T (no ingest, L kept).
-__global__ void __launch_bounds__(256) k_footprint(Dev d, int verb) {
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= d.N || (!verb && d.ctr->err != TA_OK)) return;
-  const i64 T = verb ? d.ctr->T : d.ctr->now_ms;
-  if (!verb && p == 0 && lane_id() == 0) d.ctr->T = T;
-  SlotNow v{};
-  if (lane_id() == 0) v = slot_now(d, p);
-  footprint_warp(d, p, T, verb, bcast(v));
+// Trace mode: steps 0-2 of the tick.
+__global__ void __launch_bounds__(FP_THREADS) k_tick_front(Dev d) { footprint_cta<0>(d); }
+
+// API mode (the events were applied by k_ev_*) and verbs (verb != 0: the state left by
+// the last tick, at its time T; no ingest, L kept): steps 1-2.
+__global__ void __launch_bounds__(FP_THREADS) k_footprint(Dev d, int verb) {
+  if (verb) {
+    footprint_cta<2>(d);
+  } else {
+    if (d.ctr->err != TA_OK) return;
+    footprint_cta<1>(d);
+  }
 }

@@ -144,8 +144,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   if (crank == 2) {
     ull fr = 0, es = 0;
     for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(hf[w]);
-    const u32* el = d.ec_list + (size_t)r * N;      // home == r with HBM blocks (footprint pass)
-    const int nel = (int)d.ec_cnt[r];
+    const u32* el = nullptr;                        // home == r with HBM blocks (footprint pass)
+    const int nel = (int)cta_bits_to_list(d.ec_bits + (size_t)r * d.NW, d.NW, reinterpret_cast<u32*>(sm->k[0]),
+                                          small_paths(d) ? 8u : 8192u, d.ec_list + (size_t)r * N, s_tmp, &el);
     for (int i = threadIdx.x; i < nel; i += CTA) {
       const u32 p = el[i];
       const u8 s = d.status[p];
@@ -172,31 +173,43 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       nF = 1;
       __syncthreads();
     } else {
-      // candidates: the footprint pass's actives on r, plus programs restored onto r
-      // this tick that were not active on r at footprint time; in slot order
-      u64* fka = d.ska + (size_t)r * N;
-      u64* fkb = d.skb + (size_t)r * N;
-      u32* fva = d.sva + (size_t)r * N;
-      u32* fvb = d.svb + (size_t)r * N;
-      __shared__ u32 s_cnt;
-      const int na = (int)d.act_cnt[r];
-      u32 n1 = cta_list_gather(d.act_list + (size_t)r * N, na, &s_cnt,
-          [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r; },
-          [&](u32 pos, int i) { fka[pos] = 0; fva[pos] = (u32)i; });
-      u32 n2 = cta_list_gather(d.restore_pid, (int)d.ctr->restore_cnt, &s_cnt,
-          [&](int i) { return d.status[i] == TA_REASONING && d.placement[i] == r && d.fpl[i] != r; },
-          [&](u32 pos, int i) { fka[n1 + pos] = 0; fva[n1 + pos] = (u32)i; });
-      nF = n1 + n2;
-      if (N <= 32 * 8192 && !small_paths(d)) {   // slot order by rank in a slot bitmap (sort buffers free)
-        cta_slot_order(fva, (int)nF, N, fp, sm->p[0], s_big, s_tmp);
-      } else {
-        dbg_hit(d, DBG_F_SORT);
-        const int res = cta_sort_kv(fka, fva, fkb, fvb, (int)nF, s_big, s_tmp, sm, sort_lim(d));
-        const u32* fs = res ? fvb : fva;
-        for (u32 i = threadIdx.x; i < nF; i += CTA) fp[i] = fs[i];
-        __syncthreads();
+      // F_r = REASONING placed on r now: the footprint pass's REASONING set on r, minus
+      // the programs this tick's pause pass took off r, plus the phase-R programs the
+      // restore pass put on r.  The bitmap (in shared memory; NW <= 8192) gives the slot
+      // order; the sort buffers are free here.
+      u32* s_bits = reinterpret_cast<u32*>(sm->k[0]);
+      u32* s_fpl = reinterpret_cast<u32*>(sm->k[1]);      // the list, for the need pass
+      const int NW = d.NW;
+      const u32 np = d.pause_cnt[r], nr = d.ctr->restore_cnt;
+      for (int w = threadIdx.x; w < NW; w += CTA) s_bits[w] = d.reas_bits[(size_t)r * NW + w];
+      __syncthreads();
+      for (u32 i = threadIdx.x; i < np; i += CTA) {
+        const u32 q = d.pause_list[(size_t)r * N + i];
+        atomicAnd(&s_bits[q >> 5], ~(1u << (q & 31)));
       }
-      for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, fp[i], r);
+      __syncthreads();
+      for (u32 i = threadIdx.x; i < nr; i += CTA) {
+        const u32 x = d.restore_dst[i];
+        if ((int)(x & 0xFFu) == r && !((x >> 24) & 1u)) {   // restored onto r in phase R
+          const u32 q = d.restore_pid[i];
+          atomicOr(&s_bits[q >> 5], 1u << (q & 31));
+        }
+      }
+      __syncthreads();
+      cta_bitmap_prefix(s_bits, NW, s_big, s_tmp);
+      nF = s_big[NW];
+      for (int w = threadIdx.x; w < NW; w += CTA) {
+        u32 m = s_bits[w], pos = s_big[w];
+        while (m) {
+          const u32 q = (u32)w * 32u + (u32)(__ffs(m) - 1);
+          m &= m - 1;
+          fp[pos] = q;
+          if (pos < 8192) s_fpl[pos] = q;
+          ++pos;
+        }
+      }
+      __syncthreads();
+      for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, i < 8192 ? s_fpl[i] : fp[i], r);
       __syncthreads();
       cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
@@ -209,8 +222,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   }
   cl.sync();                                           // #0: rank 2's supply reaches the leader
   if (lead) {
-    const u32* el = d.ec_list + (size_t)r * N;      // home == r with HBM blocks (footprint pass)
-    const int nel = (int)d.ec_cnt[r];
+    const u32* el = nullptr;                        // home == r with HBM blocks (footprint pass)
+    int nel = 0;
     const ull fr = sh.fr, es = sh.es;
     const ull supply = fr + es;
     // ---- 5.2 stall cut: longest prefix of F_r with sum(need) <= supply
@@ -249,6 +262,14 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           return (u32)(d.phase[i] == TA_PHASE_A ? 0 : 1) * NBK + (NBK - 1 - (d.nb[i] >> shf));
         return (u32)(d.placement[i] != r ? 2 : 3) * NBK + (d.contrib[i] >> shf);
       };
+      // the candidates as a slot list in shared memory (s_ec and s_hw, 8192 words, free
+      // until the sorted order is staged), else in global scratch
+      {
+        const u32 cap = small_paths(d) ? 8u : 8192u;
+        nel = (int)cta_bits_to_list(d.ec_bits + (size_t)r * d.NW, d.NW, s_ec, cap, d.ec_list + (size_t)r * N,
+                                    s_tmp, &el);
+        if ((u32)nel > cap) dbg_hit(d, DBG_LIST_GLOBAL);
+      }
       const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
                                        [&](int i) { return d.n_hbm[i] - d.sb; });
       PSTAMP(2, 3);

@@ -39,11 +39,16 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
   u64* kb = d.skb + (size_t)r * N;
   u32* va = d.sva + (size_t)r * N;
   u32* vb = d.svb + (size_t)r * N;
-  // the actives on r are exactly the footprint pass's list for r (statuses have not
-  // changed since); ordered by (S_pause key, slot) whatever the list order
+  // the actives on r are exactly the footprint pass's set for r (statuses have not
+  // changed since), as a slot list in the free tail of the dynamic shared memory (or
+  // global scratch when it does not fit); ordered below by (S_pause key, slot)
   __shared__ u32 s_cnt;
-  const u32* al = d.act_list + (size_t)r * N;
-  const int na = (int)d.act_cnt[r];
+  const u32* al = nullptr;
+  const u32 lcap = small_paths(d) ? 8u : 3u * 4096u;
+  const int na = (int)cta_bits_to_list(d.act_bits + (size_t)r * d.NW, d.NW,
+                                       reinterpret_cast<u32*>(dsm + sizeof(SortSmem)), lcap,
+                                       d.act_list + (size_t)r * N, s_tmp, &al);
+  if ((u32)na > lcap) dbg_hit(d, DBG_LIST_GLOBAL);
   const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware baseline (A46)
   auto bucket = [&](int i) { return ra ? 0u : (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
   const u32 T = cta_list_threshold(al, na, 2 * NBK, 0, dC, s_big, s_tmp, [](int) { return true; }, bucket,
@@ -197,7 +202,8 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
             d.status[pl] = phl == TA_PHASE_A ? TA_ACTING : TA_REASONING;
             d.placement[pl] = (i8)t;
             d.restore_pid[cnt] = pl;
-            d.restore_dst[cnt] = t | ((u32)(hml + 1) << 8);   // dst | (home before + 1) << 8
+            // dst | (home before + 1) << 8 | phase A << 24
+            d.restore_dst[cnt] = t | ((u32)(hml + 1) << 8) | ((u32)(phl == TA_PHASE_A) << 24);
           }
           ++cnt;
         }

@@ -16,7 +16,7 @@ __global__ void k_verb_reset(Dev d) {
   if (t < d.R) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;
     d.evd_cnt[t] = 0; d.fed_cnt[t] = 0; d.fld_cnt[t] = 0; d.dfh_cnt[t] = 0; d.dfs_cnt[t] = 0;
-    d.cpd_cnt[t] = 0; d.act_cnt[t] = 0; d.ec_cnt[t] = 0;
+    d.cpd_cnt[t] = 0;
   }
   for (u32 b = threadIdx.x; b < 2 * d.nbk; b += blockDim.x) d.rhist[b] = 0;
 }

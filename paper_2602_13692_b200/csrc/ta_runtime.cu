@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -106,6 +107,7 @@ static const char* validate(const ta_config* c) {
   if (c->replicas_here < 1 || c->first_replica < 0 || c->first_replica + c->replicas_here > c->n_replicas)
     return "replicas_here/first_replica out of range";
   if (c->max_programs < 1 || c->max_blocks_per_program < 1) return "max_programs/max_blocks must be >= 1";
+  if (c->max_programs > 262144) return "max_programs must be <= 262144 (planner slot bitmaps in shared memory)";
   if (c->max_blocks_per_program >= (1 << 23)) return "max_blocks_per_program must be < 2^23";
   if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (1ull << 32))
     return "max_programs * max_blocks_per_program must be < 2^32";
@@ -176,9 +178,10 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.gsync = L.take<ull>(2);
   x.dbg = L.take<ull>(DBG_N);
   x.t_rep = L.take<u32>(3 * R);
-  x.act_list = L.take<u32>(R * N); x.act_cnt = L.take<u32>(R);
-  x.ec_list = L.take<u32>(R * N); x.ec_cnt = L.take<u32>(R);
-  x.rhist = L.take<u32>(2 * 2048 + 2); x.rb = L.take<u32>(N); x.fpl = L.take<i8>(N);
+  const size_t NWs = (N + 31) / 32;
+  x.act_bits = L.take<u32>(R * NWs); x.reas_bits = L.take<u32>(R * NWs); x.ec_bits = L.take<u32>(R * NWs);
+  x.act_list = L.take<u32>(R * N); x.ec_list = L.take<u32>(R * N);
+  x.rhist = L.take<u32>(2 * 2048 + 2); x.rb = L.take<u32>(N);
   if (d) *d = x;
   return L.off + 256;
 }
@@ -302,9 +305,9 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     k_ev_single<<<eg, 256, 0, s>>>(d);
     k_ev_multi<<<1, CTA, PLAN_DSMEM, s>>>(d);
     k_ev_apply<<<eg, 256, 0, s>>>(d);
-    k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 0);
+    k_footprint<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d, 0);
   } else {
-    k_tick_front<<<(N * 32 + 255) / 256, 256, 0, s>>>(d);   // ingest + footprint + load
+    k_tick_front<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d);   // ingest + footprint + load
   }
   rec(x, 1);
   if (x->split_pr) {                       // A/B aid: the two passes as separate kernels
@@ -404,6 +407,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   host_carve(cfg, (char*)bufs->host_workspace, &x->h);
   x->ev_dev = d.events;
   d.N = cfg->max_programs;
+  d.NW = (cfg->max_programs + 31) / 32;
   d.MAXB = cfg->max_blocks_per_program;
   d.MAXBP = (cfg->max_blocks_per_program + 3) & ~3;
   d.R = cfg->n_replicas;
@@ -468,6 +472,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_move_fused, 256, BULK_CHUNK);
+    if (const char* e = getenv("TA_MOVE_CTAS_PER_SM"))   // A/B aid: fewer resident copy CTAs
+      per_sm = std::max(1, std::min(per_sm, atoi(e)));
     x->move_grid = (sms * per_sm) & ~1;
     if (x->move_grid < 2) d.fused = 0;
     // k_close: one 1024-thread CTA per 1024 slots (at least R), at most one per SM
@@ -812,7 +818,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   cudaStream_t s = ctx->stream;
   const int N = d.N;
   k_verb_reset<<<1, 32, 0, s>>>(d);
-  k_footprint<<<(N * 32 + 255) / 256, 256, 0, s>>>(d, 1);
+  k_footprint<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d, 1);
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
   k_plan<<<d.R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARGS = ["--impl", "reference", "--steps", "1", "--warmup", "3", "--preroll", "0", "--config", "c2_swe"]
+ARGS = ["--impl", "reference", "--steps", "1", "--warmup", "3", "--window-start", "1", "--config", "c2_swe"]
 
 
 def _one_line(out):

@@ -2,16 +2,23 @@
 send/recv baseline (BASELINE.json north_star: "cross-replica migration as P2P stores
 over NVLink, with NCCL send/recv only as the comparison baseline").
 
-torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/p2p_bench.py [n_blocks]
+torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/p2p_bench.py [n_blocks] [layout]
 
-Both replicas hold a layer-major Qwen3-32B pool (4 MiB blocks = 128 segments of
-32 KiB).  n random source blocks of rank 0 move to n random free blocks of rank 1:
-  ours_push  ta_move_blocks(P2P, 0 -> 1) on rank 0: loads from local HBM, stores into
-             the peer pool mapped with CUDA IPC (one kernel, NVLink writes)
-  ours_pull  ta_move_blocks(P2P, 0 -> 1) on rank 1: loads over NVLink from rank 0's pool
-  nccl       rank 0 gathers the blocks into a contiguous buffer (torch index_select),
-             dist.send -> dist.recv (NCCL), rank 1 scatters them (torch index_copy_)
-  nccl_link  dist.send/recv of one contiguous buffer of the same bytes (link reference)
+Both replicas hold a Qwen3-32B pool (4 MiB blocks = 128 segments of 32 KiB); layout 0
+is layer-major (a block's 128 segments are 32 KiB pieces NB*32 KiB apart, vLLM-like),
+layout 1 block-major (a block is one contiguous 4 MiB range).  n random source blocks
+of rank 0 move to n random free blocks of rank 1:
+  ours_push   ta_move_blocks(P2P, 0 -> 1) on rank 0: loads from local HBM, stores into
+              the peer pool mapped with CUDA IPC (one kernel, NVLink writes)
+  ours_pull   ta_move_blocks(P2P, 0 -> 1) on rank 1: loads over NVLink from rank 0's pool
+  nccl_p2p    the fair NCCL baseline: grouped ncclSend / ncclRecv
+              (torch batch_isend_irecv) straight from the source pool into the
+              destination pool, no staging: one send/recv pair per contiguous piece --
+              per 4 MiB block in layout 1, per 32 KiB segment in layout 0 (groups of
+              4096 pairs)
+  nccl_staged rank 0 gathers the blocks into a contiguous buffer (torch index_select),
+              dist.send -> dist.recv, rank 1 scatters them (torch index_copy_)
+  nccl_link   dist.send/recv of one contiguous buffer of the same bytes (link reference)
 Bytes are checked after every variant.  Times: CUDA events, max over the two ranks.
 Rank 0 prints one JSON line."""
 import json
@@ -30,12 +37,13 @@ from paper_2602_13692_b200.dist import connect  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+    layout = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     assert world == 2
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", device_id=dev)
-    cfg = tracegen.get_config("bench_10k", n_replicas=2, hbm_blocks=4 * n, host_blocks=0)
+    cfg = tracegen.get_config("bench_10k", n_replicas=2, hbm_blocks=4 * n, host_blocks=0, layout=layout)
     pool = Pool(cfg, 16, max_turns=1, fill=False, device=rank, replicas_here=1, first_replica=rank)
     connect(pool)
     bb = pool.block_bytes
@@ -52,8 +60,12 @@ def main():
     s = pool.stream
     torch.cuda.synchronize(dev)
 
+    def pool_view():                      # [nseg, NB, seg] whatever the layout
+        v = pool.hbm[rank]
+        return v.view(nseg, pool.NB, seg) if layout == 0 else v.view(pool.NB, nseg, seg).transpose(0, 1)
+
     def blocks(idx):
-        return pool.hbm[rank].view(nseg, pool.NB, seg)[:, idx.long(), :]
+        return pool_view()[:, idx.long(), :]
 
     want = blocks(src).clone() if rank == 0 else None
     if rank == 1:
@@ -87,8 +99,7 @@ def main():
 
     def scrub():
         if rank == 1:
-            blocks_view = pool.hbm[1].view(nseg, pool.NB, seg)
-            blocks_view[:, dst.long(), :] = 0
+            pool_view()[:, dst.long(), :] = 0
         torch.cuda.synchronize(dev)
 
     res = {}
@@ -97,20 +108,43 @@ def main():
         scrub()
         ms = timed(lambda: pool.move_blocks(binding.MOVE_P2P, 0, 1, src, dst) if rank == actor else None)
         res[name] = {"ms": round(ms, 3), "gbs": round(n * bb / (ms * 1e-3) / 1e9, 1), "bytes_ok": check()}
-    # NCCL baseline: gather -> send/recv -> scatter
+    # the fair NCCL baseline: grouped send/recv of every contiguous piece, pool to pool
+    src_l, dst_l = src.tolist(), dst.tolist()
+    if layout == 1:
+        flat = pool.hbm[rank].view(pool.NB, bb)
+        pieces = [flat[b] for b in (src_l if rank == 0 else dst_l)]
+    else:
+        lv = pool.hbm[rank].view(nseg, pool.NB, seg)
+        pieces = [lv[q, b] for b in (src_l if rank == 0 else dst_l) for q in range(nseg)]
+    GROUP = 4096
+
+    def nccl_p2p_fn():
+        for i in range(0, len(pieces), GROUP):
+            ops = [dist.P2POp(dist.isend if rank == 0 else dist.irecv, t, 1 - rank) for t in pieces[i:i + GROUP]]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+    scrub()
+    nccl_p2p_fn()                               # NCCL's first grouped call sets up its P2P channels
+    scrub()
+    ms = timed(nccl_p2p_fn)
+    res["nccl_p2p"] = {"ms": round(ms, 3), "gbs": round(n * bb / (ms * 1e-3) / 1e9, 1), "bytes_ok": check(),
+                       "pieces": len(pieces), "piece_bytes": bb if layout == 1 else seg,
+                       "how": "torch batch_isend_irecv (ncclGroupStart, ncclSend/ncclRecv per contiguous piece, "
+                              f"ncclGroupEnd; groups of {GROUP}), pool to pool, no staging"}
+    # NCCL with staging: gather -> send/recv -> scatter
     stage = torch.empty(nseg, n, seg, dtype=torch.uint8, device=dev)
 
     def nccl_fn():
         if rank == 0:
-            torch.index_select(pool.hbm[0].view(nseg, pool.NB, seg), 1, src.long(), out=stage)
+            stage.copy_(blocks(src))
             dist.send(stage, dst=1)
         else:
             dist.recv(stage, src=0)
-            pool.hbm[1].view(nseg, pool.NB, seg).index_copy_(1, dst.long(), stage)
+            pool_view()[:, dst.long(), :] = stage
     scrub()
     ms = timed(nccl_fn)
-    res["nccl"] = {"ms": round(ms, 3), "gbs": round(n * bb / (ms * 1e-3) / 1e9, 1), "bytes_ok": check(),
-                   "how": "torch index_select gather + dist.send/recv (NCCL) + index_copy_ scatter"}
+    res["nccl_staged"] = {"ms": round(ms, 3), "gbs": round(n * bb / (ms * 1e-3) / 1e9, 1), "bytes_ok": check(),
+                          "how": "torch gather into a contiguous buffer + dist.send/recv (NCCL) + scatter"}
 
     def link_fn():
         if rank == 0:
@@ -121,10 +155,13 @@ def main():
     res["nccl_link"] = {"ms": round(ms, 3), "gbs": round(n * bb / (ms * 1e-3) / 1e9, 1),
                         "how": "dist.send/recv of one contiguous buffer of the same bytes"}
     if rank == 0:
-        out = {"blocks": n, "block_bytes": bb, "bytes": n * bb, "peak_gbs_nvlink_per_direction": 900,
+        out = {"blocks": n, "layout": "layer-major" if layout == 0 else "block-major", "block_bytes": bb,
+               "bytes": n * bb, "peak_gbs_nvlink_per_direction": 900,
                "measured_peer_copy_gbs": 770, "results": res,
+               "frac_of_900": {k: round(v["gbs"] / 900.0, 3) for k, v in res.items()},
                "frac_of_770": {k: round(v["gbs"] / 770.0, 3) for k, v in res.items()},
-               "ours_vs_nccl": round(res["ours_push"]["gbs"] / res["nccl"]["gbs"], 2)}
+               "ours_push_vs_nccl_p2p": round(res["ours_push"]["gbs"] / res["nccl_p2p"]["gbs"], 2),
+               "ours_pull_vs_nccl_p2p": round(res["ours_pull"]["gbs"] / res["nccl_p2p"]["gbs"], 2)}
         print(json.dumps(out), flush=True)
     dist.barrier()
     pool.close()
