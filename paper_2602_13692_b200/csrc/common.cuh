@@ -361,6 +361,45 @@ __device__ u32 cta_ordered_gather(int n, u32* s_tmp, Pred pred, Emit emit) {
   return total;
 }
 
+// Ordered stream compaction over [0, n) with coalesced reads: warp w owns a contiguous
+// range of indices and its lanes take consecutive ones (ballot counts per warp, a scan
+// over the warps, then the emit pass re-evaluates pred).  Items keep index order.
+// emit(pos, i, total) -- the total is known before the first emit.
+template <typename Pred, typename Emit>
+__device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
+  const int w = threadIdx.x >> 5, lane = (int)lane_id();
+  const int per = (((n + NWARP - 1) / NWARP) + 31) & ~31;
+  const int lo = w * per, hi = min(n, lo + per);
+  u32 cnt = 0;
+  for (int b = lo; b < hi; b += 128) {            // four independent loads per lane in flight
+    bool t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { const int i = b + 32 * k + lane; t[k] = i < hi && pred(i); }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cnt += __popc(__ballot_sync(FULL_MASK, t[k]));
+  }
+  if (lane == 0) s_tmp[w] = cnt;
+  __syncthreads();
+  if (w == 0) {
+    const u32 x = lane < NWARP ? s_tmp[lane] : 0u;
+    const u32 xi = warp_incl_scan(x);
+    if (lane < NWARP) s_tmp[lane] = xi - x;
+    if (lane == NWARP - 1) s_tmp[NWARP] = xi;
+  }
+  __syncthreads();
+  u32 pos = s_tmp[w];
+  const u32 total = s_tmp[NWARP];
+  for (int b = lo; b < hi; b += 32) {
+    const int i = b + lane;
+    const bool t = i < hi && pred(i);
+    const u32 m = __ballot_sync(FULL_MASK, t);
+    if (t) emit(pos + __popc(m & lanemask_lt()), i, total);
+    pos += __popc(m);
+  }
+  __syncthreads();
+  return total;
+}
+
 // In-place inclusive scan of a global u32 array a[0..n) by one CTA.
 __device__ void cta_incl_scan_array(u32* a, int n, u32* s_tmp) {
   int chunk = (n + CTA - 1) / CTA;
@@ -495,9 +534,11 @@ __device__ __forceinline__ void bitonic_pick(u64& k, u32& p, u64 ok, u32 op, boo
 __device__ __forceinline__ void cta_rank_sort(const u64* ka, u64* kb, u32* vb, int n, SortSmem* sm,
                                               bool tie_is_val, const u32* va) {
   const int t = threadIdx.x;
+  u32 myv = 0;                                  // read before any write: (kb, vb) may be (ka, va)
   if (t < n) {
+    myv = va[t];
     sm->k[0][t] = ka[t];
-    sm->p[0][t] = tie_is_val ? va[t] : (u32)t;
+    sm->p[0][t] = tie_is_val ? myv : (u32)t;
   }
   __syncthreads();
   if (t < n) {
@@ -510,7 +551,7 @@ __device__ __forceinline__ void cta_rank_sort(const u64* ka, u64* kb, u32* vb, i
       rank += (kj < k) | ((kj == k) & (vj < v));
     }
     kb[rank] = k;
-    vb[rank] = tie_is_val ? v : va[t];
+    vb[rank] = myv;
   }
   __syncthreads();
 }
@@ -599,11 +640,20 @@ __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, 
       }
     }
   }
+  u32 vv[SORT_SMALL / CTA];                     // read every value before any write (in place)
   if (act) {
 #pragma unroll
     for (int e = 0; e < SORT_SMALL / CTA; ++e) {
       const int i = t + e * CTA;
-      if (e < E && i < n) { kb[i] = k[e]; vb[i] = va[p[e]]; }
+      vv[e] = (e < E && i < n) ? va[p[e]] : 0u;
+    }
+  }
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int e = 0; e < SORT_SMALL / CTA; ++e) {
+      const int i = t + e * CTA;
+      if (e < E && i < n) { kb[i] = k[e]; vb[i] = vv[e]; }
     }
   }
   __syncthreads();

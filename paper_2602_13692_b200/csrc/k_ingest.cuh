@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 #ifndef FP_THREADS
 #define FP_THREADS 256                   // FP_SLOTS / (FP_THREADS / 32) slots per warp
 #endif
-#define FP_STAGE (FP_SLOTS * 80)         // 16-B chunks staged per CTA (320 block-table entries per slot)
+#define FP_STAGE (FP_SLOTS * 104)        // 16-B chunks staged per CTA (416 block-table entries per slot, 52 KiB)
 #define FP_SMEM (FP_STAGE * 16)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

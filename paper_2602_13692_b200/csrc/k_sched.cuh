@@ -17,6 +17,8 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   __shared__ ull s_L;
   if (d.ctr->err != TA_OK) return;              // API batch rejected: the tick does not run
+  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[threadIdx.x] = 0;
+  PSTAMP(0, 0);
   if (threadIdx.x == 0) {                       // publish this tick's load (eq. 7) of replica r
     s_L = d.Lacc[r];
     d.Lacc[r] = 0;
@@ -49,10 +51,12 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
                                        reinterpret_cast<u32*>(dsm + sizeof(SortSmem)), lcap,
                                        d.act_list + (size_t)r * N, s_tmp, &al);
   if ((u32)na > lcap) dbg_hit(d, DBG_LIST_GLOBAL);
+  PSTAMP(0, 1);
   const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware baseline (A46)
   auto bucket = [&](int i) { return ra ? 0u : (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
   const u32 T = cta_list_threshold(al, na, 2 * NBK, 0, dC, s_big, s_tmp, [](int) { return true; }, bucket,
                                    [&](int i) { return d.contrib[i]; });
+  PSTAMP(0, 2);
   u32 n = cta_list_gather(al, na, &s_cnt,
       [&](int i) { return bucket(i) <= T; },
       [&](u32 pos, int i) {
@@ -60,7 +64,9 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
                      : pause_key(d.phase[i], d.nb[i], d.acting_since[i]);
         va[pos] = (u32)i;
       });
+  PSTAMP(0, 3);
   int res = cta_sort_kv(ka, va, kb, vb, (int)n, s_big, s_tmp, sm, sort_lim(d));
+  PSTAMP(0, 4);
   const u32* sv = res ? vb : va;
   u32* cum = (u32*)(res ? ka : kb);             // free key buffer as u32 scratch
   for (u32 i = threadIdx.x; i < n; i += CTA) cum[i] = d.contrib[sv[i]];
@@ -82,6 +88,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
     d.rb[p] = b;
     atomicAdd(&d.rhist[b], 1u);
   }
+  PSTAMP(0, 5);
   if (threadIdx.x == 0) {
     d.pause_cnt[r] = m;
     d.L[r] = Lr - (m ? cum[m - 1] : 0);
@@ -153,17 +160,31 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
   while (true) {
     const u32 T = cta_hist_threshold(d.rhist, 2 * NBK, lo, chunk, s_big, s_tmp);
     if (it < 7) PSTAMP(1, 1 + 4 * it);
-    u32 n = cta_ordered_gather(N, s_tmp,
+    // the chunk's entries (slot order) with their S_restore keys, into the free tail of
+    // the dynamic shared memory when they fit (sorted there in place), else global
+    const u32 scap = small_paths(d) ? 16u : (u32)SORT_SMALL;
+    u64* s_gk = reinterpret_cast<u64*>(dsm + sizeof(SortSmem));
+    u32* s_gv = reinterpret_cast<u32*>(s_gk + SORT_SMALL);
+    u32 n = cta_ordered_gather_w(N, s_tmp,
         [&](int i) { const u32 b = d.rb[i]; return b >= lo && b <= T; },
-        [&](u32 pos, int i) {
-          ka[pos] = (d.flags & TA_F_REQUEST_AWARE) ? (u64)d.paused_since[i]            // FCFS (A46)
-                                                   : restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
-          va[pos] = (u32)i;
+        [&](u32 pos, int i, u32 total) {
+          const u64 key = (d.flags & TA_F_REQUEST_AWARE) ? (u64)d.paused_since[i]            // FCFS (A46)
+                                                         : restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
+          if (total <= scap) { s_gk[pos] = key; s_gv[pos] = (u32)i; }
+          else { ka[pos] = key; va[pos] = (u32)i; }
         });
     if (it < 7) PSTAMP(1, 2 + 4 * it);
     if ((d.flags & TA_F_TIMING) && threadIdx.x == 0 && it < 4) d.pst[1 * 32 + 27 + it] = n | (1ull << 62);
-    int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm, sort_lim(d));
-    const u32* q = res ? vb : va;
+    const u32* q;
+    if (n <= scap) {
+      const int res = cta_sort(s_gk, s_gv, s_gk, s_gv, (int)n, s_big, s_tmp, sm, sort_lim(d));
+      (void)res;                          // in place: the result is in (s_gk, s_gv) either way
+      q = s_gv;
+    } else {
+      dbg_hit(d, DBG_LIST_GLOBAL);
+      const int res = cta_sort(ka, va, kb, vb, (int)n, s_big, s_tmp, sm, sort_lim(d));
+      q = res ? vb : va;
+    }
     if (it < 7) PSTAMP(1, 3 + 4 * it);
     if (w0) {
       bool stop = false;

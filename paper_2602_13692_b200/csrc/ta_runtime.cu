@@ -510,6 +510,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ev_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tick_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_footprint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_SMEM);
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));

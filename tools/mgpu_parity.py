@@ -1,13 +1,14 @@
 """Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
 
 torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs] [--api]
-    [--shared TOKENS]
+    [--shared TOKENS] [--c3]
 Every rank runs the replicated control plane for all N replicas and moves only its
 own replica's bytes; every rank compares its decisions and full state with its own
 oracle copy, and verifies the KV content of its local pool.  --api: the same ticks in
 API mode (the engine's recorded events, tools/api_events.py) against the trace-mode
 oracle.  --shared: NEXT-3 shared system prompt of TOKENS tokens (reserved blocks on
-every GPU).  Exit code 0 = parity."""
+every GPU).  --c3: configs[2] (2k programs) with one replica per GPU, decision-only KV
+shape.  Exit code 0 = parity."""
 import os
 import random
 import sys
@@ -32,9 +33,12 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spt = int(sys.argv[sys.argv.index("--shared") + 1]) if "--shared" in sys.argv else 0
-    cfg = tracegen.get_config("c1_toy", n_replicas=world, hbm_blocks=64, host_blocks=16, compact_every=3,
-                              trace=dict(n=12 * world, n_initial=5 * world, seed=77),
-                              shared_prefix_tokens=spt)
+    if "--c3" in sys.argv:    # configs[2]'s 2k OpenHands + ToolOrchestra programs, one replica per GPU,
+        cfg = tracegen.get_config("c3_mixed", kv="mini", n_replicas=world, compact_every=4)   # decision-only KV
+    else:
+        cfg = tracegen.get_config("c1_toy", n_replicas=world, hbm_blocks=64, host_blocks=16, compact_every=3,
+                                  trace=dict(n=12 * world, n_initial=5 * world, seed=77),
+                                  shared_prefix_tokens=spt)
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     api = "--api" in sys.argv
@@ -58,7 +62,7 @@ def main():
         got = dec_tuples(got)
         assert got == want, f"rank {rank} tick {k}: decisions differ"
         n_dec += len(got)
-        if not api:                        # API mode keeps no tool_return: decisions + bytes only
+        if not api and (k % 4 == 0 or "--c3" not in sys.argv):   # API mode: decisions + bytes only
             compare_state(o, pool.debug_download(), where=f"rank {rank} tick {k}")
         bad, seen = pool.verify_content()
         assert bad == 0, f"rank {rank} tick {k}: {bad} of {seen} local KV words wrong"
