@@ -97,6 +97,8 @@ struct Dev {
   u32* loc;                        // [N][MAXBP]
   // ---- per-tick derived values ----
   u32 *nb, *n_hbm, *n_host, *prefix_hbm, *contrib;
+  u8* hcls;                        // [N] where the last history block (entry ceil(c_kv/bt) - 1) is:
+                                   //     0 NONE, 1 HBM, 2 host tier (footprint pass; hit accounting)
   u8* released;                    // released during this tick's ingest
   u8* sat_new;                     // 1 + replica that satisfied the program this tick
   u32 *pend, *busy;                // [N] synthetic engine (A48): tokens waiting for prefill;
@@ -518,7 +520,7 @@ struct SortSmem {                 // 96 KiB of dynamic shared memory
   u64 k[2][SORT_SMALL];
   u32 p[2][SORT_SMALL];
 };
-#define PLAN_DSMEM (sizeof(SortSmem) + 3 * 4096 * sizeof(u32))   // sort + staged arrays
+#define PLAN_DSMEM (sizeof(SortSmem) + 4 * 4096 * sizeof(u32))   // sort + staged arrays
 
 // keep the smaller (take_min) or larger pair of self and other; pairs are distinct
 __device__ __forceinline__ void bitonic_pick(u64& k, u32& p, u64 ok, u32 op, bool take_min) {

@@ -5,9 +5,9 @@
 
 // Deferred frees (P2P sources and fetched host slots become free only after the
 // movement, reading A16) and the per-program results of step 5.7.
-__device__ __forceinline__ void finalize_part(const Dev& d, int verb) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int stride = gridDim.x * blockDim.x;
+__device__ __forceinline__ void finalize_part(const Dev& d, int verb, int first_cta) {
+  const int t = ((int)blockIdx.x - first_cta) * blockDim.x + threadIdx.x;
+  const int stride = ((int)gridDim.x - first_cta) * blockDim.x;
   for (int r = 0; r < d.R; ++r) {
     const u32 nh = d.dfh_cnt[r], ns = d.dfs_cnt[r];
     const u32* fh = d.dfh + (size_t)r * d.NB;
@@ -116,9 +116,10 @@ __device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32
 
 // Canonical decision list (PAUSE by replica, RESTORE in queue order, EVICT by
 // replica, FETCH/STALL by replica in slot order, COMPACT by replica), written to
-// the host-mapped buffer; tick bookkeeping and occupancy statistics.
-__device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp) {
-  __shared__ ull s_red[NWARP];
+// the host-mapped buffer; tick bookkeeping and occupancy statistics.  In two parts:
+// the records of steps 3-5 (their inputs are final when k_close starts), and after the
+// frees and the compaction plan, the COMPACT records, statistics and clears.
+__device__ __forceinline__ u32 assemble_records(const Dev& d, u32* s_tmp) {
   const int N = d.N, R = d.R;
   const u32 cap = d.dec_cap;
   u32 pos = 0;                           // uniform across the CTA
@@ -150,7 +151,7 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
     for (u32 i = threadIdx.x; i < n; i += CTA) put(pos + i, d.dec_ev[(size_t)r * N + i]);
     pos += n;
   }
-  PSTAMP(3, 5);
+  PSTAMP(3, 10);
   for (int r = 0; r < R; ++r) {          // FETCH / STALL (kind 0 = no decision)
     const ta_decision* fs = d.dec_fs + (size_t)r * N;
     u32 n = cta_ordered_gather((int)d.f_cnt[r], s_tmp,
@@ -158,6 +159,14 @@ __device__ __forceinline__ void assemble_pass(const Dev& d, int verb, u32* s_tmp
         [&](u32 at, int i) { put(pos + at, fs[i]); });
     pos += n;
   }
+  return pos;
+}
+
+__device__ __forceinline__ void assemble_close(const Dev& d, int verb, u32 pos) {
+  __shared__ ull s_red[NWARP];
+  const int R = d.R;
+  const u32 cap = d.dec_cap;
+  auto put = [&](u32 at, const ta_decision& rec) { if (at < cap) d.dec_out[at] = rec; };
   for (int r = 0; r < R; ++r) {          // COMPACT
     u32 n = d.cpd_cnt[r];
     if (n) {
@@ -246,7 +255,11 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
   if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[3 * 32 + threadIdx.x] = 0;
   PSTAMP(3, 0);
-  finalize_part(d, verb);
+  // CTA 0 assembles the records of steps 3-5 while the other CTAs finalize (one CTA: both)
+  u32 pos = 0;
+  if (blockIdx.x == 0) pos = assemble_records(d, s_tmp);
+  PSTAMP(3, 5);
+  if (gridDim.x == 1 || blockIdx.x > 0) finalize_part(d, verb, gridDim.x == 1 ? 0 : 1);
   PSTAMP(3, 1);
   grid_sync(d, 1);
   PSTAMP(3, 2);
@@ -259,6 +272,6 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) grid_sync(d, 1);   // plans -> decisions
   else __syncthreads();
   PSTAMP(3, 4);
-  if (blockIdx.x == 0) assemble_pass(d, verb, s_tmp);
+  if (blockIdx.x == 0) assemble_close(d, verb, pos);
   PSTAMP(3, 9);
 }

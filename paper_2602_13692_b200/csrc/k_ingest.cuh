@@ -310,7 +310,8 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   __shared__ u32 s_off[FP_SLOTS + 1];    // chunk offsets (exclusive prefix of ceil(nbo/4))
   __shared__ u32 s_nbo[FP_SLOTS], s_nh[FP_SLOTS], s_ns[FP_SLOTS], s_first[FP_SLOTS];
   __shared__ int s_home[FP_SLOTS];
-  __shared__ u8 s_rel[FP_SLOTS];
+  __shared__ u8 s_rel[FP_SLOTS], s_hcls[FP_SLOTS];
+  __shared__ u32 s_jh[FP_SLOTS];          // entry of the last history block (ceil(c_kv/bt) - 1), or ~0
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const int p0 = blockIdx.x * FP_SLOTS;
   const int p = p0 + lane;
@@ -342,6 +343,9 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     if (lane == 31) s_off[FP_SLOTS] = inc;
     s_nbo[lane] = nbo;
     s_nh[lane] = 0; s_ns[lane] = 0; s_first[lane] = 0xFFFFFFFFu;
+    const u32 ckv = p < d.N ? d.c_kv[p] : 0u;
+    s_jh[lane] = ckv ? ceil_div_u32(ckv, d.bt) - 1 : 0xFFFFFFFFu;
+    s_hcls[lane] = 0;
   }
   __syncthreads();
   const u32* rows = d.loc + (size_t)p0 * d.MAXBP;
@@ -395,9 +399,14 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
       continue;
     }
     u32 a_h = 0, a_s = 0, a_f = 0xFFFFFFFFu;
+    const u32 jh = s_jh[sl];
     for (u32 c = lane; c < nch; c += 32) {
       const uint4 q = staged ? s_stage[o + c] : grow[c];
       const u32 e[4] = {q.x, q.y, q.z, q.w};
+      if ((jh >> 2) == c && jh < nbo) {  // the last history block's location class
+        const u32 x = e[jh & 3];
+        s_hcls[sl] = is_hbm(x) ? 1 : (is_host(x) ? 2 : 0);
+      }
 #pragma unroll
       for (int t = 3; t >= 0; --t) {
         const u32 j = 4 * c + t;
@@ -443,7 +452,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   }
   if (valid) {
     d.nb[p] = nbv; d.n_hbm[p] = n_h; d.n_host[p] = n_s; d.contrib[p] = cb;
-    d.rb[p] = rbv;
+    d.rb[p] = rbv; d.hcls[p] = s_hcls[lane];
   }
   // candidate bitmaps: this CTA's 32 slots are word blockIdx.x of every replica's maps
   // (whole-word stores, every word rewritten each pass); the decayed load of the actives

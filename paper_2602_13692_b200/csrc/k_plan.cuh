@@ -96,6 +96,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   u32* s_fc = reinterpret_cast<u32*>(dsm + sizeof(SortSmem));   // staged need prefix  [4096]
   u32* s_ec = s_fc + 4096;                                         // staged evict prefix [4096]
   u32* s_hw = s_ec + 4096;                                         // staged HBM free bitmap [4096]
+  u32* s_fl = s_hw + 4096;                                         // F_r in slot order, first 4096 [4096]
   // sort buffers, reused once the sorts are done: host-tier free words, victims,
   // per-F-program values of the request loop
   u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
@@ -139,6 +140,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   if (crank == 1) {
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     cl_copy(s_sfw, sf, d.NHW);
+    // the HBM free bitmap before the evictions; the eviction loop ORs the evicted blocks
+    // in (DSMEM), so the allocation prefix of part B needs no global round trip
+    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
   }
   // ================= rank 2, concurrent with F_r: free blocks on r and eviction supply
   if (crank == 2) {
@@ -176,25 +180,31 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       // F_r = REASONING placed on r now: the footprint pass's REASONING set on r, minus
       // the programs this tick's pause pass took off r, plus the phase-R programs the
       // restore pass put on r.  The bitmap (in shared memory; NW <= 8192) gives the slot
-      // order; the sort buffers are free here.
+      // order; the sort buffers are free here.  The words, the pause list and the restore
+      // entries are loaded together (one round trip after their counts).
       u32* s_bits = reinterpret_cast<u32*>(sm->k[0]);
-      u32* s_fpl = reinterpret_cast<u32*>(sm->k[1]);      // the list, for the need pass
       const int NW = d.NW;
       const u32 np = d.pause_cnt[r], nr = d.ctr->restore_cnt;
       for (int w = threadIdx.x; w < NW; w += CTA) s_bits[w] = d.reas_bits[(size_t)r * NW + w];
+      u32 pq = 0xFFFFFFFFu, rq = 0xFFFFFFFFu, rx = 0;
+      if (threadIdx.x < np) pq = d.pause_list[(size_t)r * N + threadIdx.x];
+      if (threadIdx.x < nr) { rx = d.restore_dst[threadIdx.x]; rq = d.restore_pid[threadIdx.x]; }
       __syncthreads();
-      for (u32 i = threadIdx.x; i < np; i += CTA) {
+      for (u32 i = threadIdx.x + CTA; i < np; i += CTA) {          // long lists: the rest
         const u32 q = d.pause_list[(size_t)r * N + i];
         atomicAnd(&s_bits[q >> 5], ~(1u << (q & 31)));
       }
+      if (pq != 0xFFFFFFFFu) atomicAnd(&s_bits[pq >> 5], ~(1u << (pq & 31)));
       __syncthreads();
-      for (u32 i = threadIdx.x; i < nr; i += CTA) {
+      for (u32 i = threadIdx.x + CTA; i < nr; i += CTA) {
         const u32 x = d.restore_dst[i];
-        if ((int)(x & 0xFFu) == r && !((x >> 24) & 1u)) {   // restored onto r in phase R
+        if ((int)(x & 0xFFu) == r && !((x >> 24) & 1u)) {
           const u32 q = d.restore_pid[i];
           atomicOr(&s_bits[q >> 5], 1u << (q & 31));
         }
       }
+      if (rq != 0xFFFFFFFFu && (int)(rx & 0xFFu) == r && !((rx >> 24) & 1u))   // restored onto r, phase R
+        atomicOr(&s_bits[rq >> 5], 1u << (rq & 31));
       __syncthreads();
       cta_bitmap_prefix(s_bits, NW, s_big, s_tmp);
       nF = s_big[NW];
@@ -204,12 +214,12 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           const u32 q = (u32)w * 32u + (u32)(__ffs(m) - 1);
           m &= m - 1;
           fp[pos] = q;
-          if (pos < 8192) s_fpl[pos] = q;
+          if (pos < 4096) s_fl[pos] = q;
           ++pos;
         }
       }
       __syncthreads();
-      for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, i < 8192 ? s_fpl[i] : fp[i], r);
+      for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, i < 4096 ? s_fl[i] : fp[i], r);
       __syncthreads();
       cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
@@ -357,7 +367,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     ull l_dec = 0, l_pre = 0, l_rec = 0;             // NEXT-1 STP ledger (token-ms)
     // ---- 5.6 hit accounting, FETCH / STALL records, new tokens into a resident partial block
     for (u32 i = threadIdx.x; i < nF; i += CTA) {
-      u32 p = fp[i];
+      u32 p = (verb || i >= 4096) ? fp[i] : s_fl[i];
       u32 need = fcs[i] - (i ? fcs[i - 1] : 0);
       int h = d.home[p];
       ta_decision rec;
@@ -376,8 +386,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           u32 shs = bt - (ckv - (hb - 1) * bt);        // missing slots of the last block
           u32 nh = nhp, ns = d.n_host[p], nn = hb - nh - ns;
           ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
-          u32 el = d.loc[(size_t)p * d.MAXBP + hb - 1];
-          if (is_hbm(el)) th -= shs; else if (is_host(el)) ts -= shs; else tn -= shs;
+          const u8 cls = d.hcls[p];                    // entry hb - 1, classified by the footprint pass
+          if (cls == 1) th -= shs; else if (cls == 2) ts -= shs; else tn -= shs;
           if (d.sb) {                                  // shared prefix: resident on r (hit)
             const ull sh = (ull)d.sb * bt;             // c_kv >= every prompt >= sb * bt
             if (h >= 0) th -= sh; else tn -= sh;
@@ -447,6 +457,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     const u32 hfree = s_big[d.NHW];
     const u32* ecs = ecs_sm ? s_ec : ec;
     u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
+    u32* R1hw = cl.map_shared_rank(s_hw, 1);           // rank 1's free-block snapshot
     const u32 per = (X + PLAN_CL - 2) / (PLAN_CL - 1); // ranks 1..PLAN_CL-1
     const u32 e_lo = (crank - 1) * per, e_hi = min(X, e_lo + per);
     // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
@@ -474,6 +485,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         const u32 idx = ik[k], j = jk[k], p = pk[k];
         u32* ent = d.loc + (size_t)p * d.MAXBP + j;
         atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
+        atomicOr(&R1hw[idx >> 5], 1u << (idx & 31));        // ... and in rank 1's snapshot
         if (e < hfree) {
           if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
           const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
@@ -497,10 +509,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // the leader's victims and D2H order run beside the request loop, and the other ranks
   // stage the leader's lists before they wait for it.
   if (crank == 1) {
-    // ---- 5.4 allocation prefix (after the evictions' frees) and free-word snapshot
-    cta_bitmap_prefix(hf, d.NBW, s_big, s_tmp);
-    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
-    __syncthreads();
+    // ---- 5.4 allocation prefix (after the evictions' frees) over the free snapshot
+    cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);
   }
   cl.barrier_arrive();                                 // #3 (arrive; release)
   if (lead && X > 0) {

@@ -144,7 +144,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.loc = L.take<u32>(N * MAXBP);
   x.nb = L.take<u32>(N); x.n_hbm = L.take<u32>(N); x.n_host = L.take<u32>(N);
   x.prefix_hbm = L.take<u32>(N); x.contrib = L.take<u32>(N);
-  x.pend = L.take<u32>(N); x.busy = L.take<u32>(N);
+  x.pend = L.take<u32>(N); x.busy = L.take<u32>(N); x.hcls = L.take<u8>(N);
   x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
   x.evc = L.take<u32>(N);
   x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
