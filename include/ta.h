@@ -317,10 +317,11 @@ ta_status ta_set_copy_bulk(ta_ctx* ctx, int32_t on);
  * compaction plan + decision assembly [7] compaction copies [8] unused.  n <= 9. */
 ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n);
 
-/* Developer aid (TA_F_TIMING only): raw SM-clock stamps (clock64) taken by thread 0
- * of CTA 0 at the phase boundaries of the planner kernels during the last tick:
- * out[32*k + i], k = 0 pause, 1 restore, 2 plan, 3 reserved; 0 = phase not reached.
- * n <= 128.  Synchronizes the stream.  Errors: TA_E_STATE (no TA_F_TIMING). */
+/* Developer aid (TA_F_TIMING only): globaltimer stamps (ns) taken by thread 0 of
+ * CTA 0 at the phase boundaries of the planner kernels during the last tick:
+ * out[32*k + i], k = 0 pause, 1 restore, 2 plan, 3 close, 4 / 5 plan cluster ranks
+ * 1 / 3 of replica 0; 0 = phase not reached.  n <= 256.  Synchronizes the stream.
+ * Errors: TA_E_STATE (no TA_F_TIMING). */
 ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n);
 
 /* Developer / test aid: cumulative size-branch counters since ta_init_pool, out[i] =

@@ -384,14 +384,23 @@ class Pool:
         return list(a)
 
     def phase_stamps(self):
-        """Raw clock64 stamps of the planner kernels' phases in the last tick (TA_F_TIMING):
-        {kernel: [(phase index, cycles since the kernel's first stamp), ...]}."""
-        a = (C.c_uint64 * 128)()
-        self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 128), "ta_debug_phase_stamps")
+        """Globaltimer stamps (ns) of the planner kernels' phases in the last tick (TA_F_TIMING):
+        {kernel: [(phase index, ns since that kernel's first stamp), ...]}; plan_cta1 / plan_cta3
+        are cluster ranks 1 and 3 of replica 0's planner cluster."""
+        a = (C.c_uint64 * 256)()
+        self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 256), "ta_debug_phase_stamps")
         out = {}
-        for k, name in enumerate(("pause", "restore", "plan", "close")):
+        names = ("pause", "restore", "plan", "close", "plan_cta1", "plan_cta3")
+        first = {}
+        for k, name in enumerate(names):
+            v = [a[32 * k + i] for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
+            first[name] = min(v) if v else 0
+        # the planner's cluster ranks share the leader's time origin
+        first["plan"] = first["plan_cta1"] = first["plan_cta3"] = min(
+            [x for x in (first["plan"], first["plan_cta1"], first["plan_cta3"]) if x] or [0])
+        for k, name in enumerate(names):
             v = [(i, a[32 * k + i]) for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
-            out[name] = [(i, c - v[0][1]) for i, c in v] if v else []
+            out[name] = [(i, c - first[name]) for i, c in v] if v else []
             # sizes recorded next to the stamps (bit 62 set): ("n<i>", value)
             out[name] += [(f"n{i}", a[32 * k + i] & ((1 << 62) - 1)) for i in range(32) if a[32 * k + i] >> 62 == 1]
         return out

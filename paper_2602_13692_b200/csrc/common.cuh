@@ -158,7 +158,7 @@ struct Dev {
   ull* mbox;                       // [TA_MAX_REPLICAS] this rank's barrier mailbox (epochs)
   ull* mbox_peer[TA_MAX_REPLICAS]; // peers' mailboxes (CUDA IPC)
   ull* epoch;                      // barrier epoch counter (device)
-  ull* pst;                        // [4][32] in-kernel phase stamps (TA_F_TIMING; developer aid)
+  ull* pst;                        // [8][32] in-kernel phase stamps, globaltimer ns (TA_F_TIMING; developer aid)
   // ---- candidate sets built by the footprint pass as slot bitmaps (one word per 32
   // slots, written whole by the CTA that owns those slots: no atomics), so the planner
   // kernels never scan all N slots except the restore gather; consumers turn a bitmap
@@ -241,10 +241,21 @@ __device__ __forceinline__ bool evp_owner(const Dev& d, int r) { return d.fused 
 
 // Phase stamp: SM clock of thread 0 of CTA 0 at a phase boundary of a planner kernel
 // (kernel slot kk: 0 pause, 1 restore, 2 plan, 3 other).  Only with TA_F_TIMING.
+__device__ __forceinline__ ull gtimer() {
+  ull t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define PSTAMP(kk, i)                                                              \
   do {                                                                             \
     if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x == 0)            \
-      d.pst[(kk) * 32 + (i)] = clock64();                                          \
+      d.pst[(kk) * 32 + (i)] = gtimer();                                           \
+  } while (0)
+// the same from thread 0 of block `b` into kernel slot kk (cluster ranks of k_plan)
+#define PSTAMP_B(kk, b, i)                                                         \
+  do {                                                                             \
+    if ((d.flags & TA_F_TIMING) && blockIdx.x == (b) && threadIdx.x == 0)          \
+      d.pst[(kk) * 32 + (i)] = gtimer();                                           \
   } while (0)
 
 // ------------------------------------------------------------------ helpers
@@ -547,7 +558,8 @@ __device__ __forceinline__ void cta_rank_sort(const u64* ka, u64* kb, u32* vb, i
     const u64 k = sm->k[0][t];
     const u32 v = sm->p[0][t];
     u32 rank = 0;
-    for (int j = 0; j < n; ++j) {
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {                // independent broadcast loads: unrolled for ILP
       const u64 kj = sm->k[0][j];
       const u32 vj = sm->p[0][j];
       rank += (kj < k) | ((kj == k) & (vj < v));

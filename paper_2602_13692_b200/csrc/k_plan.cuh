@@ -120,6 +120,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
                d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
   if ((d.flags & TA_F_TIMING) && r == 0 && lead && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
+  if ((d.flags & TA_F_TIMING) && (blockIdx.x == 1 || blockIdx.x == 3) && threadIdx.x < 32)
+    d.pst[(blockIdx.x == 1 ? 4 : 5) * 32 + threadIdx.x] = 0;
+  PSTAMP_B(4, 1, 0); PSTAMP_B(5, 3, 0);
   PSTAMP(2, 0);
   if (threadIdx.x < 4) s_app[threadIdx.x] = 0;
   if (threadIdx.x < PC_N) s_pc[threadIdx.x] = 0;
@@ -345,6 +348,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   }
   }                                                    // part A scope
   cl.sync();                                           // #1: part A visible to the cluster
+  PSTAMP_B(4, 1, 1); PSTAMP_B(5, 3, 1);
 
   // ================= all CTAs: the eviction loop, split by cluster rank
   PSTAMP(2, 15);
@@ -369,24 +373,26 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     for (u32 i = threadIdx.x; i < nF; i += CTA) {
       u32 p = (verb || i >= 4096) ? fp[i] : s_fl[i];
       u32 need = fcs[i] - (i ? fcs[i - 1] : 0);
-      int h = d.home[p];
+      // every per-program value up front: one memory round trip for the whole record
+      const int h = d.home[p];
+      const u32 ckv = d.c_kv[p], c = d.c[p], nhp = d.n_hbm[p], uidp = d.uid[p], nsp = d.n_host[p];
+      const u32 pendp = d.pend[p];
+      const u8 satp = d.satisfied[p], cls = d.hcls[p];
       ta_decision rec;
       rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
       rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
       if (i < m) {
-        const u32 ckv = d.c_kv[p], c = d.c[p];
-        const u32 nhp = d.n_hbm[p];
         if (fst) {
           s_fp[i] = p; s_fj[i] = h == r ? nhp : d.sb; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
-          s_fu[i] = d.uid[p];
+          s_fu[i] = uidp;
         }
-        const bool resumed = !(d.satisfied[p] && h == r);
+        const bool resumed = !(satp && h == r);
         if (resumed && ckv > 0) {
           u32 hb = ceil_div_u32(ckv, bt);
           u32 shs = bt - (ckv - (hb - 1) * bt);        // missing slots of the last block
-          u32 nh = nhp, ns = d.n_host[p], nn = hb - nh - ns;
+          u32 nh = nhp, ns = nsp, nn = hb - nh - ns;
           ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
-          const u8 cls = d.hcls[p];                    // entry hb - 1, classified by the footprint pass
+          // cls: entry hb - 1, classified by the footprint pass
           if (cls == 1) th -= shs; else if (cls == 2) ts -= shs; else tn -= shs;
           if (d.sb) {                                  // shared prefix: resident on r (hit)
             const ull sh = (ull)d.sb * bt;             // c_kv >= every prompt >= sb * bt
@@ -402,7 +408,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         l_dec += (ull)c * (ull)d.dt;                    // holds c while decoding the interval
         // engine time of this materialize: recompute + prefill of waiting tokens (A48)
         const u32 q = (u32)d.chunk_q;
-        d.busy[p] = (u32)d.chunk_ms * (ceil_div_u32(rec.miss_tok, q) + ceil_div_u32(d.pend[p], q));
+        d.busy[p] = (u32)d.chunk_ms * (ceil_div_u32(rec.miss_tok, q) + ceil_div_u32(pendp, q));
         d.pend[p] = 0;
         l_pre += (ull)d.chunk_ms * stp_stair(c - ckv, (ull)d.chunk_q, ckv);
         l_rec += (ull)d.chunk_ms * stp_stair(rec.miss_tok, (ull)d.chunk_q, 0);
@@ -415,7 +421,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
             pc[PC_FILLTOK] += t1 - ckv;
             if (fill) {
               u32 pos = atomicAdd(&s_app[1], 1u);
-              fld[pos] = FillDesc{d.loc[(size_t)p * d.MAXBP + j], d.uid[p], ckv, t1, j, 0};
+              fld[pos] = FillDesc{d.loc[(size_t)p * d.MAXBP + j], uidp, ckv, t1, j, 0};
             }
           }
         }
@@ -501,7 +507,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     }
   }
   PSTAMP(2, 16);
+  PSTAMP_B(4, 1, 2); PSTAMP_B(5, 3, 2);
   cl.sync();                                           // #2: evictions done
+  PSTAMP_B(4, 1, 3); PSTAMP_B(5, 3, 3);
   PSTAMP(2, 6);
 
   // ================= part B.  Rank 1: the allocation prefix, the only input of the
@@ -512,6 +520,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     // ---- 5.4 allocation prefix (after the evictions' frees) over the free snapshot
     cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);
   }
+  PSTAMP_B(4, 1, 4); PSTAMP_B(5, 3, 4);
   cl.barrier_arrive();                                 // #3 (arrive; release)
   if (lead && X > 0) {
     // D2H copies are issued in ascending HBM-block order, the order in which the
@@ -578,7 +587,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
                    {s_fu, cl.map_shared_rank(s_fu, 0), mf}};
     cl_copy_segs(sg);
   }
+  PSTAMP_B(4, 1, 5); PSTAMP_B(5, 3, 5);
   cl.barrier_wait();                                   // #3 (wait; acquire): rank 1's prefix
+  PSTAMP_B(4, 1, 6); PSTAMP_B(5, 3, 6);
   if (crank >= 2) {                                    // rank 1's free snapshot and prefix
     CpSeg sg[2] = {{s_hw, cl.map_shared_rank(s_hw, 1), (u32)d.NBW},
                    {s_big, cl.map_shared_rank(s_big, 1), (u32)d.NBW + 1}};
@@ -664,6 +675,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     }
   }
   PSTAMP(2, 18);
+  PSTAMP_B(4, 1, 7); PSTAMP_B(5, 3, 7);
   // per-CTA counters: warp sums (one redux per counter), then shared 64-bit atomics
 #pragma unroll
   for (int i = 0; i < PC_N; ++i) {
@@ -674,6 +686,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // no CTA has to outlive the others (no closing cluster barrier)
   if (threadIdx.x < PLAN_CL) cl.map_shared_rank(&sh, threadIdx.x)->fcnt[crank] = nfed;
   cl.sync();                                           // #4: counts of every CTA known
+  PSTAMP_B(4, 1, 8); PSTAMP_B(5, 3, 8);
   u32 base = 0, total_fed = 0;
   for (u32 c = 0; c < PLAN_CL; ++c) {
     const u32 n = sh.fcnt[c];

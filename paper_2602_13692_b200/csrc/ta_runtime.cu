@@ -174,7 +174,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.ev_pcnt = L.take<u32>(N);
   x.ev_mk = L.take<u64>(EC); x.ev_mk2 = L.take<u64>(EC);
   x.ev_mv = L.take<u32>(EC); x.ev_mv2 = L.take<u32>(EC);
-  x.pst = L.take<ull>(4 * 32);
+  x.pst = L.take<ull>(8 * 32);
   x.gsync = L.take<ull>(2);
   x.dbg = L.take<ull>(DBG_N);
   x.t_rep = L.take<u32>(3 * R);
@@ -687,7 +687,7 @@ ta_status ta_phase_times(ta_ctx* ctx, float* us, int32_t n) {
 ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n) {
   if (ta_status s = check_ctx(ctx)) return s;
   if (!ctx->timing) FAIL(ctx, TA_E_STATE, "context created without TA_F_TIMING");
-  if (!out || n < 0 || n > 128) FAIL(ctx, TA_E_INVAL, "bad stamp buffer");
+  if (!out || n < 0 || n > 256) FAIL(ctx, TA_E_INVAL, "bad stamp buffer");
   CK(ctx, cudaStreamSynchronize(ctx->stream));
   CK(ctx, cudaMemcpy(out, ctx->d.pst, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return TA_OK;

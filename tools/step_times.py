@@ -43,6 +43,7 @@ for k in range(ticks):
           flush=True)
     if "--phases" in sys.argv:
         print("   phases us: " + " ".join(f"{x:.1f}" for x in ph))
-        for kname, v in pool.phase_stamps().items():   # in-kernel stamps, cycles -> us at 1965 MHz
-            print(f"   {kname:8s}: " + " ".join(f"{i}:{c / 1965.0:.1f}" if isinstance(i, int) else f"{i}={c}"
-                                                for i, c in v))
+        st = pool.phase_stamps()                    # in-kernel globaltimer stamps (ns)
+        for kname, v in st.items():
+            print(f"   {kname:9s}: " + " ".join(f"{i}:{c / 1e3:.1f}" if isinstance(i, int) else f"{i}={c}"
+                                                 for i, c in v))
