@@ -40,6 +40,7 @@ enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_
 
 struct PlanSh {                  // leader's scalars, read by the cluster through DSMEM
   u32 stop, X, hfree, nv, vst, ecs_sm, m, tot, fst, fcs_sm, nF;
+  u32 hfree0;                    // free host-tier slots before the evictions (rank 1, part A)
   u32 fcnt[PLAN_CL];
   ull fr, es;                    // free blocks and eviction supply (rank 2, before #0)
 };
@@ -102,10 +103,11 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   u32* s_sfw = sm->p[0];                               // [8192] >= NHW (NH <= 262112)
   u32* s_vp = reinterpret_cast<u32*>(sm->k[0]);        // [8192]
   u32* s_vn = s_vp + 8192;                             // [8192]
-  // [FST_MAX] x 6 in the host-snapshot buffer: the leader fills them during the eviction
-  // phase (nobody reads the leader's copy of that buffer), the others after #3
-  constexpr u32 FST_MAX = 1024;
-  u32* s_fp = sm->p[0];
+  // [FST_MAX] x 6 per-program values of the request loop, in the F-list region of the
+  // request-loop ranks (unused there): the leader writes them into every rank's copy
+  // through DSMEM during its hit accounting, so nobody reads them remotely after #2
+  constexpr u32 FST_MAX = 640;
+  u32* s_fp = s_fl;
   u32* s_fj = s_fp + FST_MAX;
   u32* s_fh = s_fp + 2 * FST_MAX;
   u32* s_fk = s_fp + 3 * FST_MAX;
@@ -142,6 +144,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // its select prefix (the host bitmap is not touched before the eviction loop)
   if (crank == 1) {
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
+    if (threadIdx.x == 0) L->hfree0 = s_big[d.NHW];
     cl_copy(s_sfw, sf, d.NHW);
     // the HBM free bitmap before the evictions; the eviction loop ORs the evicted blocks
     // in (DSMEM), so the allocation prefix of part B needs no global round trip
@@ -229,7 +232,15 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     // short lists are searched many times below: stage them in shared memory
     fcs_sm = nF <= (small_paths(d) ? 8u : 4096u);
     if (!fcs_sm) dbg_hit(d, DBG_F_GLOBAL);
-    if (fcs_sm) cl_copy(s_fc, fc, nF);
+    if (fcs_sm) {                        // the need prefix, into every rank's s_fc (DSMEM stores)
+      for (u32 i = threadIdx.x; i < nF; i += CTA) {
+        const u32 v = fc[i];
+        s_fc[i] = v;
+#pragma unroll
+        for (int k = 1; k < PLAN_CL; ++k) cl.map_shared_rank(s_fc, k)[i] = v;
+      }
+      __syncthreads();
+    }
     fcs = fcs_sm ? s_fc : fc;
     PSTAMP(2, 1);
   }
@@ -383,8 +394,13 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
       if (i < m) {
         if (fst) {
-          s_fp[i] = p; s_fj[i] = h == r ? nhp : d.sb; s_fh[i] = (u32)h; s_fk[i] = ckv; s_fcn[i] = c;
-          s_fu[i] = uidp;
+          const u32 fj = h == r ? nhp : d.sb;
+#pragma unroll
+          for (int k = 1; k < PLAN_CL; ++k) {          // every request-loop rank's copy (DSMEM)
+            u32* b = cl.map_shared_rank(s_fp, k);
+            b[i] = p; b[FST_MAX + i] = fj; b[2 * FST_MAX + i] = (u32)h; b[3 * FST_MAX + i] = ckv;
+            b[4 * FST_MAX + i] = c; b[5 * FST_MAX + i] = uidp;
+          }
         }
         const bool resumed = !(satp && h == r);
         if (resumed && ckv > 0) {
@@ -451,7 +467,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   } else if (X > 0) {
     const u32 nv = L->nv, vst = L->vst, ecs_sm = L->ecs_sm;
     {                                                  // the leader's lists, rank 1's host snapshot
-      const u32 n1 = crank == 1 ? 0u : 1u;
+      const u32 n1 = (crank == 1 || L->hfree0 == 0) ? 0u : 1u;   // no free host slot: all drops
       CpSeg sg[5] = {{s_ec, cl.map_shared_rank(s_ec, 0), ecs_sm ? nv : 0u},
                      {s_vp, cl.map_shared_rank(s_vp, 0), vst ? nv : 0u},
                      {s_vn, cl.map_shared_rank(s_vn, 0), vst ? nv : 0u},
@@ -460,7 +476,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       cl_copy_segs(sg);
       __syncthreads();
     }
-    const u32 hfree = s_big[d.NHW];
+    const u32 hfree = (crank == 1 || L->hfree0) ? s_big[d.NHW] : 0u;
     const u32* ecs = ecs_sm ? s_ec : ec;
     u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
     u32* R1hw = cl.map_shared_rank(s_hw, 1);           // rank 1's free-block snapshot
@@ -517,8 +533,17 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // the leader's victims and D2H order run beside the request loop, and the other ranks
   // stage the leader's lists before they wait for it.
   if (crank == 1) {
-    // ---- 5.4 allocation prefix (after the evictions' frees) over the free snapshot
+    // ---- 5.4 allocation prefix (after the evictions' frees) over the free snapshot, then
+    // the snapshot and its prefix into ranks 2..7 (DSMEM stores, published by #3)
     cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);
+    for (u32 w = threadIdx.x; w <= (u32)d.NBW; w += CTA) {
+      const u32 hw = w < (u32)d.NBW ? s_hw[w] : 0u, pre = s_big[w];
+#pragma unroll
+      for (int k = 2; k < PLAN_CL; ++k) {
+        if (w < (u32)d.NBW) cl.map_shared_rank(s_hw, k)[w] = hw;
+        cl.map_shared_rank(s_big, k)[w] = pre;
+      }
+    }
   }
   PSTAMP_B(4, 1, 4); PSTAMP_B(5, 3, 4);
   cl.barrier_arrive();                                 // #3 (arrive; release)
@@ -528,7 +553,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     // block rarely waits for its eviction (fused movement kernel).
     const u32 ntoh = min(X, sh.hfree);
     EvDesc* evd = d.evd + (size_t)r * d.NB;
-    cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);      // s_hw: blocks evicted to host (bitmap)
+    if (ntoh) cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);   // s_hw: blocks evicted to host (bitmap)
     for (u32 e = threadIdx.x; e < ntoh; e += CTA) {
       const EvDesc x = evt[e];
       const u32 k = s_big[x.src >> 5] + __popc(s_hw[x.src >> 5] & ((1u << (x.src & 31)) - 1));
@@ -576,25 +601,12 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // live bitmap at once.  Only requests that move or write bytes get a descriptor
   // (copies; fills when the engine stand-in is on), compacted in request order.
   const u32 m = L->m, tot = L->tot, fst = L->fst, fcs_sm = L->fcs_sm;
-  if (!lead) {                                         // the leader's lists (complete since #2)
-    const u32 mf = fst ? m : 0u;                       // six arrays of FST_MAX, m used each
-    CpSeg sg[7] = {{s_fc, cl.map_shared_rank(s_fc, 0), fcs_sm ? m : 0u},
-                   {s_fp, cl.map_shared_rank(s_fp, 0), mf},
-                   {s_fj, cl.map_shared_rank(s_fj, 0), mf},
-                   {s_fh, cl.map_shared_rank(s_fh, 0), mf},
-                   {s_fk, cl.map_shared_rank(s_fk, 0), mf},
-                   {s_fcn, cl.map_shared_rank(s_fcn, 0), mf},
-                   {s_fu, cl.map_shared_rank(s_fu, 0), mf}};
-    cl_copy_segs(sg);
-  }
+  // (the leader's lists and rank 1's snapshot were written into this CTA's shared
+  // memory by their owners before #2 / #3)
   PSTAMP_B(4, 1, 5); PSTAMP_B(5, 3, 5);
   cl.barrier_wait();                                   // #3 (wait; acquire): rank 1's prefix
   PSTAMP_B(4, 1, 6); PSTAMP_B(5, 3, 6);
-  if (crank >= 2) {                                    // rank 1's free snapshot and prefix
-    CpSeg sg[2] = {{s_hw, cl.map_shared_rank(s_hw, 1), (u32)d.NBW},
-                   {s_big, cl.map_shared_rank(s_big, 1), (u32)d.NBW + 1}};
-    cl_copy_segs(sg);
-  }
+
   __syncthreads();
   const u32* fcs = fcs_sm ? s_fc : fc;
   const u32* hws = s_hw;
