@@ -146,9 +146,6 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     cta_bitmap_prefix(sf, d.NHW, s_big, s_tmp);
     if (threadIdx.x == 0) L->hfree0 = s_big[d.NHW];
     cl_copy(s_sfw, sf, d.NHW);
-    // the HBM free bitmap before the evictions; the eviction loop ORs the evicted blocks
-    // in (DSMEM), so the allocation prefix of part B needs no global round trip
-    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
   }
   // ================= rank 2, concurrent with F_r: free blocks on r and eviction supply
   if (crank == 2) {
@@ -394,13 +391,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
       if (i < m) {
         if (fst) {
-          const u32 fj = h == r ? nhp : d.sb;
-#pragma unroll
-          for (int k = 1; k < PLAN_CL; ++k) {          // every request-loop rank's copy (DSMEM)
-            u32* b = cl.map_shared_rank(s_fp, k);
-            b[i] = p; b[FST_MAX + i] = fj; b[2 * FST_MAX + i] = (u32)h; b[3 * FST_MAX + i] = ckv;
-            b[4 * FST_MAX + i] = c; b[5 * FST_MAX + i] = uidp;
-          }
+          u32* lf = sm->p[0];                          // leader-local staging, pushed below
+          lf[i] = p; lf[FST_MAX + i] = h == r ? nhp : d.sb; lf[2 * FST_MAX + i] = (u32)h;
+          lf[3 * FST_MAX + i] = ckv; lf[4 * FST_MAX + i] = c; lf[5 * FST_MAX + i] = uidp;
         }
         const bool resumed = !(satp && h == r);
         if (resumed && ckv > 0) {
@@ -451,6 +444,15 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       d.dec_fs[(size_t)r * N + i] = rec;
     }
     if (threadIdx.x == 0) sh.fst = fst;
+    if (fst && m) {                                    // the six staged arrays into every request-loop
+      __syncthreads();                                 // rank's copy (DSMEM stores, published by #2)
+      const u32* lf = sm->p[0];
+      for (u32 x = threadIdx.x; x < 6 * m; x += CTA) {
+        const u32 a6 = x / m, i = x - a6 * m, v = lf[a6 * FST_MAX + i];
+#pragma unroll
+        for (int k = 1; k < PLAN_CL; ++k) cl.map_shared_rank(s_fp, k)[a6 * FST_MAX + i] = v;
+      }
+    }
     if (!verb) {
       l_dec = warp_sum_ull(l_dec); l_pre = warp_sum_ull(l_pre); l_rec = warp_sum_ull(l_rec);
       if (lane_id() == 0) {
@@ -479,7 +481,6 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     const u32 hfree = (crank == 1 || L->hfree0) ? s_big[d.NHW] : 0u;
     const u32* ecs = ecs_sm ? s_ec : ec;
     u32* Lhw = cl.map_shared_rank(s_hw, 0);            // leader's evicted-to-host bitmap
-    u32* R1hw = cl.map_shared_rank(s_hw, 1);           // rank 1's free-block snapshot
     const u32 per = (X + PLAN_CL - 2) / (PLAN_CL - 1); // ranks 1..PLAN_CL-1
     const u32 e_lo = (crank - 1) * per, e_hi = min(X, e_lo + per);
     // e-th evicted block: victim v, its block j = n_hbm - 1 - (e - excl) (tail first);
@@ -507,7 +508,6 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         const u32 idx = ik[k], j = jk[k], p = pk[k];
         u32* ent = d.loc + (size_t)p * d.MAXBP + j;
         atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
-        atomicOr(&R1hw[idx >> 5], 1u << (idx & 31));        // ... and in rank 1's snapshot
         if (e < hfree) {
           if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
           const u32 slot = bitmap_select(s_sfw, s_big, d.NHW, e);
@@ -528,25 +528,16 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   PSTAMP_B(4, 1, 3); PSTAMP_B(5, 3, 3);
   PSTAMP(2, 6);
 
-  // ================= part B.  Rank 1: the allocation prefix, the only input of the
-  // request loop still missing; it is published by a split cluster barrier (#3), so
-  // the leader's victims and D2H order run beside the request loop, and the other ranks
-  // stage the leader's lists before they wait for it.
-  if (crank == 1) {
-    // ---- 5.4 allocation prefix (after the evictions' frees) over the free snapshot, then
-    // the snapshot and its prefix into ranks 2..7 (DSMEM stores, published by #3)
+  // ================= part B.  Every request-loop rank (1..7): a snapshot of the free
+  // bitmap after the evictions (the live bitmap; nobody writes it until #4, the request
+  // loop's allocations are cleared after #4) and its select prefix, in its own shared
+  // memory; meanwhile the leader orders the D2H copies and writes the EVICT records.
+  if (!lead) {
+    cl_copy(s_hw, hf, d.NBW);                          // NBW <= 4095 (NB <= 131040)
+    __syncthreads();
     cta_bitmap_prefix(s_hw, d.NBW, s_big, s_tmp);
-    for (u32 w = threadIdx.x; w <= (u32)d.NBW; w += CTA) {
-      const u32 hw = w < (u32)d.NBW ? s_hw[w] : 0u, pre = s_big[w];
-#pragma unroll
-      for (int k = 2; k < PLAN_CL; ++k) {
-        if (w < (u32)d.NBW) cl.map_shared_rank(s_hw, k)[w] = hw;
-        cl.map_shared_rank(s_big, k)[w] = pre;
-      }
-    }
   }
   PSTAMP_B(4, 1, 4); PSTAMP_B(5, 3, 4);
-  cl.barrier_arrive();                                 // #3 (arrive; release)
   if (lead && X > 0) {
     // D2H copies are issued in ascending HBM-block order, the order in which the
     // allocation hands the freed blocks out again, so a fetch that reuses an evicted
@@ -601,11 +592,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // live bitmap at once.  Only requests that move or write bytes get a descriptor
   // (copies; fills when the engine stand-in is on), compacted in request order.
   const u32 m = L->m, tot = L->tot, fst = L->fst, fcs_sm = L->fcs_sm;
-  // (the leader's lists and rank 1's snapshot were written into this CTA's shared
-  // memory by their owners before #2 / #3)
-  PSTAMP_B(4, 1, 5); PSTAMP_B(5, 3, 5);
-  cl.barrier_wait();                                   // #3 (wait; acquire): rank 1's prefix
-  PSTAMP_B(4, 1, 6); PSTAMP_B(5, 3, 6);
+  // (the leader's lists were written into this CTA's shared memory before #2)
 
   __syncthreads();
   const u32* fcs = fcs_sm ? s_fc : fc;
@@ -678,7 +665,6 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         }
         d.loc[(size_t)p * d.MAXBP + j] = dst;
         d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
-        atomicAnd(&hf[dst >> 5], ~(1u << (dst & 31)));
       }
       u32 round_n;
       const u32 pos = cta_excl_scan(x.kind != MV_NONE ? 1u : 0u, s_tmp, &round_n);
@@ -699,6 +685,14 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   if (threadIdx.x < PLAN_CL) cl.map_shared_rank(&sh, threadIdx.x)->fcnt[crank] = nfed;
   cl.sync();                                           // #4: counts of every CTA known
   PSTAMP_B(4, 1, 8); PSTAMP_B(5, 3, 8);
+  if (!lead && tot) {                                  // allocated = the first tot free blocks of the
+    for (u32 w = (u32)(crank - 1) * CTA + threadIdx.x; w < (u32)d.NBW; w += (PLAN_CL - 1) * CTA) {
+      const u32 pre = s_big[w], fw = s_hw[w];          // snapshot: clear them in the live bitmap
+      if (pre >= tot || fw == 0) continue;
+      const u32 k = tot - pre;                         // the lowest k free bits of this word are taken
+      hf[w] = k >= (u32)__popc(fw) ? 0u : fw & ~((1u << __fns(fw, 0, (int)k + 1)) - 1u);
+    }
+  }
   u32 base = 0, total_fed = 0;
   for (u32 c = 0; c < PLAN_CL; ++c) {
     const u32 n = sh.fcnt[c];
