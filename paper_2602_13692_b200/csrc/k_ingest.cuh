@@ -475,11 +475,10 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   }
 }
 
-// Trace mode: steps 0-2 of the tick.
+#define FP_GRID(N) (((N) + FP_SLOTS - 1) / FP_SLOTS)
+#define FP_BLOCK FP_THREADS
+#define FP_DSMEM FP_SMEM
 __global__ void __launch_bounds__(FP_THREADS) k_tick_front(Dev d) { footprint_cta<0>(d); }
-
-// API mode (the events were applied by k_ev_*) and verbs (verb != 0: the state left by
-// the last tick, at its time T; no ingest, L kept): steps 1-2.
 __global__ void __launch_bounds__(FP_THREADS) k_footprint(Dev d, int verb) {
   if (verb) {
     footprint_cta<2>(d);

@@ -305,9 +305,9 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     k_ev_single<<<eg, 256, 0, s>>>(d);
     k_ev_multi<<<1, CTA, PLAN_DSMEM, s>>>(d);
     k_ev_apply<<<eg, 256, 0, s>>>(d);
-    k_footprint<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d, 0);
+    k_footprint<<<FP_GRID(N), FP_BLOCK, FP_DSMEM, s>>>(d, 0);
   } else {
-    k_tick_front<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d);   // ingest + footprint + load
+    k_tick_front<<<FP_GRID(N), FP_BLOCK, FP_DSMEM, s>>>(d);   // ingest + footprint + load
   }
   rec(x, 1);
   if (x->split_pr) {                       // A/B aid: the two passes as separate kernels
@@ -510,8 +510,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ev_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tick_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_SMEM);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_footprint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_SMEM);
+  if (e == cudaSuccess && FP_DSMEM > 48 * 1024) e = cudaFuncSetAttribute(k_tick_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_DSMEM);
+  if (e == cudaSuccess && FP_DSMEM > 48 * 1024) e = cudaFuncSetAttribute(k_footprint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_DSMEM);
   if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
   if (e != cudaSuccess) {
     fprintf(stderr, "ta_init_pool: %s\n", cudaGetErrorString(e));
@@ -820,7 +820,7 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   cudaStream_t s = ctx->stream;
   const int N = d.N;
   k_verb_reset<<<1, 32, 0, s>>>(d);
-  k_footprint<<<(N + FP_SLOTS - 1) / FP_SLOTS, FP_THREADS, FP_SMEM, s>>>(d, 1);
+  k_footprint<<<FP_GRID(N), FP_BLOCK, FP_DSMEM, s>>>(d, 1);
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
   k_plan<<<d.R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 1);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);

@@ -1,6 +1,6 @@
 """Per-kernel device times of the decision path (developer tool, GPU box).
 
-usage: python tools/tick_phases.py [--config bench_10k] [--start 13] [--ticks 100]
+usage: python tools/tick_phases.py [--config bench_10k] [--start 13] [--ticks 100] [--tile R]
 
 Runs the full ta_sched_step graph with TA_F_TIMING on the decision-identical `mini` KV
 shape (no decision depends on bytes per block), the L2 flushed before every tick, and
@@ -26,10 +26,15 @@ def main():
     name, start, n = arg("--config", "bench_10k"), int(arg("--start", "13")), int(arg("--ticks", "100"))
     cfg = tracegen.get_config(name)
     cfg["kv"] = "mini"
+    tile = int(arg("--tile", "1"))            # R replicas on this GPU over R copies of the trace
+    if tile > 1:
+        cfg["n_replicas"] = tile
+        cfg["trace"]["tile"] = tile
     tr = tracegen.make_trace(cfg)
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    out = {"lib": os.environ.get("TA_LIB", "libta.so"), "config": name, "ticks": f"{start}..{start + n - 1}"}
+    out = {"lib": os.environ.get("TA_LIB", "libta.so"), "config": name, "replicas": tile, "programs": tr.n_slots,
+           "ticks": f"{start}..{start + n - 1}"}
     for mode in ("timing", "plain"):
         pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False,
                     flags=binding.F_TIMING if mode == "timing" else 0)
