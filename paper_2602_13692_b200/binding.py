@@ -383,14 +383,14 @@ class Pool:
         self._chk(lib().ta_phase_times(self.ctx, a, 9), "ta_phase_times")
         return list(a)
 
-    def phase_stamps(self):
+    def phase_stamps(self, absolute: bool = False):
         """Globaltimer stamps (ns) of the planner kernels' phases in the last tick (TA_F_TIMING):
         {kernel: [(phase index, ns since that kernel's first stamp), ...]}; plan_cta1 / plan_cta3
         are cluster ranks 1 and 3 of replica 0's planner cluster."""
         a = (C.c_uint64 * 256)()
         self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 256), "ta_debug_phase_stamps")
         out = {}
-        names = ("pause", "restore", "plan", "close", "plan_cta1", "plan_cta3")
+        names = ("pause", "restore", "plan", "close", "plan_cta1", "plan_cta3", "front_cta0", "front_last")
         first = {}
         for k, name in enumerate(names):
             v = [a[32 * k + i] for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
@@ -398,6 +398,11 @@ class Pool:
         # the planner's cluster ranks share the leader's time origin
         first["plan"] = first["plan_cta1"] = first["plan_cta3"] = min(
             [x for x in (first["plan"], first["plan_cta1"], first["plan_cta3"]) if x] or [0])
+        first["front_cta0"] = first["front_last"] = min(
+            [x for x in (first["front_cta0"], first["front_last"]) if x] or [0])
+        if absolute:                       # one origin for every kernel: the tick's first stamp
+            t0 = min([x for x in first.values() if x] or [0])
+            first = {k: t0 for k in first}
         for k, name in enumerate(names):
             v = [(i, a[32 * k + i]) for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
             out[name] = [(i, c - first[name]) for i, c in v] if v else []

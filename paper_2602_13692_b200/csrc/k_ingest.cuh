@@ -316,6 +316,9 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   const int p0 = blockIdx.x * FP_SLOTS;
   const int p = p0 + lane;
   const bool w0 = warp == 0;
+  if (MODE == 0 && (d.flags & TA_F_TIMING) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x < 32)
+    d.pst[(blockIdx.x == 0 ? 6 : 7) * 32 + threadIdx.x] = 0;
+  if (MODE == 0) { PSTAMP_B(6, 0, 0); PSTAMP_B(7, gridDim.x - 1, 0); }
   const i64 T = MODE == 0 ? d.ctr->tick * d.dt : (MODE == 1 ? d.ctr->now_ms : d.ctr->T);
   if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     d.ctr->T = T;
@@ -353,6 +356,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   // chunks go to the staging buffer at s_off[slot] if they fit, else they are read
   // straight from global memory in step 3
   constexpr int SPW = FP_SLOTS / (FP_THREADS / 32);
+  if (MODE == 0) { PSTAMP_B(6, 0, 1); PSTAMP_B(7, gridDim.x - 1, 1); }
   // ---- 2. rows -> shared memory (each warp its slots), ingest (warp 0)
 #pragma unroll
   for (int k = 0; k < SPW; ++k) {
@@ -366,8 +370,10 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     s_rel[lane] = (MODE != 2 && p < d.N && v.released) ? 1 : 0;
     s_home[lane] = v.home;
   }
+  if (MODE == 0) { PSTAMP_B(6, 0, 2); PSTAMP_B(7, gridDim.x - 1, 2); }
   cp_async_wait_all();
   __syncthreads();
+  if (MODE == 0) { PSTAMP_B(6, 0, 3); PSTAMP_B(7, gridDim.x - 1, 3); }
   // ---- 3. per slot (its warp): counts, or the frees of a released row
 #pragma unroll 1
   for (int k = 0; k < SPW; ++k) {
@@ -400,6 +406,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     }
     u32 a_h = 0, a_s = 0, a_f = 0xFFFFFFFFu;
     const u32 jh = s_jh[sl];
+#pragma unroll 4
     for (u32 c = lane; c < nch; c += 32) {
       const uint4 q = staged ? s_stage[o + c] : grow[c];
       const u32 e[4] = {q.x, q.y, q.z, q.w};
@@ -424,6 +431,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     if (lane == 0) { s_nh[sl] = a_h; s_ns[sl] = a_s; s_first[sl] = a_f; }
   }
   __syncthreads();
+  if (MODE == 0) { PSTAMP_B(6, 0, 4); PSTAMP_B(7, gridDim.x - 1, 4); }
   // ---- 4. per slot: derived values and candidate sets (warp 0)
   if (!w0) return;
   const bool valid = p < d.N;
@@ -473,6 +481,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
       if (MODE != 2 && sum) atomicAdd(&d.Lacc[r], (ull)sum);
     }
   }
+  if (MODE == 0) { PSTAMP_B(6, 0, 5); PSTAMP_B(7, gridDim.x - 1, 5); }
 }
 
 #define FP_GRID(N) (((N) + FP_SLOTS - 1) / FP_SLOTS)

@@ -43,7 +43,7 @@ for k in range(ticks):
           flush=True)
     if "--phases" in sys.argv:
         print("   phases us: " + " ".join(f"{x:.1f}" for x in ph))
-        st = pool.phase_stamps()                    # in-kernel globaltimer stamps (ns)
+        st = pool.phase_stamps(absolute=True)       # in-kernel globaltimer stamps (ns), one origin
         for kname, v in st.items():
             print(f"   {kname:9s}: " + " ".join(f"{i}:{c / 1e3:.1f}" if isinstance(i, int) else f"{i}={c}"
                                                  for i, c in v))
