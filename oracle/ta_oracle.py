@@ -43,7 +43,7 @@ OK, E_INVAL, E_NOMEM, E_DUP_ID, E_UNKNOWN_PROGRAM, E_ILLEGAL_TRANSITION, E_CAPAC
 PAUSE_LAZY, PAUSE_OFFLOAD, PAUSE_DROP = 0, 1, 2
 
 MOVE_D2H, MOVE_P2P, MOVE_H2D, MOVE_D2D, MOVE_DROP = 1, 2, 3, 4, 5
-FILL_NEW, FILL_RECOMPUTE = 1, 2
+FILL_NEW, FILL_RECOMPUTE, FILL_PROMPT = 1, 2, 3
 
 INT64_MAX = (1 << 63) - 1
 
@@ -59,7 +59,8 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-SHARED = -1        # owner_hbm tag of a shared-prefix block: (SHARED, j)
+PROMPT = -1        # owner_hbm tag of a shared-prompt block: (PROMPT, k, j)
+PROMPT_UID = 0xFF0000   # KV content identity of shared prompt k: PROMPT_UID + k
 
 
 def decision(kind, pid=NONE, src=-1, dst=-1, blocks=0, to_host=0, dropped=0,
@@ -80,6 +81,9 @@ STAT_KEYS = (
     # NEXT-4 guard: how far memory pressure had grown when the periodic monitor found it
     # (context growth triggers thrashing mid-execution between checks)
     "overshoot_blocks", "overshoot_max_blocks",
+    # NEXT-3 (reading A51): blocks allocated for shared prompts (a prompt materialized on a
+    # replica where no program held it)
+    "prefix_blocks",
 )
 
 
@@ -153,22 +157,30 @@ class Oracle:
         self.host_free = [bytearray([1]) * self.NH for _ in range(self.R)]
         self.owner_hbm = [[None] * self.NB for _ in range(self.R)]
         self.owner_host = [[None] * self.NH for _ in range(self.R)]
-        # NEXT-3 (reading A49): the agents' shared system prompt, the first sb blocks of
-        # every program, is stored once per replica in the top sb HBM blocks (reserved:
-        # never free, never evicted, moved or compacted); a homed program's first sb
-        # entries point at them.  Load accounting still counts every program's full c
-        # ("the shared prompt across programs implicitly reserves
-        # sufficient memory buffer").
-        spt = int(cfg.get("shared_prefix_tokens", 0))
-        assert spt % self.bt == 0 and (spt == 0 or spt // self.bt < self.NB), "shared prefix: whole blocks"
-        self.sb = spt // self.bt
-        self.shared_base = self.NB - self.sb
-        for r in range(self.R):
-            for j in range(self.sb):
-                self.hbm_free[r][self.shared_base + j] = 0
-                self.owner_hbm[r][self.shared_base + j] = (SHARED, j)
-        if trace is not None and self.sb:
-            assert int(min(trace.p0)) >= spt, "every prompt starts with the shared prefix"
+        # NEXT-3 (reading A51): K shared system prompts (one per agent preset; PAPER.md:230
+        # "agentic system prompts are identical across workflows").  Program p's first
+        # sbk[kp[p]] blocks are its prompt, stored once per replica: a program homed on r
+        # points them at prompt k's blocks on r (pblk[r][k]); pref[r][k] counts those
+        # programs; the prompt is materialized (allocated lowest-free and prefilled) by the
+        # first program that needs it on r, and released -- its blocks freed -- when the
+        # last one leaves (release, move to another replica, failure).  Prompt blocks are
+        # never evicted, moved or compacted.  Load accounting still counts every
+        # program's full c.
+        import tracegen                                   # input parameters only
+        spec = tracegen.prefix_spec(cfg)
+        self.K = len(spec)
+        assert all(t > 0 and t % self.bt == 0 for t, _ in spec), "shared prompts: whole blocks"
+        self.sbk = [t // self.bt for t, _ in spec]
+        self.kp = [-1] * N
+        self.trace_kp = None
+        if trace is not None and self.K:
+            ids = tracegen.prefix_ids(cfg, trace)
+            self.trace_kp = [int(x) if x != 255 else -1 for x in ids]
+            for q in range(N):
+                kq = self.trace_kp[q]
+                assert kq < 0 or int(trace.p0[q]) >= self.sbk[kq] * self.bt, "a prompt starts with its shared prefix"
+        self.pref = [[0] * self.K for _ in range(self.R)]
+        self.pblk = [[None] * self.K for _ in range(self.R)]
         self.cap_max = [(self.lmax * self.NB) >> 16 for _ in range(self.R)]
         self.cap_min = [(self.lmin * self.NB) >> 16 for _ in range(self.R)]
         self.L = [0] * self.R
@@ -185,6 +197,21 @@ class Oracle:
     # ------------------------------------------------------------------ helpers
     def nb_of(self, p: int) -> int:
         return ceil_div(self.c[p], self.bt)
+
+    def sbp(self, p: int) -> int:
+        """Blocks of program p's shared prompt (0 without one)."""
+        k = self.kp[p]
+        return self.sbk[k] if k >= 0 else 0
+
+    def _unref(self, r: int, k: int):
+        """A program using prompt k stopped being homed on r; the last one releases it."""
+        self.pref[r][k] -= 1
+        assert self.pref[r][k] >= 0
+        if self.pref[r][k] == 0:
+            for b in self.pblk[r][k]:
+                self.hbm_free[r][b] = 1
+                self.owner_hbm[r][b] = None
+            self.pblk[r][k] = None
 
     @staticmethod
     def is_hbm(e: int) -> bool:
@@ -224,12 +251,13 @@ class Oracle:
     def _free_all(self, p: int):
         h = self.home[p]
         row = self.loc[p]
+        sb = self.sbp(p)
         for j in range(self.MAXB):
             e = row[j]
             if e == NONE:
                 continue
             assert h >= 0, "KV without a home replica"
-            if j < self.sb:                    # shared prefix: a reference, not an owner
+            if j < sb:                         # shared prompt: a reference, not an owner
                 row[j] = NONE
                 continue
             if e & HOST_BIT:
@@ -240,6 +268,8 @@ class Oracle:
                 self.hbm_free[h][e] = 1
                 self.owner_hbm[h][e] = None
             row[j] = NONE
+        if h >= 0 and self.kp[p] >= 0:         # it no longer uses its prompt on h
+            self._unref(h, self.kp[p])
 
     def _release(self, p: int):
         """STOPPED: placement cleared, every block freed (A26)."""
@@ -250,9 +280,11 @@ class Oracle:
         self.satisfied[p] = 0
         self.stats["stops"] += 1
 
-    def _arrive(self, p: int, k: int, uid: int, p0: int):
-        """Arrivals enter PAUSED, phase R (A12)."""
+    def _arrive(self, p: int, k: int, uid: int, p0: int, prompt: int = -1):
+        """Arrivals enter PAUSED, phase R (A12).  prompt: the shared
+        prompt the program uses (-1: none; A51)."""
         self.uid[p] = uid
+        self.kp[p] = prompt
         self.status[p] = PAUSED
         self.phase[p] = PHASE_R
         self.c[p] = p0
@@ -328,7 +360,7 @@ class Oracle:
         n_arr = (tr.n_initial if k == 0 else 0) + stops
         hi = min(self.N, self.next_arrival + n_arr)
         for p in range(self.next_arrival, hi):
-            self._arrive(p, k, int(tr.uid[p]), int(tr.p0[p]))
+            self._arrive(p, k, int(tr.uid[p]), int(tr.p0[p]), self.trace_kp[p] if self.trace_kp else -1)
         self.next_arrival = hi
 
     # ------------------------------------------------------------------ step 1
@@ -465,17 +497,18 @@ class Oracle:
 
     # ------------------------------------------------------------------ step 5
     def _need(self, p: int, r: int) -> int:
-        """#{sb <= j < nb : loc[j] is not HBM on r} (the shared prefix is on every replica)."""
+        """#{sbp <= j < nb : loc[j] is not HBM on r}: the program's private blocks (its
+        shared prompt, if it must be materialized on r, is added by _materialize)."""
         row = self.loc[p]
         here = self.home[p] == r
-        return sum(1 for j in range(self.sb, self.fp["nb"][p]) if not (here and self.is_hbm(row[j])))
+        return sum(1 for j in range(self.sbp(p), self.fp["nb"][p]) if not (here and self.is_hbm(row[j])))
 
     def _evict_order(self, r: int):
         """Eviction candidates E_r and their order (reading A21):
         group 0 PAUSED in exact reverse of the restore order; group 1 ACTING placed
         elsewhere; group 2 ACTING placed on r; groups 1-2 by (contrib, slot)."""
         nb, n_hbm, contrib = self.fp["nb"], self.fp["n_hbm"], self.contrib
-        E = [p for p in range(self.N) if self.home[p] == r and n_hbm[p] > self.sb
+        E = [p for p in range(self.N) if self.home[p] == r and n_hbm[p] > self.sbp(p)
              and self.status[p] in (PAUSED, ACTING)]
         if self.request_aware:                 # LRU over idle caches, not program-aware (A46)
             return sorted(E, key=lambda p: (self.paused_since[p] * self.dt if self.status[p] == PAUSED
@@ -494,16 +527,25 @@ class Oracle:
         Returns False (and changes nothing) if all_or_nothing and F does not fit."""
         nb, n_hbm = self.fp["nb"], self.fp["n_hbm"]
         need = {p: self._need(p, r) for p in F}
+        # NEXT-3 (A51): a prompt not resident on r is materialized by the first program of
+        # F (slot order) that uses it; its blocks are that program's first requests
+        extra, claimed = {}, set()
+        for p in F:
+            k = self.kp[p]
+            extra[p] = 0
+            if k >= 0 and self.pblk[r][k] is None and k not in claimed:
+                extra[p] = self.sbk[k]
+                claimed.add(k)
         E = self._evict_order(r)
         free_r = sum(self.hbm_free[r])
-        supply = free_r + sum(n_hbm[p] - self.sb for p in E)   # private HBM blocks
+        supply = free_r + sum(n_hbm[p] - self.sbp(p) for p in E)   # private HBM blocks
         # 5.2 stall cut: longest prefix of F with sum(need) <= supply
         S, tot = [], 0
         for p in F:
-            if tot + need[p] > supply:
+            if tot + need[p] + extra[p] > supply:
                 break
             S.append(p)
-            tot += need[p]
+            tot += need[p] + extra[p]
         if all_or_nothing and len(S) < len(F):
             return False
         stalled = F[len(S):]
@@ -515,7 +557,7 @@ class Oracle:
             if X == 0:
                 break
             row = self.loc[p]
-            hbm_js = [j for j in range(self.sb, nb[p]) if self.is_hbm(row[j])]
+            hbm_js = [j for j in range(self.sbp(p), nb[p]) if self.is_hbm(row[j])]
             take = min(X, len(hbm_js))
             to_host = dropped = 0
             for j in sorted(hbm_js, reverse=True)[:take]:
@@ -547,6 +589,8 @@ class Oracle:
         for p in S:
             row = self.loc[p]
             h = self.home[p]
+            k = self.kp[p]
+            sb = self.sbp(p)
             resumed = not (self.satisfied[p] and h == r)
             hit = peer = host = miss = 0
             if resumed:
@@ -554,8 +598,11 @@ class Oracle:
                 for j in range(ceil_div(H, self.bt)):
                     tok = min(self.bt, H - j * self.bt)
                     e = row[j]
-                    if j < self.sb:                    # shared prefix: resident on r
-                        hit += tok
+                    if j < sb:                         # shared prompt: resident on r, or
+                        if extra[p]:                   # prefilled now by this program
+                            miss += tok
+                        else:
+                            hit += tok
                     elif e == NONE:
                         miss += tok
                     elif e & HOST_BIT:
@@ -566,9 +613,23 @@ class Oracle:
                         peer += tok
             c0, c1 = self.c_kv[p], self.c[p]
             hist_blocks = ceil_div(c0, self.bt)
-            for j in range(self.sb):                   # shared prefix (same index on every replica)
-                row[j] = self.shared_base + j
-            for j in range(self.sb, nb[p]):
+            if extra[p]:                               # materialize prompt k on r
+                blocks = []
+                for j in range(sb):
+                    while not self.hbm_free[r][hptr]:
+                        hptr += 1
+                    dst = hptr
+                    self.hbm_free[r][dst] = 0
+                    self.owner_hbm[r][dst] = (PROMPT, k, j)
+                    blocks.append(dst)
+                    self.fills.append((FILL_PROMPT, r, dst, PROMPT_UID + k, j, j * self.bt, (j + 1) * self.bt))
+                    self.stats["fill_tok"] += self.bt
+                    self.stats["prefix_blocks"] += 1
+                    self.stats["fetch_blocks"] += 1
+                self.pblk[r][k] = blocks
+            for j in range(sb):                        # the prompt (same blocks for every user on r)
+                row[j] = self.pblk[r][k][j]
+            for j in range(sb, nb[p]):
                 e = row[j]
                 recompute = False
                 if h == r and self.is_hbm(e):
@@ -607,9 +668,13 @@ class Oracle:
             self.stats["host_tok"] += host
             self.stats["miss_tok"] += miss
             self.stats["new_tok"] += c1 - c0
-            if need[p] > 0 or resumed:
-                fx.append(decision(D_FETCH, p, src=h, dst=r, blocks=need[p],
+            if need[p] + extra[p] > 0 or resumed:
+                fx.append(decision(D_FETCH, p, src=h, dst=r, blocks=need[p] + extra[p],
                                    hit=hit, peer=peer, host=host, miss=miss, new=c1 - c0))
+            if h != r and k >= 0:                      # the program now uses prompt k on r
+                self.pref[r][k] += 1
+                if h >= 0:
+                    deferred.append(("unref", h, k))   # ... and no longer on h (step 7)
             self.home[p] = r
             self.c_kv[p] = c1
             n_hbm[p] = nb[p]
@@ -620,7 +685,7 @@ class Oracle:
             self.pend[p] = 0
             self._ledger_s.append((p, c0, c1, miss))
         for p in stalled:
-            fx.append(decision(D_STALL, p, src=self.home[p], dst=r, blocks=need[p]))
+            fx.append(decision(D_STALL, p, src=self.home[p], dst=r, blocks=need[p] + extra[p]))
             self.stats["stalls"] += 1
         stat_out.extend(ev_out)
         fetch_out.extend(fx)
@@ -644,21 +709,25 @@ class Oracle:
             if kind == "hbm":
                 self.hbm_free[h][i] = 1
                 self.owner_hbm[h][i] = None
-            else:
+            elif kind == "host":
                 self.host_free[h][i] = 1
                 self.owner_host[h][i] = None
+            else:                                      # "unref": a program left prompt i on h
+                self._unref(h, i)
 
     def _compact(self, r: int, out: list):
         """Two-finger compaction (reading A20): move the highest used block to the
-        lowest free block until the fingers cross."""
+        lowest free block until the fingers cross.  Shared-prompt blocks stay put (A51):
+        the upper finger skips them."""
         free = self.hbm_free[r]
-        lo, hi, moves = 0, self.shared_base - 1, 0       # the shared prefix stays put
+        owner = self.owner_hbm[r]
+        lo, hi, moves = 0, self.NB - 1, 0
         while True:
-            while lo < self.shared_base and not free[lo]:
+            while lo < self.NB and not free[lo]:
                 lo += 1
-            while hi >= 0 and free[hi]:
+            while hi >= 0 and (free[hi] or owner[hi][0] == PROMPT):
                 hi -= 1
-            if lo >= self.shared_base or hi < 0 or lo > hi:
+            if lo >= self.NB or hi < 0 or lo > hi:
                 break
             p, j = self.owner_hbm[r][hi]
             self.loc[p][j] = lo
@@ -747,6 +816,16 @@ class Oracle:
         return OK, pauses + restores + evicts + fetches + compacts
 
     # ------------------------------------------------------------------ API mode
+    def event_prompt(self, ev) -> int:
+        """The shared prompt of an ARRIVE event (A51): none without prompts, prompt 0 with
+        one, else t_ms (the prompt index; -2 = invalid)."""
+        if self.K == 0:
+            return -1
+        if self.K == 1:
+            return 0
+        t = int(ev[4])
+        return t if 0 <= t < self.K else -2
+
     def validate_events(self, events) -> int:
         """All-or-nothing validation in order (SURVEY.md §8(c) API table)."""
         status = {}
@@ -763,8 +842,12 @@ class Oracle:
                 c = ev[3] if kind == E_ARRIVE else ctx.get(pid, self.c[pid]) + ev[3]
                 if c > cap and not (kind == E_ARRIVE and st != UNARRIVED):
                     return E_INVAL
-                if kind == E_ARRIVE and st == UNARRIVED and c < self.sb * self.bt:
-                    return E_INVAL                        # the prompt starts with the shared prefix
+                if kind == E_ARRIVE and st == UNARRIVED:
+                    k = self.event_prompt(ev)
+                    if k == -2:
+                        return E_INVAL                    # no such shared prompt (A51)
+                    if k >= 0 and c < self.sbk[k] * self.bt:
+                        return E_INVAL                    # the prompt starts with its shared prefix
                 ctx[pid] = c
             if kind == E_ARRIVE:
                 if st != UNARRIVED:
@@ -795,7 +878,7 @@ class Oracle:
         for ev in events:
             kind, pid, uid, tokens, t_ms = ev
             if kind == E_ARRIVE:
-                self._arrive(pid, k, uid, tokens)
+                self._arrive(pid, k, uid, tokens, self.event_prompt(ev))
             elif kind == E_DECODE:
                 self.c[pid] += tokens
             elif kind == E_TOOL_CALL:
@@ -837,7 +920,7 @@ class Oracle:
         if mode in (PAUSE_OFFLOAD, PAUSE_DROP):
             h = self.home[pid]
             row = self.loc[pid]
-            hbm_js = [j for j in range(self.sb, self.fp["nb"][pid]) if self.is_hbm(row[j])]
+            hbm_js = [j for j in range(self.sbp(pid), self.fp["nb"][pid]) if self.is_hbm(row[j])]
             to_host = dropped = 0
             hslot = 0
             for j in sorted(hbm_js, reverse=True):
@@ -954,7 +1037,7 @@ class Oracle:
         for p in range(self.N):
             if self.home[p] != r:
                 continue
-            lost = sum(1 for j, e in enumerate(self.loc[p]) if e != NONE and j >= self.sb)
+            lost = sum(1 for j, e in enumerate(self.loc[p]) if e != NONE and j >= self.sbp(p))
             self._free_all(p)
             self.home[p] = -1
             if lost:
@@ -969,9 +1052,13 @@ class Oracle:
         """I1-I10; I6 (content) and I8 (no-thrash) are checked by tests."""
         used_h = [[None] * self.NB for _ in range(self.R)]
         used_s = [[None] * self.NH for _ in range(self.R)]
+        users = [[0] * self.K for _ in range(self.R)]
         for p in range(self.N):
             row = self.loc[p]
             nb = self.nb_of(p) if self.status[p] in (PAUSED, REASONING, ACTING) else 0
+            sb = self.sbp(p)
+            if self.home[p] >= 0 and self.kp[p] >= 0:
+                users[self.home[p]][self.kp[p]] += 1
             first_non_hbm = None
             n_hbm = 0
             for j in range(self.MAXB):
@@ -983,8 +1070,9 @@ class Oracle:
                 assert j < nb, f"I2: block beyond nb for p={p}"
                 h = self.home[p]
                 assert h >= 0, f"I5: KV without home p={p}"
-                if j < self.sb:                            # NEXT-3: shared prefix reference
-                    assert e == self.shared_base + j, f"shared prefix entry p={p} j={j}"
+                if j < sb:                                 # NEXT-3: shared prompt reference
+                    blk = self.pblk[h][self.kp[p]]
+                    assert blk is not None and e == blk[j], f"shared prompt entry p={p} j={j}"
                     n_hbm += 1
                     continue
                 if e & HOST_BIT:
@@ -1001,17 +1089,20 @@ class Oracle:
                     n_hbm += 1
             if nb:
                 assert (nb if first_non_hbm is None else first_non_hbm) == n_hbm, f"I10 p={p}"
-                if self.sb and self.home[p] >= 0:
-                    assert n_hbm >= self.sb, f"homed program without its shared prefix p={p}"
+                if sb and self.home[p] >= 0:
+                    assert n_hbm >= sb, f"homed program without its shared prompt p={p}"
             st = self.status[p]
             assert (self.placement[p] >= 0) == (st in (REASONING, ACTING)), f"I5 p={p}"
             if st in (UNARRIVED, STOPPED):
                 assert self.home[p] == -1 and n_hbm == 0
         for r in range(self.R):
-            for j in range(self.sb):
-                b = self.shared_base + j
-                assert not self.hbm_free[r][b] and self.owner_hbm[r][b] == (SHARED, j), "shared block"
-                used_h[r][b] = (SHARED, j)
+            for k in range(self.K):                    # A51: refcounts and prompt blocks
+                assert self.pref[r][k] == users[r][k], f"prompt refcount r={r} k={k}"
+                assert (self.pblk[r][k] is not None) == (users[r][k] > 0), f"prompt residency r={r} k={k}"
+                for j, b in enumerate(self.pblk[r][k] or ()):
+                    assert not self.hbm_free[r][b] and self.owner_hbm[r][b] == (PROMPT, k, j), "prompt block"
+                    assert used_h[r][b] is None
+                    used_h[r][b] = (PROMPT, k, j)
             for b in range(self.NB):
                 assert (used_h[r][b] is None) == bool(self.hbm_free[r][b]), "I1/I2 hbm free-set"
             for s in range(self.NH):

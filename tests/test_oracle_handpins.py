@@ -56,17 +56,23 @@ def test_two_finger_compaction_adjacent_last_pair_by_hand():
     assert _free(o, 0) == [4, 5, 6, 7]
 
 
-def test_two_finger_compaction_spares_shared_prefix_and_runs_in_the_tick():
-    """Same used set with a 2-block shared prefix (NEXT-3, reading A49): the reserved
-    blocks [10, 12) stay put, so compaction runs over [0, 10): used {0, 2, 3, 7, 9}
-    -> 9 -> 1, 7 -> 4, then lowest free 5 > highest used 3: 2 moves.  Through
-    sched_step with compact_every = 1, the COMPACT record is the last decision."""
+def test_two_finger_compaction_spares_shared_prompt_and_runs_in_the_tick():
+    """A shared prompt (reading A51) of 2 blocks sits at blocks 4, 5 (used by p0 and p1);
+    private blocks: p0 {0, 2, 3}, p1 {7, 9}; free {1, 6, 8, 10, 11}.  The upper finger
+    skips the prompt's blocks: 9 -> 1, 7 -> 6, then the lowest free block (7) is above
+    the highest movable used block (3): 2 moves.  Through sched_step with compact_every
+    = 1, the COMPACT record is the last decision."""
     cfg = base_cfg(hbm_blocks=12, max_ctx=16, compact_every=1, shared_prefix_tokens=2)
     o = oracle.Oracle(cfg, flat_trace(2, p0=2, d_ms=10 ** 9))
-    # p0: prefix (10, 11) + private 0, 2, 3;  p1: prefix + private 7, 9
+    o.kp[0] = o.kp[1] = 0
+    o.pblk[0][0] = [4, 5]
+    o.pref[0][0] = 2
+    for j, b in enumerate((4, 5)):
+        o.hbm_free[0][b] = 0
+        o.owner_hbm[0][b] = (oracle.ta_oracle.PROMPT, 0, j)
     for p, priv in ((0, (0, 2, 3)), (1, (7, 9))):
         set_program(o, p, oracle.PAUSED, oracle.PHASE_R, 2 + len(priv), home=0)
-        o.loc[p][0], o.loc[p][1] = 10, 11
+        o.loc[p][0], o.loc[p][1] = 4, 5
         for j, b in enumerate(priv, start=2):
             o.loc[p][j] = b
             o.hbm_free[0][b] = 0
@@ -78,10 +84,11 @@ def test_two_finger_compaction_spares_shared_prefix_and_runs_in_the_tick():
     st, dec = o.sched_step()
     assert st == oracle.OK
     assert dec[-1] == decision(oracle.D_COMPACT, oracle.NONE, src=0, dst=0, blocks=2)
-    assert list(o.loc[1][:4]) == [10, 11, 4, 1]            # j2: 7 -> 4, j3: 9 -> 1
+    assert list(o.loc[1][:4]) == [4, 5, 6, 1]             # j2: 7 -> 6, j3: 9 -> 1
+    assert list(o.loc[0][:5]) == [4, 5, 0, 2, 3]
     assert [m for m in o.moves if m[0] == MOVE_D2D] == [(MOVE_D2D, 0, 9, 0, 1, 1, 3),
-                                                            (MOVE_D2D, 0, 7, 0, 4, 1, 2)]
-    assert _free(o, 0) == [5, 6, 7, 8, 9]
+                                                        (MOVE_D2D, 0, 7, 0, 6, 1, 2)]
+    assert _free(o, 0) == [7, 8, 9, 10, 11]
     o.check_invariants()
 
 

@@ -15,8 +15,8 @@ SRC = open(oracle.ta_oracle.__file__).read()
 
 MUTANTS = {
     "compaction stops one pair early": (
-        "if lo >= self.shared_base or hi < 0 or lo > hi:",
-        "if lo >= self.shared_base or hi < 0 or lo + 1 >= hi:"),
+        "if lo >= self.NB or hi < 0 or lo > hi:",
+        "if lo >= self.NB or hi < 0 or lo + 1 >= hi:"),
     "compaction moves lowest used to highest free": (
         "            p, j = self.owner_hbm[r][hi]\n            self.loc[p][j] = lo",
         "            lo, hi = hi, lo\n            p, j = self.owner_hbm[r][hi]\n            self.loc[p][j] = lo"),

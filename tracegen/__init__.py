@@ -11,4 +11,4 @@ labelled synthetic: the paper only gives qualitative tool-latency shapes,
 PAPER.md:775-808, 433, 445).
 """
 from .presets import PRESETS, Trace, gen_trace, tile_trace  # noqa: F401
-from .configs import CONFIGS, KV_SHAPES, get_config, make_trace  # noqa: F401
+from .configs import CONFIGS, KV_SHAPES, get_config, make_trace, prefix_ids, prefix_spec  # noqa: F401

@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import copy
 
+import numpy as np
+
 from .presets import gen_trace, tile_trace
 
 # KV shapes (2-byte elements).  toy: BASELINE.json configs[0]; q32: Qwen3-32B GQA
@@ -67,6 +69,31 @@ def ttl_pin_table(ttl_units: int) -> list:
     for ttl_units decay units after its tool call, then not at all.  A parameter table
     (Q32, 64 entries), like the decay base x; the policy arithmetic stays on each side."""
     return [(1 << 32) if k < ttl_units else 0 for k in range(64)]
+
+
+def prefix_spec(cfg: dict):
+    """The shared system prompts of a run (NEXT-3, reading A51): a list of K token
+    counts and, per prompt, the agent preset whose programs use it.  `shared_prefixes`
+    = [(tokens, preset), ...]; the single-prompt form `shared_prefix_tokens` = T means one
+    prompt used by every program (preset None).  Parameters only."""
+    if cfg.get("shared_prefixes"):
+        return [(int(t), p) for t, p in cfg["shared_prefixes"]]
+    t = int(cfg.get("shared_prefix_tokens", 0) or 0)
+    return [(t, None)] if t else []
+
+
+def prefix_ids(cfg: dict, trace) -> np.ndarray:
+    """Per trace slot, the index of the shared prompt its program uses (255: none): the
+    prompt listed for its preset, or prompt 0 for everyone with the single-prompt form.
+    Input data for both sides (no method arithmetic)."""
+    spec = prefix_spec(cfg)
+    out = np.full(trace.n_slots, 255, np.uint8)
+    for k, (_, preset) in enumerate(spec):
+        if preset is None:
+            out[:] = k
+        else:
+            out[np.array([pr == preset for pr in trace.preset], bool)] = k
+    return out
 
 
 def get_config(name: str, **override) -> dict:
