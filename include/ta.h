@@ -42,8 +42,11 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 2
+#define TA_ABI_VERSION 3
 #define TA_MAX_REPLICAS 32
+#define TA_MAX_PREFIXES 8          /* shared system prompts (NEXT-3) */
+#define TA_PROMPT_UID 0xFF0000u    /* KV content identity of prompt k: TA_PROMPT_UID + k */
+#define TA_OWNER_PROMPT 0xF8000000u /* owner_hbm of prompt k's block j: TA_OWNER_PROMPT | k << 20 | j */
 #define TA_LOC_NONE 0xFFFFFFFFu
 #define TA_LOC_HOST 0x80000000u
 
@@ -119,17 +122,27 @@ typedef struct {
   uint32_t flags;              /* TA_F_* */
   int32_t prefill_chunk_tokens; /* STP ledger (NEXT-1): chunked-prefill tokens per engine step (>= 1) */
   int32_t prefill_chunk_ms;    /* STP ledger: duration of one chunk step in ms (>= 0) */
-  /* NEXT-3 (reading A49; "agentic system prompts are identical across
-   * workflows"): the first shared_prefix_tokens tokens of every program are
-   * the same system prompt, stored ONCE per replica in its top sb = shared_prefix_tokens
-   * / block_tokens HBM blocks [NB - sb, NB), which are never free, evicted, copied or
-   * compacted (content: uid 0 of the closed form).  A homed program's entries j < sb
-   * point at them; need, eviction supply and allocation cover j >= sb only; resumed
-   * programs count the prefix tokens as hit.  The load (Eq. 7) still counts every
-   * program's full context.  Multiple of block_tokens, < NB * block_tokens; every
-   * prompt (trace p0, ARRIVE tokens) must be at least this long (else TA_E_INVAL).
-   * 0 = off (the former reserved field). */
+  /* NEXT-3, single-prompt form: one shared system prompt of this many tokens used by
+   * every program (= n_prefixes 1, prefix_tokens[0]); 0 = off.  See n_prefixes. */
   int32_t shared_prefix_tokens;
+  /* NEXT-3 (reading A51; "agentic system prompts are identical across
+   * workflows"): K = n_prefixes shared system prompts (one per agent
+   * preset), prompt k = the first prefix_tokens[k] tokens of every program that uses it
+   * (multiples of block_tokens, below hbm_blocks blocks).  A program's prompt comes from
+   * the trace (ta_trace_view.prefix_id) or its ARRIVE event (t_ms = prompt index when
+   * K > 1; prompt 0 when K == 1).  Prompt k is stored once per replica: the first
+   * program (F_r slot order) that needs it on replica r materializes it -- its first
+   * requests get the lowest free blocks, prefilled (content: uid TA_PROMPT_UID + k) --
+   * every program homed on r points its first entries at those blocks, a per-replica
+   * refcount counts them, and the last one to leave (release, fetch to another replica,
+   * replica failure) frees them (at step 0 for releases, step 7 otherwise).  Prompt
+   * blocks are never evicted, copied or compacted; need, eviction supply and eviction
+   * cover a program's private blocks only; a resumed program counts its prompt tokens
+   * as hit, or as miss when it materializes the prompt.  The load (Eq. 7) still counts
+   * full contexts.  Every prompt (trace p0, ARRIVE tokens) must cover its shared prefix
+   * (else TA_E_INVAL).  0 = use shared_prefix_tokens. */
+  int32_t n_prefixes;
+  int32_t prefix_tokens[TA_MAX_PREFIXES];
 } ta_config;
 
 typedef struct {
@@ -186,6 +199,9 @@ typedef struct {               /* cumulative counters (order fixed; see DESIGN.m
    * maximum.  Shrinking delta_t_ms to one decode step (1000 / decode rate) bounds it by
    * one step's growth. */
   uint64_t overshoot_blocks, overshoot_max_blocks;
+  /* NEXT-3 (reading A51): blocks allocated for shared prompts (a prompt materialized on a
+   * replica where no program held it). */
+  uint64_t prefix_blocks;
 } ta_stats_t;
 
 typedef struct {               /* trace-mode program scripts (tracegen layout; host pointers) */
@@ -197,6 +213,8 @@ typedef struct {               /* trace-mode program scripts (tracegen layout; h
   const uint32_t* g;           /* tokens generated per turn */
   const uint32_t* d_ms;        /* tool latency after the turn */
   const uint32_t* o;           /* tool-result tokens after the turn */
+  const uint8_t* prefix_id;    /* [n_slots] shared prompt of each slot (< n_prefixes, 255 = none);
+                                  NULL: prompt 0 when there is one, else none */
 } ta_trace_view;
 
 typedef struct {               /* host mirror of the device state (parity tests); NULL = skip */
@@ -212,6 +230,9 @@ typedef struct {               /* host mirror of the device state (parity tests)
   uint64_t *L;                /* [R] */
   uint32_t *nb, *n_hbm, *n_host, *prefix_hbm, *contrib;   /* [N] step-1/2 values of the last tick (download only) */
   int64_t *scalars;           /* [4]: tick, next_arrival, last_T, reserved */
+  uint8_t *prefix_id;         /* [N] shared prompt of each program (255 = none) */
+  uint32_t *prefix_ref;       /* [R * K] programs homed on r using prompt k */
+  uint32_t *prefix_blk;       /* [R * K * max prompt blocks] blocks of prompt k on r (valid if ref > 0) */
 } ta_state_view;
 
 /* Bytes of device / page-locked host workspace a context needs for cfg. */

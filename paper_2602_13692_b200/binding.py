@@ -44,7 +44,8 @@ class Config(C.Structure):
                 ("lambda_max_q16", C.c_uint32), ("lambda_min_q16", C.c_uint32),
                 ("decay_q32", C.c_uint64 * 64), ("decode_tok_per_s", C.c_int32),
                 ("compact_every", C.c_int32), ("flags", C.c_uint32), ("prefill_chunk_tokens", C.c_int32),
-                ("prefill_chunk_ms", C.c_int32), ("shared_prefix_tokens", C.c_int32)]
+                ("prefill_chunk_ms", C.c_int32), ("shared_prefix_tokens", C.c_int32),
+                ("n_prefixes", C.c_int32), ("prefix_tokens", C.c_int32 * 8)]
 
 
 class Buffers(C.Structure):
@@ -75,7 +76,8 @@ STAT_KEYS = ("ticks", "arrivals", "stops", "pauses", "restores", "oversized_skip
 
 LEDGER_KEYS = ("cost_decode", "cost_prefill", "cost_recompute", "cost_unused", "cost_caching",
                "unused_bound_checks", "unused_bound_violations",
-               "overshoot_blocks", "overshoot_max_blocks")       # + the NEXT-4 guard counters
+               "overshoot_blocks", "overshoot_max_blocks",       # + the NEXT-4 guard counters
+               "prefix_blocks")                                  # + NEXT-3 prompt blocks (A51)
 
 
 class Stats(C.Structure):
@@ -92,7 +94,8 @@ class TickInfo(C.Structure):
 
 class TraceView(C.Structure):
     _fields_ = [("n_slots", C.c_int32), ("n_initial", C.c_int32)] + [
-        (k, C.POINTER(C.c_uint32)) for k in ("uid", "p0", "turn_off", "g", "d_ms", "o")]
+        (k, C.POINTER(C.c_uint32)) for k in ("uid", "p0", "turn_off", "g", "d_ms", "o")] + [
+        ("prefix_id", C.POINTER(C.c_uint8))]
 
 
 _VIEW_FIELDS = [
@@ -104,7 +107,8 @@ _VIEW_FIELDS = [
     ("loc", C.c_uint32), ("hbm_free", C.c_uint32), ("host_free", C.c_uint32),
     ("owner_hbm", C.c_uint32), ("owner_host", C.c_uint32), ("L", C.c_uint64),
     ("nb", C.c_uint32), ("n_hbm", C.c_uint32), ("n_host", C.c_uint32), ("prefix_hbm", C.c_uint32),
-    ("contrib", C.c_uint32), ("scalars", C.c_int64)]
+    ("contrib", C.c_uint32), ("scalars", C.c_int64),
+    ("prefix_id", C.c_uint8), ("prefix_ref", C.c_uint32), ("prefix_blk", C.c_uint32)]
 
 
 class StateView(C.Structure):
@@ -206,7 +210,12 @@ def make_config(cfg: dict, n_programs: int, max_turns: int, trace_mode: bool = T
     c.compact_every = cfg.get("compact_every", 0)
     c.prefill_chunk_tokens = cfg.get("prefill_chunk_tokens", 2048)   # STP ledger (NEXT-1)
     c.prefill_chunk_ms = cfg.get("prefill_chunk_ms", 100)
-    c.shared_prefix_tokens = cfg.get("shared_prefix_tokens", 0)        # NEXT-3
+    from tracegen import prefix_spec  # parameters only
+    spec = prefix_spec(cfg)                                             # NEXT-3 prompts (A51)
+    c.shared_prefix_tokens = 0
+    c.n_prefixes = len(spec)
+    for k, (t, _) in enumerate(spec):
+        c.prefix_tokens[k] = t
     # TMA bulk copies are the default engine (measured faster or equal on every path);
     # pass flags=F_NO_BULK_DEFAULT to keep the 128-bit load/store engine
     if not flags & F_NO_BULK_DEFAULT:
@@ -245,6 +254,8 @@ class Pool:
         self.N = n_programs
         self.R = self.c.n_replicas
         self.MAXB = self.c.max_blocks_per_program
+        self.K = self.c.n_prefixes                      # NEXT-3 shared prompts
+        self.SBM = max([1] + [self.c.prefix_tokens[k] // self.c.block_tokens for k in range(self.K)])
         self.NB, self.NH = self.c.hbm_blocks, self.c.host_blocks
         self.first, self.here = self.c.first_replica, self.c.replicas_here
         self.dev_ws = torch.empty(dev_b.value, dtype=torch.uint8, device=self.device)
@@ -312,6 +323,9 @@ class Pool:
         v.n_initial = tr.n_initial
         for name, a in zip(("uid", "p0", "turn_off", "g", "d_ms", "o"), self._trace_arrays):
             setattr(v, name, _u32p(a))
+        from tracegen import prefix_ids  # input data: each slot's shared prompt (NEXT-3)
+        self._trace_kp = np.ascontiguousarray(prefix_ids(self.cfg, tr), dtype=np.uint8)
+        v.prefix_id = self._trace_kp.ctypes.data_as(C.POINTER(C.c_uint8))
         self._chk(lib().ta_load_trace(self.ctx, C.byref(v)), "ta_load_trace")
 
     def step(self, now_ms: int = -1, events=None, decisions: bool = True, raise_on_error=True):
@@ -428,7 +442,8 @@ class Pool:
                       phase=N, satisfied=N, placement=N, home=N, acting_since=N, tool_return=N,
                       loc=N * MAXB, hbm_free=R * NBW, host_free=max(1, R * NHW), owner_hbm=R * NB,
                       owner_host=max(1, R * NH), L=R, nb=N, n_hbm=N, n_host=N, prefix_hbm=N, contrib=N,
-                      scalars=4)
+                      scalars=4, prefix_id=N, prefix_ref=R * max(1, self.K),
+                      prefix_blk=R * max(1, self.K) * self.SBM)
         npt = {C.c_uint32: np.uint32, C.c_uint8: np.uint8, C.c_int8: np.int8, C.c_int64: np.int64,
                C.c_uint64: np.uint64}
         return {n: np.zeros(shapes[n], dtype=npt[t]) for n, t in _VIEW_FIELDS if fields is None or n in fields}

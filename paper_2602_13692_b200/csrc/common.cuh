@@ -21,7 +21,8 @@ typedef unsigned long long ull;
 
 #define LOC_NONE 0xFFFFFFFFu
 #define LOC_HOST 0x80000000u
-#define OWNER_SHARED 0xFFFFFFFFu         // owner_hbm of a reserved shared-prefix block (NEXT-3)
+#define OWNER_PROMPT TA_OWNER_PROMPT      // owner_hbm of a shared-prompt block: | k << 20 | j (NEXT-3)
+#define KP_NONE 0xFFu                     // prefix_id of a program without a shared prompt
 #define FULL_MASK 0xFFFFFFFFu
 #define CTA 1024          // threads of the single-CTA planner kernels
 #define NWARP (CTA / 32)
@@ -33,7 +34,7 @@ enum StatIdx {
   ST_NEW_TOK, ST_FILL_TOK, ST_IMB_MAX, ST_IMB_LAST,
   ST_BASE_N,                                   // counters before block_bytes in ta_stats_t
   ST_COST_DECODE = ST_BASE_N, ST_COST_PREFILL, ST_COST_RECOMPUTE, ST_COST_UNUSED, ST_COST_CACHING,
-  ST_UNUSED_CHECKS, ST_UNUSED_VIOL, ST_OVERSHOOT, ST_OVERSHOOT_MAX, ST_N
+  ST_UNUSED_CHECKS, ST_UNUSED_VIOL, ST_OVERSHOOT, ST_OVERSHOOT_MAX, ST_PREFIX_BLOCKS, ST_N
 };
 
 // per-request descriptor kinds (step 5.5): copy from a peer's HBM, copy from a host
@@ -79,7 +80,9 @@ struct Dev {
   u32 flags;
   int compact_every;
   int chunk_q, chunk_ms;           // STP ledger: prefill chunk tokens / ms per chunk
-  u32 sb, sbase;                   // NEXT-3: shared-prefix blocks, first reserved block (NB - sb)
+  int K;                           // NEXT-3 (A51): shared prompts
+  u32 sbk[TA_MAX_PREFIXES];        // blocks of each prompt
+  u32 SBM;                         // max over sbk (stride of pblk)
   i64 seg_bytes, block_bytes;
   int first_local, n_local;
   int api_mode;
@@ -101,6 +104,12 @@ struct Dev {
                                    //     0 NONE, 1 HBM, 2 host tier (footprint pass; hit accounting)
   u8* released;                    // released during this tick's ingest
   u8* sat_new;                     // 1 + replica that satisfied the program this tick
+  u8* kp;                          // [N] shared prompt of each program (KP_NONE: none)
+  u8* t_kp;                        // [N] trace mode: prompt of each slot's program
+  u32* pref;                       // [R][K] programs homed on r using prompt k
+  u32* pblk;                       // [R][K][SBM] blocks of prompt k on r (valid while pref > 0)
+  u32* pfix;                       // [R][NBW] prompt blocks (bit set): never evicted, moved or compacted
+  u32* f_x;                        // [R][N] F_r entry: prompt blocks it materializes | prompt << 16
   u32 *pend, *busy;                // [N] synthetic engine (A48): tokens waiting for prefill;
                                    //     ms the last materialize spent (re)prefilling
   u8* evs;                         // [3N] API-mode validation scratch (kept zero)
@@ -260,6 +269,17 @@ __device__ __forceinline__ ull gtimer() {
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u32 ceil_div_u32(u32 a, u32 b) { return (a + b - 1) / b; }
+// blocks of a program's shared prompt (0 without one)
+__device__ __forceinline__ u32 sb_of(const Dev& d, u8 k) { return k == KP_NONE ? 0u : d.sbk[k]; }
+// Free the blocks of prompt k on replica r (its last user left; A51).
+__device__ __forceinline__ void prompt_free(const Dev& d, int r, u32 k, u32 lane, u32 nl) {
+  const u32* blk = d.pblk + ((size_t)r * d.K + k) * d.SBM;
+  for (u32 j = lane; j < d.sbk[k]; j += nl) {
+    const u32 b = blk[j];
+    atomicAnd(&d.pfix[(size_t)r * d.NBW + (b >> 5)], ~(1u << (b & 31)));
+    atomicOr(&d.hbm_free[(size_t)r * d.NBW + (b >> 5)], 1u << (b & 31));
+  }
+}
 __device__ __forceinline__ bool is_hbm(u32 e) { return e != LOC_NONE && !(e & LOC_HOST); }
 __device__ __forceinline__ bool is_host(u32 e) { return e != LOC_NONE && (e & LOC_HOST); }
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }

@@ -446,9 +446,9 @@ __global__ void __launch_bounds__(256) k_verify(Dev d, int tier) {
     if (fw[b >> 5] & (1u << (b & 31))) continue;      // free
     u32 o = tier ? d.owner_host[(size_t)r * d.NH + b] : d.owner_hbm[(size_t)r * d.NB + b];
     u32 j, t0, t1, uid;
-    if (!tier && o == OWNER_SHARED) {                   // shared prefix block: uid 0, full
-      j = b - d.sbase;
-      t0 = j * (u32)d.bt; t1 = t0 + (u32)d.bt; uid = 0;
+    if (!tier && o >= OWNER_PROMPT) {                    // shared prompt k's block j: full
+      j = o & 0xFFFFFu;
+      t0 = j * (u32)d.bt; t1 = t0 + (u32)d.bt; uid = TA_PROMPT_UID + ((o >> 20) & 0x7Fu);
     } else {
       const u32 p = o / (u32)d.MAXB;
       j = o % (u32)d.MAXB;

@@ -26,6 +26,14 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int verb, int first_
   for (int p = t; p < d.N; p += stride) {
     u8 s = d.sat_new[p];
     if (s) {
+      const int r = s - 1, h = d.home[p];
+      const u8 k = d.kp[p];
+      if (h != r && k != KP_NONE) {      // NEXT-3 (A51): its prompt entries now point at r's copy;
+        const u32* blk = d.pblk + ((size_t)r * d.K + k) * d.SBM;   // h's copy loses a user, and
+        for (u32 j = 0; j < d.sbk[k]; ++j) d.loc[(size_t)p * d.MAXBP + j] = blk[j];   // the last
+        if (h >= 0 && atomicSub(&d.pref[(size_t)h * d.K + k], 1u) == 1u)  // one frees its blocks
+          prompt_free(d, h, k, 0, 1);
+      }
       d.satisfied[p] = 1;
       d.home[p] = (i8)(s - 1);
       d.c_kv[p] = d.c[p];
@@ -50,53 +58,39 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int verb, int first_
   }
 }
 
-// Two-finger compaction (reading A20), one CTA per replica: with U used blocks, the
-// m-th lowest free block below U receives the m-th highest used block (all moves
-// of the sequential two-finger loop, computed at once by rank/select).
+// Two-finger compaction (reading A20), one CTA per replica, over the movable blocks
+// (used, not a shared-prompt block: A51): the m-th lowest free block receives the m-th
+// highest movable block while the former lies below the latter -- all moves of the
+// sequential two-finger loop, computed at once by rank/select (the fingers only pass
+// blocks they have not touched, so the pairs are those of the initial sets).
 __device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32* s_big, u32* s_tmp) {
+  __shared__ u32 s_K;
   u32* fw = d.hbm_free + (size_t)r * d.NBW;
+  const u32* fx = d.pfix + (size_t)r * d.NBW;
   const int nw = d.NBW;
   u32* s_free = s_big;                  // [nw + 1]
   u32* s_used = s_big + nw + 1;         // [nw + 1]
-  cta_bitmap_prefix(fw, nw, s_free, s_tmp);
-  // blocks [0, NBc) take part; the shared-prefix blocks above NBc stay put (NEXT-3)
-  const u32 NBc = d.sbase;
-  const u32 U = NBc - s_free[nw];
-  // bits of word w that are blocks below NBc
-  auto valid_of = [&](int w) -> u32 {
-    const i64 n = (i64)NBc - (i64)w * 32;
+  u32* s_mw = s_big + 2 * (nw + 1);     // [nw] movable words
+  auto valid_of = [&](int w) -> u32 {   // bits of word w that are blocks
+    const i64 n = (i64)d.NB - (i64)w * 32;
     return n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
   };
-  // used bitmap prefix (bits >= NBc are neither free nor used here)
-  {
-    int chunk = (nw + CTA - 1) / CTA;
-    int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
-    auto used_word = [&](int w) { return ~fw[w] & valid_of(w); };
-    u32 s = 0;
-    for (int w = lo; w < hi; ++w) s += __popc(used_word(w));
-    u32 total;
-    u32 run = cta_excl_scan(s, s_tmp, &total);
-    for (int w = lo; w < hi; ++w) { s_used[w] = run; run += __popc(used_word(w)); }
-    if (threadIdx.x == 0) s_used[nw] = total;
-    __syncthreads();
-  }
-  // K = free blocks below U
-  u32 K = 0;
-  if (U > 0) {
-    u32 wU = U >> 5, bU = U & 31;
-    K = s_free[wU] + (bU ? __popc(fw[wU] & ((1u << bU) - 1)) : 0);
-  }
+  for (int w = threadIdx.x; w < nw; w += CTA) s_mw[w] = ~fw[w] & ~fx[w] & valid_of(w);
+  if (threadIdx.x == 0) s_K = 0xFFFFFFFFu;
+  __syncthreads();
+  cta_bitmap_prefix(fw, nw, s_free, s_tmp);
+  cta_bitmap_prefix(s_mw, nw, s_used, s_tmp);
+  const u32 F = s_free[nw], U = s_used[nw], lim = min(F, U);
+  for (u32 m = threadIdx.x; m < lim; m += CTA)          // first m whose pair does not cross
+    if (bitmap_select(fw, s_free, nw, m) > bitmap_select(s_mw, s_used, nw, U - 1 - m)) atomicMin(&s_K, m);
+  __syncthreads();
+  const u32 K = min(s_K, lim);
   CpDesc* cp = d.cpd + (size_t)r * (d.NB / 2 + 1);
   for (u32 m = threadIdx.x; m < K; m += CTA) {
-    u32 dst = bitmap_select(fw, s_free, nw, m);
-    // (U-1-m)-th used block in ascending order = m-th highest used
-    u32 q = U - 1 - m;
-    int lo = 0, hi = nw;
-    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_used[mid] <= q) lo = mid; else hi = mid; }
-    u32 uw = ~fw[lo] & valid_of(lo);
-    u32 src = (u32)lo * 32u + __fns(uw, 0, (int)(q - s_used[lo]) + 1);
-    u32 o = d.owner_hbm[(size_t)r * d.NB + src];
-    u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
+    const u32 dst = bitmap_select(fw, s_free, nw, m);
+    const u32 src = bitmap_select(s_mw, s_used, nw, U - 1 - m);   // m-th highest movable block
+    const u32 o = d.owner_hbm[(size_t)r * d.NB + src];
+    const u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
     d.loc[(size_t)p * d.MAXBP + j] = dst;
     d.owner_hbm[(size_t)r * d.NB + dst] = o;
     cp[m] = CpDesc{src, dst};

@@ -111,7 +111,7 @@ __device__ __forceinline__ SlotNow ingest_apply(const Dev& d, int p, i64 T, cons
 struct EvRes {                 // final state of one program after its events (owner event)
   i64 as;                      // acting_since (if a TOOL_CALL ran)
   u32 c, uid, calls, pend;     // pend: tokens waiting for prefill (prompt, tool results; A48)
-  u8 st, ph, fl, pad[5];       // fl: EVF_*
+  u8 st, ph, fl, kp, pad[4];   // fl: EVF_*; kp: shared prompt of an ARRIVE (A51)
 };
 static_assert(sizeof(EvRes) == 32, "EvRes layout (workspace carving)");
 enum { EVF_OWNER = 1, EVF_ARRIVE = 2, EVF_CALL = 4 };
@@ -124,6 +124,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
   u8 st = d.status[p], ph = d.phase[p];
   u64 c = d.c[p];
   u32 uid = d.uid[p], calls = 0, fl = 0, pend = d.pend[p];
+  u8 kp = d.kp[p];
   i64 as = 0;
   for (int q = 0; q < n; ++q) {
     const u32 i = idx(q);
@@ -131,8 +132,14 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
     if (e.kind == TA_EV_ARRIVE || e.kind == TA_EV_DECODE || e.kind == TA_EV_TOOL_RESULT) {
       const u64 cn = e.kind == TA_EV_ARRIVE ? (u64)e.tokens : c + e.tokens;
       if (cn > cap && !(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) return ((ull)i << 8) | TA_E_INVAL;
-      if (e.kind == TA_EV_ARRIVE && st == TA_UNARRIVED && (u64)e.tokens < (u64)d.sb * (u64)d.bt)
-        return ((ull)i << 8) | TA_E_INVAL;           // the prompt starts with the shared prefix
+      if (e.kind == TA_EV_ARRIVE && st == TA_UNARRIVED) {   // its shared prompt (A51): none, the
+        const i64 t = e.t_ms;                             // only one, or the one t_ms names
+        if (d.K > 1 && (t < 0 || t >= d.K)) return ((ull)i << 8) | TA_E_INVAL;
+        const u8 k = d.K == 0 ? (u8)KP_NONE : (d.K == 1 ? (u8)0 : (u8)t);
+        if (k != KP_NONE && (u64)e.tokens < (u64)d.sbk[k] * (u64)d.bt)
+          return ((ull)i << 8) | TA_E_INVAL;         // the prompt starts with its shared prefix
+        kp = k;
+      }
       if (!(e.kind == TA_EV_ARRIVE && st != TA_UNARRIVED)) c = cn;
     }
     switch (e.kind) {
@@ -164,7 +171,7 @@ __device__ ull ev_run(const Dev& d, const ta_event* ev, u32 p, int n, Idx idx, E
     }
   }
   o->as = as; o->c = (u32)c; o->uid = uid; o->calls = calls; o->pend = pend;
-  o->st = st; o->ph = ph; o->fl = (u8)(fl | EVF_OWNER);
+  o->st = st; o->ph = ph; o->fl = (u8)(fl | EVF_OWNER); o->kp = kp;
   return ~0ull;
 }
 
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
     if (!ok || !(o.fl & EVF_OWNER)) continue;
     const u8 st0 = d.status[p];
     if (o.fl & EVF_ARRIVE) {              // _arrive (reading A12)
-      d.uid[p] = o.uid; d.c_kv[p] = 0; d.paused_since[p] = k;
+      d.uid[p] = o.uid; d.c_kv[p] = 0; d.paused_since[p] = k; d.kp[p] = o.kp;
       d.placement[p] = -1; d.home[p] = -1; d.turn[p] = 0; d.gen_done[p] = 0;
       d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
       d.tool_return[p] = INT64_MAX;
@@ -310,7 +317,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   __shared__ u32 s_off[FP_SLOTS + 1];    // chunk offsets (exclusive prefix of ceil(nbo/4))
   __shared__ u32 s_nbo[FP_SLOTS], s_nh[FP_SLOTS], s_ns[FP_SLOTS], s_first[FP_SLOTS];
   __shared__ int s_home[FP_SLOTS];
-  __shared__ u8 s_rel[FP_SLOTS], s_hcls[FP_SLOTS];
+  __shared__ u8 s_rel[FP_SLOTS], s_hcls[FP_SLOTS], s_kp[FP_SLOTS];
   __shared__ u32 s_jh[FP_SLOTS];          // entry of the last history block (ceil(c_kv/bt) - 1), or ~0
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const int p0 = blockIdx.x * FP_SLOTS;
@@ -347,6 +354,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     s_nbo[lane] = nbo;
     s_nh[lane] = 0; s_ns[lane] = 0; s_first[lane] = 0xFFFFFFFFu;
     const u32 ckv = p < d.N ? d.c_kv[p] : 0u;
+    s_kp[lane] = p < d.N ? d.kp[p] : (u8)KP_NONE;
     s_jh[lane] = ckv ? ceil_div_u32(ckv, d.bt) - 1 : 0xFFFFFFFFu;
     s_hcls[lane] = 0;
   }
@@ -383,6 +391,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
     if (s_rel[sl]) {                     // free every block of a STOPPED program (A26)
       const int h = s_home[sl];
+      const u32 sbs = sb_of(d, s_kp[sl]);
       u32* row = d.loc + (size_t)(p0 + sl) * d.MAXBP;
       for (u32 c = lane; c < nch; c += 32) {
         const uint4 q = staged ? s_stage[o + c] : grow[c];
@@ -391,7 +400,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
         for (int t = 0; t < 4; ++t) {
           const u32 j = 4 * c + t;
           if (j >= nbo || e[t] == LOC_NONE) continue;
-          if (j >= d.sb) {                 // the shared prefix is a reference, not owned
+          if (j >= sbs) {                  // the shared prompt is a reference, not owned
             if (e[t] & LOC_HOST) {
               const u32 s2 = e[t] & ~LOC_HOST;
               atomicOr(&d.host_free[(size_t)h * d.NHW + (s2 >> 5)], 1u << (s2 & 31));
@@ -401,6 +410,12 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
           }
           row[j] = LOC_NONE;
         }
+      }
+      if (h >= 0 && s_kp[sl] != KP_NONE) {  // it no longer uses its prompt on h: the last
+        const u32 k = s_kp[sl];              // user frees the prompt's blocks (A51)
+        u32 last = 0;
+        if (lane == 0) last = atomicSub(&d.pref[(size_t)h * d.K + k], 1u) == 1u;
+        if (__shfl_sync(FULL_MASK, last, 0)) prompt_free(d, h, k, lane, 32);
       }
       continue;
     }
@@ -466,7 +481,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   // (whole-word stores, every word rewritten each pass); the decayed load of the actives
   // (Eq. 7) summed per replica (one reduction per replica per warp, a commutative u64 add)
   const int h = v.home;
-  const bool ecand = live && n_h > d.sb && h >= 0;
+  const bool ecand = live && n_h > sb_of(d, s_kp[lane]) && h >= 0;
   const size_t wi = blockIdx.x;
   for (int r = 0; r < d.R; ++r) {
     const bool on_r = pl == r;

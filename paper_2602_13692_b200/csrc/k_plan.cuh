@@ -11,7 +11,30 @@
 // appends, eviction is tail-first), so need = nb - n_hbm on the home replica; the sb
 // shared-prefix blocks (NEXT-3) are resident on every replica.
 __device__ __forceinline__ u32 need_of(const Dev& d, u32 p, int r) {
-  return d.home[p] == r ? d.nb[p] - d.n_hbm[p] : d.nb[p] - d.sb;
+  return d.home[p] == r ? d.nb[p] - d.n_hbm[p] : d.nb[p] - sb_of(d, d.kp[p]);
+}
+
+// NEXT-3 (A51): the prompt blocks F_r entries bring.  A prompt not resident on r (no
+// program homed there uses it) is materialized by the first entry (slot order) that uses
+// it: fc[i] += its blocks, f_x[i] = blocks | prompt << 16.  One CTA, fp / fc global.
+__device__ __forceinline__ void prompt_extras(const Dev& d, int r, const u32* fp, u32 nF, u32* fc, u32* f_x) {
+  __shared__ u32 s_kfirst[TA_MAX_PREFIXES];
+  if (threadIdx.x < TA_MAX_PREFIXES) s_kfirst[threadIdx.x] = 0xFFFFFFFFu;
+  __syncthreads();
+  if (d.K) {
+    for (u32 i = threadIdx.x; i < nF; i += CTA) {
+      const u8 k = d.kp[fp[i]];
+      if (k != KP_NONE && d.pref[(size_t)r * d.K + k] == 0) atomicMin(&s_kfirst[k], i);
+    }
+    __syncthreads();
+  }
+  for (u32 i = threadIdx.x; i < nF; i += CTA) {
+    const u8 k = d.K ? d.kp[fp[i]] : (u8)KP_NONE;
+    const u32 x = (k != KP_NONE && s_kfirst[k] == i) ? d.sbk[k] : 0u;
+    fc[i] += x;
+    f_x[i] = x | ((u32)k << 16);
+  }
+  __syncthreads();
 }
 
 // warp-aggregated add of a per-thread counter into a shared accumulator
@@ -22,7 +45,7 @@ __device__ __forceinline__ void warp_add_shared(ull v, ull* s) {
 }
 
 enum { PC_P2P, PC_H2D, PC_REC, PC_NEW, PC_FILLTOK, PC_HIT, PC_PEER, PC_HOST, PC_MISS, PC_NEWTOK,
-       PC_STALL, PC_N };
+       PC_STALL, PC_PREFIX, PC_N };
 
 // Step 5 of replica r by a thread-block cluster of PLAN_CL CTAs (SM90+ clusters with
 // distributed shared memory).  The leader CTA (rank 0) runs the inherently serial
@@ -106,13 +129,14 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   // [FST_MAX] x 6 per-program values of the request loop, in the F-list region of the
   // request-loop ranks (unused there): the leader writes them into every rank's copy
   // through DSMEM during its hit accounting, so nobody reads them remotely after #2
-  constexpr u32 FST_MAX = 640;
+  constexpr u32 FST_MAX = 576;                         // 7 arrays in the 4096-word region
   u32* s_fp = s_fl;
   u32* s_fj = s_fp + FST_MAX;
   u32* s_fh = s_fp + 2 * FST_MAX;
   u32* s_fk = s_fp + 3 * FST_MAX;
   u32* s_fcn = s_fp + 4 * FST_MAX;
   u32* s_fu = s_fp + 5 * FST_MAX;
+  u32* s_fx = s_fp + 6 * FST_MAX;                      // prompt blocks brought | prompt << 16
   PlanSh* L = cl.map_shared_rank(&sh, 0);              // leader's scalars
   const int N = d.N;
   const u32 bt = (u32)d.bt;
@@ -157,7 +181,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     for (int i = threadIdx.x; i < nel; i += CTA) {
       const u32 p = el[i];
       const u8 s = d.status[p];
-      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p] - d.sb;   // private HBM blocks
+      if (s == TA_PAUSED || s == TA_ACTING) es += d.n_hbm[p] - sb_of(d, d.kp[p]);   // private HBM blocks
     }
     auto add = [](ull a, ull b) { return a + b; };
     fr = cta_reduce<ull>(fr, s_red, add, 0ull);
@@ -179,6 +203,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       }
       nF = 1;
       __syncthreads();
+      prompt_extras(d, r, fp, nF, fc, d.f_x + (size_t)r * N);
     } else {
       // F_r = REASONING placed on r now: the footprint pass's REASONING set on r, minus
       // the programs this tick's pause pass took off r, plus the phase-R programs the
@@ -224,6 +249,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       __syncthreads();
       for (u32 i = threadIdx.x; i < nF; i += CTA) fc[i] = need_of(d, i < 4096 ? s_fl[i] : fp[i], r);
       __syncthreads();
+      prompt_extras(d, r, fp, nF, fc, d.f_x + (size_t)r * N);
       cta_incl_scan_array(fc, (int)nF, s_tmp);
     }
     // short lists are searched many times below: stage them in shared memory
@@ -292,7 +318,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
         if ((u32)nel > cap) dbg_hit(d, DBG_LIST_GLOBAL);
       }
       const u32 T = cta_list_threshold(el, nel, 4 * NBK, 0, X, s_big, s_tmp, epred, ebucket,
-                                       [&](int i) { return d.n_hbm[i] - d.sb; });
+                                       [&](int i) { return d.n_hbm[i] - sb_of(d, d.kp[i]); });
       PSTAMP(2, 3);
       // keys: group 0 (PAUSED) = exact reverse of the restore order, ties slot-down (the
       // tie-break value N-1-slot); groups 1-2 (ACTING) = (group, contrib), ties slot-up
@@ -327,7 +353,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       for (u32 i = threadIdx.x; i < ne; i += CTA) {
         const u32 p = (sk[i] >> 62) == 0 ? (u32)(N - 1) - sv[i] : sv[i];   // undo the group-0 tie-break
         ep[i] = p;
-        ec[i] = d.n_hbm[p] - d.sb;
+        ec[i] = d.n_hbm[p] - sb_of(d, d.kp[p]);
       }
       __syncthreads();
       cta_incl_scan_array(ec, (int)ne, s_tmp);
@@ -384,16 +410,18 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       // every per-program value up front: one memory round trip for the whole record
       const int h = d.home[p];
       const u32 ckv = d.c_kv[p], c = d.c[p], nhp = d.n_hbm[p], uidp = d.uid[p], nsp = d.n_host[p];
-      const u32 pendp = d.pend[p];
+      const u32 pendp = d.pend[p], fx = d.f_x[(size_t)r * N + i];
       const u8 satp = d.satisfied[p], cls = d.hcls[p];
+      const u32 sbp = sb_of(d, (u8)(fx >> 16)), xb = fx & 0xFFFFu;   // prompt blocks, brought now
       ta_decision rec;
       rec.pid = p; rec.src = h; rec.dst = r; rec.blocks = need; rec.to_host = 0; rec.dropped = 0;
       rec.hit_tok = rec.peer_tok = rec.host_tok = rec.miss_tok = rec.new_tok = 0;
       if (i < m) {
         if (fst) {
           u32* lf = sm->p[0];                          // leader-local staging, pushed below
-          lf[i] = p; lf[FST_MAX + i] = h == r ? nhp : d.sb; lf[2 * FST_MAX + i] = (u32)h;
+          lf[i] = p; lf[FST_MAX + i] = h == r ? nhp : sbp; lf[2 * FST_MAX + i] = (u32)h;
           lf[3 * FST_MAX + i] = ckv; lf[4 * FST_MAX + i] = c; lf[5 * FST_MAX + i] = uidp;
+          lf[6 * FST_MAX + i] = fx;
         }
         const bool resumed = !(satp && h == r);
         if (resumed && ckv > 0) {
@@ -403,14 +431,16 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
           ull th = (ull)nh * bt, ts = (ull)ns * bt, tn = (ull)nn * bt;
           // cls: entry hb - 1, classified by the footprint pass
           if (cls == 1) th -= shs; else if (cls == 2) ts -= shs; else tn -= shs;
-          if (d.sb) {                                  // shared prefix: resident on r (hit)
-            const ull sh = (ull)d.sb * bt;             // c_kv >= every prompt >= sb * bt
-            if (h >= 0) th -= sh; else tn -= sh;
-            rec.hit_tok = (u32)sh;
+          u32 sh_hit = 0, sh_miss = 0;
+          if (sbp) {                                   // the shared prompt: resident on r (hit), or
+            const ull sh = (ull)sbp * bt;              // materialized now by this program (miss);
+            if (h >= 0) th -= sh; else tn -= sh;       // c_kv >= its prompt >= sbp * bt
+            if (xb) sh_miss = (u32)sh; else sh_hit = (u32)sh;
           }
+          rec.hit_tok = sh_hit;
           if (h == r) rec.hit_tok += (u32)th; else rec.peer_tok = (u32)th;
           rec.host_tok = (u32)ts;
-          rec.miss_tok = (u32)tn;
+          rec.miss_tok = (u32)tn + sh_miss;
         }
         rec.new_tok = c - ckv;
         rec.kind = (need > 0 || resumed) ? TA_D_FETCH : 0;
@@ -434,8 +464,9 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
             }
           }
         }
-        if (d.sb && h < 0)                             // first materialize: point at the prefix
-          for (u32 j = 0; j < d.sb; ++j) d.loc[(size_t)p * d.MAXBP + j] = d.sbase + j;
+        // it now uses its prompt on r (the rows' prompt entries and the old home's release
+        // follow in step 7, after every replica's materialize: k_close)
+        if (sbp && h != r) atomicAdd(&d.pref[(size_t)r * d.K + (fx >> 16)], 1u);
         d.sat_new[p] = (u8)(r + 1);
       } else {
         rec.kind = TA_D_STALL;
@@ -447,7 +478,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     if (fst && m) {                                    // the six staged arrays into every request-loop
       __syncthreads();                                 // rank's copy (DSMEM stores, published by #2)
       const u32* lf = sm->p[0];
-      for (u32 x = threadIdx.x; x < 6 * m; x += CTA) {
+      for (u32 x = threadIdx.x; x < 7 * m; x += CTA) {
         const u32 a6 = x / m, i = x - a6 * m, v = lf[a6 * FST_MAX + i];
 #pragma unroll
         for (int k = 1; k < PLAN_CL; ++k) cl.map_shared_rank(s_fp, k)[a6 * FST_MAX + i] = v;
@@ -560,7 +591,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
       for (u32 v = threadIdx.x; v < nv; v += CTA) {
         u32 p = ep[v];
         u32 excl = v ? ecs[v - 1] : 0;
-        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p] - d.sb;
+        u32 take = (v == nv - 1) ? X - excl : d.n_hbm[p] - sb_of(d, d.kp[p]);
         u32 toh = hfree > excl ? min(take, hfree - excl) : 0;
         ta_decision rec;
         rec.kind = TA_D_EVICT; rec.pid = p; rec.src = r; rec.dst = -1; rec.blocks = take;
@@ -605,31 +636,47 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
   FeDesc* fstage = d.fedt + (size_t)r * d.NB + q_lo;  // this CTA's descriptors, compacted
   u32 nfed = 0;
   for (u32 q0 = q_lo; q0 < q_hi; q0 += 2 * CTA) {
-    u32 ik[2], pk[2], jk[2], dk[2];
+    u32 ik[2], pk[2], jk[2], dk[2], xk[2];
     int hk[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {                       // block-table loads of both in flight
       const u32 q = q0 + k * CTA + threadIdx.x;
-      ik[k] = pk[k] = jk[k] = dk[k] = 0;
+      ik[k] = pk[k] = jk[k] = dk[k] = xk[k] = 0;
       hk[k] = 0;
       if (q < q_hi) {
         const u32 i = (u32)upper_bound_u32(fcs, (int)m, q);
         const u32 excl = i ? fcs[i - 1] : 0;
         const u32 p = fst ? s_fp[i] : fp[i];
         const int h = fst ? (int)s_fh[i] : d.home[p];
-        const u32 j = (fst ? s_fj[i] : (h == r ? d.n_hbm[p] : d.sb)) + (q - excl);
+        const u32 fx = fst ? s_fx[i] : d.f_x[(size_t)r * N + i];
+        const u32 xb = fx & 0xFFFFu, off = q - excl;
+        dk[k] = bitmap_select(hws, s_big, d.NBW, q);
         pk[k] = fst ? i : p;
         hk[k] = h;
-        jk[k] = j;
-        dk[k] = bitmap_select(hws, s_big, d.NBW, q);
-        ik[k] = d.loc[(size_t)p * d.MAXBP + j];
+        if (off < xb) {                                 // one of the prompt blocks it brings (A51)
+          jk[k] = off;
+          xk[k] = 1u | (fx & 0xFFFF0000u);
+          ik[k] = LOC_NONE;
+        } else {
+          const u32 j = (fst ? s_fj[i] : (h == r ? d.n_hbm[p] : sb_of(d, (u8)(fx >> 16)))) + (off - xb);
+          jk[k] = j;
+          ik[k] = d.loc[(size_t)p * d.MAXBP + j];
+        }
       }
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const u32 q = q0 + k * CTA + threadIdx.x;
       FeDesc x{MV_NONE, 0, 0, 0, 0, 0, 0, 0};
-      if (q < q_hi) {
+      if (q < q_hi && xk[k]) {                          // prompt block jj of prompt pk: prefilled
+        const u32 pr = xk[k] >> 16, jj = jk[k], dst = dk[k];
+        d.pblk[((size_t)r * d.K + pr) * d.SBM + jj] = dst;
+        d.owner_hbm[(size_t)r * d.NB + dst] = OWNER_PROMPT | (pr << 20) | jj;
+        atomicOr(&d.pfix[(size_t)r * d.NBW + (dst >> 5)], 1u << (dst & 31));
+        pc[PC_PREFIX] += 1;
+        pc[PC_FILLTOK] += bt;
+        if (fill) x = FeDesc{MV_FILL, 0, 0, dst, TA_PROMPT_UID + pr, jj * bt, (jj + 1) * bt, jj};
+      } else if (q < q_hi) {
         const u32 p = fst ? s_fp[pk[k]] : pk[k];
         const int h = hk[k];
         const u32 j = jk[k], dst = dk[k], old = ik[k];
@@ -717,6 +764,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int v
     atomicAdd(&d.stats[ST_MISS], s_pc[PC_MISS]);
     atomicAdd(&d.stats[ST_NEW_TOK], s_pc[PC_NEWTOK]);
     atomicAdd(&d.stats[ST_STALLS], s_pc[PC_STALL]);
+    if (s_pc[PC_PREFIX]) atomicAdd(&d.stats[ST_PREFIX_BLOCKS], s_pc[PC_PREFIX]);
     if (lead) {
       d.f_cnt[r] = sh.nF;
       d.s_cnt[r] = m;

@@ -143,6 +143,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       d.satisfied[p] = 0; d.step_count[p] = 0; d.acting_since[p] = 0;
       d.tool_return[p] = INT64_MAX;
       d.pend[p] = d.t_p0[p]; d.busy[p] = 0;      // the prompt waits for its prefill (A48)
+      d.kp[p] = d.t_kp[p];                       // its shared prompt (A51)
       const u32 nbv = ceil_div_u32(d.t_p0[p], d.bt);
       d.nb[p] = nbv; d.n_hbm[p] = 0; d.n_host[p] = 0; d.prefix_hbm[p] = 0; d.contrib[p] = nbv;
       const u32 b = restore_bucket(d, TA_PHASE_R, nbv);

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   __shared__ int s_err, s_h;
-  __shared__ u32 s_nh;
+  __shared__ u32 s_nh, s_sb;
   if (threadIdx.x == 0) {
     int err = TA_OK;
     u8 st = pid < (u32)d.N ? d.status[pid] : TA_UNARRIVED;
@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
       u32 nh = 0;                          // HBM prefix length (I10)
       const u32* row = d.loc + (size_t)pid * d.MAXBP;
       while (nh < nbv && is_hbm(row[nh])) ++nh;
-      s_nh = (mode == TA_PAUSE_LAZY || s_h < 0 || nh <= d.sb) ? 0 : nh - d.sb;   // private blocks
+      const u32 sbp = sb_of(d, d.kp[pid]);
+      s_sb = sbp;
+      s_nh = (mode == TA_PAUSE_LAZY || s_h < 0 || nh <= sbp) ? 0 : nh - sbp;   // private blocks
     }
   }
   __syncthreads();
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
   EvDesc* evd = d.evd + (size_t)h * d.NB;
   u32* scr = d.evx + (size_t)h * d.NB;
   for (u32 e = threadIdx.x; e < X; e += CTA) {
-    u32 j = d.sb + X - 1 - e;             // tail first, down to the shared prefix
+    u32 j = s_sb + X - 1 - e;             // tail first, down to the shared prompt
     u32 idx = row[j];
     scr[e] = idx;
     if (e < hfree) {
@@ -200,10 +202,10 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ 
   for (u32 q = warp; q < nh; q += NWARP) {            // one warp per program: drop its row
     const u32 p = hl[q];
     u32* row = d.loc + (size_t)p * d.MAXBP;
-    const u32 nbv = ceil_div_u32(d.c[p], d.bt);
+    const u32 nbv = ceil_div_u32(d.c[p], d.bt), sbp = sb_of(d, d.kp[p]);
     u32 cnt = 0;
-    for (u32 j = lane; j < nbv; j += 32) {          // lost: private blocks (j >= sb)
-      if (row[j] != LOC_NONE) { cnt += j >= d.sb; row[j] = LOC_NONE; }
+    for (u32 j = lane; j < nbv; j += 32) {          // lost: private blocks (j >= its prompt)
+      if (row[j] != LOC_NONE) { cnt += j >= sbp; row[j] = LOC_NONE; }
     }
     cnt = __reduce_add_sync(FULL_MASK, cnt);
     if (lane == 0) { lost[q] = cnt; d.home[p] = -1; }
@@ -221,11 +223,14 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ 
         ev[pos] = rec;
         atomicAdd(&s_lost, (ull)lost[q]);
       });
-  // every block of r belonged to a program homed on r: the pools are empty now
-  for (int w = threadIdx.x; w < d.NBW; w += CTA) {   // shared-prefix blocks stay reserved
-    const i64 lo = (i64)w * 32, n = (i64)d.sbase - lo;
+  // every block of r belonged to a program homed on r or to a prompt they used: the pools
+  // are empty now, and r holds no prompt (A51)
+  for (int w = threadIdx.x; w < d.NBW; w += CTA) {
+    const i64 lo = (i64)w * 32, n = (i64)d.NB - lo;
     d.hbm_free[(size_t)r * d.NBW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
+    d.pfix[(size_t)r * d.NBW + w] = 0u;
   }
+  for (int k = threadIdx.x; k < d.K; k += CTA) d.pref[(size_t)r * d.K + k] = 0u;
   for (int w = threadIdx.x; w < d.NHW; w += CTA) {
     const i64 lo = (i64)w * 32, n = d.NH - lo;
     d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));

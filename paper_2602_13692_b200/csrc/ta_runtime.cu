@@ -121,6 +121,14 @@ static const char* validate(const ta_config* c) {
   if (c->shared_prefix_tokens < 0 || c->shared_prefix_tokens % c->block_tokens != 0 ||
       c->shared_prefix_tokens / c->block_tokens >= c->hbm_blocks)
     return "shared_prefix_tokens must be a multiple of block_tokens, below hbm_blocks blocks";
+  if (c->n_prefixes < 0 || c->n_prefixes > TA_MAX_PREFIXES) return "n_prefixes must be in [0, TA_MAX_PREFIXES]";
+  if (c->compact_every > 0 && c->hbm_blocks > 87360) return "compaction needs hbm_blocks <= 87360 (its plan in shared memory)";
+  for (int k = 0; k < c->n_prefixes; ++k)
+    if (c->prefix_tokens[k] <= 0 || c->prefix_tokens[k] % c->block_tokens != 0 ||
+        c->prefix_tokens[k] / c->block_tokens >= c->hbm_blocks || c->prefix_tokens[k] / c->block_tokens >= (1 << 20))
+      return "prefix_tokens must be positive multiples of block_tokens, below hbm_blocks blocks";
+  if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (uint64_t)TA_OWNER_PROMPT)
+    return "max_programs * max_blocks_per_program must be below TA_OWNER_PROMPT";
   return nullptr;
 }
 
@@ -145,6 +153,17 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
   x.nb = L.take<u32>(N); x.n_hbm = L.take<u32>(N); x.n_host = L.take<u32>(N);
   x.prefix_hbm = L.take<u32>(N); x.contrib = L.take<u32>(N);
   x.pend = L.take<u32>(N); x.busy = L.take<u32>(N); x.hcls = L.take<u8>(N);
+  {                                        // NEXT-3 prompts (A51)
+    int K = c->n_prefixes ? c->n_prefixes : (c->shared_prefix_tokens ? 1 : 0);
+    size_t SBM = 1;
+    for (int k = 0; k < K; ++k) {
+      const int t = c->n_prefixes ? c->prefix_tokens[k] : c->shared_prefix_tokens;
+      SBM = std::max<size_t>(SBM, (size_t)(t / c->block_tokens));
+    }
+    x.kp = L.take<u8>(N); x.t_kp = L.take<u8>(N);
+    x.pref = L.take<u32>(R * std::max(K, 1)); x.pblk = L.take<u32>(R * std::max(K, 1) * SBM);
+    x.pfix = L.take<u32>(R * NBW); x.f_x = L.take<u32>(R * N);
+  }
   x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
   x.evc = L.take<u32>(N);
   x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
@@ -202,11 +221,10 @@ static size_t host_carve(const ta_config* c, char* base, HostWs* h) {
 __global__ void k_init(Dev d) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   for (int r = 0; r < d.R; ++r) {
-    for (int w = t; w < d.NBW; w += stride) {           // the shared-prefix blocks are never free
-      i64 lo = (i64)w * 32, n = (i64)d.sbase - lo;
+    for (int w = t; w < d.NBW; w += stride) {
+      i64 lo = (i64)w * 32, n = d.NB - lo;
       d.hbm_free[(size_t)r * d.NBW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
     }
-    for (u32 j = t; j < d.sb; j += stride) d.owner_hbm[(size_t)r * d.NB + d.sbase + j] = OWNER_SHARED;
     for (int w = t; w < d.NHW; w += stride) {
       i64 lo = (i64)w * 32, n = d.NH - lo;
       d.host_free[(size_t)r * d.NHW + w] = n <= 0 ? 0u : (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1));
@@ -217,19 +235,8 @@ __global__ void k_init(Dev d) {
     d.tool_return[p] = INT64_MAX;
     d.placement[p] = -1;
     d.home[p] = -1;
-  }
-}
-
-// NEXT-3: the shared system prompt's KV (uid 0 of the closed form) in the reserved top
-// blocks of every local replica (engine stand-in, with TA_F_FILL).
-__global__ void __launch_bounds__(256) k_fill_shared(Dev d) {
-  const int nseg = 2 * d.nL;
-  const i64 per = (i64)d.sb * nseg, items = (i64)d.n_local * per;
-  for (i64 it = blockIdx.x; it < items; it += gridDim.x) {
-    const int r = d.first_local + (int)(it / per);
-    const u32 j = (u32)((it % per) / nseg);
-    const int s = (int)(it % nseg);
-    fill_segment(d, r, d.sbase + j, s, 0u, j, j * (u32)d.bt, (j + 1) * (u32)d.bt);
+    d.kp[p] = KP_NONE;
+    d.t_kp[p] = d.K ? 0 : KP_NONE;                     // trace prompts: ta_load_trace
   }
 }
 
@@ -420,8 +427,13 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   d.flags = cfg->flags; d.compact_every = cfg->compact_every;
   d.chunk_q = cfg->prefill_chunk_tokens;
   d.chunk_ms = cfg->prefill_chunk_ms;
-  d.sb = (u32)(cfg->shared_prefix_tokens / cfg->block_tokens);
-  d.sbase = (u32)(d.NB - d.sb);
+  d.K = cfg->n_prefixes ? cfg->n_prefixes : (cfg->shared_prefix_tokens ? 1 : 0);
+  d.SBM = 1;
+  for (int k = 0; k < TA_MAX_PREFIXES; ++k) {
+    const int t = k < d.K ? (cfg->n_prefixes ? cfg->prefix_tokens[k] : cfg->shared_prefix_tokens) : 0;
+    d.sbk[k] = (u32)(t / cfg->block_tokens);
+    d.SBM = std::max(d.SBM, d.sbk[k]);
+  }
   d.seg_bytes = (i64)cfg->block_tokens * cfg->n_kv_heads * cfg->head_dim * cfg->elem_bytes;
   d.block_bytes = (i64)x->block_bytes;
   d.first_local = cfg->first_replica; d.n_local = cfg->replicas_here;
@@ -500,10 +512,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
   if (e == cudaSuccess) { k_init<<<148, 256, 0, x->stream>>>(d); e = cudaGetLastError(); }
-  if (e == cudaSuccess && d.sb && (d.flags & TA_F_FILL)) {
-    k_fill_shared<<<kCopyGrid, 256, 0, x->stream>>>(d);
-    e = cudaGetLastError();
-  }
+
   // planner kernels: small sorts and staged lists in dynamic shared memory
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
@@ -535,8 +544,10 @@ ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* t) {
   if (total > (u32)ctx->cfg.max_trace_turns) FAIL(ctx, TA_E_INVAL, "trace has %u turns > max_trace_turns", total);
   for (int p = 0; p < t->n_slots; ++p) {
     if (t->turn_off[p + 1] <= t->turn_off[p]) FAIL(ctx, TA_E_INVAL, "slot %d has no turns", p);
-    if ((u64)t->p0[p] < (u64)ctx->d.sb * (u64)ctx->d.bt)
-      FAIL(ctx, TA_E_INVAL, "slot %d: prompt shorter than the shared prefix", p);
+    const u8 k = t->prefix_id ? t->prefix_id[p] : (ctx->d.K ? 0 : KP_NONE);
+    if (k != KP_NONE && (int)k >= ctx->d.K) FAIL(ctx, TA_E_INVAL, "slot %d: prefix_id %u >= n_prefixes", p, k);
+    if (k != KP_NONE && (u64)t->p0[p] < (u64)ctx->d.sbk[k] * (u64)ctx->d.bt)
+      FAIL(ctx, TA_E_INVAL, "slot %d: prompt shorter than its shared prefix", p);
     u64 ctx_max = t->p0[p];
     for (u32 q = t->turn_off[p]; q < t->turn_off[p + 1]; ++q) ctx_max += (u64)t->g[q] + t->o[q];
     if ((ctx_max + ctx->d.bt - 1) / ctx->d.bt > (u64)ctx->d.MAXB)
@@ -550,6 +561,7 @@ ta_status ta_load_trace(ta_ctx* ctx, const ta_trace_view* t) {
   CK(ctx, cudaMemcpyAsync(d.t_g, t->g, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
   CK(ctx, cudaMemcpyAsync(d.t_d, t->d_ms, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
   CK(ctx, cudaMemcpyAsync(d.t_o, t->o, sizeof(u32) * total, cudaMemcpyHostToDevice, s));
+  if (t->prefix_id) CK(ctx, cudaMemcpyAsync(d.t_kp, t->prefix_id, t->n_slots, cudaMemcpyHostToDevice, s));
   CK(ctx, cudaStreamSynchronize(s));
   d.n_slots = t->n_slots;
   d.n_initial = t->n_initial;
@@ -644,6 +656,7 @@ ta_status ta_stats(ta_ctx* ctx, ta_stats_t* out) {
   out->unused_bound_violations = st[ST_UNUSED_VIOL];
   out->overshoot_blocks = st[ST_OVERSHOOT];
   out->overshoot_max_blocks = st[ST_OVERSHOOT_MAX];
+  out->prefix_blocks = st[ST_PREFIX_BLOCKS];
   for (int r = 0; r < d.R; ++r) {
     out->L[r] = L[r];
     u64 f = 0, g = 0;
@@ -772,6 +785,25 @@ ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v) {
     CK(ctx, mv(v->nb, d.nb, N * 4)); CK(ctx, mv(v->n_hbm, d.n_hbm, N * 4));
     CK(ctx, mv(v->n_host, d.n_host, N * 4)); CK(ctx, mv(v->prefix_hbm, d.prefix_hbm, N * 4));
     CK(ctx, mv(v->contrib, d.contrib, N * 4));
+  }
+  {                                        // NEXT-3 prompts (A51)
+    const size_t RK = (size_t)R * (d.K ? d.K : 1);
+    CK(ctx, mv(v->prefix_id, d.kp, N));
+    CK(ctx, mv(v->prefix_ref, d.pref, RK * 4));
+    CK(ctx, mv(v->prefix_blk, d.pblk, RK * d.SBM * 4));
+    if (dir == 1 && v->prefix_blk && v->prefix_ref) {   // the prompt-block bitmap follows the upload
+      std::vector<u32> ref(RK), blk(RK * d.SBM), fix((size_t)R * d.NBW, 0u);
+      memcpy(ref.data(), v->prefix_ref, RK * 4);
+      memcpy(blk.data(), v->prefix_blk, RK * d.SBM * 4);
+      for (size_t r = 0; r < R; ++r)
+        for (int k = 0; k < d.K; ++k)
+          if (ref[r * d.K + k])
+            for (u32 j = 0; j < d.sbk[k]; ++j) {
+              const u32 b = blk[(r * d.K + k) * d.SBM + j];
+              fix[r * d.NBW + (b >> 5)] |= 1u << (b & 31);
+            }
+      CK(ctx, cudaMemcpy(d.pfix, fix.data(), fix.size() * 4, cudaMemcpyHostToDevice));
+    }
   }
   if (v->scalars) {
     Ctr c;

@@ -32,13 +32,24 @@ def oracle_arrays(o) -> dict:
                    if o.NH else np.zeros(1, np.uint32)),
         L=np.array(o.L, np.uint64),
         scalars=np.array([o.tick, o.next_arrival, o.last_T, 0], np.int64),
+        prefix_id=np.array([k if k >= 0 else 255 for k in o.kp], np.uint8),
     )
+    K, SBM = max(1, o.K), max([1] + o.sbk)                 # NEXT-3 prompts (A51)
+    ref = np.zeros(R * K, np.uint32)
+    blk = np.zeros(R * K * SBM, np.uint32)
+    for r in range(R):
+        for k in range(o.K):
+            ref[r * K + k] = o.pref[r][k]
+            for j, b in enumerate(o.pblk[r][k] or ()):
+                blk[(r * K + k) * SBM + j] = b
+    d["prefix_ref"], d["prefix_blk"] = ref, blk
     own_h = np.zeros(R * o.NB, np.uint32)
     own_s = np.zeros(max(1, R * o.NH), np.uint32)
     for r in range(R):
         for b, ow in enumerate(o.owner_hbm[r]):
-            if ow is not None:       # shared-prefix blocks (NEXT-3): the OWNER_SHARED tag
-                own_h[r * o.NB + b] = 0xFFFFFFFF if ow[0] == oracle.ta_oracle.SHARED else ow[0] * MAXB + ow[1]
+            if ow is not None:       # shared-prompt blocks (NEXT-3): TA_OWNER_PROMPT | k << 20 | j
+                own_h[r * o.NB + b] = (0xF8000000 | (ow[1] << 20) | ow[2]) if ow[0] == oracle.ta_oracle.PROMPT \
+                    else ow[0] * MAXB + ow[1]
         for s, ow in enumerate(o.owner_host[r]):
             if ow is not None:
                 own_s[r * o.NH + s] = ow[0] * MAXB + ow[1]
@@ -75,6 +86,17 @@ def compare_state(o, g: dict, where=""):
         ia, ig = a["owner_hbm"][r * o.NB:(r + 1) * o.NB][m], g["owner_hbm"][r * o.NB:(r + 1) * o.NB][m]
         assert np.array_equal(ia, ig), f"{where}: owner_hbm r={r}"
     assert int(g["scalars"][0]) == o.tick and int(g["scalars"][1]) == o.next_arrival, where
+    if o.K:                                                # NEXT-3: prompts, refcounts, blocks
+        assert np.array_equal(a["prefix_id"][live], g["prefix_id"][live]), f"{where}: prefix_id"
+        assert np.array_equal(a["prefix_ref"], g["prefix_ref"][:a["prefix_ref"].size]), \
+            f"{where}: prompt refcounts oracle {a['prefix_ref']} gpu {g['prefix_ref']}"
+        SBM = max(o.sbk)
+        for r in range(o.R):
+            for k in range(o.K):
+                if o.pref[r][k]:
+                    lo = (r * o.K + k) * SBM
+                    assert np.array_equal(a["prefix_blk"][lo:lo + o.sbk[k]], g["prefix_blk"][lo:lo + o.sbk[k]]), \
+                        f"{where}: prompt {k} blocks on r{r}"
 
 
 def dec_tuples(arr) -> list:
@@ -95,11 +117,16 @@ def check_blocks_content(o, pool, samples, rng):
     pick = rng.choice(len(owned), size=min(samples, len(owned)), replace=False)
     n = 0
     for i in pick:
-        tier, r, idx, (p, j) = owned[i]
-        shared = p == oracle.ta_oracle.SHARED                     # the shared prompt: uid 0
+        tier, r, idx, ow = owned[i]
+        shared = ow[0] == oracle.ta_oracle.PROMPT                 # shared prompt k: uid PROMPT_UID + k
+        if shared:
+            _, k, j = ow
+        else:
+            p, j = ow
         valid = bt if shared else min(bt, o.c_kv[p] - j * bt)
         got = pool.read_block(r, tier, idx)                       # [2L, bt, H, D/4]
-        want = block_words(0 if shared else o.uid[p], j, bt, L, H, D).reshape(2 * L, bt, H, D // 4)
+        want = block_words(oracle.ta_oracle.PROMPT_UID + k if shared else o.uid[p], j, bt, L, H,
+                           D).reshape(2 * L, bt, H, D // 4)
         assert np.array_equal(got[:, :valid], want[:, :valid]), (tier, r, idx, p, j)
         n += 1
     return n

@@ -29,11 +29,11 @@ def test_exports_every_declared_symbol(libta):
 
 
 def test_abi_version_and_struct_sizes(libta):
-    assert libta.ta_abi_version() == 2
+    assert libta.ta_abi_version() == 3
     assert C.sizeof(binding.Event) == 24
     assert binding.DECISION_DTYPE.itemsize == 48
-    # ta_stats_t: 25 counters, L/hbm_used/host_used[32], block_bytes, 7 ledger fields, 2 guard (ta.h)
-    assert C.sizeof(binding.Stats) == (25 + 3 * 32 + 1 + 7 + 2) * 8
+    # ta_stats_t: 25 counters, L/hbm_used/host_used[32], block_bytes, 7 ledger, 2 guard, prefix_blocks (ta.h)
+    assert C.sizeof(binding.Stats) == (25 + 3 * 32 + 1 + 7 + 2 + 1) * 8
     # ta_tick_info: tick, 6 u32 counters, 3 x u32[32] per-replica link counts
     assert C.sizeof(binding.TickInfo) == 8 + 6 * 4 + 3 * 32 * 4
     # ta_config ends with flags, prefill_chunk_tokens, prefill_chunk_ms, reserved

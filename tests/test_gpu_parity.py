@@ -184,7 +184,7 @@ def test_gpu_shared_prefix(seed, R, spt):
     tight pools with host tier and compaction; the reserved blocks' bytes (uid 0) are
     verified with the rest."""
     o, n = run_parity(stress(seed, R, NB=56 if R > 1 else 80, shared_prefix_tokens=spt), 300, seed=seed)
-    assert o.stats["evict_blocks"] > 0 and o.stats["compact_blocks"] > 0 and o.sb == spt // 16
+    assert o.stats["evict_blocks"] > 0 and o.stats["compact_blocks"] > 0 and o.sbk == [spt // 16]
 
 
 def test_gpu_shared_prefix_swe_decisions_full_n():
@@ -193,6 +193,26 @@ def test_gpu_shared_prefix_swe_decisions_full_n():
     cfg = tracegen.get_config("c2_swe", kv="mini", shared_prefix_tokens=1024)
     o, n = run_parity(cfg, 40, state_every=5, content_every=10, samples=8)
     assert n > 0
+
+
+@pytest.mark.parametrize("seed,R", [(86, 1), (87, 2), (88, 3)])
+def test_gpu_two_shared_prompts(seed, R):
+    """NEXT-3 widened (reading A51): two shared prompts (48 and 32 tokens), one per agent
+    label, materialized by their first user on a replica, refcounted and released by
+    the last; tight pools with host tier and compaction."""
+    cfg = stress(seed, R, NB=56 if R > 1 else 80, n=32, n0=14)
+    cfg["trace"]["labels"] = ["a", "b"]
+    cfg["shared_prefixes"] = [(48, "a"), (32, "b")]
+    o, n = run_parity(cfg, 300, seed=seed)
+    assert o.stats["prefix_blocks"] > 0 and o.stats["evict_blocks"] > 0 and o.K == 2
+
+
+def test_gpu_two_prompts_configs3_full_n():
+    """configs[2] (2k programs, 8 replicas on one GPU, decision-only KV) with one shared
+    prompt per preset: OpenHands 960 tokens, ToolOrchestra 640 tokens."""
+    cfg = tracegen.get_config("c3_mixed", kv="mini", shared_prefixes=[(960, "openhands"), (640, "toolorch")])
+    o, n = run_parity(cfg, 20, state_every=4, content_every=4, samples=8)
+    assert n > 0 and o.sbk == [60, 40] and o.stats["prefix_blocks"] > 0
 
 
 def test_gpu_decode_step_guard():
@@ -207,4 +227,4 @@ def test_gpu_shared_prefix_configs3_full_n():
     960-token shared system prompt (every preset's prompt is at least 1,000 tokens)."""
     cfg = tracegen.get_config("c3_mixed", kv="mini", shared_prefix_tokens=960)
     o, n = run_parity(cfg, 20, state_every=4, content_every=4, samples=8)
-    assert n > 0 and o.sb == 60
+    assert n > 0 and o.sbk == [60]

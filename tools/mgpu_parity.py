@@ -1,14 +1,15 @@
 """Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
 
 torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs] [--api]
-    [--shared TOKENS] [--c3]
+    [--shared TOKENS] [--c3] [--prompts2]
 Every rank runs the replicated control plane for all N replicas and moves only its
 own replica's bytes; every rank compares its decisions and full state with its own
 oracle copy, and verifies the KV content of its local pool.  --api: the same ticks in
 API mode (the engine's recorded events, tools/api_events.py) against the trace-mode
 oracle.  --shared: NEXT-3 shared system prompt of TOKENS tokens (reserved blocks on
 every GPU).  --c3: configs[2] (2k programs) with one replica per GPU, decision-only KV
-shape.  Exit code 0 = parity."""
+shape.  --prompts2: two shared prompts, one per agent label (NEXT-3, A51).  Exit code 0 =
+parity."""
 import os
 import random
 import sys
@@ -35,10 +36,15 @@ def main():
     spt = int(sys.argv[sys.argv.index("--shared") + 1]) if "--shared" in sys.argv else 0
     if "--c3" in sys.argv:    # configs[2]'s 2k OpenHands + ToolOrchestra programs, one replica per GPU,
         cfg = tracegen.get_config("c3_mixed", kv="mini", n_replicas=world, compact_every=4)   # decision-only KV
+        if "--prompts2" in sys.argv:                   # one shared prompt per preset (NEXT-3, A51)
+            cfg["shared_prefixes"] = [(960, "openhands"), (640, "toolorch")]
     else:
         cfg = tracegen.get_config("c1_toy", n_replicas=world, hbm_blocks=64, host_blocks=16, compact_every=3,
                                   trace=dict(n=12 * world, n_initial=5 * world, seed=77),
                                   shared_prefix_tokens=spt)
+        if "--prompts2" in sys.argv:                   # two shared prompts, alternating labels (A51)
+            cfg["trace"]["labels"] = ["a", "b"]
+            cfg["shared_prefixes"] = [(48, "a"), (32, "b")]
     tr = tracegen.make_trace(cfg)
     o = oracle.Oracle(cfg, tr)
     api = "--api" in sys.argv

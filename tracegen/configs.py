@@ -108,4 +108,7 @@ def get_config(name: str, **override) -> dict:
 def make_trace(cfg: dict):
     t = cfg["trace"]
     tr = gen_trace(t["mix"], t["n"], t["seed"], t["max_ctx"], t.get("n_initial"))
+    if t.get("labels"):           # agent labels cycled over the slots (e.g. one shared prompt each)
+        lab = list(t["labels"])
+        tr.preset = [lab[p % len(lab)] for p in range(tr.n_slots)]
     return tile_trace(tr, int(t.get("tile", 1)))
