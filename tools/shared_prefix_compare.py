@@ -4,9 +4,12 @@ buffer"), through libta on the GPU (the kernels tests/test_gpu_parity.py::
 test_gpu_shared_prefix checks against the oracle).
 
 usage: python tools/shared_prefix_compare.py [--config c2_swe] [--sim-s 2400] [--spts 0,1024,1984]
+       python tools/shared_prefix_compare.py --config c3_mixed --per-preset openhands:960,toolorch:640
 
 Each point runs the config's trace (decision-identical `mini` KV shape) for sim_s
-seconds of simulated time with shared_prefix_tokens = spt, and reports per simulated
+seconds of simulated time with shared_prefix_tokens = spt (one prompt for every program),
+or with --per-preset one prompt per listed preset (NEXT-3, reading A51: materialized by
+the first user on a replica, refcounted, released by the last), and reports per simulated
 second the tokens written, the resume hit rate, evictions and recomputed blocks, and
 the mean physical HBM occupancy (sampled every 10 ticks).  The load (Eq. 7) counts full
 contexts either way, so pause/restore see the same loads; the reserved-once prompt
@@ -31,8 +34,13 @@ def main():
     name = arg("--config", "c2_swe")
     sim_s = int(arg("--sim-s", "2400"))
     spts = [int(v) for v in arg("--spts", "0,1024,1984").split(",")]
-    for spt in spts:
-        cfg = tracegen.get_config(name, kv="mini", shared_prefix_tokens=spt)
+    points = [("shared_prefix_tokens", spt) for spt in spts]
+    if "--per-preset" in sys.argv:                   # no prompt, then one prompt per preset
+        spec = [(int(t), pr) for pr, t in (x.split(":") for x in arg("--per-preset", "").split(","))]
+        points = [("shared_prefix_tokens", 0), ("shared_prefixes", spec)]
+    for key, val in points:
+        cfg = tracegen.get_config(name, kv="mini", **{key: val})
+        spt = val
         tr = tracegen.make_trace(cfg)
         pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False)
         pool.load_trace(tr)
@@ -46,7 +54,8 @@ def main():
                 used.append(cfg["n_replicas"] * cfg["hbm_blocks"] - free)
         st = pool.stats()
         hist = st["hit_tok"] + st["peer_tok"] + st["host_tok"] + st["miss_tok"]
-        out = {"config": name, "shared_prefix_tokens": spt, "ticks": ticks, "sim_s": sim_s,
+        out = {"config": name, key: spt, "ticks": ticks, "sim_s": sim_s,
+               "prefix_blocks": st["prefix_blocks"],
                "tokens_per_sim_s": round(st["new_tok"] / sim_s, 1),
                "hit_rate": round(st["hit_tok"] / hist, 4) if hist else None,
                "no_recompute_rate": round((hist - st["miss_tok"]) / hist, 4) if hist else None,
