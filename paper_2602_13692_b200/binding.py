@@ -165,6 +165,11 @@ EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_tra
             "ta_debug_state", "ta_export_pool_handle", "ta_import_peer_pool", "ta_destroy",
             "ta_last_error", "ta_abi_version", "ta_move_blocks", "ta_last_tick", "ta_set_copy_bulk",
             "ta_debug_phase_stamps", "ta_set_health", "ta_debug_counters")
+def e_any(spans):
+    return any(e for _, e in spans.values())
+
+
+SPAN_KERNELS = ("front", "pause_restore", "plan", "move", "close", "compact")   # KSpan k order
 DEBUG_COUNTERS = ("radix_sort", "bitonic_sort", "rank_sort", "list_global", "plan_f_global", "plan_e_global",
                   "plan_v_global", "plan_fst_global", "restore_chunks", "evict_ticks")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
@@ -405,6 +410,11 @@ class Pool:
         self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 256), "ta_debug_phase_stamps")
         out = {}
         names = ("pause", "restore", "plan", "close", "plan_cta1", "plan_cta3", "front_cta0", "front_last")
+        # kernel spans (first CTA start, last thread-0 exit) live in slot 3, entries 16..27
+        spans = {n: (a[3 * 32 + 16 + 2 * i], a[3 * 32 + 17 + 2 * i]) for i, n in enumerate(SPAN_KERNELS)}
+        probes = [a[3 * 32 + 28 + i] for i in range(4)]
+        for i in range(16, 32):
+            a[3 * 32 + i] = 0
         first = {}
         for k, name in enumerate(names):
             v = [a[32 * k + i] for i in range(32) if a[32 * k + i] and not a[32 * k + i] >> 62]
@@ -422,6 +432,11 @@ class Pool:
             out[name] = [(i, c - first[name]) for i, c in v] if v else []
             # sizes recorded next to the stamps (bit 62 set): ("n<i>", value)
             out[name] += [(f"n{i}", a[32 * k + i] & ((1 << 62) - 1)) for i in range(32) if a[32 * k + i] >> 62 == 1]
+        t0 = min([b for b, e in spans.values() if e] or [0])
+        out["spans"] = [(n, round((b - t0) / 1e3, 1), round((e - t0) / 1e3, 1))
+                        for n, (b, e) in spans.items() if e]      # (kernel, start us, end us)
+        out["spans"] += [(f"probe{i}", round((t - t0) / 1e3, 1), round((t - t0) / 1e3, 1))
+                         for i, t in enumerate(probes) if t and e_any(spans)]
         return out
 
     def debug_counters(self) -> dict:

@@ -267,6 +267,19 @@ __device__ __forceinline__ ull gtimer() {
       d.pst[(kk) * 32 + (i)] = gtimer();                                           \
   } while (0)
 
+// Kernel span (TA_F_TIMING only): the earliest CTA start and the latest exit of any
+// warp, as globaltimer ns in pst[3*32 + 16 + 2k] / [.. + 1] (reset to ~0 / 0 at
+// the head of each tick by k_span_reset).  The kernel wrappers call kspan_begin / the
+// body / kspan_end.  k: 0 front, 1 pause+restore, 2 plan, 3 movement, 4 close,
+// 5 compaction.
+enum { KS_FRONT = 0, KS_PR = 1, KS_PLAN = 2, KS_MOVE = 3, KS_CLOSE = 4, KS_COMPACT = 5, KS_N = 6 };
+__device__ __forceinline__ void kspan_begin(const Dev& d, int k, ull t_in) {
+  if ((d.flags & TA_F_TIMING) && threadIdx.x == 0) atomicMin(d.pst + 3 * 32 + 16 + 2 * k, t_in);
+}
+__device__ __forceinline__ void kspan_end(const Dev& d, int k) {
+  if ((d.flags & TA_F_TIMING) && (threadIdx.x & 31) == 0) atomicMax(d.pst + 3 * 32 + 17 + 2 * k, gtimer());
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ u32 ceil_div_u32(u32 a, u32 b) { return (a + b - 1) / b; }
 // blocks of a program's shared prompt (0 without one)

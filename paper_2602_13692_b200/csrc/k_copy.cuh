@@ -201,6 +201,21 @@ __global__ void __launch_bounds__(256) k_copy_push(Dev d) {
 // Cross-process barrier through IPC-mapped mailboxes (one replica per GPU): lane i
 // publishes this rank's epoch into peer i's mailbox, then waits for peer i's epoch
 // in its own.  Bounded spin: a dead peer poisons the context instead of hanging.
+// A/B aid (env TA_GAP_PROBES at init, timing mode): a one-warp kernel between two tick
+// kernels stamps its first instruction into pst[3*32 + 28 + i].
+__global__ void k_probe(Dev d, int i) {
+  const ull t = gtimer();
+  if (threadIdx.x == 0) d.pst[3 * 32 + 28 + i] = t;
+}
+
+// Timing mode only: reset the kernel spans (KSpan) at the head of a tick.
+__global__ void k_span_reset(Dev d) {
+  if (threadIdx.x < KS_N) {
+    d.pst[3 * 32 + 16 + 2 * threadIdx.x] = ~0ull;
+    d.pst[3 * 32 + 17 + 2 * threadIdx.x] = 0;
+  }
+}
+
 __global__ void k_barrier(Dev d) {
   if (!d.multi) return;
   __shared__ ull e;
@@ -223,7 +238,7 @@ __global__ void k_barrier(Dev d) {
 // not run (rejected API batch, peer failure) planned no compaction: the descriptor list
 // still holds the previous tick's moves, whose destinations the engine may have written
 // since, so nothing is copied.
-__global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
+__device__ __forceinline__ void copy_compact(const Dev& d) {
   if (d.ctr->err != TA_OK) return;
   const int nseg = 2 * d.nL;
   const i64 items = local_items(d, d.cpd_cnt, nseg);
@@ -237,6 +252,12 @@ __global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
     seg_copy(d, bk, src, dst);
   }
   bulk_end(d);
+}
+__global__ void __launch_bounds__(256) k_copy_compact(Dev d) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
+  kspan_begin(d, KS_COMPACT, t_in);
+  copy_compact(d);
+  kspan_end(d, KS_COMPACT);
 }
 
 // ta_move_blocks: n whole blocks from one pool to another, block-list driven.
@@ -339,7 +360,7 @@ __device__ __forceinline__ bool wait_evicted(const Dev& d, const u32* flag, bool
 // grid is fully resident, so the waits always terminate.  Multi-process: fills and
 // new-token tails run in k_fill after the closing barrier (a pushed block's tail is
 // written by its destination process).
-__global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
+__device__ __forceinline__ void move_fused(const Dev& d) {
   const int nseg = 2 * d.nL;
   const int role = blockIdx.x & 1;
   const int G = gridDim.x >> 1;
@@ -426,6 +447,12 @@ __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   }
   bulk_end(d);
   if (d.multi) __threadfence_system();             // pushed bytes visible before the barrier
+}
+__global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
+  kspan_begin(d, KS_MOVE, t_in);
+  move_fused(d);
+  kspan_end(d, KS_MOVE);
 }
 
 // Test aid: count words of every owned block (HBM and host tier of the local

@@ -244,10 +244,12 @@ __device__ __forceinline__ void assemble_close(const Dev& d, int verb, u32 pos) 
 // grid barrier, the canonical decision list and statistics on CTA 0.  The
 // compaction copies (k_copy_compact) run after this kernel.
 __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d, int verb) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
-  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[3 * 32 + threadIdx.x] = 0;
+  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 16) d.pst[3 * 32 + threadIdx.x] = 0;
+  kspan_begin(d, KS_CLOSE, t_in);
   PSTAMP(3, 0);
   // CTA 0 assembles the records of steps 3-5 while the other CTAs finalize (one CTA: both)
   u32 pos = 0;
@@ -268,4 +270,5 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   PSTAMP(3, 4);
   if (blockIdx.x == 0) assemble_close(d, verb, pos);
   PSTAMP(3, 9);
+  kspan_end(d, KS_CLOSE);
 }

@@ -360,36 +360,82 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   }
   __syncthreads();
   const u32* rows = d.loc + (size_t)p0 * d.MAXBP;
-  // warp w owns slots w, w + 8, w + 16, w + 24 (interleaved for balance); a slot's
-  // chunks go to the staging buffer at s_off[slot] if they fit, else they are read
-  // straight from global memory in step 3
-  constexpr int SPW = FP_SLOTS / (FP_THREADS / 32);
   if (MODE == 0) { PSTAMP_B(6, 0, 1); PSTAMP_B(7, gridDim.x - 1, 1); }
-  // ---- 2. rows -> shared memory (each warp its slots), ingest (warp 0)
-#pragma unroll
-  for (int k = 0; k < SPW; ++k) {
-    const int sl = warp + k * (FP_THREADS / 32);
-    const u32 o = s_off[sl], nch = s_off[sl + 1] - o;
-    if (o + nch <= FP_STAGE)
-      for (u32 c = lane; c < nch; c += 32) cp_async16(&s_stage[o + c], rows + (size_t)sl * d.MAXBP + 4 * c);
-  }
-  if (w0) {
-    if (MODE == 0 && p < d.N) v = ingest_apply(d, p, T, f);
-    s_rel[lane] = (MODE != 2 && p < d.N && v.released) ? 1 : 0;
+  // ---- 2 + 3. warps 1..7: each stages its slots' rows (slots w-1, w+6, ...) and counts
+  //      them as soon as its own copies land; meanwhile warp 0 runs the ingest and the
+  //      per-slot values that need no counts (a slot's chunks go to the staging buffer at
+  //      s_off[slot] if they fit, else they are read straight from global memory)
+  const bool valid = p < d.N;
+  u32 nbv = 0, cb = 0, rbv = 0xFFFFFFFFu;
+  bool live = false;
+  if (!w0) {
+    constexpr int CW = FP_THREADS / 32 - 1;       // counting warps
+    for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
+      const u32 o = s_off[sl], nch = s_off[sl + 1] - o;
+      if (o + nch <= FP_STAGE)
+        for (u32 c = lane; c < nch; c += 32) cp_async16(&s_stage[o + c], rows + (size_t)sl * d.MAXBP + 4 * c);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
+      const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
+      const bool staged = o + nch <= FP_STAGE;
+      const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
+      u32 a_h = 0, a_n = 0, a_f = 0xFFFFFFFFu;   // HBM entries, non-HBM entries, first non-HBM
+      const u32 jh = s_jh[sl];
+#pragma unroll 4
+      for (u32 c = lane; c < nch; c += 32) {
+        uint4 q = staged ? s_stage[o + c] : grow[c];
+        if (4 * c + 4 > nbo) {           // the row's last chunk: entries j >= nbo do not count
+          const u32 k = nbo - 4 * c;     // 1..3
+          if (k < 2) q.y = LOC_NONE;
+          if (k < 3) q.z = LOC_NONE;
+          q.w = LOC_NONE;
+        }
+        if ((jh >> 2) == c && jh < nbo) {  // the last history block's location class
+          const u32 t = jh & 3;
+          const u32 x = t == 0 ? q.x : t == 1 ? q.y : t == 2 ? q.z : q.w;
+          s_hcls[sl] = is_hbm(x) ? 1 : (is_host(x) ? 2 : 0);
+        }
+        // HBM entries have bit 31 clear; host entries set it, and so does LOC_NONE
+        const u32 n0 = q.x >> 31, n1 = q.y >> 31, n2 = q.z >> 31, n3 = q.w >> 31;
+        const u32 nn = n0 + n1 + n2 + n3;
+        a_h += 4 - nn;
+        a_n += nn - (q.x == LOC_NONE) - (q.y == LOC_NONE) - (q.z == LOC_NONE) - (q.w == LOC_NONE);
+        if (nn && a_f == 0xFFFFFFFFu) a_f = 4 * c + (n0 ? 0 : n1 ? 1 : n2 ? 2 : 3);
+      }
+      a_h = __reduce_add_sync(FULL_MASK, a_h);
+      a_n = __reduce_add_sync(FULL_MASK, a_n);
+      a_f = __reduce_min_sync(FULL_MASK, a_f);
+      if (lane == 0) { s_nh[sl] = a_h; s_ns[sl] = a_n; s_first[sl] = a_f; }
+    }
+  } else {
+    if (MODE == 0 && valid) v = ingest_apply(d, p, T, f);
+    const bool rel = MODE != 2 && valid && v.released;
+    s_rel[lane] = rel ? 1 : 0;
     s_home[lane] = v.home;
+    const u8 st = (u8)v.st;
+    live = valid && !rel && (st == TA_PAUSED || st == TA_REASONING || st == TA_ACTING);
+    if (live) {
+      nbv = ceil_div_u32(v.c, d.bt);
+      cb = contrib_of(d, nbv, (u8)v.ph, v.as, T);
+      if (st == TA_PAUSED) {
+        rbv = restore_bucket(d, (u8)v.ph, nbv);
+        atomicAdd(&d.rhist[rbv], 1u);
+      }
+    }
   }
   if (MODE == 0) { PSTAMP_B(6, 0, 2); PSTAMP_B(7, gridDim.x - 1, 2); }
-  cp_async_wait_all();
   __syncthreads();
   if (MODE == 0) { PSTAMP_B(6, 0, 3); PSTAMP_B(7, gridDim.x - 1, 3); }
-  // ---- 3. per slot (its warp): counts, or the frees of a released row
-#pragma unroll 1
-  for (int k = 0; k < SPW; ++k) {
-    const int sl = warp + k * (FP_THREADS / 32);
-    const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
-    const bool staged = o + nch <= FP_STAGE;
-    const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
-    if (s_rel[sl]) {                     // free every block of a STOPPED program (A26)
+  if (!w0) {
+    // ---- 3b. free every block of a program STOPPED this tick (A26), by its counting warp
+    constexpr int CW = FP_THREADS / 32 - 1;
+    for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
+      if (!s_rel[sl]) continue;
+      const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
+      const bool staged = o + nch <= FP_STAGE;
+      const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
       const int h = s_home[sl];
       const u32 sbs = sb_of(d, s_kp[sl]);
       u32* row = d.loc + (size_t)(p0 + sl) * d.MAXBP;
@@ -417,57 +463,20 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
         if (lane == 0) last = atomicSub(&d.pref[(size_t)h * d.K + k], 1u) == 1u;
         if (__shfl_sync(FULL_MASK, last, 0)) prompt_free(d, h, k, lane, 32);
       }
-      continue;
     }
-    u32 a_h = 0, a_s = 0, a_f = 0xFFFFFFFFu;
-    const u32 jh = s_jh[sl];
-#pragma unroll 4
-    for (u32 c = lane; c < nch; c += 32) {
-      const uint4 q = staged ? s_stage[o + c] : grow[c];
-      const u32 e[4] = {q.x, q.y, q.z, q.w};
-      if ((jh >> 2) == c && jh < nbo) {  // the last history block's location class
-        const u32 x = e[jh & 3];
-        s_hcls[sl] = is_hbm(x) ? 1 : (is_host(x) ? 2 : 0);
-      }
-#pragma unroll
-      for (int t = 3; t >= 0; --t) {
-        const u32 j = 4 * c + t;
-        if (j < nbo) {
-          const bool h = is_hbm(e[t]);
-          a_h += h;
-          a_s += is_host(e[t]);
-          if (!h) a_f = j;
-        }
-      }
-    }
-    a_h = __reduce_add_sync(FULL_MASK, a_h);
-    a_s = __reduce_add_sync(FULL_MASK, a_s);
-    a_f = __reduce_min_sync(FULL_MASK, a_f);
-    if (lane == 0) { s_nh[sl] = a_h; s_ns[sl] = a_s; s_first[sl] = a_f; }
+    return;
   }
-  __syncthreads();
   if (MODE == 0) { PSTAMP_B(6, 0, 4); PSTAMP_B(7, gridDim.x - 1, 4); }
   // ---- 4. per slot: derived values and candidate sets (warp 0)
-  if (!w0) return;
-  const bool valid = p < d.N;
   const u8 st = (u8)v.st;
-  const bool live = valid && !(MODE != 2 && v.released) &&
-                    (st == TA_PAUSED || st == TA_REASONING || st == TA_ACTING);
-  u32 nbv = 0, n_h = 0, n_s = 0, cb = 0, rbv = 0xFFFFFFFFu;
+  u32 n_h = 0, n_s = 0;
   int pl = -1;
   if (live) {
-    nbv = ceil_div_u32(v.c, d.bt);
     n_h = s_nh[lane];
     n_s = s_ns[lane];
     const u32 first = s_first[lane];
-    cb = contrib_of(d, nbv, (u8)v.ph, v.as, T);
-    if (st == TA_PAUSED) {
-      rbv = restore_bucket(d, (u8)v.ph, nbv);
-      atomicAdd(&d.rhist[rbv], 1u);
-    } else {
-      pl = v.pl;
-    }
-    d.prefix_hbm[p] = first == 0xFFFFFFFFu ? s_nbo[lane] : first;   // entries [nbo, nbv) are NONE
+    if (st != TA_PAUSED) pl = v.pl;
+    d.prefix_hbm[p] = min(first, s_nbo[lane]);   // entries [nbo, nbv) are NONE
   } else if (valid) {
     d.prefix_hbm[p] = 0;
     if (MODE != 2 && v.released) d.home[p] = -1;
@@ -475,7 +484,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   }
   if (valid) {
     d.nb[p] = nbv; d.n_hbm[p] = n_h; d.n_host[p] = n_s; d.contrib[p] = cb;
-    d.rb[p] = rbv; d.hcls[p] = s_hcls[lane];
+    d.rb[p] = rbv; d.hcls[p] = s_rel[lane] ? 0 : s_hcls[lane];
   }
   // candidate bitmaps: this CTA's 32 slots are word blockIdx.x of every replica's maps
   // (whole-word stores, every word rewritten each pass); the decayed load of the actives
@@ -502,7 +511,12 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
 #define FP_GRID(N) (((N) + FP_SLOTS - 1) / FP_SLOTS)
 #define FP_BLOCK FP_THREADS
 #define FP_DSMEM FP_SMEM
-__global__ void __launch_bounds__(FP_THREADS) k_tick_front(Dev d) { footprint_cta<0>(d); }
+__global__ void __launch_bounds__(FP_THREADS, 2) k_tick_front(Dev d) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
+  kspan_begin(d, KS_FRONT, t_in);
+  footprint_cta<0>(d);
+  kspan_end(d, KS_FRONT);
+}
 __global__ void __launch_bounds__(FP_THREADS) k_footprint(Dev d, int verb) {
   if (verb) {
     footprint_cta<2>(d);

@@ -798,18 +798,24 @@ __global__ void __launch_bounds__(CTA, 1) k_restore(const __grid_constant__ Dev 
 // Steps 3 + 4 in one cooperative launch of R CTAs: CTA r's pause pass, a grid barrier,
 // the restore pass on CTA 0 (one launch less per tick than k_pause + k_restore).
 __global__ void __launch_bounds__(CTA, 1) k_pause_restore(const __grid_constant__ Dev d) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
+  kspan_begin(d, KS_PR, t_in);
   pause_pass(d, blockIdx.x, s_big, s_tmp);
   grid_sync(d, 0);
   if (blockIdx.x == 0) restore_pass(d, s_big, s_tmp);
+  kspan_end(d, KS_PR);
 }
 
 // Step 5 per replica: cluster r (PLAN_CL CTAs); verb != 0: ta_resume / ta_migrate,
 // the verb's program only.  Grid = R * PLAN_CL.
 __global__ void __cluster_dims__(PLAN_CL, 1, 1) __launch_bounds__(CTA, 1)
 k_plan(const __grid_constant__ Dev d, int verb) {
+  const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
   __shared__ u32 s_tmp[NWARP + 1];
+  kspan_begin(d, KS_PLAN, t_in);
   plan_pass(d, blockIdx.x / PLAN_CL, verb, s_big, s_tmp);
+  kspan_end(d, KS_PLAN);
 }

@@ -187,6 +187,19 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       q = res ? vb : va;
     }
     if (it < 7) PSTAMP(1, 3 + 4 * it);
+    // the entries' contribution, home and phase for the sequential loop, gathered by the
+    // whole CTA in one round trip (the keys' space is free after the sort)
+    const bool pre = n <= scap;
+    u32* s_cr = reinterpret_cast<u32*>(s_gk);
+    u32* s_hp = s_cr + SORT_SMALL;                // (home + 1) | phase << 8
+    if (pre) {
+      for (u32 i = threadIdx.x; i < n; i += CTA) {
+        const u32 p = q[i];
+        s_cr[i] = d.contrib[p];
+        s_hp[i] = (u32)(d.home[p] + 1) | ((u32)d.phase[p] << 8);
+      }
+      __syncthreads();
+    }
     if (w0) {
       bool stop = false;
       const bool pinned = (d.flags & TA_F_PINNED_ROUTING) != 0;
@@ -194,9 +207,10 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       for (u32 base = 0; base < n && !stop; base += 32) {
         u32 i = base + lane;
         u32 pl = i < n ? q[i] : 0;
-        u32 crl = i < n ? d.contrib[pl] : 0;
-        int hml = i < n ? d.home[pl] : -1;
-        u32 phl = i < n ? d.phase[pl] : 0;
+        const u32 hp = (i < n && pre) ? s_hp[i] : 0u;
+        u32 crl = i < n ? (pre ? s_cr[i] : d.contrib[pl]) : 0;
+        int hml = i < n ? (pre ? (int)(hp & 0xFF) - 1 : d.home[pl]) : -1;
+        u32 phl = i < n ? (pre ? hp >> 8 : d.phase[pl]) : 0;
         u32 mcount = min(32u, n - base);
         for (u32 jj = 0; jj < mcount; ++jj) {
           u32 cr = __shfl_sync(FULL_MASK, crl, jj);

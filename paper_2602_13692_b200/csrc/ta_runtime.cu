@@ -70,6 +70,8 @@ struct ta_ctx {
   void* peer_base[TA_MAX_REPLICAS] = {};    // IPC-opened peer pool allocations
   void* peer_mbox[TA_MAX_REPLICAS] = {};    // IPC-opened peer mailboxes
   bool split_pr = false;                    // A/B aid (env TA_SPLIT_PR at init): k_pause + k_restore
+  bool probes = false;                      // A/B aid (env TA_GAP_PROBES, timing mode): k_probe between kernels
+  bool no_events = false;                   // A/B aid (env TA_NO_EVENTS): device stamps without event nodes
 };
 
 #define FAIL(ctx, code, ...)                                          \
@@ -241,9 +243,9 @@ __global__ void k_init(Dev d) {
 }
 
 // ------------------------------------------------------------------ tick launch sequence
-static void rec(ta_ctx* x, int i) {
+static void rec(ta_ctx* x, int i, cudaStream_t s = nullptr) {
   // external event-record nodes keep working inside the captured CUDA graph
-  if (x->timing) cudaEventRecordWithFlags(x->ev[i], x->stream, cudaEventRecordExternal);
+  if (x->timing && !x->no_events) cudaEventRecordWithFlags(x->ev[i], s ? s : x->stream, cudaEventRecordExternal);
 }
 
 // dynamic shared memory of the copy kernels: the TMA staging buffer in bulk mode
@@ -282,8 +284,8 @@ static void launch_movement(ta_ctx* x, cudaStream_t s) {
     // makes the whole grid co-resident or fails the launch (never a partial grid)
     launch_coop_b(k_move_fused, x->move_grid, 256, csm(d), s, (Dev)d);
     if (d.multi) k_barrier<<<1, 32, 0, s>>>(d);
-    rec(x, 4);
-    rec(x, 5);
+    rec(x, 4, s);
+    rec(x, 5, s);
     if (d.multi && (d.flags & TA_F_FILL)) k_fill<<<kCopyGrid, 256, 0, s>>>(d);
     return;
   }
@@ -303,6 +305,7 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
   Dev& d = x->d;
   cudaStream_t s = x->stream;
   const int N = d.N, R = d.R;
+  if (x->timing) k_span_reset<<<1, 32, 0, s>>>(d);
   rec(x, 0);
   // per-tick lists and counters were cleared by the previous tick's k_assemble
   if (d.api_mode) {
@@ -317,6 +320,7 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     k_tick_front<<<FP_GRID(N), FP_BLOCK, FP_DSMEM, s>>>(d);   // ingest + footprint + load
   }
   rec(x, 1);
+  if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 0);
   if (x->split_pr) {                       // A/B aid: the two passes as separate kernels
     k_pause<<<R, CTA, PLAN_DSMEM, s>>>(d);
     k_restore<<<1, CTA, PLAN_DSMEM, s>>>(d);
@@ -324,8 +328,10 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
     launch_coop(k_pause_restore, R, PLAN_DSMEM, s, (Dev)d);
   }
   rec(x, 2);
+  if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 1);
   k_plan<<<R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 0);   // one CTA cluster per replica
   rec(x, 3);
+  if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 2);
   launch_movement(x, s);
   rec(x, 6);
   launch_coop(k_close, x->close_grid, 0, s, (Dev)d, 0);     // frees, compaction plan, decisions
@@ -530,6 +536,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   }
   if (x->timing)
     for (int i = 0; i < 10; ++i) cudaEventCreate(&x->ev[i]);
+  x->probes = x->timing && getenv("TA_GAP_PROBES") != nullptr;
+  x->no_events = getenv("TA_NO_EVENTS") != nullptr;
   *out = x;
   return TA_OK;
 }

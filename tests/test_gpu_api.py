@@ -318,3 +318,56 @@ def test_gpu_rejected_batch_after_compaction_moves_no_bytes():
             break
     assert hit >= 3
     pool.close()
+
+
+def test_gpu_api_two_shared_prompts_events_and_verbs():
+    """NEXT-3 (reading A51) in API mode: ARRIVE's t_ms names the program's prompt (two
+    prompts of 2 and 1 blocks); random legal / illegal batches, then resumes and
+    migrations (verbs materialize prompts too), against the oracle."""
+    need_gpu()
+    from paper_2602_13692_b200 import Pool
+    cfg = tracegen.get_config("c1_toy", n_replicas=2, hbm_blocks=64, host_blocks=16, max_ctx=4096,
+                              compact_every=4, shared_prefixes=[(32, "a"), (16, "b")])
+    N = 40
+    o = oracle.Oracle(cfg, api_mode=True, n_slots=N)
+    pool = Pool(cfg, N, trace_mode=False)
+    rng = random.Random(17)
+    errs = verbs = 0
+    for k in range(150):
+        T = 5000 * k
+        evs = []
+        for e in random_events(o, rng, T, illegal_p=0.05):
+            if e[0] == A:                              # prompt index in t_ms; sometimes too short
+                e = (A, e[1], e[2], rng.randint(8, 400), rng.choice((0, 1, 1, 0, 2)))
+            evs.append(e)
+        st_o, dec_o = o.sched_step(T, evs)
+        st_g, dec_g = pool.step(T, evs, raise_on_error=False)
+        assert st_o == st_g, (k, st_o, st_g, evs)
+        if st_o != oracle.OK:
+            errs += 1
+            continue
+        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        for _ in range(2):
+            p = rng.randrange(N)
+            if o.status[p] == oracle.PAUSED:
+                rep = rng.randrange(-1, 2)
+                st_o, d_o = o.resume(p, rep)
+                st_g, d_g = pool.resume(p, rep)
+                assert st_o == st_g, (k, "resume", p, st_o, st_g)
+                if st_o == oracle.OK:
+                    assert dec_tuples(d_g) == d_o
+                    verbs += 1
+            elif o.status[p] in (oracle.REASONING, oracle.ACTING):
+                rep = rng.randrange(2)
+                st_o, d_o = o.migrate(p, rep)
+                st_g, d_g = pool.migrate(p, rep)
+                assert st_o == st_g, (k, "migrate", p, st_o, st_g)
+                if st_o == oracle.OK:
+                    assert dec_tuples(d_g) == d_o
+                    verbs += 1
+        if k % 5 == 0:
+            compare_state(o, pool.debug_download(), where=f"api tick {k}")
+        bad, _ = pool.verify_content()
+        assert bad == 0
+    assert errs > 0 and o.stats["prefix_blocks"] > 0 and verbs > 0, (errs, verbs)
+    pool.close()

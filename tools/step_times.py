@@ -1,6 +1,7 @@
 """Per-step device/host timing of the bench workload (developer tool, GPU box).
 usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing] [--flush] [--mini]
 --flush: 256 MiB memset before every tick (outside the timed pair); --mini: 4 KiB-block KV shape"""
+import os
 import sys
 import time
 
@@ -33,7 +34,7 @@ for k in range(ticks):
     e1.record(s)
     e1.synchronize()
     t1 = time.perf_counter()
-    ph = pool.phase_times() if flags & binding.F_TIMING else [0.0] * 9
+    ph = pool.phase_times() if flags & binding.F_TIMING and not os.environ.get("TA_NO_EVENTS") else [0.0] * 9
     st = pool.stats()
     d2h = st["evict_to_host"] - prev["evict_to_host"]
     h2d = st["h2d_blocks"] - prev["h2d_blocks"]
@@ -44,6 +45,7 @@ for k in range(ticks):
     if "--phases" in sys.argv:
         print("   phases us: " + " ".join(f"{x:.1f}" for x in ph))
         st = pool.phase_stamps(absolute=True)       # in-kernel globaltimer stamps (ns), one origin
+        print("   spans    : " + "  ".join(f"{n} {b:.1f}-{e:.1f}" for n, b, e in st.pop("spans", [])))
         for kname, v in st.items():
             print(f"   {kname:9s}: " + " ".join(f"{i}:{c / 1e3:.1f}" if isinstance(i, int) else f"{i}={c}"
                                                  for i, c in v))
