@@ -687,12 +687,14 @@ __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, 
       }
     }
   }
-  u32 vv[SORT_SMALL / CTA];                     // read every value before any write (in place)
+  // keys first (nothing reads the key array any more: its reads preceded the network's
+  // barriers / shuffles); the values through the scratch buffer the network read last
+  // two barriers ago (every value read before any is written: in place is allowed)
   if (act) {
 #pragma unroll
     for (int e = 0; e < SORT_SMALL / CTA; ++e) {
       const int i = t + e * CTA;
-      vv[e] = (e < E && i < n) ? va[p[e]] : 0u;
+      if (e < E && i < n) { kb[i] = k[e]; sm->p[buf][i] = va[p[e]]; }
     }
   }
   __syncthreads();
@@ -700,7 +702,7 @@ __device__ int cta_sort(u64* ka, u32* va, u64* kb, u32* vb, int n, u32* s_hist, 
 #pragma unroll
     for (int e = 0; e < SORT_SMALL / CTA; ++e) {
       const int i = t + e * CTA;
-      if (e < E && i < n) { kb[i] = k[e]; vb[i] = vv[e]; }
+      if (e < E && i < n) vb[i] = sm->p[buf][i];
     }
   }
   __syncthreads();
