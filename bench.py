@@ -502,6 +502,7 @@ def main():
     e2e_ms = max_over_ranks(e2e_ms)
     e2e_value = K * progs_total / 1e4 / (e2e_ms * 1e-3)
 
+
     # ---- host-link peaks of this run: one GPU alone (rank 0), and with N > 1 every rank
     # copying at once (GPUs share host-side PCIe / memory bandwidth): the movement floor
     # uses the concurrent figure of the slowest rank
@@ -605,6 +606,8 @@ def main():
         "compaction": ({"gbs_rw": round(2 * mv["d2d"] / (ph_sum[7] * 1e-6) / G, 1),
                         "frac_hbm": round(mv["d2d_floor_s"] / (ph_sum[7] * 1e-6), 4)}
                        if mv["d2d"] > 0 and ph_sum[7] > 0 else None),
+        "compaction_in_trace": "bench_10k never compacts (its pool stays full); in-trace D2D is "
+                               "measured on configs[1] by tools/compaction_trace.py (DESIGN.md 6.1)",
         "host_link_peaks_gbs": peaks,
     }
     tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.sched_start, args.sched_ticks, flush)
