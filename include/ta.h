@@ -91,12 +91,17 @@ enum {
   TA_F_REQUEST_AWARE = 1u << 7, /* baseline (NEXT-2): stateless request-level engine -- running
                                   requests preempted latest program first, FCFS waiting queue, LRU
                                   eviction of idle caches; pass an all-zero decay table (A46) */
-  TA_F_SMALL_PATHS = 1u << 8    /* test aid: lower the size thresholds of the shared-memory fast
+  TA_F_SMALL_PATHS = 1u << 8,   /* test aid: lower the size thresholds of the shared-memory fast
                                   paths (CTA sort 4096 -> 64, rank sort 512 -> 16, staged planner
                                   lists 4096 / 8192 / 1024 -> 8 / 8 / 4, candidate slot lists in
                                   shared memory 12288 / 8192 -> 8, restore chunks 32..4096 -> 4..64, restore buckets <= 8) so that
                                   small runs take the code paths of full-size runs.  Results are
                                   identical; only the speed differs. */
+  TA_F_DECIDE_ONLY = 1u << 9    /* measurement aid: the tick runs steps 0-5 and 7 (decisions,
+                                  block tables, free sets, statistics) but issues no block copy
+                                  (no step 6, no compaction copies): the pools' bytes are not
+                                  maintained.  Decisions are identical (none depends on bytes);
+                                  it times the decision path alone.  Single process only. */
 };
 
 typedef struct {

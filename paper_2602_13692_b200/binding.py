@@ -22,6 +22,7 @@ TA_E_ILLEGAL_TRANSITION, TA_E_CAPACITY, TA_E_TRUNCATED, TA_E_CUDA, TA_E_PEER, TA
 F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE, F_PINNED_ROUTING = 1, 2, 4, 8, 16, 32, 64
 F_REQUEST_AWARE = 128
 F_SMALL_PATHS = 256                  # test aid: small runs take the full-size code paths
+F_DECIDE_ONLY = 512                  # measurement aid: decisions without block copies
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",

@@ -5,7 +5,8 @@
 
 // Deferred frees (P2P sources and fetched host slots become free only after the
 // movement, reading A16) and the per-program results of step 5.7.
-__device__ __forceinline__ void finalize_part(const Dev& d, int verb, int first_cta) {
+template <int verb>
+__device__ __forceinline__ void finalize_part(const Dev& d, int first_cta) {
   const int t = ((int)blockIdx.x - first_cta) * blockDim.x + threadIdx.x;
   const int stride = ((int)gridDim.x - first_cta) * blockDim.x;
   for (int r = 0; r < d.R; ++r) {
@@ -156,7 +157,8 @@ __device__ __forceinline__ u32 assemble_records(const Dev& d, u32* s_tmp) {
   return pos;
 }
 
-__device__ __forceinline__ void assemble_close(const Dev& d, int verb, u32 pos) {
+template <int verb>
+__device__ __forceinline__ void assemble_close(const Dev& d, u32 pos) {
   __shared__ ull s_red[NWARP];
   const int R = d.R;
   const u32 cap = d.dec_cap;
@@ -243,7 +245,8 @@ __device__ __forceinline__ void assemble_close(const Dev& d, int verb, u32 pos) 
 // CTAs, grid barrier, the two-finger compaction plan (CTA r, on compaction ticks),
 // grid barrier, the canonical decision list and statistics on CTA 0.  The
 // compaction copies (k_copy_compact) run after this kernel.
-__global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d, int verb) {
+template <int verb>   // 0: tick, 1: verbs (a kernel of its own)
+__global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d) {
   const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   u32 pos = 0;
   if (blockIdx.x == 0) pos = assemble_records(d, s_tmp);
   PSTAMP(3, 5);
-  if (gridDim.x == 1 || blockIdx.x > 0) finalize_part(d, verb, gridDim.x == 1 ? 0 : 1);
+  if (gridDim.x == 1 || blockIdx.x > 0) finalize_part<verb>(d, gridDim.x == 1 ? 0 : 1);
   PSTAMP(3, 1);
   grid_sync(d, 1);
   PSTAMP(3, 2);
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d,
   if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) grid_sync(d, 1);   // plans -> decisions
   else __syncthreads();
   PSTAMP(3, 4);
-  if (blockIdx.x == 0) assemble_close(d, verb, pos);
+  if (blockIdx.x == 0) assemble_close<verb>(d, pos);
   PSTAMP(3, 9);
   kspan_end(d, KS_CLOSE);
 }

@@ -105,7 +105,11 @@ __device__ __forceinline__ void cl_copy_segs(const CpSeg (&sg)[K]) {
   }
 }
 
-__device__ __forceinline__ void plan_pass(const Dev& d, const int r, const int verb, u32* s_big, u32* s_tmp) {
+// VERB (compile time): 0 = tick, 1 = ta_resume / ta_migrate (each a kernel of its own,
+// so the tick kernel carries no verb code)
+template <int VERB>
+__device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big, u32* s_tmp) {
+  constexpr int verb = VERB;
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const u32 crank = cl.block_rank();
@@ -810,12 +814,13 @@ __global__ void __launch_bounds__(CTA, 1) k_pause_restore(const __grid_constant_
 
 // Step 5 per replica: cluster r (PLAN_CL CTAs); verb != 0: ta_resume / ta_migrate,
 // the verb's program only.  Grid = R * PLAN_CL.
+template <int VERB>
 __global__ void __cluster_dims__(PLAN_CL, 1, 1) __launch_bounds__(CTA, 1)
-k_plan(const __grid_constant__ Dev d, int verb) {
+k_plan(const __grid_constant__ Dev d) {
   const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
   __shared__ u32 s_tmp[NWARP + 1];
   kspan_begin(d, KS_PLAN, t_in);
-  plan_pass(d, blockIdx.x / PLAN_CL, verb, s_big, s_tmp);
+  plan_pass<VERB>(d, blockIdx.x / PLAN_CL, s_big, s_tmp);
   kspan_end(d, KS_PLAN);
 }

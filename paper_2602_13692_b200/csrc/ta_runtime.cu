@@ -131,6 +131,8 @@ static const char* validate(const ta_config* c) {
       return "prefix_tokens must be positive multiples of block_tokens, below hbm_blocks blocks";
   if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (uint64_t)TA_OWNER_PROMPT)
     return "max_programs * max_blocks_per_program must be below TA_OWNER_PROMPT";
+  if ((c->flags & TA_F_DECIDE_ONLY) && c->replicas_here < c->n_replicas)
+    return "TA_F_DECIDE_ONLY is single-process only";
   return nullptr;
 }
 
@@ -329,14 +331,15 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
   }
   rec(x, 2);
   if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 1);
-  k_plan<<<R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 0);   // one CTA cluster per replica
+  k_plan<0><<<R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d);   // one CTA cluster per replica
   rec(x, 3);
   if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 2);
-  launch_movement(x, s);
+  const bool copies = !(d.flags & TA_F_DECIDE_ONLY);
+  if (copies) launch_movement(x, s);
   rec(x, 6);
-  launch_coop(k_close, x->close_grid, 0, s, (Dev)d, 0);     // frees, compaction plan, decisions
+  launch_coop(k_close<0>, x->close_grid, 0, s, (Dev)d);     // frees, compaction plan, decisions
   rec(x, 7);
-  if (d.compact_every > 0) k_copy_compact<<<kCopyGrid, 256, csm(d), s>>>(d);
+  if (copies && d.compact_every > 0) k_copy_compact<<<kCopyGrid, 256, csm(d), s>>>(d);
   rec(x, 8);
   rec(x, 9);
   return cudaGetLastError();
@@ -523,7 +526,8 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pause_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_plan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ev_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DSMEM);
   if (e == cudaSuccess && FP_DSMEM > 48 * 1024) e = cudaFuncSetAttribute(k_tick_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_DSMEM);
   if (e == cudaSuccess && FP_DSMEM > 48 * 1024) e = cudaFuncSetAttribute(k_footprint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FP_DSMEM);
@@ -847,7 +851,7 @@ ta_status ta_pause(ta_ctx* ctx, uint32_t pid, uint32_t mode, ta_decision* out, i
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_verb_pause<<<1, CTA, 0, s>>>(d, pid, mode);
   launch_movement(ctx, ctx->stream);
-  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
+  launch_coop(k_close<1>, ctx->close_grid, 0, s, (Dev)d);
   return verb_finish(ctx, "ta_pause", out, out_cap, n_out);
 }
 
@@ -862,10 +866,10 @@ static ta_status activate(ta_ctx* ctx, uint32_t pid, int32_t replica, int migrat
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_footprint<<<FP_GRID(N), FP_BLOCK, FP_DSMEM, s>>>(d, 1);
   k_verb_admit<<<1, 32, 0, s>>>(d, pid, replica, migrate);
-  k_plan<<<d.R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d, 1);
+  k_plan<1><<<d.R * PLAN_CL, CTA, PLAN_DSMEM, s>>>(d);
   k_verb_commit<<<1, 32, 0, s>>>(d, migrate);
   launch_movement(ctx, ctx->stream);
-  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
+  launch_coop(k_close<1>, ctx->close_grid, 0, s, (Dev)d);
   return verb_finish(ctx, migrate ? "ta_migrate" : "ta_resume", out, out_cap, n_out);
 }
 
@@ -892,7 +896,7 @@ ta_status ta_set_health(ta_ctx* ctx, int32_t replica, int32_t healthy, ta_decisi
   cudaStream_t s = ctx->stream;
   k_verb_reset<<<1, 32, 0, s>>>(d);
   k_verb_health<<<1, CTA, 0, s>>>(d, replica);
-  launch_coop(k_close, ctx->close_grid, 0, s, (Dev)d, 1);
+  launch_coop(k_close<1>, ctx->close_grid, 0, s, (Dev)d);
   return verb_finish(ctx, "ta_set_health", out, out_cap, n_out);
 }
 

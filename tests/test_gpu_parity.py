@@ -228,3 +228,15 @@ def test_gpu_shared_prefix_configs3_full_n():
     cfg = tracegen.get_config("c3_mixed", kv="mini", shared_prefix_tokens=960)
     o, n = run_parity(cfg, 20, state_every=4, content_every=4, samples=8)
     assert n > 0 and o.sbk == [60]
+
+
+@pytest.mark.gpu
+def test_gpu_decide_only_same_decisions():
+    """TA_F_DECIDE_ONLY (the bench's decision-latency probe: no block copies): decisions,
+    block tables, free sets, owners and statistics still equal the oracle's tick by tick
+    (no decision depends on bytes); the pools' contents are not checked."""
+    need_gpu()
+    from paper_2602_13692_b200 import binding
+    for seed, R in ((41, 1), (42, 3)):
+        run_parity(stress(seed, R, compact=4), 200, state_every=2, seed=seed, fill=False,
+                   flags=binding.F_DECIDE_ONLY)

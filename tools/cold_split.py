@@ -48,6 +48,7 @@ def main():
         us = []
         for _ in range(n):
             with torch.cuda.stream(s):
+                torch.cuda._sleep(1_000_000)        # host submission ahead of the GPU (bench.py)
                 if mode != "warm":
                     flush.zero_()
                 if mode == "data":

@@ -1,6 +1,6 @@
 """Per-kernel device times of the decision path (developer tool, GPU box).
 
-usage: python tools/tick_phases.py [--config bench_10k] [--start 13] [--ticks 100] [--tile R]
+usage: python tools/tick_phases.py [--config bench_10k] [--start 13] [--ticks 100] [--tile R] [--decide-only]
 
 Runs the full ta_sched_step graph with TA_F_TIMING on the decision-identical `mini` KV
 shape (no decision depends on bytes per block), the L2 flushed before every tick, and
@@ -36,8 +36,9 @@ def main():
     out = {"lib": os.environ.get("TA_LIB", "libta.so"), "config": name, "replicas": tile, "programs": tr.n_slots,
            "ticks": f"{start}..{start + n - 1}"}
     for mode in ("timing", "plain"):
+        extra = binding.F_DECIDE_ONLY if "--decide-only" in sys.argv else 0
         pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False,
-                    flags=binding.F_TIMING if mode == "timing" else 0)
+                    flags=(binding.F_TIMING if mode == "timing" else 0) | extra)
         pool.load_trace(tr)
         s = pool.stream
         for _ in range(start):
@@ -45,6 +46,7 @@ def main():
         rows = []
         for _ in range(n):
             with torch.cuda.stream(s):
+                torch.cuda._sleep(1_000_000)        # host submission ahead of the GPU (bench.py)
                 flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
