@@ -201,9 +201,19 @@ enum DbgIdx {
 __device__ __forceinline__ void dbg_hit(const Dev& d, int i) {
   if (threadIdx.x == 0) atomicAdd(&d.dbg[i], 1ull);
 }
+// Per-context option flags read by the tick kernels.  TA_PROD_VARIANT (developer A/B
+// build) compiles the measurement / baseline / test options out: timing stamps,
+// PinnedRouting, RequestAware, small paths.
+#ifdef TA_PROD_VARIANT
+#define TA_FLAG(d, f) ((((f) & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS)) == 0) && \
+                       (((d).flags & (f)) != 0))
+#else
+#define TA_FLAG(d, f) (((d).flags & (f)) != 0)
+#endif
+
 // Size thresholds of the shared-memory fast paths.  TA_F_SMALL_PATHS (test aid) lowers
 // them so that toy-sized runs take the branches of full-size runs.
-__device__ __forceinline__ bool small_paths(const Dev& d) { return (d.flags & TA_F_SMALL_PATHS) != 0; }
+__device__ __forceinline__ bool small_paths(const Dev& d) { return TA_FLAG(d, TA_F_SMALL_PATHS); }
 
 // Barrier across the CTAs of a cooperative launch (all co-resident).  Counter k is
 // used by one kernel only and grows by gridDim.x per barrier, so arrival t waits for
@@ -257,13 +267,13 @@ __device__ __forceinline__ ull gtimer() {
 }
 #define PSTAMP(kk, i)                                                              \
   do {                                                                             \
-    if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x == 0)            \
+    if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x == 0)            \
       d.pst[(kk) * 32 + (i)] = gtimer();                                           \
   } while (0)
 // the same from thread 0 of block `b` into kernel slot kk (cluster ranks of k_plan)
 #define PSTAMP_B(kk, b, i)                                                         \
   do {                                                                             \
-    if ((d.flags & TA_F_TIMING) && blockIdx.x == (b) && threadIdx.x == 0)          \
+    if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == (b) && threadIdx.x == 0)          \
       d.pst[(kk) * 32 + (i)] = gtimer();                                           \
   } while (0)
 
@@ -274,10 +284,10 @@ __device__ __forceinline__ ull gtimer() {
 // 5 compaction.
 enum { KS_FRONT = 0, KS_PR = 1, KS_PLAN = 2, KS_MOVE = 3, KS_CLOSE = 4, KS_COMPACT = 5, KS_N = 6 };
 __device__ __forceinline__ void kspan_begin(const Dev& d, int k, ull t_in) {
-  if ((d.flags & TA_F_TIMING) && threadIdx.x == 0) atomicMin(d.pst + 3 * 32 + 16 + 2 * k, t_in);
+  if (TA_FLAG(d, TA_F_TIMING) && threadIdx.x == 0) atomicMin(d.pst + 3 * 32 + 16 + 2 * k, t_in);
 }
 __device__ __forceinline__ void kspan_end(const Dev& d, int k) {
-  if ((d.flags & TA_F_TIMING) && (threadIdx.x & 31) == 0) atomicMax(d.pst + 3 * 32 + 17 + 2 * k, gtimer());
+  if (TA_FLAG(d, TA_F_TIMING) && (threadIdx.x & 31) == 0) atomicMax(d.pst + 3 * 32 + 17 + 2 * k, gtimer());
 }
 
 // ------------------------------------------------------------------ helpers
@@ -321,7 +331,7 @@ __device__ __forceinline__ i64 trace_arrivals(const Dev& d) {
 
 // Coarse restore bucket (monotone in the S_restore key): tau = R first, then nb.
 __device__ __forceinline__ u32 restore_bucket(const Dev& d, u8 ph, u32 nbv) {
-  if (d.flags & TA_F_REQUEST_AWARE) return 0;        // FCFS key: one bucket
+  if TA_FLAG(d, TA_F_REQUEST_AWARE) return 0;        // FCFS key: one bucket
   return (u32)(ph == TA_PHASE_A) * d.nbk + (nbv >> d.nb_shift);
 }
 
@@ -895,9 +905,12 @@ __device__ void cta_bitmap_prefix(const u32* words, int nw, u32* s_pre, u32* s_t
   int chunk = (nw + CTA - 1) / CTA;
   int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
   u32 s = 0;
+  // one word per thread up to 32K-word bitmaps: rolled loops (compact code, see DESIGN 6.2)
+#pragma unroll 1
   for (int i = lo; i < hi; ++i) s += __popc(words[i]);
   u32 total;
   u32 run = cta_excl_scan(s, s_tmp, &total);
+#pragma unroll 1
   for (int i = lo; i < hi; ++i) { s_pre[i] = run; run += __popc(words[i]); }
   if (threadIdx.x == 0) s_pre[nw] = total;
   __syncthreads();
@@ -923,10 +936,12 @@ __device__ u32 cta_bits_to_list(const u32* words, int nw, u32* s_out, u32 s_cap,
   const int chunk = (nw + CTA - 1) / CTA;
   const int lo = threadIdx.x * chunk, hi = min(nw, lo + chunk);
   u32 cnt = 0;
+#pragma unroll 1
   for (int w = lo; w < hi; ++w) cnt += __popc(words[w]);
   u32 total;
   u32 pos = cta_excl_scan(cnt, s_tmp, &total);
   u32* dst = total <= s_cap ? s_out : g_out;
+#pragma unroll 1
   for (int w = lo; w < hi; ++w) {
     u32 m = words[w];
     while (m) {

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d)
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
-  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 16) d.pst[3 * 32 + threadIdx.x] = 0;
+  if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 16) d.pst[3 * 32 + threadIdx.x] = 0;
   kspan_begin(d, KS_CLOSE, t_in);
   PSTAMP(3, 0);
   // CTA 0 assembles the records of steps 3-5 while the other CTAs finalize (one CTA: both)

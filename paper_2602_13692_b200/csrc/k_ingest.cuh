@@ -323,7 +323,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   const int p0 = blockIdx.x * FP_SLOTS;
   const int p = p0 + lane;
   const bool w0 = warp == 0;
-  if (MODE == 0 && (d.flags & TA_F_TIMING) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x < 32)
+  if (MODE == 0 && TA_FLAG(d, TA_F_TIMING) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x < 32)
     d.pst[(blockIdx.x == 0 ? 6 : 7) * 32 + threadIdx.x] = 0;
   if (MODE == 0) { PSTAMP_B(6, 0, 0); PSTAMP_B(7, gridDim.x - 1, 0); }
   const i64 T = MODE == 0 ? d.ctr->tick * d.dt : (MODE == 1 ? d.ctr->now_ms : d.ctr->T);

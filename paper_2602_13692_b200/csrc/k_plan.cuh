@@ -149,8 +149,8 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
   if (verb && (r != d.ctr->verb_replica || d.ctr->err != TA_OK ||
                d.status[d.ctr->verb_pid] != TA_REASONING)) return;   // phase-A restores move no bytes
-  if ((d.flags & TA_F_TIMING) && r == 0 && lead && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
-  if ((d.flags & TA_F_TIMING) && (blockIdx.x == 1 || blockIdx.x == 3) && threadIdx.x < 32)
+  if (TA_FLAG(d, TA_F_TIMING) && r == 0 && lead && threadIdx.x < 32) d.pst[2 * 32 + threadIdx.x] = 0;
+  if (TA_FLAG(d, TA_F_TIMING) && (blockIdx.x == 1 || blockIdx.x == 3) && threadIdx.x < 32)
     d.pst[(blockIdx.x == 1 ? 4 : 5) * 32 + threadIdx.x] = 0;
   PSTAMP_B(4, 1, 0); PSTAMP_B(5, 3, 0);
   PSTAMP(2, 0);
@@ -306,7 +306,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
         u8 s = d.status[i];
         return s == TA_PAUSED || s == TA_ACTING;
       };
-      const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware: LRU (A46)
+      const bool ra = TA_FLAG(d, TA_F_REQUEST_AWARE);   // RequestAware: LRU (A46)
       auto ebucket = [&](int i) -> u32 {
         if (ra) return 0u;
         if (d.status[i] == TA_PAUSED)    // group 0: A first, nb descending
@@ -346,7 +346,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
             }
           });
       PSTAMP(2, 4);
-      if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+      if (TA_FLAG(d, TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
         d.pst[2 * 32 + 27] = ne | (1ull << 62);
         d.pst[2 * 32 + 28] = X | (1ull << 62);
       }
@@ -497,7 +497,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
       }
     }
     PSTAMP(2, 10);
-    if ((d.flags & TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
+    if (TA_FLAG(d, TA_F_TIMING) && r == 0 && threadIdx.x == 0) {
       d.pst[2 * 32 + 29] = nF | (1ull << 62);
       d.pst[2 * 32 + 30] = sh.tot | (1ull << 62);
     }

@@ -17,7 +17,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
   SortSmem* sm = reinterpret_cast<SortSmem*>(dsm);
   __shared__ ull s_L;
   if (d.ctr->err != TA_OK) return;              // API batch rejected: the tick does not run
-  if ((d.flags & TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[threadIdx.x] = 0;
+  if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 32) d.pst[threadIdx.x] = 0;
   PSTAMP(0, 0);
   if (threadIdx.x == 0) {                       // publish this tick's load (eq. 7) of replica r
     s_L = d.Lacc[r];
@@ -52,7 +52,7 @@ __device__ __forceinline__ void pause_pass(const Dev& d, const int r, u32* s_big
                                        d.act_list + (size_t)r * N, s_tmp, &al);
   if ((u32)na > lcap) dbg_hit(d, DBG_LIST_GLOBAL);
   PSTAMP(0, 1);
-  const bool ra = (d.flags & TA_F_REQUEST_AWARE) != 0;   // RequestAware baseline (A46)
+  const bool ra = TA_FLAG(d, TA_F_REQUEST_AWARE);   // RequestAware baseline (A46)
   auto bucket = [&](int i) { return ra ? 0u : (u32)(d.phase[i] == TA_PHASE_R) * NBK + (d.nb[i] >> sh); };
   const u32 T = cta_list_threshold(al, na, 2 * NBK, 0, dC, s_big, s_tmp, [](int) { return true; }, bucket,
                                    [&](int i) { return d.contrib[i]; });
@@ -129,7 +129,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       maxcap = t > maxcap ? t : maxcap;
     }
   }
-  if ((d.flags & TA_F_TIMING) && threadIdx.x < 32) d.pst[1 * 32 + threadIdx.x] = 0;
+  if (TA_FLAG(d, TA_F_TIMING) && threadIdx.x < 32) d.pst[1 * 32 + threadIdx.x] = 0;
   PSTAMP(1, 0);
   if (!d.api_mode) {                   // closed-loop trace arrivals (reading A12):
     const i64 na = d.ctr->next_arrival;  // the lowest UNARRIVED slots, one per release
@@ -169,13 +169,13 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     u32 n = cta_ordered_gather_w(N, s_tmp,
         [&](int i) { const u32 b = d.rb[i]; return b >= lo && b <= T; },
         [&](u32 pos, int i, u32 total) {
-          const u64 key = (d.flags & TA_F_REQUEST_AWARE) ? (u64)d.paused_since[i]            // FCFS (A46)
+          const u64 key = TA_FLAG(d, TA_F_REQUEST_AWARE) ? (u64)d.paused_since[i]            // FCFS (A46)
                                                          : restore_key(d.phase[i], d.nb[i], d.paused_since[i]);
           if (total <= scap) { s_gk[pos] = key; s_gv[pos] = (u32)i; }
           else { ka[pos] = key; va[pos] = (u32)i; }
         });
     if (it < 7) PSTAMP(1, 2 + 4 * it);
-    if ((d.flags & TA_F_TIMING) && threadIdx.x == 0 && it < 4) d.pst[1 * 32 + 27 + it] = n | (1ull << 62);
+    if (TA_FLAG(d, TA_F_TIMING) && threadIdx.x == 0 && it < 4) d.pst[1 * 32 + 27 + it] = n | (1ull << 62);
     const u32* q;
     if (n <= scap) {
       const int res = cta_sort(s_gk, s_gv, s_gk, s_gv, (int)n, s_big, s_tmp, sm, sort_lim(d));
@@ -202,7 +202,7 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
     }
     if (w0) {
       bool stop = false;
-      const bool pinned = (d.flags & TA_F_PINNED_ROUTING) != 0;
+      const bool pinned = TA_FLAG(d, TA_F_PINNED_ROUTING);
       const u32 all_r = R >= 32 ? 0xFFFFFFFFu : ((1u << R) - 1);
       for (u32 base = 0; base < n && !stop; base += 32) {
         u32 i = base + lane;

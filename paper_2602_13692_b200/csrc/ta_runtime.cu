@@ -335,7 +335,12 @@ static cudaError_t launch_tick(ta_ctx* x, int) {
   rec(x, 3);
   if (x->probes) k_probe<<<1, 32, 0, s>>>(d, 2);
   const bool copies = !(d.flags & TA_F_DECIDE_ONLY);
-  if (copies) launch_movement(x, s);
+  if (copies) {
+    launch_movement(x, s);
+  } else {
+    rec(x, 4);
+    rec(x, 5);
+  }
   rec(x, 6);
   launch_coop(k_close<0>, x->close_grid, 0, s, (Dev)d);     // frees, compaction plan, decisions
   rec(x, 7);
