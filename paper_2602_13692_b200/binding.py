@@ -12,8 +12,11 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# TA_LIB: developer A/B aid (a variant built with build.py --out, inside this package)
+# libta.so: the product build; libta_dev.so: the same sources with the development
+# options compiled in (DEV_FLAGS; build.py).  TA_LIB: developer A/B aid (a variant of
+# the product build made with build.py --out, inside this package).
 LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("TA_LIB", "libta.so")))
+LIB_DEV_PATH = os.path.join(HERE, "libta_dev.so")
 MAXR = 32
 HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 
@@ -23,6 +26,7 @@ F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE, F_PINNED_ROU
 F_REQUEST_AWARE = 128
 F_SMALL_PATHS = 256                  # test aid: small runs take the full-size code paths
 F_DECIDE_ONLY = 512                  # measurement aid: decisions without block copies
+DEV_FLAGS = F_TIMING | F_PINNED_ROUTING | F_REQUEST_AWARE | F_SMALL_PATHS   # need libta_dev.so
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",
@@ -116,16 +120,17 @@ class StateView(C.Structure):
     _fields_ = [(n, C.POINTER(t)) for n, t in _VIEW_FIELDS]
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    """Load libta.so (fails loudly: there is no fallback path)."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2602_13692_b200.build`")
-        L = C.CDLL(LIB_PATH)
+def lib(dev: bool = False):
+    """Load libta.so, or libta_dev.so with dev=True (fails loudly: there is no fallback
+    path)."""
+    path = LIB_DEV_PATH if dev else LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `python -m paper_2602_13692_b200.build`")
+        L = C.CDLL(path)
         vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
         sig = {
             "ta_workspace_bytes": [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)],
@@ -157,8 +162,8 @@ def lib():
         L.ta_last_error.argtypes = [vp]
         L.ta_last_error.restype = C.c_char_p
         L.ta_abi_version.restype = C.c_int32
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 EXPORTED = ("ta_workspace_bytes", "ta_block_bytes", "ta_init_pool", "ta_load_trace", "ta_sched_step",
@@ -245,7 +250,6 @@ class Pool:
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libta needs a CUDA device (no CPU fallback)")
-        L = lib()
         self.torch = torch
         self.cfg = dict(cfg)
         if host_blocks is not None:
@@ -253,6 +257,7 @@ class Pool:
         self.device = torch.device("cuda", device)
         self.c = make_config(self.cfg, n_programs, max_turns, trace_mode, fill, flags,
                              replicas_here, first_replica)
+        L = self.L = lib(dev=(self.c.flags & DEV_FLAGS) != 0)
         dev_b, host_b, blk = C.c_size_t(), C.c_size_t(), C.c_size_t()
         self._chk(L.ta_workspace_bytes(C.byref(self.c), C.byref(dev_b), C.byref(host_b)), "workspace")
         L.ta_block_bytes(C.byref(self.c), C.byref(blk))
@@ -296,9 +301,10 @@ class Pool:
         self.close()
         if flags is not None:
             self.c.flags = flags
+            self.L = lib(dev=(self.c.flags & DEV_FLAGS) != 0)
         self.ctx = C.c_void_p()
         with torch.cuda.device(self.device):
-            st = lib().ta_init_pool(C.byref(self.c), C.byref(self.buffers),
+            st = self.L.ta_init_pool(C.byref(self.c), C.byref(self.buffers),
                                     C.c_void_p(self.stream.cuda_stream), None, C.byref(self.ctx))
         if st != TA_OK:
             raise TAError(st, "ta_init_pool (reset) failed")
@@ -306,12 +312,12 @@ class Pool:
     # ------------------------------------------------------------------ helpers
     def _chk(self, st, what):
         if st != TA_OK:
-            msg = lib().ta_last_error(self.ctx).decode() if getattr(self, "ctx", None) else ""
+            msg = self.L.ta_last_error(self.ctx).decode() if getattr(self, "ctx", None) else ""
             raise TAError(st, f"{what}: {msg}")
 
     def close(self):
         if getattr(self, "ctx", None) and self.ctx.value:
-            lib().ta_destroy(self.ctx)
+            self.L.ta_destroy(self.ctx)
             self.ctx = C.c_void_p()
 
     def __del__(self):
@@ -332,7 +338,7 @@ class Pool:
         from tracegen import prefix_ids  # input data: each slot's shared prompt (NEXT-3)
         self._trace_kp = np.ascontiguousarray(prefix_ids(self.cfg, tr), dtype=np.uint8)
         v.prefix_id = self._trace_kp.ctypes.data_as(C.POINTER(C.c_uint8))
-        self._chk(lib().ta_load_trace(self.ctx, C.byref(v)), "ta_load_trace")
+        self._chk(self.L.ta_load_trace(self.ctx, C.byref(v)), "ta_load_trace")
 
     def step(self, now_ms: int = -1, events=None, decisions: bool = True, raise_on_error=True):
         """One ta_sched_step.  Returns (status, decisions ndarray or None)."""
@@ -350,10 +356,10 @@ class Pool:
             evp, n_ev = arr, len(events)
         n_out = C.c_int32(0)
         if decisions:
-            st = lib().ta_sched_step(self.ctx, now_ms, evp, n_ev, self.dec_buf.ctypes.data,
+            st = self.L.ta_sched_step(self.ctx, now_ms, evp, n_ev, self.dec_buf.ctypes.data,
                                      len(self.dec_buf), C.byref(n_out))
         else:
-            st = lib().ta_sched_step(self.ctx, now_ms, evp, n_ev, None, 0, None)
+            st = self.L.ta_sched_step(self.ctx, now_ms, evp, n_ev, None, 0, None)
         if st not in (TA_OK,) and raise_on_error and st in (TA_E_CUDA, TA_E_PEER, TA_E_INVAL, TA_E_STATE):
             self._chk(st, "ta_sched_step")
         if not decisions or st != TA_OK:
@@ -368,20 +374,20 @@ class Pool:
         return st, (self.dec_buf[:n_out.value].copy() if st == TA_OK else None)
 
     def pause(self, pid, mode=0):
-        return self._verb(lib().ta_pause, pid, mode)
+        return self._verb(self.L.ta_pause, pid, mode)
 
     def resume(self, pid, replica=-1):
-        return self._verb(lib().ta_resume, pid, replica)
+        return self._verb(self.L.ta_resume, pid, replica)
 
     def migrate(self, pid, dst):
-        return self._verb(lib().ta_migrate, pid, dst)
+        return self._verb(self.L.ta_migrate, pid, dst)
 
     def set_health(self, replica, healthy):
-        return self._verb(lib().ta_set_health, replica, 1 if healthy else 0)
+        return self._verb(self.L.ta_set_health, replica, 1 if healthy else 0)
 
     def stats(self) -> dict:
         s = Stats()
-        self._chk(lib().ta_stats(self.ctx, C.byref(s)), "ta_stats")
+        self._chk(self.L.ta_stats(self.ctx, C.byref(s)), "ta_stats")
         out = {k: getattr(s, k) for k in STAT_KEYS + LEDGER_KEYS}
         out["L"] = list(s.L[:self.R])
         out["hbm_used"] = list(s.hbm_used[:self.R])
@@ -390,17 +396,17 @@ class Pool:
         return out
 
     def set_copy_bulk(self, on: bool):
-        self._chk(lib().ta_set_copy_bulk(self.ctx, 1 if on else 0), "ta_set_copy_bulk")
+        self._chk(self.L.ta_set_copy_bulk(self.ctx, 1 if on else 0), "ta_set_copy_bulk")
 
     def last_tick(self) -> dict:
         t = TickInfo()
-        self._chk(lib().ta_last_tick(self.ctx, C.byref(t)), "ta_last_tick")
+        self._chk(self.L.ta_last_tick(self.ctx, C.byref(t)), "ta_last_tick")
         return {k: (list(getattr(t, k))[:self.R] if k.endswith(("_of", "_to")) else getattr(t, k))
                 for k, _ in TickInfo._fields_}
 
     def phase_times(self):
         a = (C.c_float * 9)()
-        self._chk(lib().ta_phase_times(self.ctx, a, 9), "ta_phase_times")
+        self._chk(self.L.ta_phase_times(self.ctx, a, 9), "ta_phase_times")
         return list(a)
 
     def phase_stamps(self, absolute: bool = False):
@@ -408,7 +414,7 @@ class Pool:
         {kernel: [(phase index, ns since that kernel's first stamp), ...]}; plan_cta1 / plan_cta3
         are cluster ranks 1 and 3 of replica 0's planner cluster."""
         a = (C.c_uint64 * 256)()
-        self._chk(lib().ta_debug_phase_stamps(self.ctx, a, 256), "ta_debug_phase_stamps")
+        self._chk(self.L.ta_debug_phase_stamps(self.ctx, a, 256), "ta_debug_phase_stamps")
         out = {}
         names = ("pause", "restore", "plan", "close", "plan_cta1", "plan_cta3", "front_cta0", "front_last")
         # kernel spans (first CTA start, last thread-0 exit) live in slot 3, entries 16..27
@@ -443,12 +449,12 @@ class Pool:
     def debug_counters(self) -> dict:
         """Size-branch counters (ta_debug_counters): how often each large-size path ran."""
         a = (C.c_uint64 * 16)()
-        self._chk(lib().ta_debug_counters(self.ctx, a, 16), "ta_debug_counters")
+        self._chk(self.L.ta_debug_counters(self.ctx, a, 16), "ta_debug_counters")
         return {n: int(a[i]) for i, n in enumerate(DEBUG_COUNTERS)}
 
     def verify_content(self):
         bad, seen = C.c_uint64(), C.c_uint64()
-        self._chk(lib().ta_verify_content(self.ctx, C.byref(bad), C.byref(seen)), "ta_verify_content")
+        self._chk(self.L.ta_verify_content(self.ctx, C.byref(bad), C.byref(seen)), "ta_verify_content")
         return bad.value, seen.value
 
     def _view_arrays(self, fields=None):
@@ -471,7 +477,7 @@ class Pool:
         for n, t in _VIEW_FIELDS:
             if n in arrs:
                 setattr(v, n, arrs[n].ctypes.data_as(C.POINTER(t)))
-        self._chk(lib().ta_debug_state(self.ctx, 0, C.byref(v)), "ta_debug_state")
+        self._chk(self.L.ta_debug_state(self.ctx, 0, C.byref(v)), "ta_debug_state")
         if "loc" in arrs:
             arrs["loc"] = arrs["loc"].reshape(self.N, self.MAXB)
         return arrs
@@ -485,22 +491,22 @@ class Pool:
             a = np.ascontiguousarray(arrs[n]).ravel()
             keep[n] = a
             setattr(v, n, a.ctypes.data_as(C.POINTER(t)))
-        self._chk(lib().ta_debug_state(self.ctx, 1, C.byref(v)), "ta_debug_state upload")
+        self._chk(self.L.ta_debug_state(self.ctx, 1, C.byref(v)), "ta_debug_state upload")
 
     def move_blocks(self, kind: int, src_r: int, dst_r: int, src_idx, dst_idx):
         """ta_move_blocks with device index tensors (torch int32/uint32 on this device)."""
         n = int(src_idx.numel())
-        self._chk(lib().ta_move_blocks(self.ctx, kind, src_r, dst_r, src_idx.data_ptr(),
+        self._chk(self.L.ta_move_blocks(self.ctx, kind, src_r, dst_r, src_idx.data_ptr(),
                                        dst_idx.data_ptr(), n), "ta_move_blocks")
 
     def export_handle(self) -> bytes:
         h = (C.c_char * HANDLE_BYTES)()
-        self._chk(lib().ta_export_pool_handle(self.ctx, h), "ta_export_pool_handle")
+        self._chk(self.L.ta_export_pool_handle(self.ctx, h), "ta_export_pool_handle")
         return bytes(h)
 
     def import_peer(self, replica: int, handle: bytes):
         h = (C.c_char * HANDLE_BYTES).from_buffer_copy(handle)
-        self._chk(lib().ta_import_peer_pool(self.ctx, replica, h), "ta_import_peer_pool")
+        self._chk(self.L.ta_import_peer_pool(self.ctx, replica, h), "ta_import_peer_pool")
 
     def read_block(self, r: int, tier: str, idx: int) -> np.ndarray:
         """Bytes of one KV block as uint64 words, shaped [2L, bt, H, D/4] (test aid)."""

@@ -133,6 +133,11 @@ static const char* validate(const ta_config* c) {
     return "max_programs * max_blocks_per_program must be below TA_OWNER_PROMPT";
   if ((c->flags & TA_F_DECIDE_ONLY) && c->replicas_here < c->n_replicas)
     return "TA_F_DECIDE_ONLY is single-process only";
+#ifdef TA_PROD_VARIANT
+  if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS))
+    return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS need libta_dev.so "
+           "(the development build of the same sources; libta.so compiles them out)";
+#endif
   return nullptr;
 }
 

@@ -28,6 +28,26 @@ def test_exports_every_declared_symbol(libta):
     assert set(names) == set(binding.EXPORTED)
 
 
+def test_dev_build_exports_the_same_abi(libta):
+    """libta_dev.so (development options compiled in) exports the same C ABI."""
+    dev = binding.lib(dev=True)
+    for n in header_functions():
+        assert hasattr(dev, n), n
+    assert dev.ta_abi_version() == libta.ta_abi_version()
+
+
+def test_product_build_rejects_development_flags(libta):
+    """libta.so compiles the timing / baseline / test options out and refuses a config
+    that sets one (ta_workspace_bytes validates the config without a GPU)."""
+    import tracegen
+    cfg = tracegen.get_config("c1_toy")
+    for f in (binding.F_TIMING, binding.F_PINNED_ROUTING, binding.F_REQUEST_AWARE, binding.F_SMALL_PATHS):
+        c = binding.make_config(cfg, 8, 4, True, False, f, None, 0)
+        d, h = C.c_size_t(), C.c_size_t()
+        assert libta.ta_workspace_bytes(C.byref(c), C.byref(d), C.byref(h)) == binding.TA_E_INVAL, f
+        assert binding.lib(dev=True).ta_workspace_bytes(C.byref(c), C.byref(d), C.byref(h)) == binding.TA_OK, f
+
+
 def test_abi_version_and_struct_sizes(libta):
     assert libta.ta_abi_version() == 3
     assert C.sizeof(binding.Event) == 24
