@@ -1,4 +1,14 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/r2ah_pytest.log 2>&1; tail -2 gpurun_out/r2ah_pytest.log
-python tools/tick_phases.py --decide-only --ticks 200 2>&1 | tail -1
-python bench.py --steps 20 --warmup 5 > gpurun_out/r2ah_bench.json 2> gpurun_out/r2ah_bench.err; echo bench_rc=$?
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+for fl in "--flush" ""; do echo "== stamps $fl"; TA_NO_EVENTS=1 python tools/step_times.py --phases --mini --decide-only $fl --ticks 60 2>&1 | python -c "
+import sys,re,statistics
+acc={}
+cur=None
+for l in sys.stdin:
+    l=l.strip()
+    m=re.match(r'(\w+)\s*:\s*(.*)',l)
+    if not m or m.group(1) in ('tick','phases','spans'): continue
+    nm=m.group(1)
+    for i,v in re.findall(r'(\d+):([\d.]+)',m.group(2)):
+        acc.setdefault((nm,int(i)),[]).append(float(v))
+for (nm,i),v in sorted(acc.items()):
+    if len(v)>20: print(nm,i,round(statistics.median(v),1))
+"; done

@@ -1,7 +1,7 @@
 """Where the cold-L2 cost of a decision tick comes from (developer tool, GPU box):
 code (instruction fetch of the large planner kernels) or data (the context's metadata).
 
-usage: python tools/cold_split.py [--start 13] [--ticks 60]
+usage: python tools/cold_split.py [--start 13] [--ticks 60] [--decide-only] [--dev]
 
 Four modes per tick of bench_10k (mini KV), each with the 256 MiB L2 flush first:
   cold  : flush, tick
@@ -18,7 +18,11 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tracegen  # noqa: E402
-from paper_2602_13692_b200 import Pool  # noqa: E402
+from paper_2602_13692_b200 import Pool, binding  # noqa: E402
+
+
+# --decide-only: the decision path alone (TA_F_DECIDE_ONLY); --dev: the development build
+FLAGS = (binding.F_DECIDE_ONLY if "--decide-only" in sys.argv else 0) | (binding.F_TIMING if "--dev" in sys.argv else 0)
 
 
 def arg(name, default):
@@ -32,13 +36,13 @@ def main():
     tr = tracegen.make_trace(cfg)
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    out = {"config": "bench_10k", "ticks": f"{start}..{start + n - 1}"}
+    out = {"config": "bench_10k", "ticks": f"{start}..{start + n - 1}", "flags": FLAGS}
     for mode in ("cold", "code", "data", "warm"):
-        a = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0)
+        a = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=FLAGS)
         a.load_trace(tr)
         b = None
         if mode == "code":
-            b = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0, stream=a.stream)
+            b = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=FLAGS, stream=a.stream)
             b.load_trace(tr)
         for _ in range(start):
             a.step(decisions=False)

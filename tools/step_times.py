@@ -1,5 +1,5 @@
 """Per-step device/host timing of the bench workload (developer tool, GPU box).
-usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing] [--flush] [--mini]
+usage: python tools/step_times.py [--no-fuse] [--ticks N] [--phases] [--no-timing] [--flush] [--mini] [--decide-only]
 --flush: 256 MiB memset before every tick (outside the timed pair); --mini: 4 KiB-block KV shape"""
 import os
 import sys
@@ -13,6 +13,7 @@ import tracegen  # noqa: E402
 from paper_2602_13692_b200 import Pool, binding  # noqa: E402
 
 flags = (0 if "--no-timing" in sys.argv else binding.F_TIMING) | (binding.F_NO_FUSE if "--no-fuse" in sys.argv else 0)
+flags |= binding.F_DECIDE_ONLY if "--decide-only" in sys.argv else 0
 ticks = int(sys.argv[sys.argv.index("--ticks") + 1]) if "--ticks" in sys.argv else 24
 cfg = tracegen.get_config("bench_10k")
 if "--mini" in sys.argv:

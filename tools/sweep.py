@@ -1,6 +1,6 @@
 """configs[4] scaling sweep of the scheduler tick (developer tool, GPU box).
 
-usage: python tools/sweep.py [--programs 1000,2000,...] [--bt 16,32,64] [--ticks 40] [--preroll 10]
+usage: python tools/sweep.py [--programs 1000,2000,...] [--bt 16,32,64] [--ticks 40] [--preroll 10] [--decide-only]
 
 For each point (N programs, block size bt) of BASELINE.json configs[4] on one GPU
 (96 GiB of Qwen3-32B KV per GPU -> NB = 96 GiB / block bytes, no host tier;
@@ -18,7 +18,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tracegen  # noqa: E402
 from tracegen.configs import sweep_config  # noqa: E402
-from paper_2602_13692_b200 import Pool  # noqa: E402
+from paper_2602_13692_b200 import Pool, binding  # noqa: E402
 
 
 def arg(name, default):
@@ -38,7 +38,8 @@ def main():
             point += 1
             cfg["kv"] = "mini"
             tr = tracegen.make_trace(cfg)
-            pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=0)
+            pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False,
+                        flags=binding.F_DECIDE_ONLY if "--decide-only" in sys.argv else 0)
             pool.load_trace(tr)
             s = pool.stream
             for _ in range(preroll):
@@ -47,6 +48,7 @@ def main():
             st0 = pool.stats()
             for _ in range(ticks):
                 with torch.cuda.stream(s):
+                    torch.cuda._sleep(1_000_000)    # host submission ahead of the GPU (bench.py)
                     flush.zero_()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
