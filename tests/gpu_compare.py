@@ -103,6 +103,18 @@ def dec_tuples(arr) -> list:
     return [tuple(int(x) for x in rec) for rec in arr]
 
 
+def same_decisions(got_arr, want, where="") -> None:
+    """Assert the GPU decision list equals the oracle's; on a mismatch name the first
+    differing record and show both (kind, pid, src, dst, blocks, ...)."""
+    got = dec_tuples(got_arr)
+    if got == want:
+        return
+    for i, (a, b) in enumerate(zip(want, got)):
+        if a != b:
+            raise AssertionError(f"{where}: decision {i} of {len(want)} (gpu {len(got)}): oracle {a} gpu {b}")
+    raise AssertionError(f"{where}: {len(want)} oracle decisions vs {len(got)} gpu")
+
+
 def check_blocks_content(o, pool, samples, rng):
     """Byte-level check of sampled owned blocks against the closed form on the CPU."""
     from tracegen import KV_SHAPES

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 import oracle  # noqa: E402
 import tracegen  # noqa: E402
-from tests.gpu_compare import compare_state, dec_tuples  # noqa: E402
+from tests.gpu_compare import compare_state, dec_tuples, same_decisions  # noqa: E402
 from tests.test_gpu_parity import need_gpu, stress  # noqa: E402
 
 A, DEC, TC, TR, REL = (oracle.E_ARRIVE, oracle.E_DECODE, oracle.E_TOOL_CALL, oracle.E_TOOL_RESULT,
@@ -68,7 +68,7 @@ def test_gpu_api_mode_events(seed, R, spt):
         if st_o != oracle.OK:
             errs += 1
             continue
-        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        same_decisions(dec_g, dec_o, f"tick {k}")
         if k % 5 == 0:
             compare_state(o, pool.debug_download(), where=f"api tick {k}")
         bad, _ = pool.verify_content()
@@ -92,7 +92,7 @@ def test_gpu_verbs_random(seed, R, spt):
     for k in range(80):
         _, dec_o = o.sched_step()
         _, dec_g = pool.step()
-        assert dec_tuples(dec_g) == dec_o
+        same_decisions(dec_g, dec_o, f"tick {k}")
         for _ in range(rng.randint(0, 3)):
             verb = rng.choice(["pause", "resume", "migrate"])
             want = {"pause": (oracle.REASONING, oracle.ACTING), "resume": (oracle.PAUSED,),
@@ -114,7 +114,7 @@ def test_gpu_verbs_random(seed, R, spt):
             assert st_o == st_g, (k, verb, p, st_o, st_g)
             if st_o == oracle.OK:
                 n_ok[verb] += 1
-                assert dec_tuples(d_g) == d_o, (k, verb, p)
+                same_decisions(d_g, d_o, f"tick {k} verb {verb} pid {p}")
             compare_state(o, pool.debug_download(), where=f"tick {k} after {verb}({p})")
         bad, _ = pool.verify_content()
         assert bad == 0, f"tick {k}: {bad} KV words wrong"
@@ -191,7 +191,7 @@ def test_gpu_api_mode_event_sequences(seed, R):
         if st_o != oracle.OK:
             errs += 1
             continue
-        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        same_decisions(dec_g, dec_o, f"tick {k}")
         if k % 7 == 0:
             compare_state(o, pool.debug_download(), where=f"api tick {k}")
         bad, _ = pool.verify_content()
@@ -246,7 +246,7 @@ def test_gpu_health_failover_random(seed, spt):
     for k in range(90):
         _, dec_o = o.sched_step()
         _, dec_g = pool.step()
-        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        same_decisions(dec_g, dec_o, f"tick {k}")
         if rng.random() < 0.2:
             r = rng.randrange(3)
             up = r in down or len(down) == 2
@@ -294,7 +294,7 @@ def test_gpu_rejected_batch_after_compaction_moves_no_bytes():
         st_o, dec_o = o.sched_step(T, evs)
         st_g, dec_g = pool.step(T, evs, raise_on_error=False)
         assert st_o == st_g == oracle.OK
-        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        same_decisions(dec_g, dec_o, f"tick {k}")
         if o.stats["compact_blocks"] == c0:
             continue
         # this tick compacted: the engine now writes; then an illegal batch arrives
@@ -346,7 +346,7 @@ def test_gpu_api_two_shared_prompts_events_and_verbs():
         if st_o != oracle.OK:
             errs += 1
             continue
-        assert dec_tuples(dec_g) == dec_o, f"tick {k}"
+        same_decisions(dec_g, dec_o, f"tick {k}")
         for _ in range(2):
             p = rng.randrange(N)
             if o.status[p] == oracle.PAUSED:
@@ -355,7 +355,7 @@ def test_gpu_api_two_shared_prompts_events_and_verbs():
                 st_g, d_g = pool.resume(p, rep)
                 assert st_o == st_g, (k, "resume", p, st_o, st_g)
                 if st_o == oracle.OK:
-                    assert dec_tuples(d_g) == d_o
+                    same_decisions(d_g, d_o, f"tick {k} verb")
                     verbs += 1
             elif o.status[p] in (oracle.REASONING, oracle.ACTING):
                 rep = rng.randrange(2)
@@ -363,7 +363,7 @@ def test_gpu_api_two_shared_prompts_events_and_verbs():
                 st_g, d_g = pool.migrate(p, rep)
                 assert st_o == st_g, (k, "migrate", p, st_o, st_g)
                 if st_o == oracle.OK:
-                    assert dec_tuples(d_g) == d_o
+                    same_decisions(d_g, d_o, f"tick {k} verb")
                     verbs += 1
         if k % 5 == 0:
             compare_state(o, pool.debug_download(), where=f"api tick {k}")
