@@ -255,6 +255,7 @@ class Pool:
         if host_blocks is not None:
             self.cfg["host_blocks"] = host_blocks
         self.device = torch.device("cuda", device)
+        flags |= int(os.environ.get("TA_EXTRA_FLAGS", "0"))   # developer aid (e.g. TA_F_NO_GRAPH)
         self.c = make_config(self.cfg, n_programs, max_turns, trace_mode, fill, flags,
                              replicas_here, first_replica)
         L = self.L = lib(dev=(self.c.flags & DEV_FLAGS) != 0)

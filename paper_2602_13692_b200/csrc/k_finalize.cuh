@@ -254,6 +254,9 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d)
   if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 16) d.pst[3 * 32 + threadIdx.x] = 0;
   kspan_begin(d, KS_CLOSE, t_in);
   PSTAMP(3, 0);
+  // compaction tick: read by every CTA before the first grid barrier (CTA 0 advances the
+  // tick counter only after it), so all CTAs take the same barriers below
+  const bool ctick = !verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0;
   // CTA 0 assembles the records of steps 3-5 while the other CTAs finalize (one CTA: both)
   u32 pos = 0;
   if (blockIdx.x == 0) pos = assemble_records(d, s_tmp);
@@ -262,14 +265,15 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d)
   PSTAMP(3, 1);
   grid_sync(d, 1);
   PSTAMP(3, 2);
-  if (blockIdx.x < (unsigned)d.R) {
-    const int r = blockIdx.x;
-    if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) compact_plan_pass(d, r, s_big, s_tmp);
-    else if (threadIdx.x == 0) d.cpd_cnt[r] = 0;
+  if (ctick) {                                        // CTA r plans replica r's moves,
+    if (blockIdx.x < (unsigned)d.R) compact_plan_pass(d, blockIdx.x, s_big, s_tmp);
+    PSTAMP(3, 3);
+    grid_sync(d, 1);                                  // plans -> decisions
+  } else {                                            // no moves: CTA 0, which reads the
+    if (blockIdx.x == 0)                              // counts, clears them itself (a clear
+      for (int t = threadIdx.x; t < d.R; t += CTA) d.cpd_cnt[t] = 0;   // by CTA r raced
+    __syncthreads();                                  // CTA 0's read: a stale COMPACT record)
   }
-  PSTAMP(3, 3);
-  if (!verb && d.compact_every > 0 && (d.ctr->tick % d.compact_every) == 0) grid_sync(d, 1);   // plans -> decisions
-  else __syncthreads();
   PSTAMP(3, 4);
   if (blockIdx.x == 0) assemble_close<verb>(d, pos);
   PSTAMP(3, 9);

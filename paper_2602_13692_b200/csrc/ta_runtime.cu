@@ -251,8 +251,15 @@ __global__ void k_init(Dev d) {
 
 // ------------------------------------------------------------------ tick launch sequence
 static void rec(ta_ctx* x, int i, cudaStream_t s = nullptr) {
-  // external event-record nodes keep working inside the captured CUDA graph
-  if (x->timing && !x->no_events) cudaEventRecordWithFlags(x->ev[i], s ? s : x->stream, cudaEventRecordExternal);
+  if (!x->timing || x->no_events) return;
+  cudaStream_t st = s ? s : x->stream;
+  // external event-record nodes keep working inside the captured CUDA graph; outside a
+  // capture (verbs, TA_F_NO_GRAPH) a plain record
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(x->ev[i], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(x->ev[i], st);
 }
 
 // dynamic shared memory of the copy kernels: the TMA staging buffer in bulk mode

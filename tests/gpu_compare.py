@@ -112,7 +112,9 @@ def same_decisions(got_arr, want, where="") -> None:
     for i, (a, b) in enumerate(zip(want, got)):
         if a != b:
             raise AssertionError(f"{where}: decision {i} of {len(want)} (gpu {len(got)}): oracle {a} gpu {b}")
-    raise AssertionError(f"{where}: {len(want)} oracle decisions vs {len(got)} gpu")
+    n = min(len(want), len(got))
+    raise AssertionError(f"{where}: {len(want)} oracle decisions vs {len(got)} gpu; "
+                         f"oracle extra {want[n:][:4]}, gpu extra {got[n:][:4]}")
 
 
 def check_blocks_content(o, pool, samples, rng):
