@@ -97,6 +97,10 @@ enum {
                                   shared memory 12288 / 8192 -> 8, restore chunks 32..4096 -> 4..64, restore buckets <= 8) so that
                                   small runs take the code paths of full-size runs.  Results are
                                   identical; only the speed differs. */
+  TA_F_JITTER = 1u << 10,       /* test aid (development build only): every CTA of the tick kernels
+                                  sleeps a pseudo-random 0-20 us at kernel entry and after every
+                                  grid / cluster barrier, so that a missing barrier between CTAs
+                                  shows up as a wrong result.  Results are identical. */
   TA_F_DECIDE_ONLY = 1u << 9    /* measurement aid: the tick runs steps 0-5 and 7 (decisions,
                                   block tables, free sets, statistics) but issues no block copy
                                   (no step 6, no compaction copies): the pools' bytes are not

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # options compiled in (DEV_FLAGS; build.py).  TA_LIB: developer A/B aid (a variant of
 # the product build made with build.py --out, inside this package).
 LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("TA_LIB", "libta.so")))
-LIB_DEV_PATH = os.path.join(HERE, "libta_dev.so")
+LIB_DEV_PATH = os.path.join(HERE, os.path.basename(os.environ.get("TA_LIB_DEV", "libta_dev.so")))
 MAXR = 32
 HANDLE_BYTES = 192   # TA_HANDLE_BYTES
 
@@ -26,7 +26,8 @@ F_TRACE_MODE, F_FILL, F_NO_GRAPH, F_TIMING, F_COPY_BULK, F_NO_FUSE, F_PINNED_ROU
 F_REQUEST_AWARE = 128
 F_SMALL_PATHS = 256                  # test aid: small runs take the full-size code paths
 F_DECIDE_ONLY = 512                  # measurement aid: decisions without block copies
-DEV_FLAGS = F_TIMING | F_PINNED_ROUTING | F_REQUEST_AWARE | F_SMALL_PATHS   # need libta_dev.so
+F_JITTER = 1024                      # test aid: random CTA delays at entry and after barriers
+DEV_FLAGS = F_TIMING | F_PINNED_ROUTING | F_REQUEST_AWARE | F_SMALL_PATHS | F_JITTER   # need libta_dev.so
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",

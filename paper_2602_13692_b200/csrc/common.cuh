@@ -205,7 +205,8 @@ __device__ __forceinline__ void dbg_hit(const Dev& d, int i) {
 // build) compiles the measurement / baseline / test options out: timing stamps,
 // PinnedRouting, RequestAware, small paths.
 #ifdef TA_PROD_VARIANT
-#define TA_FLAG(d, f) ((((f) & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS)) == 0) && \
+#define TA_FLAG(d, f) ((((f) & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | \
+                               TA_F_JITTER)) == 0) && \
                        (((d).flags & (f)) != 0))
 #else
 #define TA_FLAG(d, f) (((d).flags & (f)) != 0)
@@ -218,6 +219,20 @@ __device__ __forceinline__ bool small_paths(const Dev& d) { return TA_FLAG(d, TA
 // Barrier across the CTAs of a cooperative launch (all co-resident).  Counter k is
 // used by one kernel only and grows by gridDim.x per barrier, so arrival t waits for
 // the next multiple of gridDim.x.  One CTA: just a CTA barrier.
+// TA_F_JITTER (test aid): thread 0 of the CTA sleeps a pseudo-random 0-20 us (a hash of
+// the CTA, the site and the tick), then the CTA waits for it.  Called where every thread
+// of the CTA is present (kernel entry, right after a grid or cluster barrier).
+__device__ __forceinline__ void jitter(const Dev& d, u32 site) {
+  if (TA_FLAG(d, TA_F_JITTER)) {
+    if (threadIdx.x == 0) {
+      u32 h = (blockIdx.x + 1u) * 0x9E3779B1u ^ site * 0x85EBCA77u ^ (u32)d.ctr->tick * 0xC2B2AE3Du;
+      h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+      const u32 ns = h % 20000u;
+      for (u32 t = 0; t < ns; t += 1000u) __nanosleep(1000u);
+    }
+    __syncthreads();
+  }
+}
 __device__ __forceinline__ void grid_sync(const Dev& d, int k) {
   __syncthreads();
   if (gridDim.x > 1) {
@@ -234,6 +249,7 @@ __device__ __forceinline__ void grid_sync(const Dev& d, int k) {
     }
     __syncthreads();
   }
+  jitter(d, 100u + (u32)k);
 }
 
 // STP staircase of a chunked prefill of n tokens over a resident base (

@@ -451,6 +451,7 @@ __device__ __forceinline__ void move_fused(const Dev& d) {
 __global__ void __launch_bounds__(256, 4) k_move_fused(Dev d) {
   const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   kspan_begin(d, KS_MOVE, t_in);
+  jitter(d, 3u);
   move_fused(d);
   kspan_end(d, KS_MOVE);
 }

@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(CTA, 1) k_close(const __grid_constant__ Dev d)
   if (!verb && d.ctr->err != TA_OK) return;           // API batch rejected: the tick does not run
   if (TA_FLAG(d, TA_F_TIMING) && blockIdx.x == 0 && threadIdx.x < 16) d.pst[3 * 32 + threadIdx.x] = 0;
   kspan_begin(d, KS_CLOSE, t_in);
+  jitter(d, 4u);
   PSTAMP(3, 0);
   // compaction tick: read by every CTA before the first grid barrier (CTA 0 advances the
   // tick counter only after it), so all CTAs take the same barriers below

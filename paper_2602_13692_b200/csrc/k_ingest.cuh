@@ -514,6 +514,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
 __global__ void __launch_bounds__(FP_THREADS, 2) k_tick_front(Dev d) {
   const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   kspan_begin(d, KS_FRONT, t_in);
+  jitter(d, 0u);
   footprint_cta<0>(d);
   kspan_end(d, KS_FRONT);
 }

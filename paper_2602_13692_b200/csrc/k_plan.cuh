@@ -272,6 +272,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
     PSTAMP(2, 1);
   }
   cl.sync();                                           // #0: rank 2's supply reaches the leader
+  jitter(d, 200u);
   if (lead) {
     const u32* el = nullptr;                        // home == r with HBM blocks (footprint pass)
     int nel = 0;
@@ -386,6 +387,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
   }
   }                                                    // part A scope
   cl.sync();                                           // #1: part A visible to the cluster
+  jitter(d, 201u);
   PSTAMP_B(4, 1, 1); PSTAMP_B(5, 3, 1);
 
   // ================= all CTAs: the eviction loop, split by cluster rank
@@ -560,6 +562,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
   PSTAMP(2, 16);
   PSTAMP_B(4, 1, 2); PSTAMP_B(5, 3, 2);
   cl.sync();                                           // #2: evictions done
+  jitter(d, 202u);
   PSTAMP_B(4, 1, 3); PSTAMP_B(5, 3, 3);
   PSTAMP(2, 6);
 
@@ -735,6 +738,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
   // no CTA has to outlive the others (no closing cluster barrier)
   if (threadIdx.x < PLAN_CL) cl.map_shared_rank(&sh, threadIdx.x)->fcnt[crank] = nfed;
   cl.sync();                                           // #4: counts of every CTA known
+  jitter(d, 203u);
   PSTAMP_B(4, 1, 8); PSTAMP_B(5, 3, 8);
   if (!lead && tot) {                                  // allocated = the first tot free blocks of the
     for (u32 w = (u32)(crank - 1) * CTA + threadIdx.x; w < (u32)d.NBW; w += (PLAN_CL - 1) * CTA) {
@@ -806,6 +810,7 @@ __global__ void __launch_bounds__(CTA, 1) k_pause_restore(const __grid_constant_
   __shared__ u32 s_big[8192 + 1];
   __shared__ u32 s_tmp[NWARP + 1];
   kspan_begin(d, KS_PR, t_in);
+  jitter(d, 1u);
   pause_pass(d, blockIdx.x, s_big, s_tmp);
   grid_sync(d, 0);
   if (blockIdx.x == 0) restore_pass(d, s_big, s_tmp);
@@ -821,6 +826,7 @@ k_plan(const __grid_constant__ Dev d) {
   __shared__ u32 s_big[8192 + 1];       // radix histogram / bitmap prefix counts
   __shared__ u32 s_tmp[NWARP + 1];
   kspan_begin(d, KS_PLAN, t_in);
+  jitter(d, 2u);
   plan_pass<VERB>(d, blockIdx.x / PLAN_CL, s_big, s_tmp);
   kspan_end(d, KS_PLAN);
 }

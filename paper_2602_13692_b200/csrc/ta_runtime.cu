@@ -134,8 +134,8 @@ static const char* validate(const ta_config* c) {
   if ((c->flags & TA_F_DECIDE_ONLY) && c->replicas_here < c->n_replicas)
     return "TA_F_DECIDE_ONLY is single-process only";
 #ifdef TA_PROD_VARIANT
-  if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS))
-    return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS need libta_dev.so "
+  if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | TA_F_JITTER))
+    return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS / TA_F_JITTER need libta_dev.so "
            "(the development build of the same sources; libta.so compiles them out)";
 #endif
   return nullptr;

@@ -240,3 +240,33 @@ def test_gpu_decide_only_same_decisions():
     for seed, R in ((41, 1), (42, 3)):
         run_parity(stress(seed, R, compact=4), 200, state_every=2, seed=seed, fill=False,
                    flags=binding.F_DECIDE_ONLY)
+
+
+@pytest.mark.gpu
+def test_gpu_jitter_schedules():
+    """TA_F_JITTER (development build): every CTA of the tick kernels sleeps a pseudo-random
+    0-20 us at entry and after every grid / cluster barrier, shifting the CTAs against each
+    other; results must stay bit-exact (a missing barrier between CTAs -- like the k_close
+    race fixed in round 2 -- shows up as a wrong decision).  Trace mode with compaction every
+    2 ticks on 3-4 replicas, then API-mode multi-event batches on 3 replicas."""
+    need_gpu()
+    import random
+    from paper_2602_13692_b200 import Pool, binding
+    from tests.test_gpu_api import random_event_sequences
+    from tests.gpu_compare import same_decisions
+    for seed, R in ((51, 3), (52, 4)):
+        run_parity(stress(seed, R, compact=2), 120, state_every=3, seed=seed, flags=binding.F_JITTER)
+    cfg = tracegen.get_config("c1_toy", n_replicas=3, hbm_blocks=48, host_blocks=16, max_ctx=4096,
+                              compact_every=5)
+    o = oracle.Oracle(cfg, api_mode=True, n_slots=48)
+    pool = Pool(cfg, 48, trace_mode=False, flags=binding.F_JITTER)
+    rng = random.Random(23)
+    for k in range(120):
+        T = 5000 * k
+        evs = random_event_sequences(o, rng, T)
+        st_o, dec_o = o.sched_step(T, evs)
+        st_g, dec_g = pool.step(T, evs, raise_on_error=False)
+        assert st_o == st_g, (k, st_o, st_g)
+        if st_o == oracle.OK:
+            same_decisions(dec_g, dec_o, f"jitter api tick {k}")
+    pool.close()
