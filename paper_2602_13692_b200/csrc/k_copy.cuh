@@ -218,6 +218,7 @@ __global__ void k_span_reset(Dev d) {
 
 __global__ void k_barrier(Dev d) {
   if (!d.multi) return;
+  jitter(d, 5u);                        // TA_F_JITTER: ranks reach the barrier out of step
   __shared__ ull e;
   if (threadIdx.x == 0) e = ++(*d.epoch);
   __syncthreads();
