@@ -56,6 +56,7 @@ struct Ctr {                 // device-resident scalars of the context
   i32 verb_replica;
   i32 verb_ok;
   u32 t_d2h, t_h2d, t_p2p, t_d2d, t_fetch;   // this tick's block moves (telemetry)
+  u32 t_cross;               // this tick's copies between processes (P2P, a peer tier's H2D)
   u32 cmin;                  // smallest footprint (blocks) among PAUSED programs after step 4 (~0: none)
   ull ev_err;                // API mode: min over programs of (event index << 8 | code); ~0 = legal
   u32 ev_multi;              // API mode: events of programs with several events in the batch
@@ -442,13 +443,20 @@ __device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
   const int w = threadIdx.x >> 5, lane = (int)lane_id();
   const int per = (((n + NWARP - 1) / NWARP) + 31) & ~31;
   const int lo = w * per, hi = min(n, lo + per);
-  u32 cnt = 0;
+  // up to 32 chunks of 32 slots per warp (n <= 32 * 32 * NWARP): the predicate bits of
+  // the counting pass are kept (bit c of tb: this lane's slot in chunk c), so the emit
+  // pass reloads nothing and issues four chunks' emits back to back
+  const bool keep = per <= 32 * 32;
+  u32 cnt = 0, tb = 0;
   for (int b = lo; b < hi; b += 128) {            // four independent loads per lane in flight
     bool t[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) { const int i = b + 32 * k + lane; t[k] = i < hi && pred(i); }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cnt += __popc(__ballot_sync(FULL_MASK, t[k]));
+    for (int k = 0; k < 4; ++k) {
+      cnt += __popc(__ballot_sync(FULL_MASK, t[k]));
+      if (keep && t[k]) tb |= 1u << (((b - lo) >> 5) + k);
+    }
   }
   if (lane == 0) s_tmp[w] = cnt;
   __syncthreads();
@@ -461,12 +469,27 @@ __device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
   __syncthreads();
   u32 pos = s_tmp[w];
   const u32 total = s_tmp[NWARP];
-  for (int b = lo; b < hi; b += 32) {
-    const int i = b + lane;
-    const bool t = i < hi && pred(i);
-    const u32 m = __ballot_sync(FULL_MASK, t);
-    if (t) emit(pos + __popc(m & lanemask_lt()), i, total);
-    pos += __popc(m);
+  if (keep) {
+    for (int b = lo; b < hi; b += 128) {
+      u32 m[4], at[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        m[k] = __ballot_sync(FULL_MASK, (tb >> (((b - lo) >> 5) + k)) & 1u);
+        at[k] = pos + __popc(m[k] & lanemask_lt());
+        pos += __popc(m[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((m[k] >> lane) & 1u) emit(at[k], b + 32 * k + lane, total);
+    }
+  } else {
+    for (int b = lo; b < hi; b += 32) {
+      const int i = b + lane;
+      const bool t = i < hi && pred(i);
+      const u32 m = __ballot_sync(FULL_MASK, t);
+      if (t) emit(pos + __popc(m & lanemask_lt()), i, total);
+      pos += __popc(m);
+    }
   }
   __syncthreads();
   return total;

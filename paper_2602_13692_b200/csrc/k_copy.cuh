@@ -218,6 +218,11 @@ __global__ void k_span_reset(Dev d) {
 
 __global__ void k_barrier(Dev d) {
   if (!d.multi) return;
+  // The barriers order copies between processes (a push into a peer's freshly evicted
+  // block, a pull from a peer's block that it frees at step 7).  A tick whose plan --
+  // the same on every rank: the control plane is replicated -- moves nothing between
+  // processes needs neither, so every rank skips both (epochs stay in step).
+  if (d.ctr->t_cross == 0) return;
   jitter(d, 5u);                        // TA_F_JITTER: ranks reach the barrier out of step
   __shared__ ull e;
   if (threadIdx.x == 0) e = ++(*d.epoch);

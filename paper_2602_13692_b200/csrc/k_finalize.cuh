@@ -230,7 +230,7 @@ __device__ __forceinline__ void assemble_close(const Dev& d, u32 pos) {
     d.ctr->stops = 0;
     d.ctr->restore_cnt = 0;
     d.ctr->n_arr = 0;
-    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
+    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = d.ctr->t_cross = 0;
   }
   for (int t = threadIdx.x; t < R; t += CTA) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;

@@ -763,6 +763,10 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
     atomicAdd(&d.stats[ST_H2D], s_pc[PC_H2D]);
     atomicAdd(&d.ctr->t_p2p, (u32)s_pc[PC_P2P]);
     atomicAdd(&d.ctr->t_h2d, (u32)s_pc[PC_H2D]);
+    u32 cross = (u32)s_pc[PC_P2P];                     // copies another process takes part in
+    for (int h = 0; h < d.R; ++h)
+      if (h != r) cross += s_h2d_src[h];
+    if (cross) atomicAdd(&d.ctr->t_cross, cross);
     atomicAdd(&d.stats[ST_RECOMPUTE], s_pc[PC_REC]);
     atomicAdd(&d.stats[ST_NEW_BLOCKS], s_pc[PC_NEW]);
     atomicAdd(&d.stats[ST_FILL_TOK], s_pc[PC_FILLTOK]);

@@ -11,7 +11,7 @@ __global__ void k_verb_reset(Dev d) {
   if (t == 0) {
     d.ctr->restore_cnt = 0; d.ctr->verb_ok = 1;
     if (d.ctr->err != TA_E_PEER) d.ctr->err = TA_OK;   // a peer failure stays until read
-    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = 0;
+    d.ctr->t_d2h = d.ctr->t_h2d = d.ctr->t_p2p = d.ctr->t_d2d = d.ctr->t_fetch = d.ctr->t_cross = 0;
   }
   if (t < d.R) {
     d.pause_cnt[t] = 0; d.f_cnt[t] = 0; d.s_cnt[t] = 0; d.ev_cnt[t] = 0;

@@ -514,8 +514,9 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
       per_sm = std::max(1, std::min(per_sm, atoi(e)));
     x->move_grid = (sms * per_sm) & ~1;
     if (x->move_grid < 2) d.fused = 0;
-    // k_close: one 1024-thread CTA per 1024 slots (at least R), at most one per SM
-    const int want = (cfg->max_programs + CTA - 1) / CTA;
+    // k_close: CTA 0 assembles the records while one 1024-thread CTA per 1024 slots
+    // finalizes (at least R CTAs: CTA r plans replica r's compaction), at most one per SM
+    const int want = (cfg->max_programs + CTA - 1) / CTA + 1;
     x->close_grid = std::min(std::max(want, cfg->n_replicas), std::max(sms, cfg->n_replicas));
   }
   if (d.multi && cfg->replicas_here != 1) {
