@@ -443,11 +443,12 @@ __device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
   const int w = threadIdx.x >> 5, lane = (int)lane_id();
   const int per = (((n + NWARP - 1) / NWARP) + 31) & ~31;
   const int lo = w * per, hi = min(n, lo + per);
-  // up to 32 chunks of 32 slots per warp (n <= 32 * 32 * NWARP): the predicate bits of
+  // up to 64 chunks of 32 slots per warp (n <= 64 * 32 * NWARP): the predicate bits of
   // the counting pass are kept (bit c of tb: this lane's slot in chunk c), so the emit
   // pass reloads nothing and issues four chunks' emits back to back
-  const bool keep = per <= 32 * 32;
-  u32 cnt = 0, tb = 0;
+  const bool keep = per <= 64 * 32;
+  u32 cnt = 0;
+  u64 tb = 0;
   for (int b = lo; b < hi; b += 128) {            // four independent loads per lane in flight
     bool t[4];
 #pragma unroll
@@ -455,7 +456,7 @@ __device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       cnt += __popc(__ballot_sync(FULL_MASK, t[k]));
-      if (keep && t[k]) tb |= 1u << (((b - lo) >> 5) + k);
+      if (keep && t[k]) tb |= 1ull << (((b - lo) >> 5) + k);
     }
   }
   if (lane == 0) s_tmp[w] = cnt;
@@ -474,7 +475,7 @@ __device__ u32 cta_ordered_gather_w(int n, u32* s_tmp, Pred pred, Emit emit) {
       u32 m[4], at[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        m[k] = __ballot_sync(FULL_MASK, (tb >> (((b - lo) >> 5) + k)) & 1u);
+        m[k] = __ballot_sync(FULL_MASK, (u32)(tb >> (((b - lo) >> 5) + k)) & 1u);
         at[k] = pos + __popc(m[k] & lanemask_lt());
         pos += __popc(m[k]);
       }

@@ -175,22 +175,37 @@ __device__ __forceinline__ void assemble_close(const Dev& d, u32 pos) {
     }
   }
   PSTAMP(3, 6);
-  // occupancy / imbalance (SPEC.md:151-157 at block granularity)
-  ull umax = 0, umin = ~0ull;
-  for (int r = 0; r < R; ++r) {
-    ull fr = 0;
-    for (int w = threadIdx.x; w < d.NBW; w += CTA) fr += __popc(d.hbm_free[(size_t)r * d.NBW + w]);
-    fr = cta_reduce<ull>(fr, s_red, [](ull a, ull b) { return a + b; }, 0ull);
-    ull used = (ull)d.NB - fr;
-    if (!verb && threadIdx.x == 0 && d.ctr->cmin != 0xFFFFFFFFu) {   // programs wait in the queue
-      const ull cap = (ull)d.cap_max[r];
-      d.stats[ST_COST_UNUSED] += (cap > used ? cap - used : 0) * (ull)d.bt * (ull)d.dt;
-      d.stats[ST_UNUSED_CHECKS] += 1;
-      const ull idle = cap > d.L[r] ? cap - d.L[r] : 0;        // C_unused < c_min
-      if (idle >= d.ctr->cmin) d.stats[ST_UNUSED_VIOL] += 1;
+  // occupancy / imbalance (SPEC.md:151-157 at block granularity): every
+  // replica's free words counted at once (NWARP / R warps per replica, one pass)
+  __shared__ u32 s_free[TA_MAX_REPLICAS];
+  if (threadIdx.x < R) s_free[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    const int wpr = R >= NWARP ? 1 : NWARP / R, w = threadIdx.x >> 5, lane = (int)lane_id();
+    for (int rr = w / wpr; rr < R && w < wpr * R; rr += NWARP / wpr) {   // R > NWARP: warps loop
+      const u32* hf = d.hbm_free + (size_t)rr * d.NBW;
+      u32 fr = 0;
+#pragma unroll 4
+      for (int x = (w % wpr) * 32 + lane; x < d.NBW; x += wpr * 32) fr += __popc(hf[x]);
+      fr = __reduce_add_sync(FULL_MASK, fr);
+      if (lane == 0) atomicAdd(&s_free[rr], fr);
     }
-    umax = used > umax ? used : umax;
-    umin = used < umin ? used : umin;
+  }
+  __syncthreads();
+  ull umax = 0, umin = ~0ull;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < R; ++r) {
+      const ull used = (ull)d.NB - s_free[r];
+      if (!verb && d.ctr->cmin != 0xFFFFFFFFu) {   // programs wait in the queue
+        const ull cap = (ull)d.cap_max[r];
+        d.stats[ST_COST_UNUSED] += (cap > used ? cap - used : 0) * (ull)d.bt * (ull)d.dt;
+        d.stats[ST_UNUSED_CHECKS] += 1;
+        const ull idle = cap > d.L[r] ? cap - d.L[r] : 0;        // C_unused < c_min
+        if (idle >= d.ctr->cmin) d.stats[ST_UNUSED_VIOL] += 1;
+      }
+      umax = used > umax ? used : umax;
+      umin = used < umin ? used : umin;
+    }
   }
   PSTAMP(3, 7);
   if (threadIdx.x < TA_MAX_REPLICAS) {   // per-replica link telemetry (host-mapped), one lane each
