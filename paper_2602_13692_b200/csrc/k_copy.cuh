@@ -208,7 +208,7 @@ __global__ void k_probe(Dev d, int i) {
   if (threadIdx.x == 0) d.pst[3 * 32 + 28 + i] = t;
 }
 
-// Timing mode only: reset the kernel spans (KSpan) at the head of a tick.
+// Timing mode only: reset the kernel spans (kspan_begin / kspan_end) at the head of a tick.
 __global__ void k_span_reset(Dev d) {
   if (threadIdx.x < KS_N) {
     d.pst[3 * 32 + 16 + 2 * threadIdx.x] = ~0ull;
