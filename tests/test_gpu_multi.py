@@ -27,3 +27,6 @@ def test_multi_gpu_parity(n, mode):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(": OK") == n
+    if mode == "trace":   # ticks with copies between processes (the device barriers run) and
+        import re         # ticks without (they are skipped) both occur in this run
+        assert max(int(x) for x in re.findall(r"p2p_blocks=(\d+)", r.stdout)) > 0, r.stdout[-2000:]
