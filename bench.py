@@ -190,7 +190,7 @@ def kv_path_microbench(pool, torch, peaks, hbm_peak, n_blocks=2048, reps=3):
     return out
 
 
-def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
+def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush, world=1, rank=0):
     """Latency of one scheduler tick at the bench's program count, decision path only:
     the same trace and pool sizes with the decision-identical `mini` KV shape (4 KiB
     blocks: no decision depends on bytes per block), so the movement kernels still run
@@ -203,7 +203,10 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
     c["kv"] = "mini"
     def run(do_flush, flags=binding.F_DECIDE_ONLY):
         pool = Pool(c, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=flags, device=dev.index,
-                    replicas_here=1, first_replica=0)
+                    replicas_here=1, first_replica=rank)
+        if world > 1:                        # one replica per GPU: every rank runs the whole
+            from paper_2602_13692_b200.dist import connect   # replicated control plane
+            connect(pool)
         pool.load_trace(tr)
         s = pool.stream
         for _ in range(start):
@@ -224,7 +227,13 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
             b.synchronize()
             us.append(a.elapsed_time(b) * 1e3)
         pool.close()
-        return np.array(us)
+        us = np.array(us)
+        if world > 1:                        # per tick, the slowest rank
+            import torch.distributed as dist
+            t = torch.tensor(us, dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            us = t.cpu().numpy()
+        return us
 
     us = run(True)
     warm = run(False)           # back-to-back ticks, L2 warm (context only; the headline is flushed)
@@ -232,7 +241,9 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush):
     return {"median_us": round(float(np.median(us)), 1), "p99_us": round(float(np.percentile(us, 99)), 1),
             "warm_l2_median_us": round(float(np.median(warm)), 1),
             "mean_us": round(float(us.mean()), 1), "ticks": f"{start}..{start + n_ticks - 1}",
-            "programs": tr.n_slots, "target_us": 100,
+            "programs": tr.n_slots, "programs_per_gpu": tr.n_slots // world, "gpus": world, "target_us": 100,
+            "ranks": "per tick the slowest rank (each runs the replicated control plane over all programs)"
+                     if world > 1 else "one GPU",
             "with_copies": {"median_us": round(float(np.median(mv)), 1), "p99_us": round(float(np.percentile(mv, 99)), 1),
                             "note": "the same ticks with the movement kernel copying the mini KV's 4 KiB blocks "
                                     "(hundreds over PCIe on host-tier ticks: the tail)"},
@@ -621,8 +632,8 @@ def main():
                                "measured on configs[1] by tools/compaction_trace.py (DESIGN.md 6.1)",
         "host_link_peaks_gbs": peaks,
     }
-    tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.sched_start, args.sched_ticks, flush)
-                if rank == 0 and world == 1 and args.sched_ticks > 0 else None)
+    tick_lat = (sched_tick_latency(cfg, tr, torch, dev, args.sched_start, args.sched_ticks, flush, world, rank)
+                if args.sched_ticks > 0 else None)   # every rank at N > 1 (max over ranks per tick)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c1 = tracegen.get_config(args.config)

@@ -105,7 +105,8 @@ enum {
                                   block tables, free sets, statistics) but issues no block copy
                                   (no step 6, no compaction copies): the pools' bytes are not
                                   maintained.  Decisions are identical (none depends on bytes);
-                                  it times the decision path alone.  Single process only. */
+                                  it times the decision path alone.  In multi-process mode the
+                                  device barriers go too (they order copies only). */
 };
 
 typedef struct {

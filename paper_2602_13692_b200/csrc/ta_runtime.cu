@@ -131,8 +131,6 @@ static const char* validate(const ta_config* c) {
       return "prefix_tokens must be positive multiples of block_tokens, below hbm_blocks blocks";
   if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (uint64_t)TA_OWNER_PROMPT)
     return "max_programs * max_blocks_per_program must be below TA_OWNER_PROMPT";
-  if ((c->flags & TA_F_DECIDE_ONLY) && c->replicas_here < c->n_replicas)
-    return "TA_F_DECIDE_ONLY is single-process only";
 #ifdef TA_PROD_VARIANT
   if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | TA_F_JITTER))
     return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS / TA_F_JITTER need libta_dev.so "
