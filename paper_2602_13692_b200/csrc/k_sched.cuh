@@ -200,7 +200,35 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       }
       __syncthreads();
     }
-    if (w0) {
+    if (w0 && pre && !TA_FLAG(d, TA_F_PINNED_ROUTING)) {
+      // the global queue (reading A10) with the entries in shared memory: every lane reads
+      // entry i (broadcast, independent of the loads), and one min-reduction over the
+      // replicas' packed keys both tells whether any replica fits and picks the target
+      bool stop = false;
+      const bool mine = lane < (u32)R;
+#pragma unroll 2
+      for (u32 i = 0; i < n; ++i) {
+        const u32 cr = s_cr[i], hp = s_hp[i];
+        if (cr > maxcap) { ++over; continue; }          // can never fit (reading A9)
+        const int hm = (int)(hp & 0xFFu) - 1;
+        const u32 key = (mine && Lr < cmin && Lr + cr <= cmax)
+                            ? (((u32)Lr << 6) | ((u32)((int)lane != hm) << 5) | lane) : 0xFFFFFFFFu;
+        const u32 kmin = __reduce_min_sync(FULL_MASK, key);
+        if (kmin == 0xFFFFFFFFu) { stop = true; break; }
+        const u32 t = kmin & 31u;
+        if (lane == t) Lr += cr;
+        if (lane == 0) {
+          const u32 pl = q[i];
+          const bool pa = (hp >> 8) == TA_PHASE_A;
+          d.status[pl] = pa ? TA_ACTING : TA_REASONING;
+          d.placement[pl] = (i8)t;
+          d.restore_pid[cnt] = pl;
+          d.restore_dst[cnt] = t | ((hp & 0xFFu) << 8) | ((u32)pa << 24);   // dst | (home + 1) << 8 | A << 24
+        }
+        ++cnt;
+      }
+      if (lane == 0) s_stop = stop || T >= 2 * NBK - 1;
+    } else if (w0) {
       bool stop = false;
       const bool pinned = TA_FLAG(d, TA_F_PINNED_ROUTING);
       const u32 all_r = R >= 32 ? 0xFFFFFFFFu : ((1u << R) - 1);
