@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sched-ticks", type=int, default=200, help="ticks of the decision-path latency probe")
     ap.add_argument("--sched-start", type=int, default=13, help="first tick of the latency probe (after the burst)")
+    ap.add_argument("--compaction-ticks", type=int, default=530,
+                    help="configs[1] ticks of the in-trace D2D (compaction) probe at N=1 (0: skip)")
     return ap.parse_args()
 
 
@@ -251,6 +253,41 @@ def sched_tick_latency(cfg, tr, torch, dev, start, n_ticks, flush, world=1, rank
             "note": "the decision path: one ta_sched_step CUDA graph with TA_F_DECIDE_ONLY (front, pause + "
                     "restore, plan, close; no block copies), L2 flushed before each tick; a 0.5 ms device "
                     "spin before the flush keeps the host's graph submission ahead of the GPU"}
+
+
+def compaction_probe(torch, ticks, hbm_peak):
+    """In-trace D2D at full block size: configs[1] (256 SWE programs, Qwen3-32B 4 MiB blocks,
+    the same 96 GiB pool and host tier as bench_10k) with two-finger compaction every 4th
+    tick.  bench_10k itself never compacts (closed-loop arrivals keep its pool full);
+    configs[1] drains once all its programs have arrived, and its compaction ticks
+    (452-520) move ~17k blocks.  k_copy_compact is timed by the TA_F_TIMING event pair
+    around it (phase 7); bytes = read + write of every moved block."""
+    import tracegen
+    from paper_2602_13692_b200 import Pool, binding
+    cfg = tracegen.get_config("c2_swe", compact_every=4)
+    tr = tracegen.make_trace(cfg)
+    pool = Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=binding.F_TIMING)
+    pool.load_trace(tr)
+    blocks, us, n = 0, 0.0, 0
+    for _ in range(ticks):
+        pool.step(decisions=False)
+        ti = pool.last_tick()
+        if ti["d2d_blocks"]:
+            ph = pool.phase_times()
+            blocks += ti["d2d_blocks"]
+            us += ph[7]
+            n += 1
+    bb = pool.block_bytes
+    pool.close()
+    if not blocks:
+        return None
+    by = 2.0 * blocks * bb
+    gbs = by / (us * 1e-6) / 1e9
+    return {"config": "configs[1] c2_swe, compact_every 4", "ticks": f"0..{ticks - 1}", "compaction_ticks": n,
+            "blocks": blocks, "gb_rw": round(by / 1e9, 3), "kernel_s": round(us * 1e-6, 6),
+            "gbs_rw": round(gbs, 1), "peak_gbs": hbm_peak, "frac_hbm": round(gbs / hbm_peak, 4),
+            "note": "k_copy_compact per compaction tick (TA_F_TIMING event pair around it, development "
+                    "build); bench_10k never compacts"}
 
 
 def workload(name, world):
@@ -640,6 +677,11 @@ def main():
         cpu = cpu_baseline(c1, tracegen.make_trace(c1), S0, args.cpu_seconds)
     dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS + binding.LEDGER_KEYS if isinstance(st0[k], int)}
     launches = 5 + (1 if cfg.get("compact_every", 0) > 0 else 0) + (2 if world > 1 else 0)
+    nb_main, nh_main = pool.NB, pool.NH
+    if world == 1 and args.compaction_ticks > 0:   # the main pool's memory goes back to torch's caches
+        pool.close()
+        pool.hbm, pool.host, pool.dev_ws, pool.host_ws = {}, {}, None, None
+        kv_moved["compaction_in_trace"] = compaction_probe(torch, args.compaction_ticks, hbm_peak)
     line = {
         "metric": metric, "value": round(value, 4), "unit": "ticks/s (10k-program ticks, summed over GPUs)",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(ms / K, 3),
@@ -647,7 +689,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": args.config, "programs": tr.n_slots, "replicas": world, "replicas_per_gpu": 1,
                    "kv": "Qwen3-32B GQA L64 H8 D128 bf16, 16-token blocks (4 MiB)",
-                   "hbm_blocks": pool.NB, "host_blocks": pool.NH,
+                   "hbm_blocks": nb_main, "host_blocks": nh_main,
                    "window": f"ticks {S0}..{S0 + K - 1} of a fresh context (fixed; the W warm-up ticks run on a "
                              f"throw-away context first)",
                    "engine_fill": "off (engine stand-in, not a hot-path row)",
