@@ -290,6 +290,53 @@ def compaction_probe(torch, ticks, hbm_peak):
                     "build); bench_10k never compacts"}
 
 
+def migrate_probe(pool, tr, world, rank, base_flags, torch, n_prog=24, ticks=12):
+    """NVLink through the product API at N >= 2: a fresh trace context runs the burst's
+    first `ticks` ticks; replica 1's active programs are paused with their blocks dropped
+    (collective ta_pause, TA_PAUSE_DROP: both replicas run at lambda = 1, so replica 1
+    needs room), then the `n_prog` REASONING programs of replica 0 with the most HBM blocks
+    are migrated to replica 1 (collective ta_migrate; replica 1 pulls the blocks over
+    NVLink from replica 0's pool).  Each verb is timed on the device (event pair on the
+    context stream, max over ranks); GB/s = blocks pulled x block bytes / time."""
+    import torch.distributed as dist
+    from paper_2602_13692_b200 import binding
+    fresh(pool, world, flags=base_flags)
+    pool.load_trace(tr)
+    for _ in range(ticks):
+        pool.step(decisions=False)
+    torch.cuda.synchronize()
+    st = pool.debug_download(["status", "home", "n_hbm", "satisfied", "placement"])
+    for p in range(tr.n_slots):
+        if st["placement"][p] == 1 and st["status"][p] in (2, 3):
+            pool.pause(p, 2)
+    cand = [p for p in range(tr.n_slots) if st["status"][p] == 2 and st["home"][p] == 0 and st["placement"][p] == 0
+            and st["satisfied"][p] == 1]                  # materialized: every block in HBM (NVLink only)
+    cand = sorted(cand, key=lambda p: -int(st["n_hbm"][p]))[:n_prog]
+    s = pool.stream
+    blocks, ms_tot = 0, 0.0
+    dev = pool.device
+    for p in cand:
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        code, _ = pool.migrate(p, 1)
+        b.record(s)
+        b.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if code == binding.TA_OK:
+            blocks += int(pool.last_tick()["p2p_blocks"])
+            ms_tot += float(t.item())
+    if not blocks:
+        return None
+    by = blocks * pool.block_bytes
+    gbs = by / (ms_tot * 1e-3) / 1e9
+    return {"migrations": len(cand), "blocks": blocks, "gb": round(by / 1e9, 2), "verb_time_ms": round(ms_tot, 2),
+            "gbs": round(gbs, 1), "peak_gbs": 770.0, "frac": round(gbs / 770.0, 3),
+            "note": "ta_migrate replica 0 -> 1 end to end on the device (plan, NVLink pull, close), max over "
+                    "ranks; peak = the measured peer copy (B200_PROFILING.md; 900 nominal)"}
+
+
 def workload(name, world):
     """The bench workload at N GPUs: N replicas, 10k programs per replica (weak scaling):
     N interleaved copies of the 1-GPU trace (tracegen.tile_trace), so every replica sees
@@ -678,6 +725,8 @@ def main():
     dstat = {k: st1[k] - st0[k] for k in binding.STAT_KEYS + binding.LEDGER_KEYS if isinstance(st0[k], int)}
     launches = 5 + (1 if cfg.get("compact_every", 0) > 0 else 0) + (2 if world > 1 else 0)
     nb_main, nh_main = pool.NB, pool.NH
+    if world > 1:
+        kv_moved["p2p_in_api"] = migrate_probe(pool, tr, world, rank, base_flags, torch)
     if world == 1 and args.compaction_ticks > 0:   # the main pool's memory goes back to torch's caches
         pool.close()
         pool.hbm, pool.host, pool.dev_ws, pool.host_ws = {}, {}, None, None

@@ -49,14 +49,15 @@ def main():
     for _ in range(ticks):
         pool.step(decisions=False)
     torch.cuda.synchronize()
-    st = pool.debug_download(["status", "home", "n_hbm", "placement"])
+    st = pool.debug_download(["status", "home", "n_hbm", "satisfied", "placement"])
     # make room on replica 1 (both replicas run at lambda = 1): pause its active programs,
     # dropping their blocks (collective verbs; every rank holds the same state)
     for p in range(tr.n_slots):
         if st["placement"][p] == 1 and st["status"][p] in (2, 3):
             pool.pause(p, 2)
     torch.cuda.synchronize()
-    cand = [p for p in range(tr.n_slots) if st["status"][p] == 2 and st["home"][p] == 0 and st["placement"][p] == 0]
+    cand = [p for p in range(tr.n_slots) if st["status"][p] == 2 and st["home"][p] == 0 and st["placement"][p] == 0
+            and st["satisfied"][p] == 1]                  # materialized: every block in HBM (NVLink only)
     cand.sort(key=lambda p: -int(st["n_hbm"][p]))
     cand = cand[:nprog]
     s = pool.stream
