@@ -727,8 +727,8 @@ def main():
         "compaction": ({"gbs_rw": round(2 * mv["d2d"] / (ph_sum[7] * 1e-6) / G, 1),
                         "frac_hbm": round(mv["d2d_floor_s"] / (ph_sum[7] * 1e-6), 4)}
                        if mv["d2d"] > 0 and ph_sum[7] > 0 else None),
-        "compaction_in_trace": "bench_10k never compacts (its pool stays full); in-trace D2D is "
-                               "measured on configs[1] by tools/compaction_trace.py (DESIGN.md 6.1)",
+        "compaction_in_trace": "bench_10k never compacts (its pool stays full); the N = 1 line runs the "
+                               "configs[1] compaction probe (DESIGN.md 8)",
         "host_link_peaks_gbs": peaks,
         "host_link_concurrent_gbs": peaks_concurrent,
     }
