@@ -5,6 +5,9 @@
 // Queue entries selected per sorted chunk of the restore loop: the loop usually stops
 // at the head (steady state) or runs long (bursts), so chunks grow geometrically.
 #define RESTORE_CHUNK0 32u
+#ifndef TA_RESTORE_CHUNK_DIV
+#define TA_RESTORE_CHUNK_DIV 512u
+#endif
 #define RESTORE_CHUNK_MAX 4096u
 
 // Step 3, one CTA per replica (reading A6): if the decayed
@@ -157,7 +160,9 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
   // queue buckets: rb[] / rhist[] from the footprint pass, plus this tick's pauses
   // (k_pause) and arrivals (above), so no pass over the slots is needed to size a chunk
   const u32 chunk_max = small_paths(d) ? 64u : RESTORE_CHUNK_MAX;
-  u32 lo = 0, chunk = small_paths(d) ? 4u : RESTORE_CHUNK0;
+  // first chunk: about one queued entry per 512 slots (32 up to 16k programs, 78 at 40k),
+  // so that large queues rarely need a second pass over the slots
+  u32 lo = 0, chunk = small_paths(d) ? 4u : max(RESTORE_CHUNK0, min(512u, (u32)N / TA_RESTORE_CHUNK_DIV));
   while (true) {
     const u32 T = cta_hist_threshold(d.rhist, 2 * NBK, lo, chunk, s_big, s_tmp);
     if (it < 7) PSTAMP(1, 1 + 4 * it);
