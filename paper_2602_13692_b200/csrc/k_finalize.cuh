@@ -147,13 +147,24 @@ __device__ __forceinline__ u32 assemble_records(const Dev& d, u32* s_tmp) {
     pos += n;
   }
   PSTAMP(3, 10);
-  for (int r = 0; r < R; ++r) {          // FETCH / STALL (kind 0 = no decision)
-    const ta_decision* fs = d.dec_fs + (size_t)r * N;
-    u32 n = cta_ordered_gather((int)d.f_cnt[r], s_tmp,
-        [&](int i) { return fs[i].kind != 0; },
-        [&](u32 at, int i) { put(pos + at, fs[i]); });
-    pos += n;
+  // FETCH / STALL (kind 0 = no decision): every replica's F records in one ordered pass
+  // over their concatenation (replica order, then F order), one CTA scan in all
+  __shared__ u32 s_fo[TA_MAX_REPLICAS + 1];
+  if (threadIdx.x == 0) {
+    u32 o = 0;
+    for (int r = 0; r < R; ++r) { s_fo[r] = o; o += d.f_cnt[r]; }
+    s_fo[R] = o;
   }
+  __syncthreads();
+  auto rec_at = [&](int x) -> const ta_decision& {
+    int r = 0;
+    while ((u32)x >= s_fo[r + 1]) ++r;
+    return d.dec_fs[(size_t)r * N + (x - (int)s_fo[r])];
+  };
+  u32 n = cta_ordered_gather((int)s_fo[R], s_tmp,
+      [&](int x) { return rec_at(x).kind != 0; },
+      [&](u32 at, int x) { put(pos + at, rec_at(x)); });
+  pos += n;
   return pos;
 }
 
