@@ -23,9 +23,12 @@ Parity status: steps 2-4 are pinned by SPEC worked examples, brute force and
 closed forms (tests/test_oracle_policy.py); step 5.6 hit accounting by an
 independent per-token simulator (tests/test_oracle_tokensim.py); the whole tick
 by the hand-computed golden W1 (tests/golden/w1.json) and invariants I1-I10.
-Steps 0, 5.1-5.3 (eviction order) and 7 (compaction) are definitional
-("parity unpinned (definitional)"): pinned only by the written
-spec in DESIGN.md and invariants I1-I10.
+Steps 0, 5.1-5.3 (eviction order) and 7 (compaction) are definitional (SURVEY.md
+P11: no paper value to compare with); since round 2 they are pinned by hand-computed
+states written from DESIGN.md's text (tests/test_oracle_handpins.py: two-finger
+compaction, all three eviction groups with a partial victim and host-slot order, the
+tool-call start time) and a mutation check that breaks each rule and sees a pin fail
+(tests/test_oracle_mutants.py), besides W1 and invariants I1-I10.
 """
 from __future__ import annotations
 
