@@ -1,6 +1,6 @@
 """Multi-GPU parity (one replica per GPU, CUDA-IPC P2P, device barriers) vs the oracle.
 
-torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_parity.py [ticks] [--verbs] [--api]
+torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_parity.py [ticks] [--verbs] [--api]
     [--shared TOKENS] [--c3] [--prompts2]
 Every rank runs the replicated control plane for all N replicas and moves only its
 own replica's bytes; every rank compares its decisions and full state with its own

@@ -1,7 +1,7 @@
 """Small end-to-end driver for compute-sanitizer runs (developer tool, GPU box):
 trace-mode ticks with fills and compaction, API-mode batches with multi-event
 programs, and every verb (pause/resume/migrate/set_health), each checked against the
-oracle.  usage: compute-sanitizer --tool memcheck python tools/sanitize_driver.py"""
+oracle.  usage: compute-sanitizer --tool memcheck python tests/sanitize_driver.py"""
 import os
 import random
 import sys

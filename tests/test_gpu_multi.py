@@ -1,4 +1,4 @@
-"""Multi-GPU parity: one replica per GPU over CUDA IPC + NVLink (tools/mgpu_parity.py under
+"""Multi-GPU parity: one replica per GPU over CUDA IPC + NVLink (tests/mgpu_parity.py under
 torchrun).  Skipped unless at least two GPUs are visible."""
 import os
 import subprocess
@@ -21,7 +21,7 @@ def test_multi_gpu_parity(n, mode):
     port = 29530 + {"trace": 1, "verbs": 3, "api": 5, "shared": 7, "c3": 9, "prompts2": 11}[mode] + 20 * n
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(ROOT, "tools", "mgpu_parity.py"), "30" if mode == "c3" else "120"] + (
+           os.path.join(ROOT, "tests", "mgpu_parity.py"), "30" if mode == "c3" else "120"] + (
                {"trace": [], "verbs": ["--verbs"], "api": ["--api"], "shared": ["--verbs", "--shared", "48"],
                 "c3": ["--c3"], "prompts2": ["--verbs", "--prompts2"]}[mode])
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
