@@ -5,7 +5,7 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 shares no code with the CUDA path (``paper_2602_13692_b200``) and never imports
 it; the only shared module is the seeded input generator ``tracegen``.
 
-Parity status per function is listed in each module header and in DESIGN.md §3.
+Parity status per function is listed in each module header and in DESIGN.md §3 (readings in §2.1).
 """
 from .ta_oracle import (  # noqa: F401
     Oracle, NONE, HOST_BIT, UNARRIVED, PAUSED, REASONING, ACTING, STOPPED, PHASE_R, PHASE_A,

@@ -6,7 +6,7 @@ CUDA path; its only input is a ``tracegen`` trace (data) and a config dict.
 
 The method is a heuristic policy applied tick by tick, so the
 oracle *is* the algorithm written out step by step in the paper's order
-(SURVEY.md §8(c) steps 0-7), with the readings A1-A27 listed in DESIGN.md §3.
+(SURVEY.md §8(c) steps 0-7), with the readings (A1 onwards) listed in DESIGN.md §2.1.
 Every order is a total order ending in the slot index, so results are unique.
 
 Paper anchors (PAPER.md line numbers):
