@@ -178,7 +178,8 @@ def e_any(spans):
 
 SPAN_KERNELS = ("front", "pause_restore", "plan", "move", "close", "compact")   # KSpan k order
 DEBUG_COUNTERS = ("radix_sort", "bitonic_sort", "rank_sort", "list_global", "plan_f_global", "plan_e_global",
-                  "plan_v_global", "plan_fst_global", "restore_chunks", "evict_ticks")
+                  "plan_v_global", "plan_fst_global", "restore_chunks", "evict_ticks",
+                  "front_rows_counted", "front_row_entries")
 MOVE_D2D, MOVE_P2P, MOVE_D2H, MOVE_H2D = 1, 2, 3, 4
 
 

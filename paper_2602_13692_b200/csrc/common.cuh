@@ -105,6 +105,8 @@ struct Dev {
                                    //     0 NONE, 1 HBM, 2 host tier (footprint pass; hit accounting)
   u8* released;                    // released during this tick's ingest
   u8* sat_new;                     // 1 + replica that satisfied the program this tick
+  u8* dirty;                       // [N] row written since the footprint pass last counted it
+                                   //     (every writer of loc sets it; the pass clears it)
   u8* kp;                          // [N] shared prompt of each program (KP_NONE: none)
   u8* t_kp;                        // [N] trace mode: prompt of each slot's program
   u32* pref;                       // [R][K] programs homed on r using prompt k
@@ -197,6 +199,8 @@ enum DbgIdx {
   DBG_FST_GLOBAL,       // k_plan request loop reads per-program values from global (m > FST limit)
   DBG_RESTORE_CHUNKS,   // restore pass chunks after the first
   DBG_EVICT_TICKS,      // k_plan replica-ticks with X > 0
+  DBG_ROWS_COUNTED,     // tick footprint pass: block-table rows counted (written since the last pass)
+  DBG_ROW_ENTRIES,      // ... and their entries read (the rest of the rows are clean, not read)
   DBG_N = 16
 };
 __device__ __forceinline__ void dbg_hit(const Dev& d, int i) {

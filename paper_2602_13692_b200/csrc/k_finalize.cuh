@@ -40,6 +40,7 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int first_cta) {
       d.c_kv[p] = d.c[p];
       d.n_hbm[p] = d.nb[p];
       d.sat_new[p] = 0;
+      d.dirty[p] = 1;                    // its row was written (fetches, prompt entries)
     } else if (!verb) {
       d.satisfied[p] = 0;
       const u8 st = d.status[p];
@@ -93,6 +94,7 @@ __device__ __forceinline__ void compact_plan_pass(const Dev& d, const int r, u32
     const u32 o = d.owner_hbm[(size_t)r * d.NB + src];
     const u32 p = o / (u32)d.MAXB, j = o % (u32)d.MAXB;
     d.loc[(size_t)p * d.MAXBP + j] = dst;
+    d.dirty[p] = 1;
     d.owner_hbm[(size_t)r * d.NB + dst] = o;
     cp[m] = CpDesc{src, dst};
   }

@@ -289,7 +289,15 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 // I2: blocks are allocated for j < nb only, and c never shrinks), so entries [nbo, nb)
 // are NONE: n_hbm and n_host are the counts over [0, nbo), and the first non-HBM entry
 // is the first one in [0, nbo), else nbo.
-#define FP_SLOTS 32                      // slots per CTA (one lane of warp 0 each)
+//
+// Only rows written since the last pass are counted (d.dirty: every writer of loc sets
+// it -- evictions and fetches in k_plan, satisfaction and compaction in k_close, the
+// verbs, a state upload -- and this pass clears it).  A clean row of a live program
+// has the counts and HBM prefix the last pass stored: c never shrinks, so its extra
+// entries [nbo_then, nbo) are NONE, which add to neither count and leave
+// min(first, nbo) where it was.  Its last-history-block class still depends on c_kv,
+// so that one entry is read (a 4-byte cp.async).
+#define FP_SLOTS 32                     // slots per CTA (one lane of warp 0 each)
 #ifndef FP_THREADS
 #define FP_THREADS 256                   // FP_SLOTS / (FP_THREADS / 32) slots per warp
 #endif
@@ -299,6 +307,10 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const u32 s = (u32)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
@@ -319,6 +331,8 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   __shared__ int s_home[FP_SLOTS];
   __shared__ u8 s_rel[FP_SLOTS], s_hcls[FP_SLOTS], s_kp[FP_SLOTS];
   __shared__ u32 s_jh[FP_SLOTS];          // entry of the last history block (ceil(c_kv/bt) - 1), or ~0
+  __shared__ u32 s_hx[FP_SLOTS];          // clean row: its entry jh
+  __shared__ u8 s_dirty[FP_SLOTS];
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const int p0 = blockIdx.x * FP_SLOTS;
   const int p = p0 + lane;
@@ -335,9 +349,14 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   // ---- 1. fields (warp 0)
   SlotFields f{};
   SlotNow v{};
+  u32 nh_old = 0, ns_old = 0;
+  u8 dv = 0;
   if (w0) {
     u32 nbo = 0;
     if (p < d.N) {
+      dv = d.dirty[p];                   // a clean row keeps last pass's counts (see above)
+      nh_old = d.n_hbm[p];
+      ns_old = d.n_host[p];
       if (MODE == 0) {
         f = ingest_load(d, p);
         nbo = row_len_of(d, f.st, f.c);
@@ -347,11 +366,17 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
         nbo = max(row_len_of(d, (u8)v.st, v.c), v.released ? ceil_div_u32(v.c, d.bt) : 0u);
       }
     }
-    const u32 nch = (nbo + 3) >> 2;
+    const u32 nch = dv ? (nbo + 3) >> 2 : 0u;     // only written rows are read
     const u32 inc = warp_incl_scan(nch);
     s_off[lane] = inc - nch;
     if (lane == 31) s_off[FP_SLOTS] = inc;
+    if (MODE == 0) {                     // rows / entries actually read (ta_debug_counters)
+      const u32 nr = __reduce_add_sync(FULL_MASK, (dv && nbo) ? 1u : 0u);
+      const u32 ne = __reduce_add_sync(FULL_MASK, dv ? nbo : 0u);
+      if (lane == 0 && nr) { atomicAdd(&d.dbg[DBG_ROWS_COUNTED], (ull)nr); atomicAdd(&d.dbg[DBG_ROW_ENTRIES], (ull)ne); }
+    }
     s_nbo[lane] = nbo;
+    s_dirty[lane] = dv;
     s_nh[lane] = 0; s_ns[lane] = 0; s_first[lane] = 0xFFFFFFFFu;
     const u32 ckv = p < d.N ? d.c_kv[p] : 0u;
     s_kp[lane] = p < d.N ? d.kp[p] : (u8)KP_NONE;
@@ -372,13 +397,23 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     constexpr int CW = FP_THREADS / 32 - 1;       // counting warps
     for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
       const u32 o = s_off[sl], nch = s_off[sl + 1] - o;
-      if (o + nch <= FP_STAGE)
+      if (!s_dirty[sl]) {                // clean row: only the last history block's entry
+        if (lane == 0 && s_jh[sl] < s_nbo[sl]) cp_async4(&s_hx[sl], rows + (size_t)sl * d.MAXBP + s_jh[sl]);
+      } else if (o + nch <= FP_STAGE) {
         for (u32 c = lane; c < nch; c += 32) cp_async16(&s_stage[o + c], rows + (size_t)sl * d.MAXBP + 4 * c);
+      }
     }
     cp_async_wait_all();
     __syncwarp();
     for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
       const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
+      if (!s_dirty[sl]) {
+        if (lane == 0 && s_jh[sl] < nbo) {
+          const u32 x = s_hx[sl];
+          s_hcls[sl] = is_hbm(x) ? 1 : (is_host(x) ? 2 : 0);
+        }
+        continue;
+      }
       const bool staged = o + nch <= FP_STAGE;
       const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
       u32 a_h = 0, a_n = 0, a_f = 0xFFFFFFFFu;   // HBM entries, non-HBM entries, first non-HBM
@@ -433,8 +468,8 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     constexpr int CW = FP_THREADS / 32 - 1;
     for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
       if (!s_rel[sl]) continue;
-      const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
-      const bool staged = o + nch <= FP_STAGE;
+      const u32 o = s_off[sl], nbo = s_nbo[sl], nch = (nbo + 3) >> 2;
+      const bool staged = s_dirty[sl] && o + nch <= FP_STAGE;   // a clean row was not staged
       const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
       const int h = s_home[sl];
       const u32 sbs = sb_of(d, s_kp[sl]);
@@ -472,18 +507,24 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   u32 n_h = 0, n_s = 0;
   int pl = -1;
   if (live) {
-    n_h = s_nh[lane];
-    n_s = s_ns[lane];
-    const u32 first = s_first[lane];
     if (st != TA_PAUSED) pl = v.pl;
-    d.prefix_hbm[p] = min(first, s_nbo[lane]);   // entries [nbo, nbv) are NONE
+    if (dv) {
+      n_h = s_nh[lane];
+      n_s = s_ns[lane];
+      d.prefix_hbm[p] = min(s_first[lane], s_nbo[lane]);   // entries [nbo, nbv) are NONE
+    } else {                             // clean: counts and prefix as last counted
+      n_h = nh_old;
+      n_s = ns_old;
+    }
   } else if (valid) {
     d.prefix_hbm[p] = 0;
     if (MODE != 2 && v.released) d.home[p] = -1;
     if (MODE == 1 && v.released) d.released[p] = 0;
   }
   if (valid) {
-    d.nb[p] = nbv; d.n_hbm[p] = n_h; d.n_host[p] = n_s; d.contrib[p] = cb;
+    d.nb[p] = nbv; d.contrib[p] = cb;
+    if (dv || !live) { d.n_hbm[p] = n_h; d.n_host[p] = n_s; }
+    if (dv) d.dirty[p] = 0;
     d.rb[p] = rbv; d.hcls[p] = s_rel[lane] ? 0 : s_hcls[lane];
   }
   // candidate bitmaps: this CTA's 32 slots are word blockIdx.x of every replica's maps
@@ -511,7 +552,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
 #define FP_GRID(N) (((N) + FP_SLOTS - 1) / FP_SLOTS)
 #define FP_BLOCK FP_THREADS
 #define FP_DSMEM FP_SMEM
-__global__ void __launch_bounds__(FP_THREADS, 2) k_tick_front(Dev d) {
+__global__ void __launch_bounds__(FP_THREADS, 4) k_tick_front(Dev d) {   // 592 CTAs in one wave: 18,944 slots
   const ull t_in = gtimer();   // the CTA's first instruction (kernel span, timing mode)
   kspan_begin(d, KS_FRONT, t_in);
   jitter(d, 0u);

@@ -544,6 +544,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
         if (e >= e_hi) continue;
         const u32 idx = ik[k], j = jk[k], p = pk[k];
         u32* ent = d.loc + (size_t)p * d.MAXBP + j;
+        d.dirty[p] = 1;
         atomicOr(&hf[idx >> 5], 1u << (idx & 31));          // freed now (intra-replica)
         if (e < hfree) {
           if (evp_owner(d, r)) evp_of(d, r)[idx] = 2u * d.nL;  // segments pending their D2H read
@@ -718,6 +719,7 @@ __device__ __forceinline__ void plan_pass(const Dev& d, const int r, u32* s_big,
           if (fill) x = FeDesc{MV_FILL, 0, 0, dst, uid, jb, je, j};
         }
         d.loc[(size_t)p * d.MAXBP + j] = dst;
+        d.dirty[p] = 1;
         d.owner_hbm[(size_t)r * d.NB + dst] = p * (u32)d.MAXB + j;
       }
       u32 round_n;

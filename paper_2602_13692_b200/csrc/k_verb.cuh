@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_pause(Dev d, u32 pid, u32 mode)
   const int h = s_h;
   const u32 X = s_nh;
   u32* row = d.loc + (size_t)pid * d.MAXBP;
+  if (threadIdx.x == 0) d.dirty[pid] = 1;
   const u32* sf = d.host_free + (size_t)h * d.NHW;
   u32 hfree = 0;
   if (mode == TA_PAUSE_OFFLOAD) {
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(CTA, 1) k_verb_health(const __grid_constant__ 
       if (row[j] != LOC_NONE) { cnt += j >= sbp; row[j] = LOC_NONE; }
     }
     cnt = __reduce_add_sync(FULL_MASK, cnt);
-    if (lane == 0) { lost[q] = cnt; d.home[p] = -1; }
+    if (lane == 0) { lost[q] = cnt; d.home[p] = -1; d.dirty[p] = 1; }
   }
   __syncthreads();
   ta_decision* ev = d.dec_ev + (size_t)r * N;

@@ -171,7 +171,7 @@ static size_t carve(const ta_config* c, char* base, Dev* d) {
     x.pref = L.take<u32>(R * std::max(K, 1)); x.pblk = L.take<u32>(R * std::max(K, 1) * SBM);
     x.pfix = L.take<u32>(R * NBW); x.f_x = L.take<u32>(R * N);
   }
-  x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
+  x.released = L.take<u8>(N); x.sat_new = L.take<u8>(N); x.dirty = L.take<u8>(N); x.evs = L.take<u8>(3 * N);
   x.evc = L.take<u32>(N);
   x.t_uid = L.take<u32>(N); x.t_p0 = L.take<u32>(N); x.t_off = L.take<u32>(N + 1);
   x.t_g = L.take<u32>(TT); x.t_d = L.take<u32>(TT); x.t_o = L.take<u32>(TT);
@@ -536,6 +536,7 @@ ta_status ta_init_pool(const ta_config* cfg, const ta_buffers* bufs, void* cuda_
   size_t dev_bytes = carve(cfg, nullptr, nullptr);
   cudaError_t e = cudaMemsetAsync(bufs->dev_workspace, 0, dev_bytes, x->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.loc, 0xFF, (size_t)d.N * d.MAXBP * sizeof(u32), x->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d.dirty, 1, (size_t)d.N, x->stream);   // first pass counts every row
   if (e == cudaSuccess) { k_init<<<148, 256, 0, x->stream>>>(d); e = cudaGetLastError(); }
 
   // planner kernels: small sorts and staged lists in dynamic shared memory
@@ -803,6 +804,9 @@ ta_status ta_debug_state(ta_ctx* ctx, int32_t dir, const ta_state_view* v) {
     size_t w = (size_t)d.MAXB * 4, sp = (size_t)d.MAXBP * 4;
     if (dir == 0) CK(ctx, cudaMemcpy2D(v->loc, w, d.loc, sp, w, N, cudaMemcpyDeviceToHost));
     else CK(ctx, cudaMemcpy2D(d.loc, sp, v->loc, w, w, N, cudaMemcpyHostToDevice));
+  }
+  if (dir == 1) {                          // uploaded state: the next footprint pass recounts every row
+    CK(ctx, cudaMemset(d.dirty, 1, N));
   }
   CK(ctx, mv(v->hbm_free, d.hbm_free, R * d.NBW * 4));
   if (d.NHW) CK(ctx, mv(v->host_free, d.host_free, R * d.NHW * 4));
