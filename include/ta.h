@@ -361,7 +361,7 @@ ta_status ta_debug_phase_stamps(ta_ctx* ctx, uint64_t* out, int32_t n);
  * memory (beyond the shared-memory list limit) [4] planner need prefix in global memory [5] eviction prefix in global
  * memory [6] victims in global memory [7] request loop reading program values from
  * global memory [8] restore-pass chunks after the first [9] replica-ticks with
- * evictions [10] block-table rows the tick's footprint pass counted (rows written
+ * evictions [10] (development build) block-table rows the tick's footprint pass counted (rows written
  * since the previous pass; clean rows keep their counts and are not read) [11] the
  * entries of those rows; [12, 16) reserved.  n <= 16.  Synchronizes the stream. */
 #define TA_DEBUG_COUNTERS 16

@@ -370,11 +370,13 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     const u32 inc = warp_incl_scan(nch);
     s_off[lane] = inc - nch;
     if (lane == 31) s_off[FP_SLOTS] = inc;
-    if (MODE == 0) {                     // rows / entries actually read (ta_debug_counters)
+#ifndef TA_PROD_VARIANT
+    if (MODE == 0) {                     // rows / entries read (ta_debug_counters; development build)
       const u32 nr = __reduce_add_sync(FULL_MASK, (dv && nbo) ? 1u : 0u);
       const u32 ne = __reduce_add_sync(FULL_MASK, dv ? nbo : 0u);
       if (lane == 0 && nr) { atomicAdd(&d.dbg[DBG_ROWS_COUNTED], (ull)nr); atomicAdd(&d.dbg[DBG_ROW_ENTRIES], (ull)ne); }
     }
+#endif
     s_nbo[lane] = nbo;
     s_dirty[lane] = dv;
     s_nh[lane] = 0; s_ns[lane] = 0; s_first[lane] = 0xFFFFFFFFu;
@@ -454,11 +456,12 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     if (live) {
       nbv = ceil_div_u32(v.c, d.bt);
       cb = contrib_of(d, nbv, (u8)v.ph, v.as, T);
-      if (st == TA_PAUSED) {
-        rbv = restore_bucket(d, (u8)v.ph, nbv);
-        atomicAdd(&d.rhist[rbv], 1u);
-      }
+      if (st == TA_PAUSED) rbv = restore_bucket(d, (u8)v.ph, nbv);
     }
+    // restore-bucket histogram: one atomic per distinct bucket per warp (thousands of
+    // PAUSED slots fall in a few buckets; per-lane atomics serialize at L2)
+    const u32 peers = __match_any_sync(FULL_MASK, rbv);
+    if (rbv != 0xFFFFFFFFu && lane == (int)(__ffs(peers) - 1)) atomicAdd(&d.rhist[rbv], (u32)__popc(peers));
   }
   if (MODE == 0) { PSTAMP_B(6, 0, 2); PSTAMP_B(7, gridDim.x - 1, 2); }
   __syncthreads();
