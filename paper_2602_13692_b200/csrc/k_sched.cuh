@@ -205,7 +205,44 @@ __device__ __forceinline__ void restore_pass(const Dev& d, u32* s_big, u32* s_tm
       }
       __syncthreads();
     }
-    if (w0 && pre && !TA_FLAG(d, TA_F_PINNED_ROUTING)) {
+    if (w0 && pre && R == 1 && !TA_FLAG(d, TA_F_PINNED_ROUTING)) {
+      // one replica: the loop below places entries in order while L < cap_min and
+      // L + c <= cap_max, skipping the oversized, up to the first that fails -- so 32
+      // entries at a time: L before entry i = L + the placed contributions before it
+      // (a warp prefix sum), and the first failing lane ends the pass
+      bool stop = false;
+      const ull c_min = __shfl_sync(FULL_MASK, cmin, 0), c_max = __shfl_sync(FULL_MASK, cmax, 0);
+      ull L0 = __shfl_sync(FULL_MASK, Lr, 0);
+      const u32 below = (1u << lane) - 1u;
+      for (u32 base = 0; base < n; base += 32) {
+        const u32 i = base + lane;
+        const bool in = i < n;
+        const u32 cr = in ? s_cr[i] : 0u;
+        const bool skip = in && cr > maxcap;             // can never fit (reading A9)
+        const u32 v = (in && !skip) ? cr : 0u;
+        const u32 inc = warp_incl_scan(v);               // < 32 x 2^23
+        const ull before = L0 + (ull)(inc - v);
+        const bool fit = skip || (before < c_min && before + cr <= c_max);
+        const u32 fail = __ballot_sync(FULL_MASK, in && !fit);
+        const u32 upto = fail ? (1u << (__ffs(fail) - 1)) - 1u : 0xFFFFFFFFu;   // lanes before it
+        const u32 placed = __ballot_sync(FULL_MASK, in && !skip) & upto;
+        over += __popc(__ballot_sync(FULL_MASK, skip) & upto);
+        if ((placed >> lane) & 1u) {
+          const u32 pl = q[i], hp = s_hp[i];
+          const bool pa = (hp >> 8) == TA_PHASE_A;
+          const u32 at = cnt + __popc(placed & below);
+          d.status[pl] = pa ? TA_ACTING : TA_REASONING;
+          d.placement[pl] = 0;
+          d.restore_pid[at] = pl;
+          d.restore_dst[at] = 0u | ((hp & 0xFFu) << 8) | ((u32)pa << 24);
+        }
+        cnt += __popc(placed);
+        const int f = fail ? __ffs(fail) - 1 : 31;      // placed before the first failure: all of them
+        L0 += (ull)__shfl_sync(FULL_MASK, fail ? inc - v : inc, f);
+        if (fail) { stop = true; break; }
+      }
+      if (lane == 0) { Lr = L0; s_stop = stop || T >= 2 * NBK - 1; }
+    } else if (w0 && pre && !TA_FLAG(d, TA_F_PINNED_ROUTING)) {
       // the global queue (reading A10) with the entries in shared memory: every lane reads
       // entry i (broadcast, independent of the loads), and one min-reduction over the
       // replicas' packed keys both tells whether any replica fits and picks the target
