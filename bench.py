@@ -681,8 +681,8 @@ def main():
                 "pcie full duplex (+ nvlink)"
         elif i == 7:
             byts, pk, bnd = 2 * mv["d2d"], hbm_peak, "hbm"
-        elif i == 0:
-            byts, pk, bnd = front_bytes, hbm_peak, "hbm"
+        elif i == 0:                                 # reads only rows written since the last tick
+            byts, pk, bnd = front_bytes, hbm_peak, "latency (two dependent round trips; fraction of HBM for context)"
         else:
             byts, pk, bnd = None, None, "latency (serial planner chain)"
         ach = byts / t / G if byts else None
