@@ -101,6 +101,10 @@ enum {
                                   sleeps a pseudo-random 0-20 us at kernel entry and after every
                                   grid / cluster barrier, so that a missing barrier between CTAs
                                   shows up as a wrong result.  Results are identical. */
+  TA_F_FULL_SCAN = 1u << 11,    /* test aid (development build only): the footprint pass counts
+                                  every live row each tick instead of only the rows written
+                                  since the previous pass (the clean-row rule).
+                                  Results are identical; tests compare the two. */
   TA_F_DECIDE_ONLY = 1u << 9    /* measurement aid: the tick runs steps 0-5 and 7 (decisions,
                                   block tables, free sets, statistics) but issues no block copy
                                   (no step 6, no compaction copies): the pools' bytes are not

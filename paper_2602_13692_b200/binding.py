@@ -27,7 +27,8 @@ F_REQUEST_AWARE = 128
 F_SMALL_PATHS = 256                  # test aid: small runs take the full-size code paths
 F_DECIDE_ONLY = 512                  # measurement aid: decisions without block copies
 F_JITTER = 1024                      # test aid: random CTA delays at entry and after barriers
-DEV_FLAGS = F_TIMING | F_PINNED_ROUTING | F_REQUEST_AWARE | F_SMALL_PATHS | F_JITTER   # need libta_dev.so
+F_FULL_SCAN = 2048                   # test aid: the footprint pass counts every live row
+DEV_FLAGS = F_TIMING | F_PINNED_ROUTING | F_REQUEST_AWARE | F_SMALL_PATHS | F_JITTER | F_FULL_SCAN   # libta_dev.so
 F_NO_BULK_DEFAULT = 1 << 30          # binding-only: do not turn TA_F_COPY_BULK on
 STATUS_NAMES = {0: "OK", 1: "E_INVAL", 2: "E_NOMEM", 3: "E_DUP_ID", 4: "E_UNKNOWN_PROGRAM",
                 5: "E_ILLEGAL_TRANSITION", 6: "E_CAPACITY", 7: "E_TRUNCATED", 8: "E_CUDA",

@@ -211,7 +211,7 @@ __device__ __forceinline__ void dbg_hit(const Dev& d, int i) {
 // PinnedRouting, RequestAware, small paths.
 #ifdef TA_PROD_VARIANT
 #define TA_FLAG(d, f) ((((f) & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | \
-                               TA_F_JITTER)) == 0) && \
+                               TA_F_JITTER | TA_F_FULL_SCAN)) == 0) && \
                        (((d).flags & (f)) != 0))
 #else
 #define TA_FLAG(d, f) (((d).flags & (f)) != 0)

@@ -354,7 +354,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   if (w0) {
     u32 nbo = 0;
     if (p < d.N) {
-      dv = d.dirty[p];                   // a clean row keeps last pass's counts (see above)
+      dv = d.dirty[p] | (TA_FLAG(d, TA_F_FULL_SCAN) ? 1 : 0);   // a clean row keeps last pass's counts
       nh_old = d.n_hbm[p];
       ns_old = d.n_host[p];
       if (MODE == 0) {

@@ -132,8 +132,10 @@ static const char* validate(const ta_config* c) {
   if ((uint64_t)c->max_programs * (uint64_t)c->max_blocks_per_program >= (uint64_t)TA_OWNER_PROMPT)
     return "max_programs * max_blocks_per_program must be below TA_OWNER_PROMPT";
 #ifdef TA_PROD_VARIANT
-  if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | TA_F_JITTER))
-    return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS / TA_F_JITTER need libta_dev.so "
+  if (c->flags & (TA_F_TIMING | TA_F_PINNED_ROUTING | TA_F_REQUEST_AWARE | TA_F_SMALL_PATHS | TA_F_JITTER |
+                  TA_F_FULL_SCAN))
+    return "TA_F_TIMING / TA_F_PINNED_ROUTING / TA_F_REQUEST_AWARE / TA_F_SMALL_PATHS / TA_F_JITTER / TA_F_FULL_SCAN "
+           "need libta_dev.so "
            "(the development build of the same sources; libta.so compiles them out)";
 #endif
   return nullptr;

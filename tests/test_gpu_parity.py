@@ -270,3 +270,57 @@ def test_gpu_jitter_schedules():
         if st_o == oracle.OK:
             same_decisions(dec_g, dec_o, f"jitter api tick {k}")
     pool.close()
+
+
+def _lockstep_full_scan(cfg, ticks, verbs_seed=None, n_slots=None):
+    """Two pools on the same trace: the product's footprint pass (counts only rows written
+    since the previous pass) and TA_F_FULL_SCAN (development build: counts every live row,
+    the round-1/2 behaviour the oracle parity was first established on).  After every tick
+    and verb: the same status, the same decisions, and the same derived arrays (nb, n_hbm,
+    n_host, prefix_hbm, contrib) and block tables."""
+    import random
+    from paper_2602_13692_b200 import Pool, binding
+    tr = tracegen.make_trace(cfg)
+    pools = [Pool(cfg, tr.n_slots, max_turns=tr.total_turns, fill=False, flags=f)
+             for f in (0, binding.F_FULL_SCAN)]
+    for p in pools:
+        p.load_trace(tr)
+    fields = ["status", "nb", "n_hbm", "n_host", "prefix_hbm", "contrib", "loc"]
+    rng = random.Random(verbs_seed)
+    for k in range(ticks):
+        outs = [p.step() for p in pools]
+        assert outs[0][0] == outs[1][0], (k, outs[0][0], outs[1][0])
+        assert np.array_equal(outs[0][1], outs[1][1]), f"tick {k}: decisions differ"
+        if verbs_seed is not None and k % 3 == 2:       # a verb between ticks (rows rewritten)
+            st = pools[0].debug_download(["status"])["status"]
+            cand = np.nonzero(st == oracle.REASONING)[0]
+            if cand.size:
+                pid = int(rng.choice(list(cand)))
+                mode = rng.choice((0, 1, 2))
+                r0 = [p.pause(pid, mode) for p in pools]
+                assert r0[0][0] == r0[1][0], (k, "pause", r0[0][0], r0[1][0])
+            cand = np.nonzero(st == oracle.PAUSED)[0]
+            if cand.size:
+                pid = int(rng.choice(list(cand)))
+                r1 = [p.resume(pid, -1) for p in pools]
+                assert r1[0][0] == r1[1][0], (k, "resume", r1[0][0], r1[1][0])
+        a, b = (p.debug_download(fields) for p in pools)
+        for f in fields:
+            if not np.array_equal(a[f], b[f]):
+                bad = np.argwhere(a[f] != b[f])[:4]
+                raise AssertionError(f"tick {k}: {f} differs at {bad.tolist()}")
+    for p in pools:
+        p.close()
+
+
+@pytest.mark.gpu
+def test_gpu_dirty_rows_equal_full_scan():
+    """The footprint pass reads only rows written since its previous pass (DESIGN.md §6,
+    dirty rows); with TA_F_FULL_SCAN it counts every live row.  Both give the same
+    decisions, derived counts and block tables tick by tick: stress traces with compaction
+    and the host tier (R 1 and 3), with pause / resume verbs between ticks, and bench_10k
+    (10k programs, mini KV) through its burst."""
+    need_gpu()
+    _lockstep_full_scan(stress(61, 1, compact=3), 150)
+    _lockstep_full_scan(stress(62, 3, compact=2), 150, verbs_seed=7)
+    _lockstep_full_scan(tracegen.get_config("bench_10k", kv="mini"), 40)
