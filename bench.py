@@ -434,8 +434,8 @@ def cpu_baseline(cfg, trace, start, seconds):
 
 
 # per-tick algorithmic bytes of the kernels: the footprint pass reads a
-# slot's 64-B program record and writes 24 B of derived values, reads 4 B per entry of
-# the rows written since the previous pass and one 4-B entry of every other live row;
+# slot's 64-B program record and writes 24 B of derived values, and reads 4 B per entry
+# of the rows written since the previous pass (clean rows are not read);
 # the movement kernel moves one block per moved block over its link; compaction reads
 # and writes each moved block in HBM
 FRONT_SLOT_BYTES = 88
@@ -569,7 +569,7 @@ def main():
         ti = pool.last_tick()
         ent = pool.debug_counters()["front_row_entries"]
         # entries read by this tick's footprint pass: the rows written since the previous
-        # pass (clean rows keep their counts; one entry each, counted with the slot)
+        # pass (clean rows keep their counts and class and are not read)
         live = np.isin(st_prev["status"], (1, 2, 3))
         ticks.append((ti, ph, ent - ent_prev, int(live.sum())))
         ent_prev = ent
@@ -660,7 +660,7 @@ def main():
                     ti["h2d_of"][r] * bb / max(peaks_concurrent["h2d"], 1e-9),
                     ti["p2p_to"][r] * bb / nvl) for r in range(len(ti["d2h_of"]))) / G
         mv["d2d_floor_s"] += 2 * ti["d2d_blocks"] * bb / world / hbm_peak / G
-        front_bytes += (FRONT_SLOT_BYTES * progs_total / world + 4 * (sum_nb + n_live) / world)
+        front_bytes += (FRONT_SLOT_BYTES * progs_total / world + 4 * sum_nb / world)
     move_s = ph_sum[3] * 1e-6                         # fused movement kernel, summed over the window
     move_bytes = mv["d2h"] + mv["h2d"] + mv["p2p"]
     # kernel names by phase slot (ta_phase_times)

@@ -295,8 +295,10 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 // verbs, a state upload -- and this pass clears it).  A clean row of a live program
 // has the counts and HBM prefix the last pass stored: c never shrinks, so its extra
 // entries [nbo_then, nbo) are NONE, which add to neither count and leave
-// min(first, nbo) where it was.  Its last-history-block class still depends on c_kv,
-// so that one entry is read (a 4-byte cp.async).
+// min(first, nbo) where it was.  Its last-history-block class (entry ceil(c_kv/bt) - 1)
+// is kept as well: c_kv changes only when the program is satisfied (k_close, which marks
+// the row) or arrives (a fresh or released row, class 0), so a clean row's entry and
+// index are the ones last classified.
 #define FP_SLOTS 32                     // slots per CTA (one lane of warp 0 each)
 #ifndef FP_THREADS
 #define FP_THREADS 256                   // FP_SLOTS / (FP_THREADS / 32) slots per warp
@@ -307,10 +309,6 @@ __global__ void __launch_bounds__(256) k_ev_apply(const __grid_constant__ Dev d)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const u32 s = (u32)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const u32 s = (u32)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
@@ -331,7 +329,6 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   __shared__ int s_home[FP_SLOTS];
   __shared__ u8 s_rel[FP_SLOTS], s_hcls[FP_SLOTS], s_kp[FP_SLOTS];
   __shared__ u32 s_jh[FP_SLOTS];          // entry of the last history block (ceil(c_kv/bt) - 1), or ~0
-  __shared__ u32 s_hx[FP_SLOTS];          // clean row: its entry jh
   __shared__ u8 s_dirty[FP_SLOTS];
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const int p0 = blockIdx.x * FP_SLOTS;
@@ -350,13 +347,14 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
   SlotFields f{};
   SlotNow v{};
   u32 nh_old = 0, ns_old = 0;
-  u8 dv = 0;
+  u8 dv = 0, hc_old = 0;
   if (w0) {
     u32 nbo = 0;
     if (p < d.N) {
       dv = d.dirty[p] | (TA_FLAG(d, TA_F_FULL_SCAN) ? 1 : 0);   // a clean row keeps last pass's counts
       nh_old = d.n_hbm[p];
       ns_old = d.n_host[p];
+      hc_old = d.hcls[p];
       if (MODE == 0) {
         f = ingest_load(d, p);
         nbo = row_len_of(d, f.st, f.c);
@@ -383,7 +381,7 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     const u32 ckv = p < d.N ? d.c_kv[p] : 0u;
     s_kp[lane] = p < d.N ? d.kp[p] : (u8)KP_NONE;
     s_jh[lane] = ckv ? ceil_div_u32(ckv, d.bt) - 1 : 0xFFFFFFFFu;
-    s_hcls[lane] = 0;
+    s_hcls[lane] = dv ? 0 : hc_old;      // clean: c_kv and the row are as last counted
   }
   __syncthreads();
   const u32* rows = d.loc + (size_t)p0 * d.MAXBP;
@@ -399,23 +397,14 @@ __device__ __forceinline__ void footprint_cta(const Dev& d) {
     constexpr int CW = FP_THREADS / 32 - 1;       // counting warps
     for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
       const u32 o = s_off[sl], nch = s_off[sl + 1] - o;
-      if (!s_dirty[sl]) {                // clean row: only the last history block's entry
-        if (lane == 0 && s_jh[sl] < s_nbo[sl]) cp_async4(&s_hx[sl], rows + (size_t)sl * d.MAXBP + s_jh[sl]);
-      } else if (o + nch <= FP_STAGE) {
+      if (s_dirty[sl] && o + nch <= FP_STAGE)    // clean rows are not read
         for (u32 c = lane; c < nch; c += 32) cp_async16(&s_stage[o + c], rows + (size_t)sl * d.MAXBP + 4 * c);
-      }
     }
     cp_async_wait_all();
     __syncwarp();
     for (int sl = warp - 1; sl < FP_SLOTS; sl += CW) {
       const u32 o = s_off[sl], nch = s_off[sl + 1] - o, nbo = s_nbo[sl];
-      if (!s_dirty[sl]) {
-        if (lane == 0 && s_jh[sl] < nbo) {
-          const u32 x = s_hx[sl];
-          s_hcls[sl] = is_hbm(x) ? 1 : (is_host(x) ? 2 : 0);
-        }
-        continue;
-      }
+      if (!s_dirty[sl]) continue;
       const bool staged = o + nch <= FP_STAGE;
       const uint4* grow = reinterpret_cast<const uint4*>(rows + (size_t)sl * d.MAXBP);
       u32 a_h = 0, a_n = 0, a_f = 0xFFFFFFFFu;   // HBM entries, non-HBM entries, first non-HBM
