@@ -205,19 +205,35 @@ __device__ __forceinline__ void assemble_close(const Dev& d, u32 pos) {
     }
   }
   __syncthreads();
+  // per replica on warp 0 (lane r; R <= 32): every value loaded in one round trip, the
+  // statistics added with fire-and-forget atomics (no read-modify-write chain on thread 0)
   ull umax = 0, umin = ~0ull;
-  if (threadIdx.x == 0) {
-    for (int r = 0; r < R; ++r) {
-      const ull used = (ull)d.NB - s_free[r];
-      if (!verb && d.ctr->cmin != 0xFFFFFFFFu) {   // programs wait in the queue
-        const ull cap = (ull)d.cap_max[r];
-        d.stats[ST_COST_UNUSED] += (cap > used ? cap - used : 0) * (ull)d.bt * (ull)d.dt;
-        d.stats[ST_UNUSED_CHECKS] += 1;
-        const ull idle = cap > d.L[r] ? cap - d.L[r] : 0;        // C_unused < c_min
-        if (idle >= d.ctr->cmin) d.stats[ST_UNUSED_VIOL] += 1;
-      }
-      umax = used > umax ? used : umax;
-      umin = used < umin ? used : umin;
+  if (threadIdx.x < 32) {
+    const int r = (int)threadIdx.x;
+    const u32 cminq = d.ctr->cmin;
+    const bool on = r < R;
+    const ull used = on ? (ull)d.NB - s_free[r] : 0ull;
+    const ull cap = on ? (ull)d.cap_max[r] : 0ull, Lr = on ? d.L[r] : 0ull;
+    ull cost = 0, viol = 0;
+    if (!verb && cminq != 0xFFFFFFFFu && on) {     // programs wait in the queue
+      cost = (cap > used ? cap - used : 0) * (ull)d.bt * (ull)d.dt;
+      const ull idle = cap > Lr ? cap - Lr : 0;    // C_unused < c_min
+      viol = idle >= cminq ? 1ull : 0ull;
+    }
+    cost = warp_sum_ull(cost);
+    viol = warp_sum_ull(viol);
+    ull mx = on ? used : 0ull, mn = on ? used : ~0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const ull a = __shfl_xor_sync(FULL_MASK, mx, o), b = __shfl_xor_sync(FULL_MASK, mn, o);
+      mx = a > mx ? a : mx;
+      mn = b < mn ? b : mn;
+    }
+    umax = mx; umin = mn;
+    if (threadIdx.x == 0 && !verb && cminq != 0xFFFFFFFFu) {
+      atomicAdd(&d.stats[ST_COST_UNUSED], cost);
+      atomicAdd(&d.stats[ST_UNUSED_CHECKS], (ull)R);
+      if (viol) atomicAdd(&d.stats[ST_UNUSED_VIOL], viol);
     }
   }
   PSTAMP(3, 7);
@@ -228,26 +244,37 @@ __device__ __forceinline__ void assemble_close(const Dev& d, u32 pos) {
     d.tick_info->p2p_to[r] = r < R ? d.t_rep[2 * R + r] : 0;
   }
   if (threadIdx.x == 0) {
+    // every counter read first (one round trip), then stores and fire-and-forget atomics
+    Ctr* c = d.ctr;
+    const i64 tick = c->tick, nxt = c->next_arrival;
+    const u32 t_d2h = c->t_d2h, t_h2d = c->t_h2d, t_p2p = c->t_p2p, t_d2d = c->t_d2d, t_fetch = c->t_fetch;
+    const u32 stops = c->stops, narr = c->n_arr;
     *d.dec_out_cnt = pos;
     ta_tick_info* ti = d.tick_info;
-    ti->tick = d.ctr->tick;
+    ti->tick = tick;
     ti->decisions = pos;
-    ti->d2h_blocks = d.ctr->t_d2h;
-    ti->h2d_blocks = d.ctr->t_h2d;
-    ti->p2p_blocks = d.ctr->t_p2p;
-    ti->d2d_blocks = d.ctr->t_d2d;
-    ti->fetch_blocks = d.ctr->t_fetch;
-    d.ctr->n_dec = pos;
+    ti->d2h_blocks = t_d2h;
+    ti->h2d_blocks = t_h2d;
+    ti->p2p_blocks = t_p2p;
+    ti->d2d_blocks = t_d2d;
+    ti->fetch_blocks = t_fetch;
+    c->n_dec = pos;
     if (!verb) {
-      ull imb = umax - umin;
+      const ull imb = umax - umin;
       d.stats[ST_IMB_LAST] = imb;
-      if (imb > d.stats[ST_IMB_MAX]) d.stats[ST_IMB_MAX] = imb;
-      i64 n_arr = d.api_mode ? (i64)d.ctr->n_arr : trace_arrivals(d);
-      d.stats[ST_ARRIVALS] += (ull)n_arr;
-      d.stats[ST_STOPS] += d.ctr->stops;
-      d.stats[ST_TICKS] += 1;
-      if (!d.api_mode) d.ctr->next_arrival += n_arr;
-      d.ctr->tick += 1;
+      atomicMax(&d.stats[ST_IMB_MAX], imb);
+      i64 n_arr;                                      // trace_arrivals() on the values read above
+      if (d.api_mode) {
+        n_arr = (i64)narr;
+      } else {
+        const i64 want = (tick == 0 ? (i64)d.n_initial : 0) + (i64)stops, room = (i64)d.n_slots - nxt;
+        n_arr = want < room ? want : room;
+        c->next_arrival = nxt + n_arr;
+      }
+      atomicAdd(&d.stats[ST_ARRIVALS], (ull)n_arr);
+      if (stops) atomicAdd(&d.stats[ST_STOPS], (ull)stops);
+      atomicAdd(&d.stats[ST_TICKS], 1ull);
+      c->tick = tick + 1;
     }
   }
   // clear the per-tick lists and counters for the next tick / call
