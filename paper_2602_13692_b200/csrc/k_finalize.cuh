@@ -25,9 +25,12 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int first_cta) {
   ull cach = 0;                          // NEXT-1: idle resident KV (token count)
   u32 cmin = 0xFFFFFFFFu;                // smallest paused footprint (blocks)
   for (int p = t; p < d.N; p += stride) {
-    u8 s = d.sat_new[p];
+    // every per-program value in one round trip (L2-resident: written this tick)
+    const u8 s = d.sat_new[p], st = d.status[p];
+    const int h = d.home[p];
+    const u32 cp = d.c[p], nbp = d.nb[p], nhp = d.n_hbm[p];
     if (s) {
-      const int r = s - 1, h = d.home[p];
+      const int r = s - 1;
       const u8 k = d.kp[p];
       if (h != r && k != KP_NONE) {      // NEXT-3 (A51): its prompt entries now point at r's copy;
         const u32* blk = d.pblk + ((size_t)r * d.K + k) * d.SBM;   // h's copy loses a user, and
@@ -37,16 +40,15 @@ __device__ __forceinline__ void finalize_part(const Dev& d, int first_cta) {
       }
       d.satisfied[p] = 1;
       d.home[p] = (i8)(s - 1);
-      d.c_kv[p] = d.c[p];
-      d.n_hbm[p] = d.nb[p];
+      d.c_kv[p] = cp;
+      d.n_hbm[p] = nbp;
       d.sat_new[p] = 0;
       d.dirty[p] = 1;                    // its row was written (fetches, prompt entries)
     } else if (!verb) {
       d.satisfied[p] = 0;
-      const u8 st = d.status[p];
       if (st == TA_PAUSED || st == TA_ACTING) {
-        if (d.home[p] >= 0) cach += min((ull)d.n_hbm[p] * (ull)d.bt, (ull)d.c[p]);
-        if (st == TA_PAUSED) cmin = min(cmin, d.nb[p]);
+        if (h >= 0) cach += min((ull)nhp * (ull)d.bt, (ull)cp);
+        if (st == TA_PAUSED) cmin = min(cmin, nbp);
       }
     }
   }
